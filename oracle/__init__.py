@@ -1,0 +1,254 @@
+"""fp64 CPU oracle for the GESR MoA candidate-scoring hot path -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` /
+``--impl reference`` legs may import this package.  The product path
+(``paper_2511_21095_b200``) never imports it, and this package never imports the product
+path: the two share no code.  Inputs come from ``paper_2511_21095_b200.inputs`` (seeded
+generators holding none of the method's arithmetic) or from the tests themselves.
+
+Every function wraps one entry point of ``oracle/oracle.cpp`` (plain C++17, fp64, no
+blocking/fusion), each citing the passage it follows:
+
+* :func:`kv_project`  -- K/V = act(U W^T + b) per head. PAPER.md:335-341 (s3.4.2).
+* :func:`tasa_score`  -- candidate rows of the target-aware masked softmax attention over the
+  request's history.  PAPER.md:341, 346 (s3.4.2).
+* :func:`full_masked_attention` -- brute force over the full (L+C)^2 mask.  SPEC.md:289-297.
+* :func:`build_mask` -- the mask itself.  PAPER.md:341.
+* :func:`hma_count` / :func:`hma_count_hash` -- HMA raw (optionally capped) match counts, two
+  independent algorithms.  PAPER.md:308-312 (s3.4.1).
+
+Parity pins: see tests/test_oracle_*.py.  Every function here is pinned.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+_c_i64p = ctypes.POINTER(ctypes.c_int64)
+_c_u16p = ctypes.POINTER(ctypes.c_uint16)
+_c_f64p = ctypes.POINTER(ctypes.c_double)
+_c_i32p = ctypes.POINTER(ctypes.c_int32)
+_c_u8p = ctypes.POINTER(ctypes.c_uint8)
+
+
+def build() -> str:
+    """Compile liboracle.so (g++ -O2, no fast-math: no reassociation)."""
+    src = os.path.join(_HERE, "oracle.cpp")
+    cmd = ["g++", "-O2", "-std=c++17", "-fPIC", "-shared", "-pthread", "-o", _LIB_PATH, src]
+    subprocess.check_call(cmd)
+    return _LIB_PATH
+
+
+def _load():
+    global _lib
+    if _lib is not None:
+        return _lib
+    src = os.path.join(_HERE, "oracle.cpp")
+    if (not os.path.exists(_LIB_PATH)) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(src):
+        build()
+    lib = ctypes.CDLL(_LIB_PATH)
+    lib.oracle_kv_project.argtypes = [_c_u16p, ctypes.c_int64, ctypes.c_int32, _c_u16p, _c_u16p,
+                                      _c_f64p, _c_f64p, ctypes.c_int32, ctypes.c_int32,
+                                      ctypes.c_int32, _c_f64p, _c_f64p, ctypes.c_int32]
+    lib.oracle_tasa_score.argtypes = [_c_u16p, ctypes.c_int64, ctypes.c_int32, _c_i64p, _c_u16p,
+                                      _c_f64p, ctypes.c_int32, _c_f64p, _c_f64p, _c_i64p,
+                                      ctypes.c_int64, ctypes.c_int64, ctypes.c_int32,
+                                      ctypes.c_int32, ctypes.c_double, ctypes.c_int32, _c_f64p,
+                                      _c_f64p, ctypes.c_int32]
+    lib.oracle_build_mask.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, _c_u8p]
+    lib.oracle_full_masked_attention.argtypes = [
+        _c_u16p, ctypes.c_int64, _c_u16p, ctypes.c_int64, ctypes.c_int32, _c_u16p, _c_u16p,
+        _c_u16p, _c_f64p, _c_f64p, _c_f64p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+        ctypes.c_double, ctypes.c_int32, _c_f64p, _c_f64p]
+    lib.oracle_hma_count.argtypes = [_c_i64p, _c_i64p, _c_i64p, _c_i64p, _c_i64p, ctypes.c_int64,
+                                     ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, _c_i32p,
+                                     ctypes.c_int32]
+    lib.oracle_hma_count_hash.argtypes = [_c_i64p, _c_i64p, _c_i64p, _c_i64p, _c_i64p,
+                                          ctypes.c_int64, ctypes.c_int64, ctypes.c_int32,
+                                          ctypes.c_int32, _c_i32p]
+    lib.oracle_round_to_bf16.argtypes = [_c_f64p, ctypes.c_int64]
+    _lib = lib
+    return lib
+
+
+def default_threads() -> int:
+    try:
+        return max(1, len(os.sched_getaffinity(0)))
+    except AttributeError:  # pragma: no cover
+        return max(1, os.cpu_count() or 1)
+
+
+# ---------------------------------------------------------------------------------------------
+# marshalling helpers (argument conversion only)
+
+def _bits(x) -> np.ndarray:
+    """bf16 tensor/array -> contiguous uint16 bit array."""
+    try:
+        import torch
+        if isinstance(x, torch.Tensor):
+            assert x.dtype == torch.bfloat16, x.dtype
+            return np.ascontiguousarray(x.detach().cpu().contiguous().view(torch.int16).numpy()
+                                        .view(np.uint16))
+    except ImportError:  # pragma: no cover
+        pass
+    a = np.asarray(x)
+    assert a.dtype == np.uint16, a.dtype
+    return np.ascontiguousarray(a)
+
+
+def _np(x, dtype) -> np.ndarray:
+    try:
+        import torch
+        if isinstance(x, torch.Tensor):
+            x = x.detach().cpu().numpy()
+    except ImportError:  # pragma: no cover
+        pass
+    return np.ascontiguousarray(np.asarray(x, dtype=dtype))
+
+
+def _p(a: np.ndarray, ctype):
+    return a.ctypes.data_as(ctype)
+
+
+def _opt_f64(b):
+    if b is None:
+        return None, None
+    a = _np(b, np.float64)
+    return a, _p(a, _c_f64p)
+
+
+# ---------------------------------------------------------------------------------------------
+
+def kv_project(U, W_k, W_v, H, d, act=1, b_k=None, b_v=None, threads=None):
+    """K, V fp64 [H, total_L, d] = act(U W^T + b) split into heads."""
+    lib = _load()
+    Ub, Wk, Wv = _bits(U), _bits(W_k), _bits(W_v)
+    total_L, D_in = Ub.shape
+    assert Wk.shape == (H * d, D_in) and Wv.shape == (H * d, D_in)
+    K = np.zeros((H, total_L, d), np.float64)
+    V = np.zeros((H, total_L, d), np.float64)
+    bk, pbk = _opt_f64(b_k)
+    bv, pbv = _opt_f64(b_v)
+    lib.oracle_kv_project(_p(Ub, _c_u16p), total_L, D_in, _p(Wk, _c_u16p), _p(Wv, _c_u16p),
+                          pbk, pbv, H, d, act, _p(K, _c_f64p), _p(V, _c_f64p),
+                          threads or default_threads())
+    return K, V
+
+
+def tasa_score(T, cand_offsets, W_q, K, V, seq_offsets, H, d, act=1, b_q=None, scale=None,
+               round_q_bf16=False, threads=None):
+    """O fp64 [total_C, H*d], lse fp64 [total_C, H]: each candidate's masked softmax attention
+    over its request's cached history K/V.  scale None -> 1/sqrt(d)."""
+    lib = _load()
+    Tb, Wq = _bits(T), _bits(W_q)
+    total_C, D_in = Tb.shape
+    co = _np(cand_offsets, np.int64)
+    so = _np(seq_offsets, np.int64)
+    B = co.shape[0] - 1
+    assert so.shape[0] == B + 1
+    Kd = _np(K, np.float64)
+    Vd = _np(V, np.float64)
+    total_L = Kd.shape[1]
+    assert Kd.shape == (H, total_L, d) and Vd.shape == (H, total_L, d)
+    if scale is None:
+        scale = 1.0 / np.sqrt(d)
+    O = np.zeros((total_C, H * d), np.float64)
+    lse = np.zeros((total_C, H), np.float64)
+    bq, pbq = _opt_f64(b_q)
+    lib.oracle_tasa_score(_p(Tb, _c_u16p), total_C, D_in, _p(co, _c_i64p), _p(Wq, _c_u16p), pbq,
+                          act, _p(Kd, _c_f64p), _p(Vd, _c_f64p), _p(so, _c_i64p), B, total_L, H,
+                          d, float(scale), int(bool(round_q_bf16)), _p(O, _c_f64p),
+                          _p(lse, _c_f64p), threads or default_threads())
+    return O, lse
+
+
+def round_to_bf16(x) -> np.ndarray:
+    """Diagnostic only: round fp64 values to the nearest bf16 (RNE), returned as fp64."""
+    lib = _load()
+    a = np.array(x, dtype=np.float64, copy=True, order="C")
+    lib.oracle_round_to_bf16(_p(a, _c_f64p), a.size)
+    return a
+
+
+def build_mask(N, n, self_key=False) -> np.ndarray:
+    """(N+n)x(N+n) uint8 target-aware mask."""
+    lib = _load()
+    m = np.zeros((N + n, N + n), np.uint8)
+    lib.oracle_build_mask(N, n, int(bool(self_key)), _p(m, _c_u8p))
+    return m
+
+
+def full_masked_attention(U, T, W_q, W_k, W_v, H, d, act=1, b_q=None, b_k=None, b_v=None,
+                          scale=None, self_key=False):
+    """Brute force for ONE request: candidate rows of masked attention over [U;T]."""
+    lib = _load()
+    Ub, Tb = _bits(U), _bits(T)
+    L, D_in = Ub.shape if Ub.size else (0, _bits(T).shape[1])
+    C = Tb.shape[0]
+    if Ub.size == 0:
+        Ub = np.zeros((1, D_in), np.uint16)
+    Wq, Wk, Wv = _bits(W_q), _bits(W_k), _bits(W_v)
+    if scale is None:
+        scale = 1.0 / np.sqrt(d)
+    O = np.zeros((C, H * d), np.float64)
+    lse = np.zeros((C, H), np.float64)
+    bq, pbq = _opt_f64(b_q)
+    bk, pbk = _opt_f64(b_k)
+    bv, pbv = _opt_f64(b_v)
+    lib.oracle_full_masked_attention(_p(Ub, _c_u16p), L, _p(Tb, _c_u16p), C, D_in,
+                                     _p(Wq, _c_u16p), _p(Wk, _c_u16p), _p(Wv, _c_u16p), pbq, pbk,
+                                     pbv, H, d, act, float(scale), int(bool(self_key)),
+                                     _p(O, _c_f64p), _p(lse, _c_f64p))
+    return O, lse
+
+
+def _hma_args(user_ids, user_offsets, item_ids, item_offsets, cand_offsets):
+    ui = _np(user_ids, np.int64)
+    uo = _np(user_offsets, np.int64)
+    ii = _np(item_ids, np.int64)
+    io = _np(item_offsets, np.int64)
+    co = _np(cand_offsets, np.int64)
+    if ui.size == 0:
+        ui = np.zeros(1, np.int64)
+    if ii.size == 0:
+        ii = np.zeros(1, np.int64)
+    return ui, uo, ii, io, co
+
+
+def hma_count(user_ids, user_offsets, item_ids, item_offsets, cand_offsets, F, cap=0,
+              threads=None) -> np.ndarray:
+    """int32 [total_C, F] pairwise match counts, optionally capped."""
+    lib = _load()
+    ui, uo, ii, io, co = _hma_args(user_ids, user_offsets, item_ids, item_offsets, cand_offsets)
+    B = co.shape[0] - 1
+    total_C = int(co[-1]) if B >= 0 and co.size else 0
+    counts = np.zeros((max(total_C, 0), F), np.int32)
+    if total_C == 0 or F == 0:
+        return counts
+    lib.oracle_hma_count(_p(ui, _c_i64p), _p(uo, _c_i64p), _p(ii, _c_i64p), _p(io, _c_i64p),
+                         _p(co, _c_i64p), B, total_C, F, cap, _p(counts, _c_i32p),
+                         threads or default_threads())
+    return counts
+
+
+def hma_count_hash(user_ids, user_offsets, item_ids, item_offsets, cand_offsets, F,
+                   cap=0) -> np.ndarray:
+    """Second, independent algorithm (multiplicity map) for the same counts."""
+    lib = _load()
+    ui, uo, ii, io, co = _hma_args(user_ids, user_offsets, item_ids, item_offsets, cand_offsets)
+    B = co.shape[0] - 1
+    total_C = int(co[-1]) if co.size else 0
+    counts = np.zeros((max(total_C, 0), F), np.int32)
+    if total_C == 0 or F == 0:
+        return counts
+    lib.oracle_hma_count_hash(_p(ui, _c_i64p), _p(uo, _c_i64p), _p(ii, _c_i64p),
+                              _p(io, _c_i64p), _p(co, _c_i64p), B, total_C, F, cap,
+                              _p(counts, _c_i32p))
+    return counts
