@@ -1,0 +1,150 @@
+/* include/gesr.h -- C ABI of libgesr.so: the GESR Mixture-of-Attention candidate-scoring hot
+ * path (arxiv 2511.21095) on B200 (sm_100a).
+ *
+ * Three calls make one scoring step over a batch of B ranking requests:
+ *
+ *   gesr_kv_project   K/V projection of every user's jagged history, computed once per user and
+ *                     cached for all of that user's candidates.
+ *                     PAPER.md:335-341 (s3.4.2 Target-Aware Self Attention: U in R^{N x D},
+ *                     D = embedding dim flattened over heads; [U, T] through self-attention),
+ *                     caching PAPER.md:203, 215 (s1 "improved caching mechanisms").
+ *   gesr_tasa_score   target-aware attention: every candidate's query attends over its own
+ *                     user's cached K/V and over no other candidate (mask rules (1)-(2),
+ *                     PAPER.md:341; output rows I_NRO), softmax normalisation
+ *                     (reading R1).
+ *   gesr_hma_count    Hard Matching Attention raw match counts between each (candidate, field)
+ *                     item ID list and the request's user ID list of the same field:
+ *                     c = sum_i sum_j [u_i == t_j], optionally min(c, M)  (PAPER.md:308-312,
+ *                     s3.4.1).
+ *
+ * Conventions (all calls):
+ *   - Every array pointer is a DEVICE pointer owned by the caller; the library never frees or
+ *     retains a pointer after the call returns.  bf16 arrays are IEEE bfloat16 bit patterns.
+ *   - `stream` is a cudaStream_t (passed as void*; NULL = legacy default stream).  Calls are
+ *     asynchronous on that stream: no host synchronisation, no device allocation, no
+ *     host<->device copies; they are CUDA-graph capturable.  Safe to call concurrently from
+ *     several threads on different streams.
+ *   - Host-checkable argument errors return GESR_ERR_INVALID_ARG BEFORE any launch and write
+ *     nothing; unsupported options return GESR_ERR_UNSUPPORTED; a too-small workspace returns
+ *     GESR_ERR_WORKSPACE; a failed launch returns GESR_ERR_CUDA.  gesr_last_error() gives a
+ *     thread-local message for the last non-OK return.
+ *   - Offsets are NOT validated on the device: offsets[0] must be 0, offsets nondecreasing and
+ *     offsets[B] equal to the stated total.  Malformed offsets are undefined behaviour.
+ *   - Empty problems (B = 0, total_C = 0, F = 0) are valid no-ops.
+ */
+#ifndef GESR_H_
+#define GESR_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  GESR_OK = 0,
+  GESR_ERR_INVALID_ARG = 1,
+  GESR_ERR_UNSUPPORTED = 2,
+  GESR_ERR_CUDA = 3,
+  GESR_ERR_WORKSPACE = 4
+} gesr_status;
+
+/* Projection activation act(x) (reading R3; SPEC.md:343 uses SiLU). */
+typedef enum { GESR_ACT_IDENTITY = 0, GESR_ACT_SILU = 1 } gesr_act;
+
+/* Element type of the attention output O. */
+typedef enum { GESR_OUT_F32 = 0, GESR_OUT_BF16 = 1 } gesr_out_dtype;
+
+/* gesr_tasa_score flag, reserved: the candidate also attends to its own key (SPEC.md:277's
+ * diagonal, reading R2).  Returns GESR_ERR_UNSUPPORTED in this version. */
+#define GESR_TASA_SELF_KEY 0x1u
+
+/* Library version (major*10000 + minor*100 + patch). */
+int gesr_version(void);
+const char* gesr_status_string(int status);
+const char* gesr_last_error(void);
+
+/* gesr_kv_project -- K = act(U W_k^T + b_k), V = act(U W_v^T + b_v), split into heads.
+ *   U        bf16 [total_L, D_in] row-major: all requests' history rows, request b owning rows
+ *            [seq_offsets[b], seq_offsets[b+1]).  Rows are projected independently, so the
+ *            offsets are not needed here; the cache keeps the same row order.
+ *   D_in     multiple of 8, 8 <= D_in <= 16384.
+ *   W_k, W_v bf16 [H*d, D_in] row-major (nn.Linear weight layout); head h = rows [h*d,(h+1)*d).
+ *   b_k, b_v fp32 [H*d] or NULL (no bias).
+ *   H, d     H >= 1, d in {32, 64, 128}.
+ *   act      gesr_act.
+ *   K_cache, V_cache  bf16 [H, total_L, d] (written): head-major, so each (request, head)
+ *            owns one contiguous L_b x d slab -- the layout gesr_tasa_score's TMA loads read.
+ *   Values are rounded to bf16 round-to-nearest-even from fp32 accumulation.
+ *   Pointers must be 16-byte aligned.  total_L = 0 is a no-op. */
+gesr_status gesr_kv_project(const void* U, int64_t total_L, int32_t D_in,
+                            const void* W_k, const void* W_v,
+                            const float* b_k, const float* b_v,
+                            int32_t H, int32_t d, int32_t act,
+                            void* K_cache, void* V_cache,
+                            void* stream);
+
+/* Workspace bytes gesr_tasa_score needs for this problem (an upper bound that depends only on
+ * the arguments, never on device data).  Returns 0 for invalid arguments. */
+size_t gesr_tasa_workspace_bytes(int64_t B, int64_t total_C, int32_t H, int32_t d,
+                                 int32_t kv_splits);
+
+/* gesr_tasa_score -- candidate rows of target-aware self-attention over the cached history.
+ *   T          bf16 [total_C, D_in]: candidate embeddings, request b owning rows
+ *              [cand_offsets[b], cand_offsets[b+1]).
+ *   cand_offsets int64 [B+1] (device).
+ *   W_q, b_q, act  as in gesr_kv_project: q = act(T W_q^T + b_q), head h = cols [h*d,(h+1)*d).
+ *   K_cache, V_cache  bf16 [H, total_L, d] from gesr_kv_project (any number of calls may reuse
+ *              one cache, e.g. candidate chunks of the same users).
+ *   seq_offsets int64 [B+1] (device) into the cache rows.
+ *   scale      score scale; <= 0 selects 1/sqrt(d) (reading R4).
+ *   kv_splits  0 = auto, >= 1 forced.  This version computes every row in a single pass over
+ *              its history (splits = 1); values > 1 return GESR_ERR_UNSUPPORTED.  Each output
+ *              row depends only on its own candidate and its user's K/V: results are
+ *              bit-identical across chunking, batch composition and GPU count (reading R9).
+ *   flags      0, or GESR_TASA_SELF_KEY (unsupported in this version).
+ *   O          [total_C, H*d] fp32 or bf16 (o_dtype): O[t][h*d+j] = sum_i p_i V[h][r_i][j] with
+ *              p = softmax_i(scale * q_h . K[h][r_i]) over the request's L_b history rows.
+ *              L_b = 0 gives an all-zero row (reading R6).
+ *   lse        fp32 [total_C, H] natural-log log-sum-exp of the scaled scores, or NULL.
+ *              L_b = 0 gives -inf.
+ *   workspace  device scratch of at least gesr_tasa_workspace_bytes(...) bytes, 256-byte
+ *              aligned; contents need not be initialised and are clobbered.
+ *   Same alignment / D_in / H / d constraints as gesr_kv_project. */
+gesr_status gesr_tasa_score(const void* T, int64_t total_C, int32_t D_in,
+                            const int64_t* cand_offsets,
+                            const void* W_q, const float* b_q, int32_t act,
+                            const void* K_cache, const void* V_cache,
+                            const int64_t* seq_offsets, int64_t B, int64_t total_L,
+                            int32_t H, int32_t d, float scale,
+                            int32_t kv_splits, uint32_t flags,
+                            void* O, int32_t o_dtype,
+                            float* lse,
+                            void* workspace, size_t workspace_bytes,
+                            void* stream);
+
+/* gesr_hma_count -- HMA per-field match counts.
+ *   user_ids / user_offsets  int64 CSR: segment b*F+f is request b's user-side ID list of
+ *              field f; user_offsets has B*F+1 entries.
+ *   item_ids / item_offsets  int64 CSR: segment t*F+f is candidate t's item-side ID list of
+ *              field f (a single ID in the paper -- a length-1 list; reading R10);
+ *              item_offsets has total_C*F+1 entries.
+ *   cand_offsets int64 [B+1]: candidate t belongs to request b iff
+ *              cand_offsets[b] <= t < cand_offsets[b+1].
+ *   cap        <= 0: raw pairwise counts; > 0: min(count, cap)  (PAPER.md:310 cap M).
+ *   counts     int32 [total_C, F] (written): counts[t*F+f] = sum_i sum_j [u_i == t_j]
+ *              (pairwise; reading R11), IDs compared as int64 within the same field only.
+ *   Exact integer arithmetic: bit-identical to any correct implementation.
+ *   user lists of any length are supported (long lists take a slower global-memory path). */
+gesr_status gesr_hma_count(const int64_t* user_ids, const int64_t* user_offsets,
+                           const int64_t* item_ids, const int64_t* item_offsets,
+                           const int64_t* cand_offsets, int64_t B, int64_t total_C, int32_t F,
+                           int32_t cap, int32_t* counts,
+                           void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GESR_H_ */

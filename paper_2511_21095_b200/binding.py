@@ -1,0 +1,219 @@
+"""Thin ctypes binding of libgesr.so (include/gesr.h) -- argument marshalling only.
+
+Every step of the hot path runs inside the library's sm_100a kernels.  torch supplies device
+memory and the current CUDA stream; there is NO CPU fallback: calling with CPU tensors, or
+without the built library, raises.
+
+  kv_project(U, W_k, W_v, H, d, ...)      -> (K_cache, V_cache)   gesr_kv_project
+  tasa_score(T, cand_offsets, W_q, K, V, seq_offsets, H, d, ...) -> (O, lse)   gesr_tasa_score
+  hma_count(user_ids, user_offsets, item_ids, item_offsets, cand_offsets, F, cap) -> counts
+  score_step(batch)                        one full scoring step (the three calls; HMA on a
+                                           second stream joined by an event)
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+import re
+from typing import Optional
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgesr.so")
+HEADER = os.path.join(os.path.dirname(_HERE), "include", "gesr.h")
+
+GESR_OK, GESR_ERR_INVALID_ARG, GESR_ERR_UNSUPPORTED, GESR_ERR_CUDA, GESR_ERR_WORKSPACE = range(5)
+GESR_ACT_IDENTITY, GESR_ACT_SILU = 0, 1
+GESR_OUT_F32, GESR_OUT_BF16 = 0, 1
+GESR_TASA_SELF_KEY = 0x1
+
+
+class GesrError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{status_string(status)}: {msg}")
+        self.status = status
+
+
+_lib = None
+_vp = ctypes.c_void_p
+_i64 = ctypes.c_int64
+_i32 = ctypes.c_int32
+
+
+def lib():
+    """Load libgesr.so (built in-tree by `make` / __graft_entry__.build()); raise if missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise GesrError(GESR_ERR_CUDA, f"{LIB_PATH} is missing: build it with `make` "
+                        "(there is no CPU fallback)")
+    L = ctypes.CDLL(LIB_PATH)
+    L.gesr_version.restype = ctypes.c_int
+    L.gesr_status_string.restype = ctypes.c_char_p
+    L.gesr_status_string.argtypes = [ctypes.c_int]
+    L.gesr_last_error.restype = ctypes.c_char_p
+    L.gesr_kv_project.restype = ctypes.c_int
+    L.gesr_kv_project.argtypes = [_vp, _i64, _i32, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _vp, _vp,
+                                  _vp]
+    L.gesr_tasa_workspace_bytes.restype = ctypes.c_size_t
+    L.gesr_tasa_workspace_bytes.argtypes = [_i64, _i64, _i32, _i32, _i32]
+    L.gesr_tasa_score.restype = ctypes.c_int
+    L.gesr_tasa_score.argtypes = [_vp, _i64, _i32, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _i64, _i64,
+                                  _i32, _i32, ctypes.c_float, _i32, ctypes.c_uint32, _vp, _i32,
+                                  _vp, _vp, ctypes.c_size_t, _vp]
+    L.gesr_hma_count.restype = ctypes.c_int
+    L.gesr_hma_count.argtypes = [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _i32, _i32, _vp, _vp]
+    _lib = L
+    return L
+
+
+def header_symbols() -> list:
+    """Names of every function include/gesr.h declares."""
+    with open(HEADER) as fh:
+        text = fh.read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(gesr_[a-z_0-9]+)\s*\(", text)))
+
+
+def status_string(s: int) -> str:
+    return lib().gesr_status_string(int(s)).decode()
+
+
+def _check(status: int):
+    if status != GESR_OK:
+        raise GesrError(status, lib().gesr_last_error().decode())
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    if t is None:
+        return None
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream) -> ctypes.c_void_p:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+
+
+def _dev(*ts):
+    for t in ts:
+        if t is not None and not t.is_cuda:
+            raise GesrError(GESR_ERR_INVALID_ARG, "all tensors must be CUDA tensors "
+                            "(no CPU fallback)")
+        if t is not None and not t.is_contiguous():
+            raise GesrError(GESR_ERR_INVALID_ARG, "all tensors must be contiguous")
+
+
+def kv_project(U, W_k, W_v, H: int, d: int, act: int = GESR_ACT_SILU, b_k=None, b_v=None,
+               K_cache=None, V_cache=None, stream=None):
+    """K_cache, V_cache bf16 [H, total_L, d] = act(U W^T + b) (gesr_kv_project)."""
+    _dev(U, W_k, W_v, b_k, b_v, K_cache, V_cache)
+    total_L, D_in = U.shape
+    if K_cache is None:
+        K_cache = torch.empty((H, total_L, d), dtype=torch.bfloat16, device=U.device)
+    if V_cache is None:
+        V_cache = torch.empty((H, total_L, d), dtype=torch.bfloat16, device=U.device)
+    _check(lib().gesr_kv_project(_ptr(U), total_L, D_in, _ptr(W_k), _ptr(W_v), _ptr(b_k),
+                                 _ptr(b_v), H, d, act, _ptr(K_cache), _ptr(V_cache),
+                                 _stream(stream)))
+    return K_cache, V_cache
+
+
+def tasa_workspace_bytes(B: int, total_C: int, H: int, d: int, kv_splits: int = 0) -> int:
+    return int(lib().gesr_tasa_workspace_bytes(B, total_C, H, d, kv_splits))
+
+
+def tasa_score(T, cand_offsets, W_q, K_cache, V_cache, seq_offsets, H: int, d: int,
+               act: int = GESR_ACT_SILU, b_q=None, scale: float = 0.0, kv_splits: int = 0,
+               flags: int = 0, out_dtype=torch.float32, want_lse: bool = True, O=None, lse=None,
+               workspace=None, stream=None):
+    """O [total_C, H*d] (fp32|bf16), lse fp32 [total_C, H] (gesr_tasa_score)."""
+    _dev(T, cand_offsets, W_q, K_cache, V_cache, seq_offsets, b_q, O, lse, workspace)
+    total_C, D_in = T.shape
+    B = cand_offsets.numel() - 1
+    total_L = K_cache.shape[1]
+    if O is None:
+        O = torch.empty((total_C, H * d), dtype=out_dtype, device=T.device)
+    o_dtype = GESR_OUT_BF16 if O.dtype == torch.bfloat16 else GESR_OUT_F32
+    if lse is None and want_lse:
+        lse = torch.empty((total_C, H), dtype=torch.float32, device=T.device)
+    if workspace is None:
+        nbytes = tasa_workspace_bytes(B, total_C, H, d, kv_splits)
+        workspace = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=T.device)
+    _check(lib().gesr_tasa_score(_ptr(T), total_C, D_in, _ptr(cand_offsets), _ptr(W_q),
+                                 _ptr(b_q), act, _ptr(K_cache), _ptr(V_cache), _ptr(seq_offsets),
+                                 B, total_L, H, d, float(scale), kv_splits, flags, _ptr(O),
+                                 o_dtype, _ptr(lse), _ptr(workspace), workspace.numel(),
+                                 _stream(stream)))
+    return O, lse
+
+
+def hma_count(user_ids, user_offsets, item_ids, item_offsets, cand_offsets, F: int, cap: int = 0,
+              counts=None, stream=None):
+    """counts int32 [total_C, F] (gesr_hma_count)."""
+    _dev(user_ids, user_offsets, item_ids, item_offsets, cand_offsets, counts)
+    B = cand_offsets.numel() - 1
+    total_C = (item_offsets.numel() - 1) // F if F > 0 else 0
+    if counts is None:
+        counts = torch.empty((total_C, F), dtype=torch.int32, device=cand_offsets.device)
+    _check(lib().gesr_hma_count(_ptr(user_ids), _ptr(user_offsets), _ptr(item_ids),
+                                _ptr(item_offsets), _ptr(cand_offsets), B, total_C, F, cap,
+                                _ptr(counts), _stream(stream)))
+    return counts
+
+
+class StepBuffers:
+    """Preallocated outputs/workspace for repeated score_step calls on one batch shape."""
+
+    def __init__(self, batch, out_dtype=torch.float32, want_lse=False):
+        cfg = batch.cfg
+        dev = batch.cand_offsets.device
+        H, d = cfg.H, cfg.d
+        self.K = torch.empty((H, batch.total_L, d), dtype=torch.bfloat16, device=dev)
+        self.V = torch.empty((H, batch.total_L, d), dtype=torch.bfloat16, device=dev)
+        self.O = torch.empty((batch.total_C, H * d), dtype=out_dtype, device=dev)
+        self.lse = torch.empty((batch.total_C, H), dtype=torch.float32, device=dev) \
+            if want_lse else None
+        self.counts = torch.empty((batch.total_C, cfg.F), dtype=torch.int32, device=dev)
+        nbytes = tasa_workspace_bytes(batch.B, batch.total_C, H, d, 0)
+        self.workspace = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=dev)
+        self.hma_stream = torch.cuda.Stream(device=dev)
+        self.ev_fork = torch.cuda.Event()
+        self.ev_join = torch.cuda.Event()
+
+
+def score_step(batch, bufs: StepBuffers, act: int = GESR_ACT_SILU, cap: int = 0,
+               chunk: int = 0, hma: bool = True, stream=None):
+    """One scoring step: gesr_kv_project -> gesr_tasa_score (optionally in candidate chunks
+    reusing one K/V cache), with gesr_hma_count on a second stream joined by an event."""
+    cfg = batch.cfg
+    main = torch.cuda.current_stream() if stream is None else stream
+    if hma:
+        bufs.ev_fork.record(main)
+        bufs.hma_stream.wait_event(bufs.ev_fork)
+        hma_count(batch.user_ids, batch.user_offsets, batch.item_ids, batch.item_offsets,
+                  batch.cand_offsets, cfg.F, cap, counts=bufs.counts, stream=bufs.hma_stream)
+        bufs.ev_join.record(bufs.hma_stream)
+    kv_project(batch.U, batch.W_k, batch.W_v, cfg.H, cfg.d, act, K_cache=bufs.K, V_cache=bufs.V,
+               stream=main)
+    if chunk and batch.B == 1:
+        # config 4: the same user's cache reused across candidate chunks (one call per chunk)
+        for c0 in range(0, batch.total_C, chunk):
+            c1 = min(batch.total_C, c0 + chunk)
+            co = bufs.__dict__.setdefault(
+                f"_co_{c0}", torch.tensor([0, c1 - c0], dtype=torch.int64, device=batch.T.device))
+            tasa_score(batch.T[c0:c1], co, batch.W_q, bufs.K, bufs.V, batch.seq_offsets, cfg.H,
+                       cfg.d, act, O=bufs.O[c0:c1],
+                       lse=None if bufs.lse is None else bufs.lse[c0:c1],
+                       want_lse=bufs.lse is not None, workspace=bufs.workspace, stream=main)
+    else:
+        tasa_score(batch.T, batch.cand_offsets, batch.W_q, bufs.K, bufs.V, batch.seq_offsets,
+                   cfg.H, cfg.d, act, O=bufs.O, lse=bufs.lse, want_lse=bufs.lse is not None,
+                   workspace=bufs.workspace, stream=main)
+    if hma:
+        main.wait_event(bufs.ev_join)
+    return bufs.O, bufs.counts

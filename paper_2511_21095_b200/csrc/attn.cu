@@ -1,0 +1,454 @@
+// attn.cu -- K-SCHED (work list) and K-ATTN: jagged many-candidates-to-one-history attention.
+//
+// For request b, head h, candidate t: O[t, h*d:(h+1)*d] = softmax_i(scale q_t . K[h, r_i]) V[h, r_i]
+// over the L_b history rows r_i of request b only (PAPER.md:341 mask rules (1)-(2): candidates
+// never attend to one another; PAPER.md:346 T_self rows; softmax per DESIGN.md R1).
+//
+// B200 design (one CTA per work unit = (request b, head h, 256 candidates)):
+//   warp 0      TMA producer: the two 128-row Q tiles once, then K_j, V_j tiles (128 keys x d,
+//               128B swizzle) of the user's head-major cache slab through a 4-slot mbarrier ring.
+//               C candidates share one L x d K/V: the cache is read once per 256 candidates.
+//   warp 1      TMEM allocator + MMA issuer (one elected thread):
+//                 S_i = Q_i K_j^T    tcgen05.mma kind::f16 SS, M=128 N=128, fp32 in TMEM
+//                 O_i += P_i V_j     tcgen05.mma kind::f16 TS: P (bf16) read from TMEM, V MN-major
+//               interleaved so that Q tile 0's softmax overlaps Q tile 1's MMAs (ping-pong).
+//   warps 4-7   softmax for Q tile 0, warps 8-11 for Q tile 1: thread = candidate row;
+//               tcgen05.ld the 128 scores, mask keys >= L_b, online max with lazy rescale
+//               (only when the max grows by > 2^8), exp2 with log2(e) folded into the scale,
+//               running row sum in fp32, P packed to bf16 and tcgen05.st back over S.
+//               Epilogue: O / l from TMEM, fp32 or bf16 stores, natural-log lse.
+// TMEM: S0 [0,128) S1 [128,256) O0 [256,256+d) O1 [256+d, 256+2d) of 512 columns.
+// Every row's arithmetic depends only on its own q and its user's K/V (fixed 128-key tiling
+// from the user's first row), so outputs are batch-composition invariant (R9).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "kernels.h"
+#include "ptx.cuh"
+
+namespace gesr {
+
+namespace {
+
+constexpr int kThreads = 384;
+constexpr int kBlockKeys = 128;
+
+template <int D>
+struct AttnCfg {
+  static constexpr int kBoxCols = D >= 64 ? 64 : 32;              // elements per swizzle row
+  static constexpr uint32_t kLayout = D >= 64 ? kSwizzle128B : kSwizzle64B;
+  static constexpr int kColBlocks = D / kBoxCols;                 // 2 for d=128, else 1
+  static constexpr uint32_t kRowBytes = kBoxCols * 2;             // 128 or 64
+  static constexpr uint32_t kBoxBytes = 128 * kRowBytes;          // one 128-row box
+  static constexpr uint32_t kTileBytes = kColBlocks * kBoxBytes;  // 128 rows x D bf16
+  static constexpr uint32_t kSBO = 8 * kRowBytes;                 // 8-row core-matrix group
+  static constexpr int kStages = 4;
+  static constexpr uint32_t kQOff = 0;
+  static constexpr uint32_t kKVOff = 2 * kTileBytes;
+  static constexpr uint32_t kBarOff = kKVOff + kStages * kTileBytes;
+  static constexpr uint32_t kSmemBytes = kBarOff + 256 + 1024;
+};
+
+// K-major operand (Q or K tile) descriptor for the 16-element K step `ks`.
+template <int D>
+__device__ __forceinline__ uint64_t kmajor_desc(uint32_t base, int ks) {
+  using C = AttnCfg<D>;
+  const int e = ks * 16;
+  const uint32_t addr = base + (e / C::kBoxCols) * C::kBoxBytes + (e % C::kBoxCols) * 2;
+  return make_sdesc(addr, 16, C::kSBO, C::kLayout);
+}
+
+// MN-major V tile descriptor for the 16-key K step `ks` (N = d spans kColBlocks atoms).
+template <int D>
+__device__ __forceinline__ uint64_t v_desc(uint32_t base, int ks) {
+  using C = AttnCfg<D>;
+  return make_sdesc(base + ks * 16 * C::kRowBytes, C::kBoxBytes, C::kSBO, C::kLayout);
+}
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
+                const __grid_constant__ CUtensorMap map_v, const AttnParams p) {
+  using C = AttnCfg<D>;
+  const int u = blockIdx.x;
+  if (u >= __ldg(p.unit_count)) return;   // uniform for the whole CTA
+  const int h = blockIdx.y;
+  const int2 unit = p.units[u];
+  const int b = unit.x;
+  const int64_t s0 = p.seq_offsets[b];
+  const int L = static_cast<int>(p.seq_offsets[b + 1] - s0);
+  const int64_t cbeg = p.cand_offsets[b] + static_cast<int64_t>(unit.y) * kUnitRows;
+  const int64_t crem = p.cand_offsets[b + 1] - cbeg;
+  const int rows_valid = crem < kUnitRows ? static_cast<int>(crem) : kUnitRows;
+  const int nq = rows_valid > 128 ? 2 : 1;
+  const int nkv = (L + kBlockKeys - 1) / kBlockKeys;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* q_full = reinterpret_cast<uint64_t*>(smem + C::kBarOff);
+  uint64_t* kv_full = q_full + 1;
+  uint64_t* kv_empty = kv_full + C::kStages;
+  uint64_t* s_full = kv_empty + C::kStages;   // [2]
+  uint64_t* p_full = s_full + 2;              // [2]
+  uint64_t* o_done = p_full + 2;              // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&map_q);
+    tma_prefetch_desc(&map_k);
+    tma_prefetch_desc(&map_v);
+    mbar_init(q_full, 1);
+    for (int s = 0; s < C::kStages; ++s) {
+      mbar_init(&kv_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&p_full[i], 128);
+      mbar_init(&o_done[i], 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    tmem_alloc(tmem_slot, 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  const uint32_t sQ = smem_u32(smem + C::kQOff);
+  const uint32_t sKV = smem_u32(smem + C::kKVOff);
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (nkv > 0 && elect_one()) {
+      const int32_t qrow = static_cast<int32_t>(static_cast<int64_t>(h) * p.total_C + cbeg);
+      mbar_arrive_expect_tx(q_full, nq * C::kTileBytes);
+      for (int i = 0; i < nq; ++i)
+        for (int cb = 0; cb < C::kColBlocks; ++cb)
+          tma_load_2d(smem + C::kQOff + i * C::kTileBytes + cb * C::kBoxBytes, &map_q, q_full,
+                      cb * C::kBoxCols, qrow + 128 * i);
+      const int32_t krow = static_cast<int32_t>(static_cast<int64_t>(h) * p.total_L + s0);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int j = 0; j < nkv; ++j) {
+        for (int which = 0; which < 2; ++which) {
+          mbar_wait(&kv_empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&kv_full[stage], C::kTileBytes);
+          const CUtensorMap* m = which ? &map_v : &map_k;
+          for (int cb = 0; cb < C::kColBlocks; ++cb)
+            tma_load_2d(smem + C::kKVOff + stage * C::kTileBytes + cb * C::kBoxBytes, m,
+                        &kv_full[stage], cb * C::kBoxCols, krow + kBlockKeys * j);
+          if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (nkv > 0) {
+      const uint32_t idesc_s = make_idesc_bf16(128, kBlockKeys, 0, 0);
+      const uint32_t idesc_o = make_idesc_bf16(128, D, 0, 1);
+      const uint32_t tS[2] = {tmem, tmem + 128};
+      const uint32_t tO[2] = {tmem + 256, tmem + 256 + D};
+      int stage = 0;
+      uint32_t phase = 0;
+      auto issue_s = [&](int i, uint32_t kbase) {
+        const uint32_t qbase = sQ + i * C::kTileBytes;
+#pragma unroll
+        for (int ks = 0; ks < D / 16; ++ks)
+          mma_ss(tS[i], kmajor_desc<D>(qbase, ks), kmajor_desc<D>(kbase, ks), idesc_s,
+                 ks > 0 ? 1u : 0u);
+      };
+      auto issue_pv = [&](int i, uint32_t vbase, int j) {
+#pragma unroll
+        for (int ks = 0; ks < kBlockKeys / 16; ++ks)
+          mma_ts(tO[i], tS[i] + ks * 8, v_desc<D>(vbase, ks), idesc_o, (j > 0 || ks > 0) ? 1u : 0u);
+      };
+      mbar_wait(q_full, 0);
+      // prologue: S_i for key tile 0
+      int kslot = stage;
+      mbar_wait(&kv_full[kslot], phase);
+      tc_fence_after();
+      if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+      if (elect_one()) {
+        const uint32_t kb = sKV + kslot * C::kTileBytes;
+        issue_s(0, kb);
+        mma_commit(&s_full[0]);
+        if (nq == 2) {
+          issue_s(1, kb);
+          mma_commit(&s_full[1]);
+        }
+        mma_commit(&kv_empty[kslot]);
+      }
+      __syncwarp();
+      for (int j = 0; j < nkv; ++j) {
+        const int vslot = stage;
+        mbar_wait(&kv_full[vslot], phase);
+        if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+        const bool has_next = j + 1 < nkv;
+        if (has_next) {
+          kslot = stage;
+          mbar_wait(&kv_full[kslot], phase);
+          if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+        }
+        const uint32_t vb = sKV + vslot * C::kTileBytes;
+        const uint32_t kb = sKV + kslot * C::kTileBytes;
+        // Q tile 0: O0 += P0 V_j, then S0 for the next key tile
+        mbar_wait(&p_full[0], j & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          issue_pv(0, vb, j);
+          mma_commit(&o_done[0]);
+          if (has_next) {
+            issue_s(0, kb);
+            mma_commit(&s_full[0]);
+          }
+        }
+        __syncwarp();
+        if (nq == 2) {
+          mbar_wait(&p_full[1], j & 1);
+          tc_fence_after();
+          if (elect_one()) {
+            issue_pv(1, vb, j);
+            mma_commit(&o_done[1]);
+            if (has_next) {
+              issue_s(1, kb);
+              mma_commit(&s_full[1]);
+            }
+          }
+          __syncwarp();
+        }
+        if (elect_one()) {
+          mma_commit(&kv_empty[vslot]);
+          if (has_next) mma_commit(&kv_empty[kslot]);
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ softmax + epilogue
+    const int i = (warp - 4) >> 2;           // Q tile of this warpgroup
+    const uint32_t sub = warp & 3;           // TMEM lane quarter
+    const int row_in_unit = i * 128 + sub * 32 + lane;
+    if (i < nq) {
+      const uint32_t lane_addr = (sub * 32) << 16;
+      const uint32_t tS = tmem + lane_addr + i * 128;
+      const uint32_t tO = tmem + lane_addr + 256 + i * D;
+      const float sl2 = p.scale_log2;
+      float m_run = -INFINITY;
+      float l = 0.f;
+      for (int j = 0; j < nkv; ++j) {
+        mbar_wait(&s_full[i], j & 1);
+        tc_fence_after();
+        uint32_t r[128];
+        tmem_ld32(tS, r);
+        tmem_ld32(tS + 32, r + 32);
+        tmem_ld32(tS + 64, r + 64);
+        tmem_ld32(tS + 96, r + 96);
+        tmem_ld_wait();
+        const int valid = L - kBlockKeys * j;
+        float mt = -INFINITY;
+#pragma unroll
+        for (int k = 0; k < 128; ++k) {
+          const float x = k < valid ? __uint_as_float(r[k]) * sl2 : -INFINITY;
+          r[k] = __float_as_uint(x);
+          mt = fmaxf(mt, x);
+        }
+        if (j == 0) {
+          m_run = mt;
+        } else {
+          const bool need = mt > m_run + 8.0f;
+          if (__any_sync(0xffffffffu, need)) {
+            // O_i must hold P_{j-1} V_{j-1} before it is rescaled
+            mbar_wait(&o_done[i], (j - 1) & 1);
+            tc_fence_after();
+            float alpha = 1.f;
+            if (need) {
+              alpha = ex2(m_run - mt);
+              m_run = mt;
+              l *= alpha;
+            }
+#pragma unroll 1
+            for (int c = 0; c < D / 32; ++c) {
+              uint32_t o[32];
+              tmem_ld32(tO + c * 32, o);
+              tmem_ld_wait();
+#pragma unroll
+              for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+              tmem_st32(tO + c * 32, o);
+            }
+            tmem_st_wait();
+          }
+        }
+        float rs = 0.f;
+        uint32_t pk[64];
+#pragma unroll
+        for (int k = 0; k < 64; ++k) {
+          const float p0 = ex2(__uint_as_float(r[2 * k]) - m_run);
+          const float p1 = ex2(__uint_as_float(r[2 * k + 1]) - m_run);
+          rs += p0 + p1;
+          pk[k] = pack_bf16x2(p0, p1);
+        }
+        l += rs;
+        tmem_st32(tS, pk);
+        tmem_st32(tS + 32, pk + 32);
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&p_full[i]);
+      }
+      // epilogue
+      const bool row_ok = row_in_unit < rows_valid;
+      const int64_t row = cbeg + row_in_unit;
+      const int64_t HD = static_cast<int64_t>(p.H) * D;
+      if (nkv > 0) {
+        mbar_wait(&o_done[i], (nkv - 1) & 1);
+        tc_fence_after();
+      }
+      const float inv_l = nkv > 0 ? 1.0f / l : 0.f;
+#pragma unroll 1
+      for (int c = 0; c < D / 32; ++c) {
+        uint32_t o[32];
+        if (nkv > 0) {
+          tmem_ld32(tO + c * 32, o);
+          tmem_ld_wait();
+        } else {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) o[e] = 0u;
+        }
+        if (row_ok) {
+          if (p.o_bf16) {
+            uint32_t pk2[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e)
+              pk2[e] = pack_bf16x2(__uint_as_float(o[2 * e]) * inv_l, __uint_as_float(o[2 * e + 1]) * inv_l);
+            uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.O) + row * HD +
+                                                  static_cast<int64_t>(h) * D + c * 32);
+#pragma unroll
+            for (int v = 0; v < 4; ++v)
+              dst[v] = make_uint4(pk2[4 * v], pk2[4 * v + 1], pk2[4 * v + 2], pk2[4 * v + 3]);
+          } else {
+            float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.O) + row * HD +
+                                                    static_cast<int64_t>(h) * D + c * 32);
+#pragma unroll
+            for (int v = 0; v < 8; ++v)
+              dst[v] = make_float4(__uint_as_float(o[4 * v]) * inv_l, __uint_as_float(o[4 * v + 1]) * inv_l,
+                                   __uint_as_float(o[4 * v + 2]) * inv_l, __uint_as_float(o[4 * v + 3]) * inv_l);
+          }
+        }
+      }
+      if (row_ok && p.lse != nullptr) {
+        // m_run and log2(l) are in log2 units of the scaled score
+        p.lse[row * p.H + h] = nkv > 0 ? (m_run + __log2f(l)) * 0.69314718055994530942f : -INFINITY;
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+__global__ void build_units_kernel(const int64_t* __restrict__ cand_offsets, int64_t B,
+                                   int2* __restrict__ units, int* __restrict__ count) {
+  __shared__ int warp_sums[32];
+  __shared__ int running;
+  const int lane = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5;
+  const int nw = blockDim.x >> 5;
+  if (threadIdx.x == 0) running = 0;
+  __syncthreads();
+  for (int64_t base = 0; base < B; base += blockDim.x) {
+    const int64_t b = base + threadIdx.x;
+    int n = 0;
+    if (b < B) {
+      const int64_t c = cand_offsets[b + 1] - cand_offsets[b];
+      n = static_cast<int>((c + kUnitRows - 1) / kUnitRows);
+    }
+    int x = n;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_sums[w] = x;
+    __syncthreads();
+    if (w == 0) {
+      int v = lane < nw ? warp_sums[lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += y;
+      }
+      warp_sums[lane] = v;
+    }
+    __syncthreads();
+    const int excl = running + (x - n) + (w > 0 ? warp_sums[w - 1] : 0);
+    for (int k = 0; k < n; ++k) units[excl + k] = make_int2(static_cast<int>(b), k);
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) running = excl + n;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *count = running;
+}
+
+// total_L == 0: every candidate has an empty history -> O = 0, lse = -inf (R6)
+__global__ void attn_empty_kernel(AttnParams p, int D) {
+  const int64_t HD = static_cast<int64_t>(p.H) * D;
+  const int64_t n = p.total_C * HD;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (p.o_bf16) static_cast<__nv_bfloat16*>(p.O)[i] = __float2bfloat16(0.f);
+    else static_cast<float*>(p.O)[i] = 0.f;
+    if (p.lse != nullptr && i < p.total_C * p.H) p.lse[i] = -INFINITY;
+  }
+}
+
+template <int D>
+cudaError_t launch_d(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
+                     const AttnParams& p, int64_t max_units, cudaStream_t stream) {
+  using C = AttnCfg<D>;
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(attn_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         C::kSmemBytes);
+    if (e != cudaSuccess) return e;
+    attr_done = true;
+  }
+  dim3 grid(static_cast<unsigned>(max_units), static_cast<unsigned>(p.H));
+  attn_kernel<D><<<grid, kThreads, C::kSmemBytes, stream>>>(mq, mk, mv, p);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_build_units(const int64_t* cand_offsets, int64_t B, int2* units, int* count,
+                               cudaStream_t stream) {
+  build_units_kernel<<<1, 1024, 0, stream>>>(cand_offsets, B, units, count);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_attn(int d, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
+                        const AttnParams& p, int64_t max_units, cudaStream_t stream) {
+  switch (d) {
+    case 32: return launch_d<32>(mq, mk, mv, p, max_units, stream);
+    case 64: return launch_d<64>(mq, mk, mv, p, max_units, stream);
+    case 128: return launch_d<128>(mq, mk, mv, p, max_units, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_attn_empty(const AttnParams& p, int d, cudaStream_t stream) {
+  attn_empty_kernel<<<1184, 256, 0, stream>>>(p, d);
+  return cudaGetLastError();
+}
+
+}  // namespace gesr

@@ -1,0 +1,291 @@
+// capi.cpp -- the C ABI of libgesr.so (include/gesr.h): argument validation, TMA tensor-map
+// encoding (cuTensorMapEncodeTiled through cudaGetDriverEntryPoint, so no -lcuda), workspace
+// carving, and kernel launches on the caller's stream.  No host synchronisation, no device
+// allocation, no copies.
+#include "../../include/gesr.h"
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "kernels.h"
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+gesr_status fail(gesr_status s, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return s;
+}
+
+gesr_status cuda_fail(cudaError_t e, const char* where) {
+  return fail(GESR_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+int num_sms() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  static int cache[64] = {0};
+  if (dev >= 0 && dev < 64 && cache[dev] > 0) return cache[dev];
+  int n = 148;
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  if (dev >= 0 && dev < 64) cache[dev] = n;
+  return n;
+}
+
+// 2D bf16 tensor map over a row-major [rows, cols] array with box [box_rows, box_cols].
+gesr_status make_map_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
+                        uint32_t box_rows, uint32_t box_cols, CUtensorMapSwizzle swz,
+                        const char* what) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return fail(GESR_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(GESR_ERR_CUDA, "cuTensorMapEncodeTiled(%s) failed: %d", what, static_cast<int>(r));
+  return GESR_OK;
+}
+
+bool valid_d(int32_t d) { return d == 32 || d == 64 || d == 128; }
+
+gesr_status check_common(int32_t D_in, int32_t H, int32_t d, int32_t act) {
+  if (D_in < 8 || D_in > 16384 || (D_in % 8) != 0)
+    return fail(GESR_ERR_INVALID_ARG, "D_in=%d must be a multiple of 8 in [8, 16384]", D_in);
+  if (H < 1 || H > 4096) return fail(GESR_ERR_INVALID_ARG, "H=%d must be in [1, 4096]", H);
+  if (!valid_d(d)) return fail(GESR_ERR_INVALID_ARG, "d=%d must be 32, 64 or 128", d);
+  if (act != GESR_ACT_IDENTITY && act != GESR_ACT_SILU)
+    return fail(GESR_ERR_INVALID_ARG, "act=%d is not a gesr_act", act);
+  return GESR_OK;
+}
+
+// Workspace layout for gesr_tasa_score: [0,256) header {int unit_count}; [256, ...) units;
+// then (1024-aligned) Q [H, total_C, d] bf16.
+int64_t max_units(int64_t B, int64_t total_C) {
+  return B + (total_C + gesr::kUnitRows - 1) / gesr::kUnitRows;
+}
+size_t units_end(int64_t B, int64_t total_C) {
+  size_t e = 256 + static_cast<size_t>(max_units(B, total_C)) * sizeof(int2);
+  return (e + 1023) & ~static_cast<size_t>(1023);
+}
+
+// Projection launch shared by K/V and Q: X [M, K] -> out0/out1 [H, M, d] head-major.
+gesr_status run_projection(const void* X, int64_t M, int32_t K, const void* W0, const void* W1,
+                           const float* b0, const float* b1, int32_t H, int32_t d, int32_t act,
+                           void* out0, void* out1, cudaStream_t stream) {
+  const int HD = H * d;
+  const int bn = gesr::proj_pick_bn(HD);
+  CUtensorMap ma, mb0, mb1;
+  gesr_status s = make_map_2d(&ma, X, static_cast<uint64_t>(M), static_cast<uint64_t>(K), 128, 64,
+                              CU_TENSOR_MAP_SWIZZLE_128B, "X");
+  if (s != GESR_OK) return s;
+  s = make_map_2d(&mb0, W0, HD, K, bn, 64, CU_TENSOR_MAP_SWIZZLE_128B, "W0");
+  if (s != GESR_OK) return s;
+  s = make_map_2d(&mb1, W1 ? W1 : W0, HD, K, bn, 64, CU_TENSOR_MAP_SWIZZLE_128B, "W1");
+  if (s != GESR_OK) return s;
+  gesr::ProjParams p{};
+  p.M = M;
+  p.K = K;
+  p.n_split = HD;
+  p.d = d;
+  p.act = act;
+  p.num_m_blocks = static_cast<int>((M + 127) / 128);
+  p.num_n_blocks = (W1 ? 2 * HD : HD) / bn;
+  p.bias0 = b0;
+  p.bias1 = b1;
+  p.out0 = static_cast<__nv_bfloat16*>(out0);
+  p.out1 = static_cast<__nv_bfloat16*>(out1);
+  cudaError_t e = gesr::launch_proj(ma, mb0, mb1, p, bn, num_sms(), stream);
+  if (e != cudaSuccess) return cuda_fail(e, "proj_kernel launch");
+  return GESR_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int gesr_version(void) { return 100; }
+
+const char* gesr_status_string(int s) {
+  switch (s) {
+    case GESR_OK: return "GESR_OK";
+    case GESR_ERR_INVALID_ARG: return "GESR_ERR_INVALID_ARG";
+    case GESR_ERR_UNSUPPORTED: return "GESR_ERR_UNSUPPORTED";
+    case GESR_ERR_CUDA: return "GESR_ERR_CUDA";
+    case GESR_ERR_WORKSPACE: return "GESR_ERR_WORKSPACE";
+    default: return "GESR_ERR_UNKNOWN";
+  }
+}
+
+const char* gesr_last_error(void) { return g_err; }
+
+gesr_status gesr_kv_project(const void* U, int64_t total_L, int32_t D_in, const void* W_k,
+                            const void* W_v, const float* b_k, const float* b_v, int32_t H,
+                            int32_t d, int32_t act, void* K_cache, void* V_cache, void* stream) {
+  gesr_status s = check_common(D_in, H, d, act);
+  if (s != GESR_OK) return s;
+  if (total_L < 0) return fail(GESR_ERR_INVALID_ARG, "total_L=%lld < 0", (long long)total_L);
+  if (total_L >= (int64_t(1) << 31) / H)
+    return fail(GESR_ERR_INVALID_ARG, "H*total_L exceeds the 2^31 TMA coordinate range");
+  if (total_L == 0) return GESR_OK;
+  if (!U || !W_k || !W_v || !K_cache || !V_cache)
+    return fail(GESR_ERR_INVALID_ARG, "null required pointer");
+  if (!aligned16(U) || !aligned16(W_k) || !aligned16(W_v) || !aligned16(K_cache) ||
+      !aligned16(V_cache) || !aligned16(b_k) || !aligned16(b_v))
+    return fail(GESR_ERR_INVALID_ARG, "pointers must be 16-byte aligned");
+  return run_projection(U, total_L, D_in, W_k, W_v, b_k, b_v, H, d, act, K_cache, V_cache,
+                        static_cast<cudaStream_t>(stream));
+}
+
+size_t gesr_tasa_workspace_bytes(int64_t B, int64_t total_C, int32_t H, int32_t d,
+                                 int32_t kv_splits) {
+  (void)kv_splits;
+  if (B < 0 || total_C < 0 || H < 1 || !valid_d(d)) return 0;
+  return units_end(B, total_C) + static_cast<size_t>(total_C) * H * d * 2;
+}
+
+gesr_status gesr_tasa_score(const void* T, int64_t total_C, int32_t D_in,
+                            const int64_t* cand_offsets, const void* W_q, const float* b_q,
+                            int32_t act, const void* K_cache, const void* V_cache,
+                            const int64_t* seq_offsets, int64_t B, int64_t total_L, int32_t H,
+                            int32_t d, float scale, int32_t kv_splits, uint32_t flags, void* O,
+                            int32_t o_dtype, float* lse, void* workspace,
+                            size_t workspace_bytes, void* stream) {
+  gesr_status s = check_common(D_in, H, d, act);
+  if (s != GESR_OK) return s;
+  if (B < 0 || total_C < 0 || total_L < 0)
+    return fail(GESR_ERR_INVALID_ARG, "B, total_C, total_L must be >= 0");
+  if (B > (int64_t(1) << 31) - 1) return fail(GESR_ERR_INVALID_ARG, "B too large");
+  if (total_C >= (int64_t(1) << 31) / H || total_L >= (int64_t(1) << 31) / H)
+    return fail(GESR_ERR_INVALID_ARG, "H*total rows exceed the 2^31 TMA coordinate range");
+  if (o_dtype != GESR_OUT_F32 && o_dtype != GESR_OUT_BF16)
+    return fail(GESR_ERR_INVALID_ARG, "o_dtype=%d is not a gesr_out_dtype", o_dtype);
+  if (kv_splits < 0) return fail(GESR_ERR_INVALID_ARG, "kv_splits=%d < 0", kv_splits);
+  if (kv_splits > 1) return fail(GESR_ERR_UNSUPPORTED, "kv_splits > 1 not supported in this version");
+  if (flags & GESR_TASA_SELF_KEY)
+    return fail(GESR_ERR_UNSUPPORTED, "GESR_TASA_SELF_KEY not supported in this version");
+  if (flags & ~GESR_TASA_SELF_KEY) return fail(GESR_ERR_INVALID_ARG, "unknown flags 0x%x", flags);
+  if (total_C == 0 || B == 0) return GESR_OK;
+  if (!T || !cand_offsets || !W_q || !seq_offsets || !O || !workspace)
+    return fail(GESR_ERR_INVALID_ARG, "null required pointer");
+  if (total_L > 0 && (!K_cache || !V_cache))
+    return fail(GESR_ERR_INVALID_ARG, "null K/V cache with total_L > 0");
+  if (!aligned16(T) || !aligned16(W_q) || !aligned16(K_cache) || !aligned16(V_cache) ||
+      !aligned16(O) || !aligned16(b_q) || !aligned16(lse) ||
+      (reinterpret_cast<uintptr_t>(workspace) & 255u) != 0 ||
+      (reinterpret_cast<uintptr_t>(cand_offsets) & 7u) != 0 ||
+      (reinterpret_cast<uintptr_t>(seq_offsets) & 7u) != 0)
+    return fail(GESR_ERR_INVALID_ARG, "misaligned pointer");
+  const size_t need = gesr_tasa_workspace_bytes(B, total_C, H, d, kv_splits);
+  if (workspace_bytes < need)
+    return fail(GESR_ERR_WORKSPACE, "workspace %zu bytes < required %zu", workspace_bytes, need);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+
+  gesr::AttnParams p{};
+  p.seq_offsets = seq_offsets;
+  p.cand_offsets = cand_offsets;
+  p.total_C = total_C;
+  p.total_L = total_L;
+  p.H = H;
+  const float sc = scale > 0.f ? scale : 1.0f / std::sqrt(static_cast<float>(d));
+  p.scale_log2 = sc * 1.4426950408889634f;
+  p.O = O;
+  p.o_bf16 = o_dtype == GESR_OUT_BF16;
+  p.lse = lse;
+  if (total_L == 0) {
+    cudaError_t e = gesr::launch_attn_empty(p, d, st);
+    return e == cudaSuccess ? GESR_OK : cuda_fail(e, "attn_empty launch");
+  }
+
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  int* count = reinterpret_cast<int*>(ws);
+  int2* units = reinterpret_cast<int2*>(ws + 256);
+  void* Q = ws + units_end(B, total_C);
+  p.units = units;
+  p.unit_count = count;
+
+  cudaError_t e = gesr::launch_build_units(cand_offsets, B, units, count, st);
+  if (e != cudaSuccess) return cuda_fail(e, "build_units launch");
+  s = run_projection(T, total_C, D_in, W_q, nullptr, b_q, nullptr, H, d, act, Q, nullptr, st);
+  if (s != GESR_OK) return s;
+
+  CUtensorMap mq, mk, mv;
+  const uint32_t box_cols = d >= 64 ? 64 : 32;
+  const CUtensorMapSwizzle swz = d >= 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
+  s = make_map_2d(&mq, Q, static_cast<uint64_t>(H) * total_C, d, 128, box_cols, swz, "Q");
+  if (s != GESR_OK) return s;
+  s = make_map_2d(&mk, K_cache, static_cast<uint64_t>(H) * total_L, d, 128, box_cols, swz, "K");
+  if (s != GESR_OK) return s;
+  s = make_map_2d(&mv, V_cache, static_cast<uint64_t>(H) * total_L, d, 128, box_cols, swz, "V");
+  if (s != GESR_OK) return s;
+  e = gesr::launch_attn(d, mq, mk, mv, p, max_units(B, total_C), st);
+  if (e != cudaSuccess) return cuda_fail(e, "attn_kernel launch");
+  return GESR_OK;
+}
+
+gesr_status gesr_hma_count(const int64_t* user_ids, const int64_t* user_offsets,
+                           const int64_t* item_ids, const int64_t* item_offsets,
+                           const int64_t* cand_offsets, int64_t B, int64_t total_C, int32_t F,
+                           int32_t cap, int32_t* counts, void* stream) {
+  if (B < 0 || total_C < 0 || F < 0)
+    return fail(GESR_ERR_INVALID_ARG, "B, total_C, F must be >= 0");
+  if (F > 256) return fail(GESR_ERR_INVALID_ARG, "F=%d > 256 fields", F);
+  if (B > 2147483647LL) return fail(GESR_ERR_INVALID_ARG, "B too large");
+  if (B == 0 || total_C == 0 || F == 0) return GESR_OK;
+  if (!user_offsets || !item_offsets || !cand_offsets || !counts)
+    return fail(GESR_ERR_INVALID_ARG, "null required pointer");
+  if (((reinterpret_cast<uintptr_t>(user_ids) | reinterpret_cast<uintptr_t>(user_offsets) |
+        reinterpret_cast<uintptr_t>(item_ids) | reinterpret_cast<uintptr_t>(item_offsets) |
+        reinterpret_cast<uintptr_t>(cand_offsets)) & 7u) != 0 ||
+      (reinterpret_cast<uintptr_t>(counts) & 3u) != 0)
+    return fail(GESR_ERR_INVALID_ARG, "misaligned pointer");
+  gesr::HmaParams p{};
+  p.user_ids = user_ids;
+  p.user_offsets = user_offsets;
+  p.item_ids = item_ids;
+  p.item_offsets = item_offsets;
+  p.cand_offsets = cand_offsets;
+  p.B = B;
+  p.total_C = total_C;
+  p.F = F;
+  p.cap = cap;
+  p.counts = counts;
+  cudaError_t e = gesr::launch_hma(p, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? GESR_OK : cuda_fail(e, "hma_kernel launch");
+}
+
+}  // extern "C"

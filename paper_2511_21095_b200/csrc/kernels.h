@@ -1,0 +1,72 @@
+// kernels.h -- internal launch interface between capi.cpp (validation, tensor maps) and the
+// sm_100a kernels.  Not part of the public ABI (include/gesr.h).
+#pragma once
+
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+namespace gesr {
+
+// ---------------------------------------------------------------- K-PROJ (proj.cu)
+struct ProjParams {
+  int64_t M;          // rows of X
+  int K;              // D_in
+  int n_split;        // columns < n_split come from W0 (out0), the rest from W1 (out1)
+  int d;              // head dim
+  int act;            // 0 identity, 1 SiLU
+  int num_m_blocks;
+  int num_n_blocks;
+  const float* bias0;
+  const float* bias1;
+  __nv_bfloat16* out0;   // [H, M, d]
+  __nv_bfloat16* out1;   // [H, M, d] or null
+};
+
+int proj_pick_bn(int n_split);
+cudaError_t launch_proj(const CUtensorMap& map_a, const CUtensorMap& map_b0,
+                        const CUtensorMap& map_b1, const ProjParams& p, int bn, int num_sms,
+                        cudaStream_t stream);
+
+// ---------------------------------------------------------------- K-SCHED + K-ATTN (attn.cu)
+struct AttnParams {
+  const int64_t* seq_offsets;
+  const int64_t* cand_offsets;
+  const int2* units;       // (b, pair index) work list
+  const int* unit_count;
+  int64_t total_C;
+  int64_t total_L;
+  int H;
+  float scale_log2;        // scale * log2(e)
+  void* O;                 // [total_C, H*d]
+  int o_bf16;
+  float* lse;              // [total_C, H] or null
+};
+
+constexpr int kUnitRows = 256;   // candidates per work unit (two 128-row Q tiles)
+
+cudaError_t launch_build_units(const int64_t* cand_offsets, int64_t B, int2* units, int* count,
+                               cudaStream_t stream);
+cudaError_t launch_attn(int d, const CUtensorMap& map_q, const CUtensorMap& map_k,
+                        const CUtensorMap& map_v, const AttnParams& p, int64_t max_units,
+                        cudaStream_t stream);
+cudaError_t launch_attn_empty(const AttnParams& p, int d, cudaStream_t stream);
+
+// ---------------------------------------------------------------- K-HMA (hma.cu)
+struct HmaParams {
+  const int64_t* user_ids;
+  const int64_t* user_offsets;
+  const int64_t* item_ids;
+  const int64_t* item_offsets;
+  const int64_t* cand_offsets;
+  int64_t B;
+  int64_t total_C;
+  int F;
+  int cap;
+  int32_t* counts;
+};
+
+cudaError_t launch_hma(const HmaParams& p, cudaStream_t stream);
+
+}  // namespace gesr

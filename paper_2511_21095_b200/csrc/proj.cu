@@ -1,0 +1,238 @@
+// proj.cu -- K-PROJ: Y = act(X W^T + b) with a head-major scatter epilogue.
+//
+// Serves gesr_kv_project (X = U [total_L, D_in], W = [W_k; W_v] as two TMA maps stacked along N,
+// outputs K_cache / V_cache [H, total_L, d]) and the Q projection inside gesr_tasa_score
+// (X = T, W = W_q, output Q [H, total_C, d] in the workspace).  PAPER.md:335-341 (s3.4.2):
+// the [U,T] self-attention layer's projections; projection form act(XW^T+b) per DESIGN.md R3.
+//
+// B200 design: persistent CTAs (grid <= #SMs), warp-specialised:
+//   warp 0   TMA producer: A tile 128x64 and B tile BNx64 (bf16, 128B swizzle) per K block,
+//            through a STAGES-deep mbarrier ring.
+//   warp 1   MMA issuer: one elected thread issues tcgen05.mma.cta_group::1.kind::f16
+//            (M=128, N=BN, K=16) into a double-buffered TMEM accumulator.
+//   warp 2   TMEM allocator (2*BN columns).
+//   warps 4-7 epilogue: tcgen05.ld 32x32b (thread = output row), bias + act in fp32, RNE to
+//            bf16, 16-byte stores into the head-major cache (each 32-column chunk is one
+//            contiguous 64-byte run of one head's row).
+// The epilogue of tile i overlaps the MMAs of tile i+1 (two accumulator buffers).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "kernels.h"
+#include "ptx.cuh"
+
+namespace gesr {
+
+namespace {
+
+constexpr int kBM = 128;
+constexpr int kBK = 64;              // 64 bf16 = 128 bytes = one 128B-swizzle row
+constexpr int kThreads = 256;
+constexpr uint32_t kABytes = kBM * kBK * 2;   // 16 KB
+
+template <int BN>
+struct ProjSmem {
+  static constexpr uint32_t kBBytes = BN * kBK * 2;
+  static constexpr uint32_t kStageBytes = kABytes + kBBytes;
+  static constexpr int kStages = (200 * 1024) / kStageBytes > 8 ? 8 : (200 * 1024) / kStageBytes;
+  static constexpr uint32_t kTmemCols = (2 * BN) < 32 ? 32 : 2 * BN;
+  static constexpr uint32_t kBarOffset = kStages * kStageBytes;
+  static constexpr uint32_t kBytes = kBarOffset + 256 + 1024;  // + barriers + alignment slack
+};
+
+__device__ __forceinline__ float apply_act(int act, float x) {
+  if (act == 1) return __fdividef(x, 1.0f + __expf(-x));
+  return x;
+}
+
+template <int BN>
+__global__ void __launch_bounds__(kThreads, 1)
+    proj_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b0,
+                const __grid_constant__ CUtensorMap map_b1, const ProjParams p) {
+  using S = ProjSmem<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + S::kBarOffset);
+  uint64_t* empty_bar = full_bar + S::kStages;
+  uint64_t* tfull_bar = empty_bar + S::kStages;     // [2]
+  uint64_t* tempty_bar = tfull_bar + 2;             // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+  const int num_tiles = p.num_m_blocks * p.num_n_blocks;
+  const int num_kb = (p.K + kBK - 1) / kBK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&map_a);
+    tma_prefetch_desc(&map_b0);
+    tma_prefetch_desc(&map_b1);
+    for (int s = 0; s < S::kStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull_bar[b], 1);
+      mbar_init(&tempty_bar[b], 128);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) {
+    tmem_alloc(tmem_slot, S::kTmemCols);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      // ---------------- TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int m_blk = tile / p.num_n_blocks;
+        const int n_blk = tile % p.num_n_blocks;
+        const int n0 = n_blk * BN;
+        // B comes from map_b0 for columns < n_split, else map_b1 (W_k / W_v stacked along N)
+        const CUtensorMap* mb = (n0 < p.n_split) ? &map_b0 : &map_b1;
+        const int nb = (n0 < p.n_split) ? n0 : n0 - p.n_split;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * S::kStageBytes;
+          uint8_t* sb = sa + kABytes;
+          mbar_arrive_expect_tx(&full_bar[stage], S::kStageBytes);
+          tma_load_2d(sa, &map_a, &full_bar[stage], kb * kBK, m_blk * kBM);
+          tma_load_2d(sb, mb, &full_bar[stage], kb * kBK, nb);
+          if (++stage == S::kStages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer
+    const uint32_t idesc = make_idesc_bf16(kBM, BN, 0, 0);
+    int stage = 0;
+    uint32_t phase = 0;
+    int local = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
+      const uint32_t buf = local & 1;
+      const uint32_t aphase = (local >> 1) & 1;
+      mbar_wait(&tempty_bar[buf], aphase ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + buf * BN;
+      for (int kb = 0; kb < num_kb; ++kb) {
+        mbar_wait(&full_bar[stage], phase);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t sa = smem_u32(smem + stage * S::kStageBytes);
+          const uint32_t sb = sa + kABytes;
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k) {
+            const uint64_t ad = make_sdesc(sa + k * 32, 16, 1024, kSwizzle128B);
+            const uint64_t bd = make_sdesc(sb + k * 32, 16, 1024, kSwizzle128B);
+            mma_ss(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+          }
+          mma_commit(&empty_bar[stage]);
+          if (kb == num_kb - 1) mma_commit(&tfull_bar[buf]);
+        }
+        __syncwarp();
+        if (++stage == S::kStages) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue: TMEM -> regs -> act -> bf16 -> head-major global
+    const uint32_t sub = warp & 3;            // TMEM lane quarter
+    int local = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
+      const int m_blk = tile / p.num_n_blocks;
+      const int n_blk = tile % p.num_n_blocks;
+      const uint32_t buf = local & 1;
+      const uint32_t aphase = (local >> 1) & 1;
+      mbar_wait(&tfull_bar[buf], aphase);
+      tc_fence_after();
+      const int64_t row = static_cast<int64_t>(m_blk) * kBM + sub * 32 + lane;
+      const bool row_ok = row < p.M;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld32(tmem_base + ((sub * 32) << 16) + buf * BN + c * 32, r);
+        tmem_ld_wait();
+        const int n0 = n_blk * BN + c * 32;   // 32-column chunk lies within one head (d >= 32)
+        const int which = n0 >= p.n_split ? 1 : 0;
+        const int within = n0 - which * p.n_split;
+        const int h = within / p.d;
+        const int j0 = within - h * p.d;
+        const float* bias = which ? p.bias1 : p.bias0;
+        uint32_t packed[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          float x0 = __uint_as_float(r[2 * i]);
+          float x1 = __uint_as_float(r[2 * i + 1]);
+          if (bias != nullptr) {
+            x0 += __ldg(bias + within + 2 * i);
+            x1 += __ldg(bias + within + 2 * i + 1);
+          }
+          packed[i] = pack_bf16x2(apply_act(p.act, x0), apply_act(p.act, x1));
+        }
+        if (row_ok) {
+          __nv_bfloat16* out = which ? p.out1 : p.out0;
+          uint4* dst = reinterpret_cast<uint4*>(out + (static_cast<int64_t>(h) * p.M + row) * p.d + j0);
+#pragma unroll
+          for (int v = 0; v < 4; ++v)
+            dst[v] = make_uint4(packed[4 * v], packed[4 * v + 1], packed[4 * v + 2], packed[4 * v + 3]);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty_bar[buf]);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, S::kTmemCols);
+  }
+}
+
+template <int BN>
+cudaError_t launch_bn(const CUtensorMap& ma, const CUtensorMap& mb0, const CUtensorMap& mb1,
+                      const ProjParams& p, int num_sms, cudaStream_t stream) {
+  using S = ProjSmem<BN>;
+  static bool attr_done = false;  // same arch on every device of the box
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(proj_kernel<BN>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, S::kBytes);
+    if (e != cudaSuccess) return e;
+    attr_done = true;
+  }
+  const int tiles = p.num_m_blocks * p.num_n_blocks;
+  const int grid = tiles < num_sms ? tiles : num_sms;
+  proj_kernel<BN><<<grid, kThreads, S::kBytes, stream>>>(ma, mb0, mb1, p);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+int proj_pick_bn(int N) {
+  if (N % 256 == 0) return 256;
+  if (N % 128 == 0) return 128;
+  if (N % 64 == 0) return 64;
+  return 32;
+}
+
+cudaError_t launch_proj(const CUtensorMap& map_a, const CUtensorMap& map_b0,
+                        const CUtensorMap& map_b1, const ProjParams& p, int bn, int num_sms,
+                        cudaStream_t stream) {
+  switch (bn) {
+    case 256: return launch_bn<256>(map_a, map_b0, map_b1, p, num_sms, stream);
+    case 128: return launch_bn<128>(map_a, map_b0, map_b1, p, num_sms, stream);
+    case 64: return launch_bn<64>(map_a, map_b0, map_b1, p, num_sms, stream);
+    case 32: return launch_bn<32>(map_a, map_b0, map_b1, p, num_sms, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace gesr

@@ -1,0 +1,123 @@
+"""CPU tests of the C-ABI boundary: the library loads, exports every symbol include/gesr.h
+declares, and host-checkable argument errors are rejected before any launch (no GPU needed:
+these paths return before touching CUDA)."""
+import ctypes
+import os
+import subprocess
+
+import pytest
+
+from paper_2511_21095_b200 import binding as gb
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def L():
+    if not os.path.exists(gb.LIB_PATH):
+        subprocess.check_call(["make", "-C", ROOT, "-j4"])
+    return gb.lib()
+
+
+def test_exports_every_header_symbol(L):
+    syms = gb.header_symbols()
+    assert set(syms) >= {"gesr_kv_project", "gesr_tasa_score", "gesr_hma_count",
+                         "gesr_tasa_workspace_bytes", "gesr_status_string", "gesr_last_error",
+                         "gesr_version"}
+    out = subprocess.check_output(["nm", "-D", "--defined-only", gb.LIB_PATH], text=True)
+    exported = {line.split()[-1] for line in out.splitlines() if line.strip()}
+    for s in syms:
+        assert s in exported, s
+        assert hasattr(L, s)
+    # nothing but the ABI is exported (the static CUDA runtime is kept local)
+    assert all(s.startswith("gesr_") for s in exported if not s.startswith("_"))
+
+
+def test_library_is_sm100a(L):
+    out = subprocess.check_output(["cuobjdump", "--list-elf", gb.LIB_PATH], text=True)
+    assert "sm_100a" in out
+    sass = subprocess.check_output(["cuobjdump", "-sass", gb.LIB_PATH], text=True)
+    assert "UTCHMMA" in sass and "UTMALDG" in sass and "LDTM" in sass   # tcgen05 + TMA + TMEM
+
+
+def test_status_strings(L):
+    assert gb.status_string(0) == "GESR_OK"
+    assert gb.status_string(1) == "GESR_ERR_INVALID_ARG"
+    assert gb.status_string(2) == "GESR_ERR_UNSUPPORTED"
+    assert gb.status_string(3) == "GESR_ERR_CUDA"
+    assert gb.status_string(4) == "GESR_ERR_WORKSPACE"
+    assert L.gesr_version() >= 100
+
+
+P = ctypes.c_void_p
+FAKE = P(0x10000)          # 16-byte aligned, never dereferenced on the error paths
+MIS = P(0x10008)           # misaligned
+
+
+def kv(L, U=FAKE, total_L=10, D_in=64, Wk=FAKE, Wv=FAKE, bk=None, bv=None, H=2, d=64, act=1,
+       K=FAKE, V=FAKE):
+    return L.gesr_kv_project(U, total_L, D_in, Wk, Wv, bk, bv, H, d, act, K, V, None)
+
+
+def test_kv_project_validation(L):
+    assert kv(L, d=48) == gb.GESR_ERR_INVALID_ARG
+    assert "d=48" in L.gesr_last_error().decode()
+    assert kv(L, D_in=20) == gb.GESR_ERR_INVALID_ARG
+    assert kv(L, H=0) == gb.GESR_ERR_INVALID_ARG
+    assert kv(L, act=7) == gb.GESR_ERR_INVALID_ARG
+    assert kv(L, total_L=-1) == gb.GESR_ERR_INVALID_ARG
+    assert kv(L, U=None) == gb.GESR_ERR_INVALID_ARG
+    assert kv(L, K=MIS) == gb.GESR_ERR_INVALID_ARG
+    assert kv(L, total_L=0, U=None) == gb.GESR_OK     # empty problem: valid no-op
+
+
+def tasa(L, T=FAKE, total_C=10, D_in=64, co=FAKE, Wq=FAKE, bq=None, act=1, K=FAKE, V=FAKE,
+         so=FAKE, B=2, total_L=10, H=2, d=64, scale=0.0, splits=0, flags=0, O=FAKE, odt=0,
+         lse=None, ws=FAKE, wsb=1 << 30):
+    return L.gesr_tasa_score(T, total_C, D_in, co, Wq, bq, act, K, V, so, B, total_L, H, d,
+                             scale, splits, flags, O, odt, lse, ws, wsb, None)
+
+
+def test_tasa_validation(L):
+    assert tasa(L, d=96) == gb.GESR_ERR_INVALID_ARG
+    assert tasa(L, odt=5) == gb.GESR_ERR_INVALID_ARG
+    assert tasa(L, B=-1) == gb.GESR_ERR_INVALID_ARG
+    assert tasa(L, flags=gb.GESR_TASA_SELF_KEY) == gb.GESR_ERR_UNSUPPORTED
+    assert tasa(L, flags=0x8) == gb.GESR_ERR_INVALID_ARG
+    assert tasa(L, splits=4) == gb.GESR_ERR_UNSUPPORTED
+    assert tasa(L, splits=-1) == gb.GESR_ERR_INVALID_ARG
+    assert tasa(L, T=None) == gb.GESR_ERR_INVALID_ARG
+    assert tasa(L, O=MIS) == gb.GESR_ERR_INVALID_ARG
+    assert tasa(L, ws=P(0x10010)) == gb.GESR_ERR_INVALID_ARG   # workspace must be 256-aligned
+    assert tasa(L, wsb=16) == gb.GESR_ERR_WORKSPACE
+    assert tasa(L, total_C=0, T=None) == gb.GESR_OK
+    assert tasa(L, B=0) == gb.GESR_OK
+
+
+def test_workspace_size(L):
+    n = gb.tasa_workspace_bytes(1024, 1024000, 4, 128)
+    # units list + Q [H, total_C, d] bf16
+    assert n >= 1024000 * 4 * 128 * 2 and n < 1024000 * 4 * 128 * 2 + (1 << 20)
+    assert gb.tasa_workspace_bytes(-1, 10, 4, 128) == 0
+    assert gb.tasa_workspace_bytes(1, 10, 4, 100) == 0
+
+
+def hma(L, ui=FAKE, uo=FAKE, ii=FAKE, io=FAKE, co=FAKE, B=2, C=5, F=3, cap=0, counts=FAKE):
+    return L.gesr_hma_count(ui, uo, ii, io, co, B, C, F, cap, counts, None)
+
+
+def test_hma_validation(L):
+    assert hma(L, F=-1) == gb.GESR_ERR_INVALID_ARG
+    assert hma(L, F=300) == gb.GESR_ERR_INVALID_ARG
+    assert hma(L, uo=None) == gb.GESR_ERR_INVALID_ARG
+    assert hma(L, ii=P(0x10004)) == gb.GESR_ERR_INVALID_ARG
+    assert hma(L, counts=P(0x10002)) == gb.GESR_ERR_INVALID_ARG
+    assert hma(L, F=0) == gb.GESR_OK
+    assert hma(L, C=0) == gb.GESR_OK
+
+
+def test_binding_rejects_cpu_tensors(L):
+    import torch
+    U = torch.zeros(4, 64, dtype=torch.bfloat16)
+    with pytest.raises(gb.GesrError):
+        gb.kv_project(U, U, U, 1, 64)

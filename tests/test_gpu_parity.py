@@ -1,0 +1,350 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the fp64 oracle on the same seeded inputs.
+
+Gates (BASELINE.json north_star): HMA counts and jagged indexing bit-exact; attention within
+max-abs 2e-2 and mean-abs 2e-3 of the pure fp64 oracle; K/V cache within one bf16 ulp plus the
+fp32-accumulation term 2^-20 * sum_k |U_k W_k| (DESIGN.md s3 R8).
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2511_21095_b200 import binding as gb
+from paper_2511_21095_b200 import configs, inputs
+
+pytestmark = pytest.mark.gpu
+
+MAX_ABS, MEAN_ABS = 2e-2, 2e-3
+
+
+def _cuda():
+    assert torch.cuda.is_available(), "GPU tests need a B200 (run through gpurun)"
+    return torch.device("cuda:0")
+
+
+def _bf16_ulp(x: np.ndarray) -> np.ndarray:
+    ax = np.maximum(np.abs(x), 2.0 ** -126)
+    return 2.0 ** (np.floor(np.log2(ax)) - 7)
+
+
+def _check_kv(U, W, K_gpu, K_or, H, d):
+    Uf = U.double()
+    acc = (Uf.abs() @ W.double().abs().T).reshape(-1, H, d).permute(1, 0, 2).numpy()
+    got = K_gpu.float().cpu().double().numpy()
+    err = np.abs(got - K_or)
+    tol = _bf16_ulp(K_or) + 2.0 ** -20 * acc + 1e-30
+    bad = err > tol
+    assert not bad.any(), f"{bad.sum()} K/V elements out of tolerance; max err {err.max()}"
+
+
+def _attn_tol(O_gpu, O_or, what=""):
+    diff = np.abs(O_gpu.astype(np.float64) - O_or)
+    assert np.isfinite(O_gpu).all(), f"{what}: non-finite output"
+    mx, mn = diff.max() if diff.size else 0.0, diff.mean() if diff.size else 0.0
+    assert mx <= MAX_ABS and mn <= MEAN_ABS, f"{what}: max-abs {mx:.3e} mean-abs {mn:.3e}"
+    return mx, mn
+
+
+def _run_oracle_attn(bt, act=1):
+    cfg = bt.cfg
+    K, V = oracle.kv_project(bt.U, bt.W_k, bt.W_v, cfg.H, cfg.d, act=act)
+    O, lse = oracle.tasa_score(bt.T, bt.cand_offsets, bt.W_q, K, V, bt.seq_offsets, cfg.H,
+                               cfg.d, act=act)
+    return K, V, O, lse
+
+
+def _run_gpu_attn(bt, act=1, out_dtype=torch.float32):
+    cfg = bt.cfg
+    g = bt.to(_cuda())
+    K, V = gb.kv_project(g.U, g.W_k, g.W_v, cfg.H, cfg.d, act)
+    O, lse = gb.tasa_score(g.T, g.cand_offsets, g.W_q, K, V, g.seq_offsets, cfg.H, cfg.d, act,
+                           out_dtype=out_dtype)
+    torch.cuda.synchronize()
+    return K.cpu(), V.cpu(), O.float().cpu().numpy(), lse.cpu().numpy()
+
+
+def _custom(Ls, Cs, H=2, d=64, D_in=128, cfg_id=77):
+    cfg = configs.Config("custom", cfg_id, B=len(Ls), L=("fixed", 1), C=("fixed", 1), H=H, d=d,
+                         D_in=D_in, F=4)
+    bt = inputs.make_batch(cfg, hma=False)
+    # overwrite lengths: regenerate rows for the requested jagged shape
+    so = torch.tensor(np.concatenate([[0], np.cumsum(Ls)]), dtype=torch.int64)
+    co = torch.tensor(np.concatenate([[0], np.cumsum(Cs)]), dtype=torch.int64)
+    g = torch.Generator().manual_seed(cfg_id * 1000 + len(Ls))
+    U = torch.randn(int(so[-1]), D_in, generator=g).to(torch.bfloat16)
+    T = torch.randn(int(co[-1]), D_in, generator=g).to(torch.bfloat16)
+    return inputs.Batch(cfg, torch.arange(len(Ls)), so, co, U, T, bt.W_q, bt.W_k, bt.W_v,
+                        None, None, None, None)
+
+
+# ----------------------------------------------------------------------------- K/V projection
+
+@pytest.mark.parametrize("name", ["1", "2"])
+@pytest.mark.parametrize("act", [0, 1])
+def test_kv_project_parity(name, act):
+    cfg = configs.get(name)
+    bt = inputs.make_batch(cfg, hma=False)
+    K_or, V_or = oracle.kv_project(bt.U, bt.W_k, bt.W_v, cfg.H, cfg.d, act=act)
+    g = bt.to(_cuda())
+    K, V = gb.kv_project(g.U, g.W_k, g.W_v, cfg.H, cfg.d, act)
+    torch.cuda.synchronize()
+    _check_kv(bt.U, bt.W_k, K.cpu(), K_or, cfg.H, cfg.d)
+    _check_kv(bt.U, bt.W_v, V.cpu(), V_or, cfg.H, cfg.d)
+
+
+@pytest.mark.parametrize("M,D_in,H,d", [(300, 512, 4, 128), (129, 64, 1, 32), (1, 40, 2, 64),
+                                         (1000, 256, 3, 64)])
+def test_kv_project_shapes(M, D_in, H, d):
+    cfg = configs.Config("kvshape", 90, B=1, L=("fixed", M), C=("fixed", 1), H=H, d=d, D_in=D_in,
+                         F=1)
+    bt = inputs.make_batch(cfg, hma=False)
+    K_or, V_or = oracle.kv_project(bt.U, bt.W_k, bt.W_v, H, d, act=1)
+    g = bt.to(_cuda())
+    K, V = gb.kv_project(g.U, g.W_k, g.W_v, H, d, 1)
+    torch.cuda.synchronize()
+    _check_kv(bt.U, bt.W_k, K.cpu(), K_or, H, d)
+    _check_kv(bt.U, bt.W_v, V.cpu(), V_or, H, d)
+
+
+def test_kv_project_bias():
+    cfg = configs.get("2").with_(B=3)
+    bt = inputs.make_batch(cfg, hma=False)
+    HD = cfg.H * cfg.d
+    bk = torch.linspace(-1, 1, HD, dtype=torch.float32)
+    bv = torch.linspace(2, -2, HD, dtype=torch.float32)
+    K_or, V_or = oracle.kv_project(bt.U, bt.W_k, bt.W_v, cfg.H, cfg.d, 1, b_k=bk.double(),
+                                   b_v=bv.double())
+    g = bt.to(_cuda())
+    K, V = gb.kv_project(g.U, g.W_k, g.W_v, cfg.H, cfg.d, 1, b_k=bk.cuda(), b_v=bv.cuda())
+    torch.cuda.synchronize()
+    # the bias adds |b| to the accumulation scale
+    _check_kv(bt.U, bt.W_k, K.cpu(), K_or, cfg.H, cfg.d)
+    _check_kv(bt.U, bt.W_v, V.cpu(), V_or, cfg.H, cfg.d)
+
+
+# ----------------------------------------------------------------------------- attention
+
+@pytest.mark.parametrize("name", ["1", "2"])
+def test_tasa_parity_configs(name):
+    cfg = configs.get(name)
+    bt = inputs.make_batch(cfg, hma=False)
+    _, _, O_or, lse_or = _run_oracle_attn(bt)
+    _, _, O, lse = _run_gpu_attn(bt)
+    _attn_tol(O, O_or, f"config {name}")
+    fin = np.isfinite(lse_or)
+    assert np.array_equal(fin, np.isfinite(lse))
+    assert np.abs(lse[fin] - lse_or[fin]).max() < 2e-2
+
+
+@pytest.mark.parametrize("d,H,D_in", [(128, 2, 256), (64, 2, 128), (32, 3, 96)])
+def test_tasa_ragged_edges(d, H, D_in):
+    # L in {0, 1, 127, 128, 129, 300}, C in {0, 1, 128, 129, 256, 257, 300}: empty, single,
+    # exact-tile and ragged tails on both axes
+    Ls = [0, 1, 127, 128, 129, 300, 5, 260]
+    Cs = [3, 1, 128, 129, 256, 257, 0, 300]
+    bt = _custom(Ls, Cs, H=H, d=d, D_in=D_in, cfg_id=d)
+    _, _, O_or, lse_or = _run_oracle_attn(bt)
+    _, _, O, lse = _run_gpu_attn(bt)
+    _attn_tol(O, O_or, "ragged")
+    # L_b = 0 rows are exactly zero with lse = -inf (reading R6)
+    assert np.all(O[:3] == 0) and np.all(np.isneginf(lse[:3]))
+
+
+def test_tasa_bf16_output():
+    bt = _custom([200, 50], [130, 7], H=2, d=128, D_in=128, cfg_id=5)
+    _, _, O_or, _ = _run_oracle_attn(bt)
+    _, _, O, _ = _run_gpu_attn(bt, out_dtype=torch.bfloat16)
+    _attn_tol(O, O_or, "bf16 out")
+
+
+def test_single_token_history_returns_cached_v_exactly():
+    bt = _custom([1, 1, 1], [5, 130, 2], H=2, d=64, D_in=128, cfg_id=11)
+    K, V, O, _ = _run_gpu_attn(bt)
+    Vf = V.float().numpy()
+    co = bt.cand_offsets.numpy()
+    for b in range(3):
+        for h in range(2):
+            want = Vf[h, b]
+            got = O[co[b]:co[b + 1], h * 64:(h + 1) * 64]
+            assert np.array_equal(got, np.broadcast_to(want, got.shape))
+
+
+def test_uniform_scores_mean_pooling():
+    bt = _custom([300, 7], [10, 140], H=2, d=64, D_in=128, cfg_id=12)
+    bt.W_q.zero_()
+    K, V, O, _ = _run_gpu_attn(bt)
+    # closed form on the GPU's own bf16 cache: O = mean of V rows (within fp32/bf16-P rounding)
+    Vf = V.double().numpy()
+    so, co = bt.seq_offsets.numpy(), bt.cand_offsets.numpy()
+    for b in range(2):
+        mean = Vf[:, so[b]:so[b + 1]].mean(axis=1).reshape(-1)     # [H*d] in head order
+        got = O[co[b]:co[b + 1]]
+        assert np.abs(got - mean).max() < 1e-5
+
+
+def test_request_boundary_canary():
+    """K = 0, V = +1 for even b and 1000 for odd b: any key leaked from a neighbour request
+    (or head) shifts O by >= 999/(L_b+1)."""
+    dev = _cuda()
+    Ls = [130, 1, 257, 128, 3, 700]
+    Cs = [260, 2, 1, 129, 300, 5]
+    H, d, D_in = 2, 128, 128
+    so = torch.tensor(np.concatenate([[0], np.cumsum(Ls)]), dtype=torch.int64, device=dev)
+    co = torch.tensor(np.concatenate([[0], np.cumsum(Cs)]), dtype=torch.int64, device=dev)
+    tl, tc = int(so[-1]), int(co[-1])
+    K = torch.zeros((H, tl, d), dtype=torch.bfloat16, device=dev)
+    V = torch.empty((H, tl, d), dtype=torch.bfloat16, device=dev)
+    for b in range(len(Ls)):
+        for h in range(H):
+            V[h, so[b]:so[b + 1]] = (1.0 if b % 2 == 0 else 1000.0) + 10 * h
+    T = torch.randn(tc, D_in, device=dev).to(torch.bfloat16)
+    Wq = (torch.randn(H * d, D_in, device=dev) * 0.05).to(torch.bfloat16)
+    O, _ = gb.tasa_score(T, co, Wq, K, V, so, H, d)
+    torch.cuda.synchronize()
+    O = O.cpu().numpy()
+    coc = co.cpu().numpy()
+    for b in range(len(Ls)):
+        for h in range(H):
+            want = (1.0 if b % 2 == 0 else 1000.0) + 10 * h
+            got = O[coc[b]:coc[b + 1], h * d:(h + 1) * d]
+            assert np.abs(got - want).max() <= 1e-2 * max(1.0, want / 100), (b, h)
+
+
+def test_output_canary_tail_untouched():
+    bt = _custom([100, 200], [3, 130], H=2, d=64, D_in=64, cfg_id=13)
+    g = bt.to(_cuda())
+    K, V = gb.kv_project(g.U, g.W_k, g.W_v, 2, 64, 1)
+    big = torch.full((bt.total_C + 37, 128), 12345.0, device="cuda")
+    lse_big = torch.full((bt.total_C + 37, 2), 777.0, device="cuda")
+    gb.tasa_score(g.T, g.cand_offsets, g.W_q, K, V, g.seq_offsets, 2, 64, O=big[:bt.total_C],
+                  lse=lse_big[:bt.total_C])
+    torch.cuda.synchronize()
+    assert torch.all(big[bt.total_C:] == 12345.0) and torch.all(lse_big[bt.total_C:] == 777.0)
+    assert not torch.any(big[:bt.total_C] == 12345.0)
+
+
+def test_chunk_invariance_and_determinism_exact():
+    """Config 4 style: one cache, candidates scored in chunks of 512 vs one call: bit-exact."""
+    cfg = configs.get("4").with_(L=("fixed", 1000), C=("fixed", 1100))
+    bt = inputs.make_batch(cfg, hma=False)
+    g = bt.to(_cuda())
+    K, V = gb.kv_project(g.U, g.W_k, g.W_v, cfg.H, cfg.d, 1)
+    O1, l1 = gb.tasa_score(g.T, g.cand_offsets, g.W_q, K, V, g.seq_offsets, cfg.H, cfg.d, kv_splits=1)
+    parts = []
+    for c0 in range(0, 1100, 512):
+        c1 = min(1100, c0 + 512)
+        co = torch.tensor([0, c1 - c0], dtype=torch.int64, device="cuda")
+        parts.append(gb.tasa_score(g.T[c0:c1].contiguous(), co, g.W_q, K, V, g.seq_offsets,
+                                   cfg.H, cfg.d, kv_splits=1)[0])
+    O2 = torch.cat(parts)
+    O3, l3 = gb.tasa_score(g.T, g.cand_offsets, g.W_q, K, V, g.seq_offsets, cfg.H, cfg.d, kv_splits=1)
+    torch.cuda.synchronize()
+    assert torch.equal(O1, O2)
+    assert torch.equal(O1, O3) and torch.equal(l1, l3)
+
+
+def test_batch_composition_invariance_exact():
+    """A request's rows are bit-identical whether scored alone or inside a batch (R9)."""
+    cfg = configs.get("2").with_(B=12)
+    full = inputs.make_batch(cfg, hma=False)
+    _, _, O_full, _ = _run_gpu_attn(full)
+    sub = [3, 7, 8]
+    part = inputs.make_batch(cfg, requests=sub, hma=False)
+    _, _, O_part, _ = _run_gpu_attn(part)
+    co = full.cand_offsets.numpy()
+    rows = np.concatenate([np.arange(co[b], co[b + 1]) for b in sub])
+    assert np.array_equal(O_full[rows], O_part)
+
+
+def test_large_scores_no_overflow():
+    bt = _custom([300, 129], [140, 20], H=2, d=64, D_in=128, cfg_id=14)
+    g = bt.to(_cuda())
+    K, V = gb.kv_project(g.U, g.W_k, g.W_v, 2, 64, 1)
+    O, lse = gb.tasa_score(g.T, g.cand_offsets, g.W_q * 40, K * 40, V, g.seq_offsets, 2, 64)
+    torch.cuda.synchronize()
+    assert torch.isfinite(O).all() and torch.isfinite(lse).all()
+    Vmax = V.float().abs().max()
+    assert O.abs().max() <= Vmax * 1.01
+
+
+# ----------------------------------------------------------------------------- HMA
+
+def _hma_gpu(bt, F, cap=0):
+    g = bt.to(_cuda())
+    c = gb.hma_count(g.user_ids, g.user_offsets, g.item_ids, g.item_offsets, g.cand_offsets, F,
+                     cap)
+    torch.cuda.synchronize()
+    return c.cpu().numpy()
+
+
+@pytest.mark.parametrize("name", ["1", "2"])
+@pytest.mark.parametrize("cap", [0, 16])
+def test_hma_bit_exact_configs(name, cap):
+    cfg = configs.get(name)
+    bt = inputs.make_batch(cfg, attention=False)
+    want = oracle.hma_count(bt.user_ids, bt.user_offsets, bt.item_ids, bt.item_offsets,
+                            bt.cand_offsets, cfg.F, cap=cap)
+    assert np.array_equal(_hma_gpu(bt, cfg.F, cap), want)
+
+
+def test_hma_duplicates_and_long_lists():
+    # duplicates (pairwise reading R11), user lists longer than the smem pool (global fallback)
+    cfg = configs.get("2").with_(B=9, user_len=(0, 3000), vocab=4096, F=3)
+    bt = inputs.make_batch(cfg, attention=False, hma_duplicates=True)
+    for cap in (0, 5):
+        want = oracle.hma_count(bt.user_ids, bt.user_offsets, bt.item_ids, bt.item_offsets,
+                                bt.cand_offsets, cfg.F, cap=cap)
+        assert np.array_equal(_hma_gpu(bt, cfg.F, cap), want)
+
+
+def test_hma_edge_ids_and_empty():
+    dev = _cuda()
+    F = 2
+    # request 0: 3 candidates; request 1: 0 candidates; request 2: 2 candidates
+    co = torch.tensor([0, 3, 3, 5], dtype=torch.int64)
+    imin, imax = -(1 << 63), (1 << 63) - 1
+    users = [[imin, imin, 5], [], [], [imax, 0], [7], [7, 7, 7]]
+    items = [[imin], [5, 5], [], [imax], [1, 2, 3], [imin, 0], [], [7, 7], [imin], [9]]
+    uo = np.concatenate([[0], np.cumsum([len(x) for x in users])])
+    io = np.concatenate([[0], np.cumsum([len(x) for x in items])])
+    ui = np.array([v for x in users for v in x], np.int64)
+    ii = np.array([v for x in items for v in x], np.int64)
+    want = oracle.hma_count(ui, uo, ii, io, co, F)
+    c = gb.hma_count(torch.tensor(ui, device=dev), torch.tensor(uo, device=dev),
+                     torch.tensor(ii, device=dev), torch.tensor(io, device=dev), co.to(dev), F)
+    torch.cuda.synchronize()
+    assert np.array_equal(c.cpu().numpy(), want)
+    assert want[0, 0] == 2   # sentinel-valued ID counted
+
+
+def test_hma_headline_subset():
+    cfg = configs.get("3h")
+    sub = list(range(0, 1024, 97))
+    bt = inputs.make_batch(cfg, requests=sub, attention=False)
+    want = oracle.hma_count(bt.user_ids, bt.user_offsets, bt.item_ids, bt.item_offsets,
+                            bt.cand_offsets, cfg.F)
+    assert np.array_equal(_hma_gpu(bt, cfg.F), want)
+
+
+# ----------------------------------------------------------------------------- full size, sampled
+
+def test_headline_full_size_sampled():
+    """Config 3h (L=2048, C=1000, B=1024) run in full on the GPU exactly as bench.py launches
+    it; sampled requests checked against the oracle (attention tolerance, HMA bit-exact)."""
+    dev = _cuda()
+    cfg = configs.get("3h")
+    bt = inputs.make_batch(cfg, device=dev)
+    bufs = gb.StepBuffers(bt, want_lse=True)
+    O, counts = gb.score_step(bt, bufs)
+    torch.cuda.synchronize()
+    sample = [0, 1, 511, 1023]
+    sub = inputs.make_batch(cfg, requests=sample)
+    _, _, O_or, _ = _run_oracle_attn(sub)
+    co = bt.cand_offsets.cpu().numpy()
+    rows = np.concatenate([np.arange(co[b], co[b + 1]) for b in sample])
+    _attn_tol(O[torch.as_tensor(rows, device=dev)].cpu().numpy(), O_or, "3h sampled")
+    want = oracle.hma_count(sub.user_ids, sub.user_offsets, sub.item_ids, sub.item_offsets,
+                            sub.cand_offsets, cfg.F)
+    assert np.array_equal(counts[torch.as_tensor(rows, device=dev)].cpu().numpy(), want)
