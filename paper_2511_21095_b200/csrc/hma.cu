@@ -151,10 +151,10 @@ __global__ void __launch_bounds__(kThreads)
     for (int64_t g = seg_begin + static_cast<int64_t>(warp) * 32; g < seg_end;
          g += static_cast<int64_t>(kWarps) * 32) {
       const int nseg = (seg_end - g) < 32 ? static_cast<int>(seg_end - g) : 32;
-      // lane k holds the start offset of segment g+k; lane nseg..31 hold the end offset
+      // lane k holds the start offset of segment g+k; lanes nseg..31 hold the end offset
       const int64_t my_off = p.item_offsets[g + (lane < nseg ? lane : nseg)];
       const int64_t start = __shfl_sync(0xffffffffu, my_off, 0);
-      const int64_t end = __shfl_sync(0xffffffffu, my_off, 31);
+      const int64_t end = p.item_offsets[g + nseg];   // same address for all lanes: broadcast
       for (int64_t base = start; base < end; base += 32) {
         const int64_t pos = base + lane;
         const bool ok = pos < end;
