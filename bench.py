@@ -347,7 +347,7 @@ def main():
         import oracle
         threads = oracle.default_threads()
         tot, c, n = 0.0, 0, 0
-        while tot < 10.0 and n < 8:
+        while tot < 12.0 and n < 64:
             dt, cc = _cpu_sample(cfg, [n], threads)
             tot += dt
             c += cc

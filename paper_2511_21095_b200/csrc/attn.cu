@@ -65,6 +65,19 @@ __device__ __forceinline__ uint64_t v_desc(uint32_t base, int ks) {
   return make_sdesc(base + ks * 16 * C::kRowBytes, C::kBoxBytes, C::kSBO, C::kLayout);
 }
 
+// 2^x on the FMA/ALU pipes: round-to-nearest split x = j + f (f in [-0.5, 0.5]) with the
+// 1.5*2^23 magic-number add, degree-3 polynomial for 2^f (max rel. error 2.1e-4, well below
+// the bf16 rounding of P), exponent added in the integer domain.  Valid for x >= -126.
+__device__ __forceinline__ float exp2_poly(float x) {
+  x = fmaxf(x, -126.0f);
+  const float t = x + 12582912.0f;           // 1.5 * 2^23: low mantissa bits hold round(x)
+  const float f = x - (t - 12582912.0f);
+  float p = fmaf(0.054848f, f, 0.24180661f);
+  p = fmaf(p, f, 0.6932482f);
+  p = fmaf(p, f, 0.99998866f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
@@ -253,13 +266,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld32(tS + 96, r + 96);
         tmem_ld_wait();
         const int valid = L - kBlockKeys * j;
-        float mt = -INFINITY;
+        // row max of the raw scores (scale > 0 commutes with max); 8 independent chains
+        float mx[8];
 #pragma unroll
-        for (int k = 0; k < 128; ++k) {
-          const float x = k < valid ? __uint_as_float(r[k]) * sl2 : -INFINITY;
-          r[k] = __float_as_uint(x);
-          mt = fmaxf(mt, x);
+        for (int e = 0; e < 8; ++e) mx[e] = -INFINITY;
+        if (valid >= 128) {
+#pragma unroll
+          for (int k = 0; k < 128; ++k) mx[k & 7] = fmaxf(mx[k & 7], __uint_as_float(r[k]));
+        } else {
+#pragma unroll
+          for (int k = 0; k < 128; ++k) {
+            if (k >= valid) r[k] = __float_as_uint(-INFINITY);   // keys beyond L_b
+            mx[k & 7] = fmaxf(mx[k & 7], __uint_as_float(r[k]));
+          }
         }
+        const float mt = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                               fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) * sl2;
         if (j == 0) {
           m_run = mt;
         } else {
@@ -286,15 +308,32 @@ __global__ void __launch_bounds__(kThreads, 1)
             tmem_st_wait();
           }
         }
-        float rs = 0.f;
+        // p = 2^(s*scale*log2e - m): one FFMA + exp2.  On full tiles one element in four takes
+        // a degree-3 polynomial exp2 on the FMA pipe (FA4-style MUFU offload); masked tiles
+        // use MUFU only so masked keys are exactly 0.
+        const float neg_m = -m_run;
+        float rsum[4] = {0.f, 0.f, 0.f, 0.f};
         uint32_t pk[64];
+        if (valid >= 128) {
 #pragma unroll
-        for (int k = 0; k < 64; ++k) {
-          const float p0 = ex2(__uint_as_float(r[2 * k]) - m_run);
-          const float p1 = ex2(__uint_as_float(r[2 * k + 1]) - m_run);
-          rs += p0 + p1;
-          pk[k] = pack_bf16x2(p0, p1);
+          for (int k = 0; k < 64; ++k) {
+            const float x0 = fmaf(__uint_as_float(r[2 * k]), sl2, neg_m);
+            const float x1 = fmaf(__uint_as_float(r[2 * k + 1]), sl2, neg_m);
+            const float p0 = ex2(x0);
+            const float p1 = (k & 1) ? exp2_poly(x1) : ex2(x1);
+            rsum[k & 3] += p0 + p1;
+            pk[k] = pack_bf16x2(p0, p1);
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < 64; ++k) {
+            const float p0 = ex2(fmaf(__uint_as_float(r[2 * k]), sl2, neg_m));
+            const float p1 = ex2(fmaf(__uint_as_float(r[2 * k + 1]), sl2, neg_m));
+            rsum[k & 3] += p0 + p1;
+            pk[k] = pack_bf16x2(p0, p1);
+          }
         }
+        const float rs = (rsum[0] + rsum[1]) + (rsum[2] + rsum[3]);
         l += rs;
         tmem_st32(tS, pk);
         tmem_st32(tS + 32, pk + 32);

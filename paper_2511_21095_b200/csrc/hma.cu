@@ -152,23 +152,27 @@ __global__ void __launch_bounds__(kThreads)
          g += static_cast<int64_t>(kWarps) * 32) {
       const int nseg = (seg_end - g) < 32 ? static_cast<int>(seg_end - g) : 32;
       // lane k holds the start offset of segment g+k; lanes nseg..31 hold the end offset
-      const int64_t my_off = p.item_offsets[g + (lane < nseg ? lane : nseg)];
-      const int64_t start = __shfl_sync(0xffffffffu, my_off, 0);
+      const int64_t my_off64 = p.item_offsets[g + (lane < nseg ? lane : nseg)];
+      const int64_t start = __shfl_sync(0xffffffffu, my_off64, 0);
       const int64_t end = p.item_offsets[g + nseg];   // same address for all lanes: broadcast
-      for (int64_t base = start; base < end; base += 32) {
-        const int64_t pos = base + lane;
-        const bool ok = pos < end;
-        const unsigned long long key =
-            ok ? static_cast<unsigned long long>(__ldg(p.item_ids + pos)) : 0ull;
+      // 32-bit relative offsets and field index for the shuffle search (seg_begin % F == 0)
+      const int my_off = static_cast<int>(my_off64 - start);
+      const int my_f = static_cast<int>(g - seg_begin + lane) % F;
+      const int n_ids = static_cast<int>(end - start);
+      const int64_t* ids = p.item_ids + start;
+      for (int base = 0; base < n_ids; base += 32) {
+        const int pos = base + lane;
+        const bool ok = pos < n_ids;
+        const unsigned long long key = ok ? static_cast<unsigned long long>(__ldg(ids + pos)) : 0ull;
         // owning segment: largest k with off[k] <= pos (offsets nondecreasing)
         int k = 0;
 #pragma unroll
         for (int step = 16; step >= 1; step >>= 1) {
-          const int64_t o = __shfl_sync(0xffffffffu, my_off, k + step);
+          const int o = __shfl_sync(0xffffffffu, my_off, k + step);
           if (o <= pos) k += step;
         }
+        const int f = __shfl_sync(0xffffffffu, my_f, k);
         if (ok) {
-          const int f = static_cast<int>((g + k) % F);
           const int c = lookup(s, p, f, key);
           if (c != 0) atomicAdd(&s.warp_cnt[warp][k], c);
         }

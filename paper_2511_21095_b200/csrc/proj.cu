@@ -27,7 +27,7 @@ namespace {
 
 constexpr int kBM = 128;
 constexpr int kBK = 64;              // 64 bf16 = 128 bytes = one 128B-swizzle row
-constexpr int kThreads = 256;
+constexpr int kThreads = 384;          // 4 control warps + 8 epilogue warps
 constexpr uint32_t kABytes = kBM * kBK * 2;   // 16 KB
 
 template <int BN>
@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull_bar[b], 1);
-      mbar_init(&tempty_bar[b], 128);
+      mbar_init(&tempty_bar[b], 256);
     }
     fence_mbar_init();
   }
@@ -143,7 +143,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 4) {
     // ---------------- epilogue: TMEM -> regs -> act -> bf16 -> head-major global
-    const uint32_t sub = warp & 3;            // TMEM lane quarter
+    // 8 warps: warp w reads TMEM lane quarter (w & 3); warps 4-7 take the first half of the
+    // tile's 32-column chunks and warps 8-11 the second half (2 warps per SM sub-partition).
+    const uint32_t sub = warp & 3;
+    const int half = (warp - 4) >> 2;
+    constexpr int kChunks = BN / 32;
+    constexpr int kPerHalf = kChunks >= 2 ? kChunks / 2 : 1;
+    const int c_begin = kChunks >= 2 ? half * kPerHalf : 0;
+    const int c_end = kChunks >= 2 ? c_begin + kPerHalf : (half == 0 ? 1 : 0);
     int local = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
       const int m_blk = tile / p.num_n_blocks;
@@ -155,7 +162,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int64_t row = static_cast<int64_t>(m_blk) * kBM + sub * 32 + lane;
       const bool row_ok = row < p.M;
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = c_begin; c < c_end; ++c) {
         uint32_t r[32];
         tmem_ld32(tmem_base + ((sub * 32) << 16) + buf * BN + c * 32, r);
         tmem_ld_wait();
