@@ -113,9 +113,10 @@ gesr_status run_projection(const void* X, int64_t M, int32_t K, const void* W0, 
   gesr_status s = make_map_2d(&ma, X, static_cast<uint64_t>(M), static_cast<uint64_t>(K), 128, 64,
                               CU_TENSOR_MAP_SWIZZLE_128B, "X");
   if (s != GESR_OK) return s;
-  s = make_map_2d(&mb0, W0, HD, K, bn, 64, CU_TENSOR_MAP_SWIZZLE_128B, "W0");
+  // a CTA pair computes 256 x bn; each CTA stages its 128 rows of X and bn/2 weight rows
+  s = make_map_2d(&mb0, W0, HD, K, bn / 2, 64, CU_TENSOR_MAP_SWIZZLE_128B, "W0");
   if (s != GESR_OK) return s;
-  s = make_map_2d(&mb1, W1 ? W1 : W0, HD, K, bn, 64, CU_TENSOR_MAP_SWIZZLE_128B, "W1");
+  s = make_map_2d(&mb1, W1 ? W1 : W0, HD, K, bn / 2, 64, CU_TENSOR_MAP_SWIZZLE_128B, "W1");
   if (s != GESR_OK) return s;
   gesr::ProjParams p{};
   p.M = M;
@@ -123,7 +124,7 @@ gesr_status run_projection(const void* X, int64_t M, int32_t K, const void* W0, 
   p.n_split = HD;
   p.d = d;
   p.act = act;
-  p.num_m_blocks = static_cast<int>((M + 127) / 128);
+  p.num_m_blocks = static_cast<int>((M + 255) / 256);
   p.num_n_blocks = (W1 ? 2 * HD : HD) / bn;
   p.bias0 = b0;
   p.bias1 = b1;

@@ -9,16 +9,18 @@
 //
 // B200 design (HBM-bound on the item-ID stream, ~8.5 int64 IDs per (candidate, field)):
 //   grid (B, Y): CTA (b, y) owns request b and candidate chunks y, y+Y, ... of kChunk rows.
-//   1. The request's F user lists are inserted into per-field open-addressing hash tables in
-//      shared memory (64-bit keys + int32 multiplicities, parallel insertion with 64-bit
-//      atomicCAS; one sentinel key value is counted on the side).  Lists whose tables do not
-//      fit the shared-memory pool fall back to a direct scan of global memory (any length).
-//   2. Each warp takes 32 consecutive (candidate, field) segments of the CSR item stream and
-//      reads their IDs COALESCED (lane k reads ID p = start + k + 32*i), finds the owning
-//      segment with a 5-step shuffle binary search over the 33 segment offsets, looks the ID
-//      up in that field's table, and accumulates into a per-warp shared counter array (only
-//      non-zero lookups touch it).  Lane k then stores segment k's count: one coalesced
-//      128-byte int32 store per 32 segments.
+//   1. The request's F user lists go into per-field hash tables in shared memory: buckets of
+//      4 slots holding a 32-bit fingerprint, the 64-bit key and its multiplicity.  Insertion is
+//      parallel (64-bit atomicCAS, linear probing over bucket-aligned slots; the one sentinel
+//      key value INT64_MIN is counted on the side); load factor <= 1/4, so a miss -- the common
+//      case -- is one 16-byte fingerprint read and four compares, uniform across the warp.
+//      Fields whose tables do not fit the pool fall back to a direct scan of global memory.
+//   2. Each warp takes 32 consecutive (candidate, field) segments of the CSR item stream.
+//      Lane k writes its segment id into a per-warp owner map (one uint16 per ID position),
+//      then the warp reads the group's IDs COALESCED (lane l reads ID start + l + 32 i), looks
+//      each up in its field's table, and adds hits into a per-warp shared counter.  Lane k then
+//      stores segment k's count: one coalesced 128-byte int32 store per 32 segments.
+//      Groups with more than kOwnerCap IDs use a shuffle binary search instead of the map.
 #include <cuda_runtime.h>
 
 #include "kernels.h"
@@ -30,38 +32,42 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kChunk = 256;               // candidates per CTA chunk
-constexpr int kPoolSlots = 4096;          // hash slots per CTA (48 KB)
-constexpr int kMaxFields = 256;           // fields handled with per-field smem metadata
+constexpr int kPoolBuckets = 1024;        // 4-slot buckets per CTA (64 KB)
+constexpr int kMaxFields = 256;
+constexpr int kOwnerCap = 512;            // IDs per 32-segment group handled with the owner map
 constexpr unsigned long long kSentinel = 0x8000000000000000ull;   // INT64_MIN
-
-__device__ __forceinline__ uint32_t hash_slot(unsigned long long key, uint32_t mask) {
-  return static_cast<uint32_t>((key * 0x9E3779B97F4A7C15ull) >> 32) & mask;
-}
+constexpr unsigned long long kGold = 0x9E3779B97F4A7C15ull;
 
 struct HmaSmem {
-  unsigned long long keys[kPoolSlots];
-  int cnt[kPoolSlots];
-  int tab_off[kMaxFields];      // slot offset of field f's table, -1 = global fallback
-  int tab_mask[kMaxFields];
-  int sent_cnt[kMaxFields];     // multiplicity of the sentinel value INT64_MIN
-  long long uoff[kMaxFields + 1];   // user_offsets for this request (F+1 entries)
+  uint4 fp[kPoolBuckets];                         // 4 fingerprints per bucket (0 = empty)
+  unsigned long long key[kPoolBuckets * 4];
+  int cnt[kPoolBuckets * 4];
+  int tab_off[kMaxFields];                        // first bucket of field f, -1 = global scan
+  int tab_mask[kMaxFields];                       // buckets - 1
+  int sent_cnt[kMaxFields];                       // multiplicity of INT64_MIN
+  long long uoff[kMaxFields + 1];                 // this request's user_offsets (F+1)
   int warp_cnt[kWarps][32];
+  unsigned short owner[kWarps][kOwnerCap];
 };
 
 __device__ __forceinline__ int lookup(const HmaSmem& s, const HmaParams& p, int f,
                                       unsigned long long key) {
-  if (key == kSentinel) {
-    if (s.tab_off[f] >= 0) return s.sent_cnt[f];
-  }
   const int off = s.tab_off[f];
   if (off >= 0) {
+    if (key == kSentinel) return s.sent_cnt[f];
+    const unsigned long long hk = key * kGold;
     const uint32_t mask = static_cast<uint32_t>(s.tab_mask[f]);
-    uint32_t h = hash_slot(key, mask);
+    uint32_t bkt = static_cast<uint32_t>(hk >> 32) & mask;
+    const uint32_t fpv = static_cast<uint32_t>(hk) | 1u;
     while (true) {
-      const unsigned long long k = s.keys[off + h];
-      if (k == key) return s.cnt[off + h];
-      if (k == kSentinel) return 0;
-      h = (h + 1) & mask;
+      const uint4 f4 = s.fp[off + bkt];
+      const int base = (off + bkt) * 4;
+      if (f4.x == fpv && s.key[base + 0] == key) return s.cnt[base + 0];
+      if (f4.y == fpv && s.key[base + 1] == key) return s.cnt[base + 1];
+      if (f4.z == fpv && s.key[base + 2] == key) return s.cnt[base + 2];
+      if (f4.w == fpv && s.key[base + 3] == key) return s.cnt[base + 3];
+      if (f4.w == 0u) return 0;        // slots fill in probe order: an empty slot ends it
+      bkt = (bkt + 1) & mask;
     }
   }
   // global fallback: direct scan of the user list
@@ -73,7 +79,7 @@ __device__ __forceinline__ int lookup(const HmaSmem& s, const HmaParams& p, int 
 
 __global__ void __launch_bounds__(kThreads)
     hma_kernel(const HmaParams p) {
-  extern __shared__ uint8_t smem_raw[];
+  extern __shared__ __align__(16) uint8_t smem_raw[];
   HmaSmem& s = *reinterpret_cast<HmaSmem*>(smem_raw);
   const int b = blockIdx.x;
   const int64_t cb = p.cand_offsets[b];
@@ -92,12 +98,12 @@ __global__ void __launch_bounds__(kThreads)
     int used = 0;
     for (int f = 0; f < F; ++f) {
       const long long n = s.uoff[f + 1] - s.uoff[f];
-      int size = 16;
-      while (size < 2 * n && size < kPoolSlots) size <<= 1;
-      if (2 * n <= size && used + size <= kPoolSlots) {
+      int nb = 2;
+      while (nb < n && nb < kPoolBuckets) nb <<= 1;     // >= n buckets: load factor <= 1/4
+      if (n <= nb && used + nb <= kPoolBuckets) {
         s.tab_off[f] = used;
-        s.tab_mask[f] = size - 1;
-        used += size;
+        s.tab_mask[f] = nb - 1;
+        used += nb;
       } else {
         s.tab_off[f] = -1;
         s.tab_mask[f] = 0;
@@ -105,8 +111,8 @@ __global__ void __launch_bounds__(kThreads)
       s.sent_cnt[f] = 0;
     }
   }
-  for (int i = tid; i < kPoolSlots; i += kThreads) {
-    s.keys[i] = kSentinel;
+  for (int i = tid; i < kPoolBuckets * 4; i += kThreads) {
+    s.key[i] = kSentinel;
     s.cnt[i] = 0;
   }
   for (int i = tid; i < kWarps * 32; i += kThreads) (&s.warp_cnt[0][0])[i] = 0;
@@ -116,8 +122,7 @@ __global__ void __launch_bounds__(kThreads)
     const long long un = s.uoff[F] - u0;
     for (long long i = tid; i < un; i += kThreads) {
       const long long pos = u0 + i;
-      // owning field: last f with uoff[f] <= pos (F is small; binary search)
-      int lo = 0, hi = F - 1;
+      int lo = 0, hi = F - 1;                 // owning field: last f with uoff[f] <= pos
       while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
         if (s.uoff[mid] <= pos) lo = mid; else hi = mid - 1;
@@ -130,21 +135,34 @@ __global__ void __launch_bounds__(kThreads)
         atomicAdd(&s.sent_cnt[f], 1);
         continue;
       }
-      const uint32_t mask = static_cast<uint32_t>(s.tab_mask[f]);
-      uint32_t h = hash_slot(key, mask);
+      const uint32_t nslots = static_cast<uint32_t>(s.tab_mask[f] + 1) * 4;
+      uint32_t slot = (static_cast<uint32_t>((key * kGold) >> 32) &
+                       static_cast<uint32_t>(s.tab_mask[f])) * 4;
       while (true) {
-        const unsigned long long prev = atomicCAS(&s.keys[off + h], kSentinel, key);
+        const unsigned long long prev = atomicCAS(&s.key[off * 4 + slot], kSentinel, key);
         if (prev == kSentinel || prev == key) {
-          atomicAdd(&s.cnt[off + h], 1);
+          atomicAdd(&s.cnt[off * 4 + slot], 1);
           break;
         }
-        h = (h + 1) & mask;
+        slot = (slot + 1 == nslots) ? 0 : slot + 1;
       }
     }
   }
   __syncthreads();
+  // fingerprints of the occupied slots
+  for (int bk = tid; bk < kPoolBuckets; bk += kThreads) {
+    uint32_t v[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const unsigned long long k = s.key[bk * 4 + e];
+      v[e] = (k == kSentinel) ? 0u : (static_cast<uint32_t>(k * kGold) | 1u);
+    }
+    s.fp[bk] = make_uint4(v[0], v[1], v[2], v[3]);
+  }
+  __syncthreads();
 
   // ---- 2. coalesced scan of the item-ID stream, 32 segments per warp step
+  unsigned short* own = s.owner[warp];
   for (int64_t c0 = first; c0 < ce; c0 += static_cast<int64_t>(gridDim.y) * kChunk) {
     const int64_t c1 = (c0 + kChunk < ce) ? c0 + kChunk : ce;
     const int64_t seg_begin = c0 * F, seg_end = c1 * F;
@@ -155,26 +173,38 @@ __global__ void __launch_bounds__(kThreads)
       const int64_t my_off64 = p.item_offsets[g + (lane < nseg ? lane : nseg)];
       const int64_t start = __shfl_sync(0xffffffffu, my_off64, 0);
       const int64_t end = p.item_offsets[g + nseg];   // same address for all lanes: broadcast
-      // 32-bit relative offsets and field index for the shuffle search (seg_begin % F == 0)
       const int my_off = static_cast<int>(my_off64 - start);
-      const int my_f = static_cast<int>(g - seg_begin + lane) % F;
+      const int nxt = __shfl_down_sync(0xffffffffu, my_off, 1);
       const int n_ids = static_cast<int>(end - start);
+      const int my_end = lane + 1 < nseg ? nxt : n_ids;
+      const int my_f = static_cast<int>(g - seg_begin + lane) % F;   // seg_begin % F == 0
       const int64_t* ids = p.item_ids + start;
-      for (int base = 0; base < n_ids; base += 32) {
-        const int pos = base + lane;
-        const bool ok = pos < n_ids;
-        const unsigned long long key = ok ? static_cast<unsigned long long>(__ldg(ids + pos)) : 0ull;
-        // owning segment: largest k with off[k] <= pos (offsets nondecreasing)
-        int k = 0;
-#pragma unroll
-        for (int step = 16; step >= 1; step >>= 1) {
-          const int o = __shfl_sync(0xffffffffu, my_off, k + step);
-          if (o <= pos) k += step;
+      if (n_ids <= kOwnerCap) {
+        if (lane < nseg)
+          for (int q = my_off; q < my_end; ++q) own[q] = static_cast<unsigned short>(lane | (my_f << 5));
+        __syncwarp();
+        for (int pos = lane; pos < n_ids; pos += 32) {
+          const unsigned long long key = static_cast<unsigned long long>(__ldg(ids + pos));
+          const int o = own[pos];
+          const int c = lookup(s, p, o >> 5, key);
+          if (c != 0) atomicAdd(&s.warp_cnt[warp][o & 31], c);
         }
-        const int f = __shfl_sync(0xffffffffu, my_f, k);
-        if (ok) {
-          const int c = lookup(s, p, f, key);
-          if (c != 0) atomicAdd(&s.warp_cnt[warp][k], c);
+      } else {
+        for (int base = 0; base < n_ids; base += 32) {
+          const int pos = base + lane;
+          const bool ok = pos < n_ids;
+          const unsigned long long key = ok ? static_cast<unsigned long long>(__ldg(ids + pos)) : 0ull;
+          int k = 0;     // owning segment: largest k with off[k] <= pos
+#pragma unroll
+          for (int step = 16; step >= 1; step >>= 1) {
+            const int o = __shfl_sync(0xffffffffu, my_off, k + step);
+            if (o <= pos) k += step;
+          }
+          const int f = __shfl_sync(0xffffffffu, my_f, k);
+          if (ok) {
+            const int c = lookup(s, p, f, key);
+            if (c != 0) atomicAdd(&s.warp_cnt[warp][k], c);
+          }
         }
       }
       __syncwarp();

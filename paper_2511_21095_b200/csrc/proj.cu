@@ -5,16 +5,22 @@
 // (X = T, W = W_q, output Q [H, total_C, d] in the workspace).  PAPER.md:335-341 (s3.4.2):
 // the [U,T] self-attention layer's projections; projection form act(XW^T+b) per DESIGN.md R3.
 //
-// B200 design: persistent CTAs (grid <= #SMs), warp-specialised:
-//   warp 0   TMA producer: A tile 128x64 and B tile BNx64 (bf16, 128B swizzle) per K block,
-//            through a STAGES-deep mbarrier ring.
-//   warp 1   MMA issuer: one elected thread issues tcgen05.mma.cta_group::1.kind::f16
-//            (M=128, N=BN, K=16) into a double-buffered TMEM accumulator.
-//   warp 2   TMEM allocator (2*BN columns).
-//   warps 4-7 epilogue: tcgen05.ld 32x32b (thread = output row), bias + act in fp32, RNE to
-//            bf16, 16-byte stores into the head-major cache (each 32-column chunk is one
-//            contiguous 64-byte run of one head's row).
-// The epilogue of tile i overlaps the MMAs of tile i+1 (two accumulator buffers).
+// B200 design: persistent CTA PAIRS (cluster of 2, tcgen05 cta_group::2), warp-specialised.
+// A pair computes a 256 x BN output tile with M=256 MMAs: each CTA stages its own 128 rows of
+// X and HALF of the BN weight rows, so every SM receives 16 KB of X plus BN*64 B of W per
+// 64-deep K block -- half the weight traffic of a single-CTA 128 x BN tile.  (ncu on the
+// single-CTA version: 25.8 GB of L2->SM traffic for the K/V projection, tensor pipe 35%.)
+//   warp 0    TMA producer (both CTAs): A 128x64 + B (BN/2)x64 per stage, completion bytes
+//             signalled on the leader CTA's full barrier.
+//   warp 1    MMA issuer (leader CTA only): tcgen05.mma.cta_group::2.kind::f16, M=256 N=BN
+//             K=16, into a double-buffered TMEM accumulator (2*BN columns in each CTA);
+//             commits multicast to both CTAs' barriers.
+//   warp 2    TMEM allocator (cta_group::2).
+//   warps 4-11 epilogue (both CTAs): tcgen05.ld 32x32b (thread = output row), bias + act in
+//             fp32, RNE to bf16, 16-byte stores into the head-major cache (each 32-column chunk
+//             is one contiguous 64-byte run of one head's row); one arrival per CTA on the
+//             leader's TMEM-empty barrier.
+// The epilogue of tile i overlaps the MMAs of tile i+1.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -25,16 +31,16 @@ namespace gesr {
 
 namespace {
 
-constexpr int kBM = 128;
+constexpr int kBM = 128;             // rows per CTA; a pair tile is 256 rows
 constexpr int kBK = 64;              // 64 bf16 = 128 bytes = one 128B-swizzle row
-constexpr int kThreads = 384;          // 4 control warps + 8 epilogue warps
+constexpr int kThreads = 384;        // 4 control warps + 8 epilogue warps
 constexpr uint32_t kABytes = kBM * kBK * 2;   // 16 KB
 
 template <int BN>
 struct ProjSmem {
-  static constexpr uint32_t kBBytes = BN * kBK * 2;
+  static constexpr uint32_t kBBytes = (BN / 2) * kBK * 2;
   static constexpr uint32_t kStageBytes = kABytes + kBBytes;
-  static constexpr int kStages = (200 * 1024) / kStageBytes > 8 ? 8 : (200 * 1024) / kStageBytes;
+  static constexpr int kStages = (196 * 1024) / kStageBytes > 8 ? 8 : (196 * 1024) / kStageBytes;
   static constexpr uint32_t kTmemCols = (2 * BN) < 32 ? 32 : 2 * BN;
   static constexpr uint32_t kBarOffset = kStages * kStageBytes;
   static constexpr uint32_t kBytes = kBarOffset + 256 + 1024;  // + barriers + alignment slack
@@ -46,7 +52,7 @@ __device__ __forceinline__ float apply_act(int act, float x) {
 }
 
 template <int BN>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     proj_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b0,
                 const __grid_constant__ CUtensorMap map_b1, const ProjParams p) {
   using S = ProjSmem<BN>;
@@ -61,7 +67,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
-  const int num_tiles = p.num_m_blocks * p.num_n_blocks;
+  const uint32_t rank = cluster_ctarank();          // 0 = leader of the pair
+  const int pair = blockIdx.x >> 1;
+  const int npairs = gridDim.x >> 1;
+  const int num_tiles = p.num_m_blocks * p.num_n_blocks;   // 256-row blocks x BN blocks
   const int num_kb = (p.K + kBK - 1) / kBK;
 
   if (warp == 0 && lane == 0) {
@@ -74,92 +83,97 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull_bar[b], 1);
-      mbar_init(&tempty_bar[b], 256);
+      mbar_init(&tempty_bar[b], 2);     // one arrival per CTA of the pair
     }
     fence_mbar_init();
   }
   if (warp == 2) {
-    tmem_alloc(tmem_slot, S::kTmemCols);
-    tmem_relinquish();
+    tmem_alloc_pair(tmem_slot, S::kTmemCols);
+    tmem_relinquish_pair();
   }
   tc_fence_before();
-  __syncthreads();
+  cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
     if (elect_one()) {
-      // ---------------- TMA producer
+      // ---------------- TMA producer (both CTAs)
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      for (int tile = pair; tile < num_tiles; tile += npairs) {
         const int m_blk = tile / p.num_n_blocks;
         const int n_blk = tile % p.num_n_blocks;
         const int n0 = n_blk * BN;
         // B comes from map_b0 for columns < n_split, else map_b1 (W_k / W_v stacked along N)
         const CUtensorMap* mb = (n0 < p.n_split) ? &map_b0 : &map_b1;
-        const int nb = (n0 < p.n_split) ? n0 : n0 - p.n_split;
+        const int nb = ((n0 < p.n_split) ? n0 : n0 - p.n_split) + static_cast<int>(rank) * (BN / 2);
+        const int ma = m_blk * 2 * kBM + static_cast<int>(rank) * kBM;
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = smem + stage * S::kStageBytes;
           uint8_t* sb = sa + kABytes;
-          mbar_arrive_expect_tx(&full_bar[stage], S::kStageBytes);
-          tma_load_2d(sa, &map_a, &full_bar[stage], kb * kBK, m_blk * kBM);
-          tma_load_2d(sb, mb, &full_bar[stage], kb * kBK, nb);
+          if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], 2 * S::kStageBytes);
+          tma_load_2d_pair(sa, &map_a, &full_bar[stage], kb * kBK, ma);
+          tma_load_2d_pair(sb, mb, &full_bar[stage], kb * kBK, nb);
           if (++stage == S::kStages) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer
-    const uint32_t idesc = make_idesc_bf16(kBM, BN, 0, 0);
-    int stage = 0;
-    uint32_t phase = 0;
-    int local = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
-      const uint32_t buf = local & 1;
-      const uint32_t aphase = (local >> 1) & 1;
-      mbar_wait(&tempty_bar[buf], aphase ^ 1);
-      tc_fence_after();
-      const uint32_t d_tmem = tmem_base + buf * BN;
-      for (int kb = 0; kb < num_kb; ++kb) {
-        mbar_wait(&full_bar[stage], phase);
+    // ---------------- MMA issuer (leader CTA only)
+    if (rank == 0) {
+      const uint32_t idesc = make_idesc_bf16(2 * kBM, BN, 0, 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      int local = 0;
+      for (int tile = pair; tile < num_tiles; tile += npairs, ++local) {
+        const uint32_t buf = local & 1;
+        const uint32_t aphase = (local >> 1) & 1;
+        mbar_wait(&tempty_bar[buf], aphase ^ 1);
         tc_fence_after();
-        if (elect_one()) {
-          const uint32_t sa = smem_u32(smem + stage * S::kStageBytes);
-          const uint32_t sb = sa + kABytes;
+        const uint32_t d_tmem = tmem_base + buf * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t sa = smem_u32(smem + stage * S::kStageBytes);
+            const uint32_t sb = sa + kABytes;
 #pragma unroll
-          for (int k = 0; k < kBK / 16; ++k) {
-            const uint64_t ad = make_sdesc(sa + k * 32, 16, 1024, kSwizzle128B);
-            const uint64_t bd = make_sdesc(sb + k * 32, 16, 1024, kSwizzle128B);
-            mma_ss(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+            for (int k = 0; k < kBK / 16; ++k) {
+              const uint64_t ad = make_sdesc(sa + k * 32, 16, 1024, kSwizzle128B);
+              const uint64_t bd = make_sdesc(sb + k * 32, 16, 1024, kSwizzle128B);
+              mma_ss_pair(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+            }
+            mma_commit_pair_mc(&empty_bar[stage], 0x3);
+            if (kb == num_kb - 1) mma_commit_pair_mc(&tfull_bar[buf], 0x3);
           }
-          mma_commit(&empty_bar[stage]);
-          if (kb == num_kb - 1) mma_commit(&tfull_bar[buf]);
+          __syncwarp();
+          if (++stage == S::kStages) { stage = 0; phase ^= 1; }
         }
-        __syncwarp();
-        if (++stage == S::kStages) { stage = 0; phase ^= 1; }
       }
     }
   } else if (warp >= 4) {
-    // ---------------- epilogue: TMEM -> regs -> act -> bf16 -> head-major global
-    // 8 warps: warp w reads TMEM lane quarter (w & 3); warps 4-7 take the first half of the
-    // tile's 32-column chunks and warps 8-11 the second half (2 warps per SM sub-partition).
+    // ---------------- epilogue (both CTAs): TMEM -> regs -> act -> bf16 -> head-major global
+    // warp w reads TMEM lane quarter (w & 3); warps 4-7 take the first half of the tile's
+    // 32-column chunks and warps 8-11 the second half (2 warps per SM sub-partition).
     const uint32_t sub = warp & 3;
     const int half = (warp - 4) >> 2;
     constexpr int kChunks = BN / 32;
     constexpr int kPerHalf = kChunks >= 2 ? kChunks / 2 : 1;
     const int c_begin = kChunks >= 2 ? half * kPerHalf : 0;
     const int c_end = kChunks >= 2 ? c_begin + kPerHalf : (half == 0 ? 1 : 0);
+    const uint32_t tempty_leader[2] = {mapa_shared(smem_u32(&tempty_bar[0]), 0),
+                                       mapa_shared(smem_u32(&tempty_bar[1]), 0)};
     int local = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
+    for (int tile = pair; tile < num_tiles; tile += npairs, ++local) {
       const int m_blk = tile / p.num_n_blocks;
       const int n_blk = tile % p.num_n_blocks;
       const uint32_t buf = local & 1;
       const uint32_t aphase = (local >> 1) & 1;
       mbar_wait(&tfull_bar[buf], aphase);
       tc_fence_after();
-      const int64_t row = static_cast<int64_t>(m_blk) * kBM + sub * 32 + lane;
+      const int64_t row = static_cast<int64_t>(m_blk) * 2 * kBM + rank * kBM + sub * 32 + lane;
       const bool row_ok = row < p.M;
 #pragma unroll 1
       for (int c = c_begin; c < c_end; ++c) {
@@ -192,15 +206,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       tc_fence_before();
-      mbar_arrive(&tempty_bar[buf]);
+      named_bar_sync(1, 256);
+      if (warp == 4 && lane == 0) mbar_arrive_cluster(tempty_leader[buf]);
     }
   }
 
   tc_fence_before();
-  __syncthreads();
+  cluster_sync();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, S::kTmemCols);
+    tmem_dealloc_pair(tmem_base, S::kTmemCols);
   }
 }
 
@@ -216,8 +231,8 @@ cudaError_t launch_bn(const CUtensorMap& ma, const CUtensorMap& mb0, const CUten
     attr_done = true;
   }
   const int tiles = p.num_m_blocks * p.num_n_blocks;
-  const int grid = tiles < num_sms ? tiles : num_sms;
-  proj_kernel<BN><<<grid, kThreads, S::kBytes, stream>>>(ma, mb0, mb1, p);
+  const int pairs = tiles < num_sms / 2 ? tiles : num_sms / 2;
+  proj_kernel<BN><<<2 * pairs, kThreads, S::kBytes, stream>>>(ma, mb0, mb1, p);
   return cudaGetLastError();
 }
 
