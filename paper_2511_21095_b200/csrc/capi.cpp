@@ -81,6 +81,24 @@ gesr_status make_map_2d(CUtensorMap* map, const void* base, uint64_t rows, uint6
   return GESR_OK;
 }
 
+// 3D bf16 tensor map over a head-major [H, M, d] output with a {32 cols, 32 rows, 1} box and
+// 64B swizzle (the projection epilogue's TMA store).
+gesr_status make_out_map(CUtensorMap* map, void* base, uint64_t H, uint64_t M, uint64_t d,
+                         const char* what) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return fail(GESR_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+  cuuint64_t dims[3] = {d, M, H};
+  cuuint64_t strides[2] = {d * 2, M * d * 2};
+  cuuint32_t box[3] = {32, 32, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, base, dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                   CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(GESR_ERR_CUDA, "cuTensorMapEncodeTiled(%s) failed: %d", what, static_cast<int>(r));
+  return GESR_OK;
+}
+
 bool valid_d(int32_t d) { return d == 32 || d == 64 || d == 128; }
 
 gesr_status check_common(int32_t D_in, int32_t H, int32_t d, int32_t act) {
@@ -118,6 +136,11 @@ gesr_status run_projection(const void* X, int64_t M, int32_t K, const void* W0, 
   if (s != GESR_OK) return s;
   s = make_map_2d(&mb1, W1 ? W1 : W0, HD, K, bn / 2, 64, CU_TENSOR_MAP_SWIZZLE_128B, "W1");
   if (s != GESR_OK) return s;
+  CUtensorMap mo0, mo1;
+  s = make_out_map(&mo0, out0, H, M, d, "out0");
+  if (s != GESR_OK) return s;
+  s = make_out_map(&mo1, out1 ? out1 : out0, H, M, d, "out1");
+  if (s != GESR_OK) return s;
   gesr::ProjParams p{};
   p.M = M;
   p.K = K;
@@ -130,7 +153,7 @@ gesr_status run_projection(const void* X, int64_t M, int32_t K, const void* W0, 
   p.bias1 = b1;
   p.out0 = static_cast<__nv_bfloat16*>(out0);
   p.out1 = static_cast<__nv_bfloat16*>(out1);
-  cudaError_t e = gesr::launch_proj(ma, mb0, mb1, p, bn, num_sms(), stream);
+  cudaError_t e = gesr::launch_proj(ma, mb0, mb1, mo0, mo1, p, bn, num_sms(), stream);
   if (e != cudaSuccess) return cuda_fail(e, "proj_kernel launch");
   return GESR_OK;
 }

@@ -26,7 +26,8 @@ struct ProjParams {
 
 int proj_pick_bn(int n_split);
 cudaError_t launch_proj(const CUtensorMap& map_a, const CUtensorMap& map_b0,
-                        const CUtensorMap& map_b1, const ProjParams& p, int bn, int num_sms,
+                        const CUtensorMap& map_b1, const CUtensorMap& map_o0,
+                        const CUtensorMap& map_o1, const ProjParams& p, int bn, int num_sms,
                         cudaStream_t stream);
 
 // ---------------------------------------------------------------- K-SCHED + K-ATTN (attn.cu)

@@ -16,10 +16,11 @@
 //             K=16, into a double-buffered TMEM accumulator (2*BN columns in each CTA);
 //             commits multicast to both CTAs' barriers.
 //   warp 2    TMEM allocator (cta_group::2).
-//   warps 4-11 epilogue (both CTAs): tcgen05.ld 32x32b (thread = output row), bias + act in
-//             fp32, RNE to bf16, 16-byte stores into the head-major cache (each 32-column chunk
-//             is one contiguous 64-byte run of one head's row); one arrival per CTA on the
-//             leader's TMEM-empty barrier.
+//   warps 4-11 epilogue (both CTAs): tcgen05.ld 32x32b (thread = output row), release of the
+//             accumulator (one arrival per CTA on the leader's TMEM-empty barrier), bias + act
+//             in fp32, RNE to bf16, swizzled 16-byte smem stores, TMA tensor stores into the
+//             head-major [H, M, d] output.  (Direct per-thread 16-byte global stores touched
+//             32 rows per instruction and capped the kernel at ~35% tensor-pipe.)
 // The epilogue of tile i overlaps the MMAs of tile i+1.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -40,9 +41,15 @@ template <int BN>
 struct ProjSmem {
   static constexpr uint32_t kBBytes = (BN / 2) * kBK * 2;
   static constexpr uint32_t kStageBytes = kABytes + kBBytes;
-  static constexpr int kStages = (196 * 1024) / kStageBytes > 8 ? 8 : (196 * 1024) / kStageBytes;
+  // epilogue staging: per epilogue warp, its 32 rows x (its half of BN) columns as 2 KB boxes
+  static constexpr int kChunks = BN / 32;
+  static constexpr int kPerHalf = kChunks >= 2 ? kChunks / 2 : 1;
+  static constexpr uint32_t kStagingBytes = 8 * kPerHalf * 2048;
+  static constexpr int kStages = (196 * 1024 - kStagingBytes) / kStageBytes > 8
+                                     ? 8 : (196 * 1024 - kStagingBytes) / kStageBytes;
   static constexpr uint32_t kTmemCols = (2 * BN) < 32 ? 32 : 2 * BN;
-  static constexpr uint32_t kBarOffset = kStages * kStageBytes;
+  static constexpr uint32_t kStagingOffset = kStages * kStageBytes;
+  static constexpr uint32_t kBarOffset = kStagingOffset + kStagingBytes;
   static constexpr uint32_t kBytes = kBarOffset + 256 + 1024;  // + barriers + alignment slack
 };
 
@@ -54,7 +61,8 @@ __device__ __forceinline__ float apply_act(int act, float x) {
 template <int BN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     proj_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b0,
-                const __grid_constant__ CUtensorMap map_b1, const ProjParams p) {
+                const __grid_constant__ CUtensorMap map_b1, const __grid_constant__ CUtensorMap map_o0,
+                const __grid_constant__ CUtensorMap map_o1, const ProjParams p) {
   using S = ProjSmem<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -154,15 +162,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp >= 4) {
-    // ---------------- epilogue (both CTAs): TMEM -> regs -> act -> bf16 -> head-major global
+    // ---------------- epilogue (both CTAs): TMEM -> regs -> act -> bf16 -> smem -> TMA store
     // warp w reads TMEM lane quarter (w & 3); warps 4-7 take the first half of the tile's
-    // 32-column chunks and warps 8-11 the second half (2 warps per SM sub-partition).
+    // 32-column chunks and warps 8-11 the second half (2 warps per SM sub-partition).  Each
+    // 32x32 chunk is written to a 2 KB 64B-swizzled staging box (conflict-free 16-byte stores)
+    // and leaves with one TMA tensor store into the [H, M, d] output (rows >= M are clipped).
     const uint32_t sub = warp & 3;
     const int half = (warp - 4) >> 2;
-    constexpr int kChunks = BN / 32;
-    constexpr int kPerHalf = kChunks >= 2 ? kChunks / 2 : 1;
-    const int c_begin = kChunks >= 2 ? half * kPerHalf : 0;
-    const int c_end = kChunks >= 2 ? c_begin + kPerHalf : (half == 0 ? 1 : 0);
+    constexpr int kPerHalf = S::kPerHalf;
+    const int c_begin = S::kChunks >= 2 ? half * kPerHalf : 0;
+    const int c_end = S::kChunks >= 2 ? c_begin + kPerHalf : (half == 0 ? 1 : 0);
+    uint8_t* stg = smem + S::kStagingOffset + (warp - 4) * kPerHalf * 2048;
     const uint32_t tempty_leader[2] = {mapa_shared(smem_u32(&tempty_bar[0]), 0),
                                        mapa_shared(smem_u32(&tempty_bar[1]), 0)};
     int local = 0;
@@ -171,44 +181,63 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const int n_blk = tile % p.num_n_blocks;
       const uint32_t buf = local & 1;
       const uint32_t aphase = (local >> 1) & 1;
+      const int row0 = m_blk * 2 * kBM + static_cast<int>(rank) * kBM + static_cast<int>(sub) * 32;
       mbar_wait(&tfull_bar[buf], aphase);
       tc_fence_after();
-      const int64_t row = static_cast<int64_t>(m_blk) * 2 * kBM + rank * kBM + sub * 32 + lane;
-      const bool row_ok = row < p.M;
-#pragma unroll 1
-      for (int c = c_begin; c < c_end; ++c) {
-        uint32_t r[32];
-        tmem_ld32(tmem_base + ((sub * 32) << 16) + buf * BN + c * 32, r);
-        tmem_ld_wait();
-        const int n0 = n_blk * BN + c * 32;   // 32-column chunk lies within one head (d >= 32)
+      uint32_t r[kPerHalf][32];
+#pragma unroll
+      for (int ci = 0; ci < kPerHalf; ++ci)
+        if (c_begin + ci < c_end)
+          tmem_ld32(tmem_base + ((sub * 32) << 16) + buf * BN + (c_begin + ci) * 32, r[ci]);
+      tmem_ld_wait();
+      // accumulator drained: release it to the MMA warp (one arrival per CTA)
+      tc_fence_before();
+      named_bar_sync(1, 256);
+      if (warp == 4 && lane == 0) mbar_arrive_cluster(tempty_leader[buf]);
+      // staging boxes must have been read by the previous tile's TMA stores
+      if (lane == 0) bulk_wait_group_read<0>();
+      __syncwarp();
+#pragma unroll
+      for (int ci = 0; ci < kPerHalf; ++ci) {
+        if (c_begin + ci >= c_end) break;
+        const int n0 = n_blk * BN + (c_begin + ci) * 32;   // chunk lies within one head (d >= 32)
         const int which = n0 >= p.n_split ? 1 : 0;
         const int within = n0 - which * p.n_split;
-        const int h = within / p.d;
-        const int j0 = within - h * p.d;
         const float* bias = which ? p.bias1 : p.bias0;
         uint32_t packed[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          float x0 = __uint_as_float(r[2 * i]);
-          float x1 = __uint_as_float(r[2 * i + 1]);
+          float x0 = __uint_as_float(r[ci][2 * i]);
+          float x1 = __uint_as_float(r[ci][2 * i + 1]);
           if (bias != nullptr) {
             x0 += __ldg(bias + within + 2 * i);
             x1 += __ldg(bias + within + 2 * i + 1);
           }
           packed[i] = pack_bf16x2(apply_act(p.act, x0), apply_act(p.act, x1));
         }
-        if (row_ok) {
-          __nv_bfloat16* out = which ? p.out1 : p.out0;
-          uint4* dst = reinterpret_cast<uint4*>(out + (static_cast<int64_t>(h) * p.M + row) * p.d + j0);
+        // 64B swizzle: 16-byte chunk q of row `lane` goes to slot q ^ ((lane >> 1) & 3)
+        uint8_t* box = stg + ci * 2048 + lane * 64;
 #pragma unroll
-          for (int v = 0; v < 4; ++v)
-            dst[v] = make_uint4(packed[4 * v], packed[4 * v + 1], packed[4 * v + 2], packed[4 * v + 3]);
-        }
+        for (int q = 0; q < 4; ++q)
+          *reinterpret_cast<uint4*>(box + ((q ^ ((lane >> 1) & 3)) << 4)) =
+              make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
       }
-      tc_fence_before();
-      named_bar_sync(1, 256);
-      if (warp == 4 && lane == 0) mbar_arrive_cluster(tempty_leader[buf]);
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+#pragma unroll
+        for (int ci = 0; ci < kPerHalf; ++ci) {
+          if (c_begin + ci >= c_end) break;
+          const int n0 = n_blk * BN + (c_begin + ci) * 32;
+          const int which = n0 >= p.n_split ? 1 : 0;
+          const int within = n0 - which * p.n_split;
+          const int h = within / p.d;
+          tma_store_3d(which ? &map_o1 : &map_o0, stg + ci * 2048, within - h * p.d, row0, h);
+        }
+        bulk_commit_group();
+      }
     }
+    if (lane == 0) bulk_wait_group<0>();
   }
 
   tc_fence_before();
@@ -221,7 +250,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
 template <int BN>
 cudaError_t launch_bn(const CUtensorMap& ma, const CUtensorMap& mb0, const CUtensorMap& mb1,
-                      const ProjParams& p, int num_sms, cudaStream_t stream) {
+                      const CUtensorMap& mo0, const CUtensorMap& mo1, const ProjParams& p,
+                      int num_sms, cudaStream_t stream) {
   using S = ProjSmem<BN>;
   static bool attr_done = false;  // same arch on every device of the box
   if (!attr_done) {
@@ -232,7 +262,7 @@ cudaError_t launch_bn(const CUtensorMap& ma, const CUtensorMap& mb0, const CUten
   }
   const int tiles = p.num_m_blocks * p.num_n_blocks;
   const int pairs = tiles < num_sms / 2 ? tiles : num_sms / 2;
-  proj_kernel<BN><<<2 * pairs, kThreads, S::kBytes, stream>>>(ma, mb0, mb1, p);
+  proj_kernel<BN><<<2 * pairs, kThreads, S::kBytes, stream>>>(ma, mb0, mb1, mo0, mo1, p);
   return cudaGetLastError();
 }
 
@@ -246,13 +276,14 @@ int proj_pick_bn(int N) {
 }
 
 cudaError_t launch_proj(const CUtensorMap& map_a, const CUtensorMap& map_b0,
-                        const CUtensorMap& map_b1, const ProjParams& p, int bn, int num_sms,
+                        const CUtensorMap& map_b1, const CUtensorMap& map_o0,
+                        const CUtensorMap& map_o1, const ProjParams& p, int bn, int num_sms,
                         cudaStream_t stream) {
   switch (bn) {
-    case 256: return launch_bn<256>(map_a, map_b0, map_b1, p, num_sms, stream);
-    case 128: return launch_bn<128>(map_a, map_b0, map_b1, p, num_sms, stream);
-    case 64: return launch_bn<64>(map_a, map_b0, map_b1, p, num_sms, stream);
-    case 32: return launch_bn<32>(map_a, map_b0, map_b1, p, num_sms, stream);
+    case 256: return launch_bn<256>(map_a, map_b0, map_b1, map_o0, map_o1, p, num_sms, stream);
+    case 128: return launch_bn<128>(map_a, map_b0, map_b1, map_o0, map_o1, p, num_sms, stream);
+    case 64: return launch_bn<64>(map_a, map_b0, map_b1, map_o0, map_o1, p, num_sms, stream);
+    case 32: return launch_bn<32>(map_a, map_b0, map_b1, map_o0, map_o1, p, num_sms, stream);
     default: return cudaErrorInvalidValue;
   }
 }
