@@ -34,23 +34,24 @@ namespace {
 
 constexpr int kBM = 128;             // rows per CTA; a pair tile is 256 rows
 constexpr int kBK = 64;              // 64 bf16 = 128 bytes = one 128B-swizzle row
-constexpr int kThreads = 384;        // 4 control warps + 8 epilogue warps
+constexpr int kEpiWarps = 16;        // 4 per SM sub-partition: latency hiding by TLP
+constexpr int kThreads = (4 + kEpiWarps) * 32;
 constexpr uint32_t kABytes = kBM * kBK * 2;   // 16 KB
 
 template <int BN>
 struct ProjSmem {
   static constexpr uint32_t kBBytes = (BN / 2) * kBK * 2;
   static constexpr uint32_t kStageBytes = kABytes + kBBytes;
-  // epilogue staging: per epilogue warp, its 32 rows x (its half of BN) columns as 2 KB boxes
+  // epilogue staging: one 2 KB box (32 rows x 32 columns, 64B swizzle) per epilogue warp
   static constexpr int kChunks = BN / 32;
-  static constexpr int kPerHalf = kChunks >= 2 ? kChunks / 2 : 1;
-  static constexpr uint32_t kStagingBytes = 8 * kPerHalf * 2048;
-  static constexpr int kStages = (196 * 1024 - kStagingBytes) / kStageBytes > 8
-                                     ? 8 : (196 * 1024 - kStagingBytes) / kStageBytes;
+  static constexpr uint32_t kStagingBytes = kEpiWarps * 2048;
+  static constexpr int kStages = (224 * 1024 - kStagingBytes) / kStageBytes > 8
+                                     ? 8 : (224 * 1024 - kStagingBytes) / kStageBytes;
   static constexpr uint32_t kTmemCols = (2 * BN) < 32 ? 32 : 2 * BN;
   static constexpr uint32_t kStagingOffset = kStages * kStageBytes;
   static constexpr uint32_t kBarOffset = kStagingOffset + kStagingBytes;
   static constexpr uint32_t kBytes = kBarOffset + 256 + 1024;  // + barriers + alignment slack
+  static_assert(kBytes <= 232448, "shared memory budget");
 };
 
 // SiLU(x) = x / (1 + 2^(-x log2 e)) with ONE MUFU op per element: exp2 on the MUFU pipe, the
@@ -171,16 +172,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 4) {
     // ---------------- epilogue (both CTAs): TMEM -> regs -> act -> bf16 -> smem -> TMA store
-    // warp w reads TMEM lane quarter (w & 3); warps 4-7 take the first half of the tile's
-    // 32-column chunks and warps 8-11 the second half (2 warps per SM sub-partition).  Each
-    // 32x32 chunk is written to a 2 KB 64B-swizzled staging box (conflict-free 16-byte stores)
-    // and leaves with one TMA tensor store into the [H, M, d] output (rows >= M are clipped).
+    // 16 warps: warp w reads TMEM lane quarter (w & 3) and column part (w - 4) / 4 of the tile
+    // (BN/4 columns = 1-2 chunks of 32).  Each 32x32 chunk goes through the warp's 2 KB
+    // 64B-swizzled staging box (conflict-free 16-byte stores) and leaves with one TMA tensor
+    // store into the [H, M, d] output (rows >= M are clipped by the tensor map).
     const uint32_t sub = warp & 3;
-    const int half = (warp - 4) >> 2;
-    constexpr int kPerHalf = S::kPerHalf;
-    const int c_begin = S::kChunks >= 2 ? half * kPerHalf : 0;
-    const int c_end = S::kChunks >= 2 ? c_begin + kPerHalf : (half == 0 ? 1 : 0);
-    uint8_t* stg = smem + S::kStagingOffset + (warp - 4) * kPerHalf * 2048;
+    const int part = (warp - 4) >> 2;
+    constexpr int kPer = S::kChunks >= 4 ? S::kChunks / 4 : 1;
+    const int c_begin = part * kPer;
+    const int c_end = c_begin + kPer <= S::kChunks ? c_begin + kPer : S::kChunks;
+    uint8_t* box = smem + S::kStagingOffset + (warp - 4) * 2048;
     const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty_bar[0]), 0);
     const uint32_t tempty_leader1 = mapa_shared(smem_u32(&tempty_bar[1]), 0);
     int local = 0;
@@ -192,29 +193,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const int row0 = m_blk * 2 * kBM + static_cast<int>(rank) * kBM + static_cast<int>(sub) * 32;
       mbar_wait(&tfull_bar[buf], aphase);
       tc_fence_after();
-      uint32_t r[kPerHalf][32];
-#pragma unroll
-      for (int ci = 0; ci < kPerHalf; ++ci)
-        if (c_begin + ci < c_end)
-          tmem_ld32(tmem_base + ((sub * 32) << 16) + buf * BN + (c_begin + ci) * 32, r[ci]);
-      tmem_ld_wait();
-      // accumulator drained: release it to the MMA warp (one arrival per CTA)
-      tc_fence_before();
-      named_bar_sync(1, 256);
-      if (warp == 4 && lane == 0) mbar_arrive_cluster(buf ? tempty_leader1 : tempty_leader0);
-      // staging boxes must have been read by the previous tile's TMA stores
-      if (lane == 0) bulk_wait_group_read<0>();
-      __syncwarp();
-#pragma unroll
-      for (int ci = 0; ci < kPerHalf; ++ci) {
-        if (c_begin + ci >= c_end) break;
-        const int n0 = n_blk * BN + (c_begin + ci) * 32;   // chunk lies within one head (d >= 32)
+#pragma unroll 1
+      for (int c = c_begin; c < c_end; ++c) {
+        uint32_t r[32];
+        tmem_ld32(tmem_base + ((sub * 32) << 16) + buf * BN + c * 32, r);
+        tmem_ld_wait();
+        const int n0 = n_blk * BN + c * 32;   // chunk lies within one head (d >= 32)
         const int which = n0 >= p.n_split ? 1 : 0;
         const int within = n0 - which * p.n_split;
         const float* bias = which ? p.bias1 : p.bias0;
         float v[32];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[ci][i]);
+        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
         if (bias != nullptr) {
           const float4* b4 = reinterpret_cast<const float4*>(bias + within);
 #pragma unroll
@@ -230,27 +220,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         uint32_t packed[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) packed[i] = pack_bf16x2(v[2 * i], v[2 * i + 1]);
+        // the staging box must have been read by this warp's previous TMA store
+        if (lane == 0) bulk_wait_group_read<0>();
+        __syncwarp();
         // 64B swizzle: 16-byte chunk q of row `lane` goes to slot q ^ ((lane >> 1) & 3)
-        uint8_t* box = stg + ci * 2048 + lane * 64;
+        uint8_t* rowp = box + lane * 64;
 #pragma unroll
         for (int q = 0; q < 4; ++q)
-          *reinterpret_cast<uint4*>(box + ((q ^ ((lane >> 1) & 3)) << 4)) =
+          *reinterpret_cast<uint4*>(rowp + ((q ^ ((lane >> 1) & 3)) << 4)) =
               make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
-      }
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) {
-#pragma unroll
-        for (int ci = 0; ci < kPerHalf; ++ci) {
-          if (c_begin + ci >= c_end) break;
-          const int n0 = n_blk * BN + (c_begin + ci) * 32;
-          const int which = n0 >= p.n_split ? 1 : 0;
-          const int within = n0 - which * p.n_split;
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
           const int h = within / p.d;
-          tma_store_3d(which ? &map_o1 : &map_o0, stg + ci * 2048, within - h * p.d, row0, h);
+          tma_store_3d(which ? &map_o1 : &map_o0, box, within - h * p.d, row0, h);
+          bulk_commit_group();
         }
-        bulk_commit_group();
       }
+      // accumulator drained by all 16 warps: one arrival per CTA on the leader's barrier
+      tc_fence_before();
+      named_bar_sync(1, kEpiWarps * 32);
+      if (warp == 4 && lane == 0) mbar_arrive_cluster(buf ? tempty_leader1 : tempty_leader0);
     }
     if (lane == 0) bulk_wait_group<0>();
   }
