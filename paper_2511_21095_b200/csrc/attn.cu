@@ -30,7 +30,7 @@ namespace gesr {
 
 namespace {
 
-constexpr int kThreads = 384;
+constexpr int kThreads = 384;     // WG0: TMA, MMA, 2 idle warps; WG1 / WG2: softmax
 constexpr int kBlockKeys = 128;
 
 template <int D>
@@ -65,17 +65,36 @@ __device__ __forceinline__ uint64_t v_desc(uint32_t base, int ks) {
   return make_sdesc(base + ks * 16 * C::kRowBytes, C::kBoxBytes, C::kSBO, C::kLayout);
 }
 
-// 2^x on the FMA/ALU pipes: round-to-nearest split x = j + f (f in [-0.5, 0.5]) with the
-// 1.5*2^23 magic-number add, degree-3 polynomial for 2^f (max rel. error 2.1e-4, well below
-// the bf16 rounding of P), exponent added in the integer domain.  Valid for x >= -126.
-__device__ __forceinline__ float exp2_poly(float x) {
-  x = fmaxf(x, -126.0f);
-  const float t = x + 12582912.0f;           // 1.5 * 2^23: low mantissa bits hold round(x)
-  const float f = x - (t - 12582912.0f);
-  float p = fmaf(0.054848f, f, 0.24180661f);
-  p = fmaf(p, f, 0.6932482f);
-  p = fmaf(p, f, 0.99998866f);
-  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+// Packed fp32x2 arithmetic (sm_100 FFMA2 / FADD2: two lanes' worth of FP32 work per issue slot).
+__device__ __forceinline__ void ffma2(float& d0, float& d1, float a0, float a1, float b0, float b1,
+                                      float c0, float c1) {
+  asm("{\n .reg .b64 a, b, c, d;\n mov.b64 a, {%2, %3};\n mov.b64 b, {%4, %5};\n"
+      " mov.b64 c, {%6, %7};\n fma.rn.f32x2 d, a, b, c;\n mov.b64 {%0, %1}, d;\n}"
+      : "=f"(d0), "=f"(d1) : "f"(a0), "f"(a1), "f"(b0), "f"(b1), "f"(c0), "f"(c1));
+}
+__device__ __forceinline__ void fadd2(float& d0, float& d1, float a0, float a1, float b0, float b1) {
+  asm("{\n .reg .b64 a, b, d;\n mov.b64 a, {%2, %3};\n mov.b64 b, {%4, %5};\n"
+      " add.rn.f32x2 d, a, b;\n mov.b64 {%0, %1}, d;\n}"
+      : "=f"(d0), "=f"(d1) : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
+
+// 2^x for a pair on the FMA/ALU pipes (FA4-style MUFU offload): round-to-nearest split
+// x = j + f (f in [-0.5, 0.5]) with the 1.5*2^23 magic-number add, degree-3 polynomial for 2^f
+// (max rel. error 2.1e-4, well below the bf16 rounding of P), exponent added in the integer
+// domain.  Inputs are clamped at -126 so the exponent field never underflows.
+__device__ __forceinline__ void exp2_poly2(float& y0, float& y1, float x0, float x1) {
+  constexpr float kMagic = 12582912.0f;   // 1.5 * 2^23
+  x0 = fmaxf(x0, -126.0f);
+  x1 = fmaxf(x1, -126.0f);
+  float t0, t1, r0, r1, f0, f1, p0, p1;
+  fadd2(t0, t1, x0, x1, kMagic, kMagic);          // low mantissa bits hold round(x)
+  fadd2(r0, r1, t0, t1, -kMagic, -kMagic);        // round(x) as float
+  ffma2(f0, f1, r0, r1, -1.0f, -1.0f, x0, x1);    // f = x - round(x)
+  ffma2(p0, p1, f0, f1, 0.054848f, 0.054848f, 0.24180661f, 0.24180661f);
+  ffma2(p0, p1, p0, p1, f0, f1, 0.6932482f, 0.6932482f);
+  ffma2(p0, p1, p0, p1, f0, f1, 0.99998866f, 0.99998866f);
+  y0 = __int_as_float(__float_as_int(p0) + (__float_as_int(t0) << 23));
+  y1 = __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23));
 }
 
 template <int D>
@@ -138,6 +157,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t sQ = smem_u32(smem + C::kQOff);
   const uint32_t sKV = smem_u32(smem + C::kKVOff);
 
+  // Register split (per SM sub-partition: one warp of each warpgroup): the control warpgroup
+  // drops to 88 registers so each softmax thread can hold its 128 scores and the packed P.
+  if (warp < 4) setmaxnreg_dec<88>();
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (nkv > 0 && elect_one()) {
@@ -167,21 +189,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (nkv > 0) {
       const uint32_t idesc_s = make_idesc_bf16(128, kBlockKeys, 0, 0);
       const uint32_t idesc_o = make_idesc_bf16(128, D, 0, 1);
-      const uint32_t tS[2] = {tmem, tmem + 128};
-      const uint32_t tO[2] = {tmem + 256, tmem + 256 + D};
       int stage = 0;
       uint32_t phase = 0;
       auto issue_s = [&](int i, uint32_t kbase) {
         const uint32_t qbase = sQ + i * C::kTileBytes;
 #pragma unroll
         for (int ks = 0; ks < D / 16; ++ks)
-          mma_ss(tS[i], kmajor_desc<D>(qbase, ks), kmajor_desc<D>(kbase, ks), idesc_s,
+          mma_ss(tmem + i * 128, kmajor_desc<D>(qbase, ks), kmajor_desc<D>(kbase, ks), idesc_s,
                  ks > 0 ? 1u : 0u);
       };
       auto issue_pv = [&](int i, uint32_t vbase, int j) {
 #pragma unroll
         for (int ks = 0; ks < kBlockKeys / 16; ++ks)
-          mma_ts(tO[i], tS[i] + ks * 8, v_desc<D>(vbase, ks), idesc_o, (j > 0 || ks > 0) ? 1u : 0u);
+          mma_ts(tmem + 256 + i * D, tmem + i * 128 + ks * 8, v_desc<D>(vbase, ks), idesc_o,
+                 (j > 0 || ks > 0) ? 1u : 0u);
       };
       mbar_wait(q_full, 0);
       // prologue: S_i for key tile 0
@@ -246,6 +267,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ softmax + epilogue
+    setmaxnreg_inc<208>();
     const int i = (warp - 4) >> 2;           // Q tile of this warpgroup
     const uint32_t sub = warp & 3;           // TMEM lane quarter
     const int row_in_unit = i * 128 + sub * 32 + lane;
@@ -266,22 +288,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld32(tS + 96, r + 96);
         tmem_ld_wait();
         const int valid = L - kBlockKeys * j;
-        // row max of the raw scores (scale > 0 commutes with max); 8 independent chains
-        float mx[8];
+        // row max of the raw scores (scale > 0 commutes with max); 4 independent chains that
+        // the compiler fuses into 3-input FMNMX3
+        if (valid < 128) {
 #pragma unroll
-        for (int e = 0; e < 8; ++e) mx[e] = -INFINITY;
-        if (valid >= 128) {
-#pragma unroll
-          for (int k = 0; k < 128; ++k) mx[k & 7] = fmaxf(mx[k & 7], __uint_as_float(r[k]));
-        } else {
-#pragma unroll
-          for (int k = 0; k < 128; ++k) {
+          for (int k = 0; k < 128; ++k)
             if (k >= valid) r[k] = __float_as_uint(-INFINITY);   // keys beyond L_b
-            mx[k & 7] = fmaxf(mx[k & 7], __uint_as_float(r[k]));
-          }
         }
-        const float mt = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
-                               fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) * sl2;
+        float mx[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) mx[e] = -INFINITY;
+#pragma unroll
+        for (int k = 0; k < 128; ++k) mx[k & 3] = fmaxf(mx[k & 3], __uint_as_float(r[k]));
+        const float mt = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * sl2;
         if (j == 0) {
           m_run = mt;
         } else {
@@ -308,35 +327,31 @@ __global__ void __launch_bounds__(kThreads, 1)
             tmem_st_wait();
           }
         }
-        // p = 2^(s*scale*log2e - m): one FFMA + exp2.  On full tiles one element in four takes
-        // a degree-3 polynomial exp2 on the FMA pipe (FA4-style MUFU offload); masked tiles
-        // use MUFU only so masked keys are exactly 0.
+        // p = 2^(s*scale*log2e - m): one FFMA2 per pair + exp2.  On full tiles one pair in four
+        // takes the polynomial exp2 on the FMA pipe; masked tiles use MUFU only so masked keys
+        // are exactly 0.  Row sum in two packed accumulators; P packed to bf16 in place.
         const float neg_m = -m_run;
-        float rsum[4] = {0.f, 0.f, 0.f, 0.f};
-        uint32_t pk[64];
-        if (valid >= 128) {
+        float a0 = 0.f, a1 = 0.f, b0 = 0.f, b1 = 0.f;
+        const bool full = valid >= 128;
 #pragma unroll
-          for (int k = 0; k < 64; ++k) {
-            const float x0 = fmaf(__uint_as_float(r[2 * k]), sl2, neg_m);
-            const float x1 = fmaf(__uint_as_float(r[2 * k + 1]), sl2, neg_m);
-            const float p0 = ex2(x0);
-            const float p1 = (k & 1) ? exp2_poly(x1) : ex2(x1);
-            rsum[k & 3] += p0 + p1;
-            pk[k] = pack_bf16x2(p0, p1);
+        for (int k = 0; k < 64; ++k) {
+          float x0, x1, p0, p1;
+          ffma2(x0, x1, __uint_as_float(r[2 * k]), __uint_as_float(r[2 * k + 1]), sl2, sl2, neg_m,
+                neg_m);
+          if ((k & 3) == 3 && full) {
+            exp2_poly2(p0, p1, x0, x1);
+          } else {
+            p0 = ex2(x0);
+            p1 = ex2(x1);
           }
-        } else {
-#pragma unroll
-          for (int k = 0; k < 64; ++k) {
-            const float p0 = ex2(fmaf(__uint_as_float(r[2 * k]), sl2, neg_m));
-            const float p1 = ex2(fmaf(__uint_as_float(r[2 * k + 1]), sl2, neg_m));
-            rsum[k & 3] += p0 + p1;
-            pk[k] = pack_bf16x2(p0, p1);
-          }
+          if (k & 1) fadd2(b0, b1, b0, b1, p0, p1);
+          else fadd2(a0, a1, a0, a1, p0, p1);
+          r[k] = pack_bf16x2(p0, p1);
         }
-        const float rs = (rsum[0] + rsum[1]) + (rsum[2] + rsum[3]);
+        const float rs = (a0 + a1) + (b0 + b1);
         l += rs;
-        tmem_st32(tS, pk);
-        tmem_st32(tS + 32, pk + 32);
+        tmem_st32(tS, r);
+        tmem_st32(tS + 32, r + 32);
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(&p_full[i]);

@@ -29,7 +29,7 @@ namespace gesr {
 
 namespace {
 
-constexpr int kThreads = 256;
+constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
 constexpr int kChunk = 256;               // candidates per CTA chunk
 constexpr int kPoolBuckets = 1024;        // 4-slot buckets per CTA (64 KB)
@@ -77,7 +77,7 @@ __device__ __forceinline__ int lookup(const HmaSmem& s, const HmaParams& p, int 
   return c;
 }
 
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 2)
     hma_kernel(const HmaParams p) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   HmaSmem& s = *reinterpret_cast<HmaSmem*>(smem_raw);
@@ -183,11 +183,23 @@ __global__ void __launch_bounds__(kThreads)
         if (lane < nseg)
           for (int q = my_off; q < my_end; ++q) own[q] = static_cast<unsigned short>(lane | (my_f << 5));
         __syncwarp();
-        for (int pos = lane; pos < n_ids; pos += 32) {
-          const unsigned long long key = static_cast<unsigned long long>(__ldg(ids + pos));
-          const int o = own[pos];
-          const int c = lookup(s, p, o >> 5, key);
-          if (c != 0) atomicAdd(&s.warp_cnt[warp][o & 31], c);
+        // 4 coalesced 256-byte loads in flight per warp before any lookup (latency hiding)
+        for (int base = 0; base < n_ids; base += 128) {
+          unsigned long long kk[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int pos = base + u * 32 + lane;
+            kk[u] = pos < n_ids ? static_cast<unsigned long long>(__ldg(ids + pos)) : 0ull;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int pos = base + u * 32 + lane;
+            if (pos < n_ids) {
+              const int o = own[pos];
+              const int c = lookup(s, p, o >> 5, kk[u]);
+              if (c != 0) atomicAdd(&s.warp_cnt[warp][o & 31], c);
+            }
+          }
         }
       } else {
         for (int base = 0; base < n_ids; base += 32) {
