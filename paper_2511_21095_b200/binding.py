@@ -21,7 +21,7 @@ from typing import Optional
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgesr.so")
+LIB_PATH = os.environ.get("GESR_LIB") or os.path.join(_HERE, "libgesr.so")
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "gesr.h")
 
 GESR_OK, GESR_ERR_INVALID_ARG, GESR_ERR_UNSUPPORTED, GESR_ERR_CUDA, GESR_ERR_WORKSPACE = range(5)

@@ -28,10 +28,25 @@
 
 namespace gesr {
 
+#ifdef GESR_TRACE
+// Debug-only timeline trace (build with -DGESR_TRACE): clock64 at pipeline events for the first
+// 64 CTAs and 32 key tiles.  Not part of the product library.
+__device__ unsigned long long g_trace[64][32][8];
+#define GESR_T(e, j)                                                                           \
+  do {                                                                                         \
+    const int _b = blockIdx.x + blockIdx.y * gridDim.x;                                        \
+    if (_b < 64 && (j) < 32) g_trace[_b][(j)][(e)] = clock64();                                \
+  } while (0)
+#else
+#define GESR_T(e, j) do {} while (0)
+#endif
+
 namespace {
 
-constexpr int kThreads = 384;     // WG0: TMA, MMA, 2 idle warps; WG1 / WG2: softmax
 constexpr int kBlockKeys = 128;
+#ifndef GESR_POLY_EVERY
+#define GESR_POLY_EVERY 1000   // one pair in N takes the FMA-pipe exp2 (off: measured slower)
+#endif
 
 template <int D>
 struct AttnCfg {
@@ -43,10 +58,23 @@ struct AttnCfg {
   static constexpr uint32_t kTileBytes = kColBlocks * kBoxBytes;  // 128 rows x D bf16
   static constexpr uint32_t kSBO = 8 * kRowBytes;                 // 8-row core-matrix group
   static constexpr int kStages = 4;
+  // softmax warps per (Q tile, TMEM lane quarter): 2 for d >= 64 (each takes half of the 128
+  // key columns of its 32 rows: more warps per sub-partition to hide latency), 1 for d = 32
+  static constexpr int kSplit = D >= 64 ? 2 : 1;
+  static constexpr int kThreads = 128 + 2 * 128 * kSplit;
+  // setmaxnreg budget: the CTA's register pool is (launch registers x threads), launch
+  // registers = floor(65536 / threads / 8) * 8; the split must fit in that pool.
+  static constexpr int kLaunchRegs = (65536 / kThreads) / 8 * 8;
+  static constexpr int kCtrlRegs = kSplit == 2 ? 56 : 88;
+  static constexpr int kSoftRegs = kSplit == 2 ? 104 : 208;
+  static_assert(128 * kCtrlRegs + 256 * kSplit * kSoftRegs <= kLaunchRegs * kThreads,
+                "setmaxnreg split exceeds the CTA register pool");
   static constexpr uint32_t kQOff = 0;
   static constexpr uint32_t kKVOff = 2 * kTileBytes;
   static constexpr uint32_t kBarOff = kKVOff + kStages * kTileBytes;
-  static constexpr uint32_t kSmemBytes = kBarOff + 256 + 1024;
+  static constexpr uint32_t kXchOff = kBarOff + 256;          // row-max / row-sum exchange
+  static constexpr uint32_t kXchBytes = 2 * 2 * 2 * 128 * 4 + 2 * 2 * 128 * 4;
+  static constexpr uint32_t kSmemBytes = kXchOff + kXchBytes + 1024;
 };
 
 // K-major operand (Q or K tile) descriptor for the 16-element K step `ks`.
@@ -98,7 +126,7 @@ __device__ __forceinline__ void exp2_poly2(float& y0, float& y1, float x0, float
 }
 
 template <int D>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(AttnCfg<D>::kThreads, 1)
     attn_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
                 const __grid_constant__ CUtensorMap map_v, const AttnParams p) {
   using C = AttnCfg<D>;
@@ -140,7 +168,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&p_full[i], 128);
+      mbar_init(&p_full[i], 128 * C::kSplit);
       mbar_init(&o_done[i], 1);
     }
     fence_mbar_init();
@@ -159,7 +187,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   // Register split (per SM sub-partition: one warp of each warpgroup): the control warpgroup
   // drops to 88 registers so each softmax thread can hold its 128 scores and the packed P.
-  if (warp < 4) setmaxnreg_dec<88>();
+  if (warp < 4) setmaxnreg_dec<C::kCtrlRegs>();
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (nkv > 0 && elect_one()) {
@@ -222,6 +250,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       __syncwarp();
       for (int j = 0; j < nkv; ++j) {
+        if (lane == 0) GESR_T(7, j);
         const int vslot = stage;
         mbar_wait(&kv_full[vslot], phase);
         if (++stage == C::kStages) { stage = 0; phase ^= 1; }
@@ -235,6 +264,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t kb = sKV + kslot * C::kTileBytes;
         // Q tile 0: O0 += P0 V_j, then S0 for the next key tile
         mbar_wait(&p_full[0], j & 1);
+        if (lane == 0) GESR_T(5, j);
         tc_fence_after();
         if (elect_one()) {
           issue_pv(0, vb, j);
@@ -247,6 +277,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         if (nq == 2) {
           mbar_wait(&p_full[1], j & 1);
+          if (lane == 0) GESR_T(6, j);
           tc_fence_after();
           if (elect_one()) {
             issue_pv(1, vb, j);
@@ -267,40 +298,59 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ softmax + epilogue
-    setmaxnreg_inc<208>();
-    const int i = (warp - 4) >> 2;           // Q tile of this warpgroup
-    const uint32_t sub = warp & 3;           // TMEM lane quarter
-    const int row_in_unit = i * 128 + sub * 32 + lane;
+    setmaxnreg_inc<C::kSoftRegs>();
+    constexpr int kSplit = C::kSplit;
+    constexpr int kCols = 128 / kSplit;        // S columns (keys) of this warp
+    constexpr int kOCols = D / kSplit;         // O columns of this warp
+    const int sw = warp - 4;
+    const int i = sw / (4 * kSplit);           // Q tile of this warp
+    const int half = (sw >> 2) % kSplit;       // column half (0 when kSplit == 1)
+    const uint32_t sub = warp & 3;             // TMEM lane quarter
+    const int rloc = sub * 32 + lane;          // row within the Q tile
+    const int row_in_unit = i * 128 + rloc;
+    // [tile][half][buffer][row] partial maxima, [tile][half][row] partial sums
+    float* xmax = reinterpret_cast<float*>(smem + C::kXchOff);
+    float* xsum = xmax + 2 * 2 * 2 * 128;
+    const uint32_t bar_id = 1 + i * 4 + sub;   // named barrier of the kSplit warps of a row set
     if (i < nq) {
       const uint32_t lane_addr = (sub * 32) << 16;
-      const uint32_t tS = tmem + lane_addr + i * 128;
-      const uint32_t tO = tmem + lane_addr + 256 + i * D;
+      const uint32_t tS = tmem + lane_addr + i * 128 + half * kCols;
+      const uint32_t tP = tmem + lane_addr + i * 128 + half * (kCols / 2);
+      const uint32_t tO = tmem + lane_addr + 256 + i * D + half * kOCols;
       const float sl2 = p.scale_log2;
       float m_run = -INFINITY;
       float l = 0.f;
       for (int j = 0; j < nkv; ++j) {
         mbar_wait(&s_full[i], j & 1);
+        const bool tr = (sub == 0 && half == 0 && lane == 0);
+        if (tr) GESR_T(i == 0 ? 0 : 3, j);
         tc_fence_after();
-        uint32_t r[128];
-        tmem_ld32(tS, r);
-        tmem_ld32(tS + 32, r + 32);
-        tmem_ld32(tS + 64, r + 64);
-        tmem_ld32(tS + 96, r + 96);
-        tmem_ld_wait();
-        const int valid = L - kBlockKeys * j;
-        // row max of the raw scores (scale > 0 commutes with max); 4 independent chains that
-        // the compiler fuses into 3-input FMNMX3
-        if (valid < 128) {
+        uint32_t r[kCols];
 #pragma unroll
-          for (int k = 0; k < 128; ++k)
+        for (int c = 0; c < kCols / 32; ++c) tmem_ld32(tS + c * 32, r + c * 32);
+        tmem_ld_wait();
+        const int valid = L - kBlockKeys * j - half * kCols;   // valid keys in my columns
+        if (valid < kCols) {
+#pragma unroll
+          for (int k = 0; k < kCols; ++k)
             if (k >= valid) r[k] = __float_as_uint(-INFINITY);   // keys beyond L_b
         }
-        float mx[4];
+        // row max of the raw scores (scale > 0 commutes with max); 8 independent chains
+        float mx[8];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) mx[e] = -INFINITY;
+        for (int e = 0; e < 8; ++e) mx[e] = -INFINITY;
 #pragma unroll
-        for (int k = 0; k < 128; ++k) mx[k & 3] = fmaxf(mx[k & 3], __uint_as_float(r[k]));
-        const float mt = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * sl2;
+        for (int k = 0; k < kCols; ++k) mx[k & 7] = fmaxf(mx[k & 7], __uint_as_float(r[k]));
+        float mraw = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                           fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+        if constexpr (kSplit == 2) {
+          float* xb = xmax + ((i * 2) * 2 + (j & 1)) * 128;   // [i][half][buf] base for half 0
+          xb[half * 2 * 128 + rloc] = mraw;
+          named_bar_sync(bar_id, 64);
+          mraw = fmaxf(mraw, xb[(1 - half) * 2 * 128 + rloc]);
+        }
+        const float mt = mraw * sl2;
+        if (tr && i == 0) GESR_T(1, j);
         if (j == 0) {
           m_run = mt;
         } else {
@@ -316,7 +366,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               l *= alpha;
             }
 #pragma unroll 1
-            for (int c = 0; c < D / 32; ++c) {
+            for (int c = 0; c < kOCols / 32; ++c) {
               uint32_t o[32];
               tmem_ld32(tO + c * 32, o);
               tmem_ld_wait();
@@ -327,36 +377,42 @@ __global__ void __launch_bounds__(kThreads, 1)
             tmem_st_wait();
           }
         }
-        // p = 2^(s*scale*log2e - m): one FFMA2 per pair + exp2.  On full tiles one pair in four
-        // takes the polynomial exp2 on the FMA pipe; masked tiles use MUFU only so masked keys
-        // are exactly 0.  Row sum in two packed accumulators; P packed to bf16 in place.
+        // p = 2^(s*scale*log2e - m): one FFMA2 per pair + exp2 (MUFU; on full tiles one pair in
+        // GESR_POLY_EVERY takes the FMA-pipe polynomial).  Masked keys give exactly 0.  Row sum
+        // in four packed accumulators; P packed to bf16 in place.
         const float neg_m = -m_run;
-        float a0 = 0.f, a1 = 0.f, b0 = 0.f, b1 = 0.f;
-        const bool full = valid >= 128;
+        float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        const bool full = valid >= kCols;
 #pragma unroll
-        for (int k = 0; k < 64; ++k) {
+        for (int k = 0; k < kCols / 2; ++k) {
           float x0, x1, p0, p1;
           ffma2(x0, x1, __uint_as_float(r[2 * k]), __uint_as_float(r[2 * k + 1]), sl2, sl2, neg_m,
                 neg_m);
-          if ((k & 3) == 3 && full) {
+          if ((k % GESR_POLY_EVERY) == GESR_POLY_EVERY - 1 && full) {
             exp2_poly2(p0, p1, x0, x1);
           } else {
             p0 = ex2(x0);
             p1 = ex2(x1);
           }
-          if (k & 1) fadd2(b0, b1, b0, b1, p0, p1);
-          else fadd2(a0, a1, a0, a1, p0, p1);
+          const int a = (k & 3) * 2;
+          fadd2(acc[a], acc[a + 1], acc[a], acc[a + 1], p0, p1);
           r[k] = pack_bf16x2(p0, p1);
         }
-        const float rs = (a0 + a1) + (b0 + b1);
-        l += rs;
-        tmem_st32(tS, r);
-        tmem_st32(tS + 32, r + 32);
+        l += ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+#pragma unroll
+        for (int c = 0; c < kCols / 64; ++c) tmem_st32(tP + c * 32, r + c * 32);
+        if constexpr (kCols / 2 % 32 != 0) tmem_st16(tP, r);
         tmem_st_wait();
         tc_fence_before();
+        if (tr) GESR_T(i == 0 ? 2 : 4, j);
         mbar_arrive(&p_full[i]);
       }
-      // epilogue
+      // epilogue: O / l for my columns
+      if constexpr (kSplit == 2) {
+        xsum[(i * 2 + half) * 128 + rloc] = l;
+        named_bar_sync(bar_id, 64);
+        l += xsum[(i * 2 + (1 - half)) * 128 + rloc];
+      }
       const bool row_ok = row_in_unit < rows_valid;
       const int64_t row = cbeg + row_in_unit;
       const int64_t HD = static_cast<int64_t>(p.H) * D;
@@ -365,8 +421,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
       }
       const float inv_l = nkv > 0 ? 1.0f / l : 0.f;
+      const int64_t col0 = static_cast<int64_t>(h) * D + half * kOCols;
 #pragma unroll 1
-      for (int c = 0; c < D / 32; ++c) {
+      for (int c = 0; c < kOCols / 32; ++c) {
         uint32_t o[32];
         if (nkv > 0) {
           tmem_ld32(tO + c * 32, o);
@@ -381,14 +438,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int e = 0; e < 16; ++e)
               pk2[e] = pack_bf16x2(__uint_as_float(o[2 * e]) * inv_l, __uint_as_float(o[2 * e + 1]) * inv_l);
-            uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.O) + row * HD +
-                                                  static_cast<int64_t>(h) * D + c * 32);
+            uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.O) + row * HD + col0 + c * 32);
 #pragma unroll
             for (int v = 0; v < 4; ++v)
               dst[v] = make_uint4(pk2[4 * v], pk2[4 * v + 1], pk2[4 * v + 2], pk2[4 * v + 3]);
           } else {
-            float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.O) + row * HD +
-                                                    static_cast<int64_t>(h) * D + c * 32);
+            float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.O) + row * HD + col0 + c * 32);
 #pragma unroll
             for (int v = 0; v < 8; ++v)
               dst[v] = make_float4(__uint_as_float(o[4 * v]) * inv_l, __uint_as_float(o[4 * v + 1]) * inv_l,
@@ -396,7 +451,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-      if (row_ok && p.lse != nullptr) {
+      if (row_ok && half == 0 && p.lse != nullptr) {
         // m_run and log2(l) are in log2 units of the scaled score
         p.lse[row * p.H + h] = nkv > 0 ? (m_run + __log2f(l)) * 0.69314718055994530942f : -INFINITY;
       }
@@ -478,11 +533,17 @@ cudaError_t launch_d(const CUtensorMap& mq, const CUtensorMap& mk, const CUtenso
     attr_done = true;
   }
   dim3 grid(static_cast<unsigned>(max_units), static_cast<unsigned>(p.H));
-  attn_kernel<D><<<grid, kThreads, C::kSmemBytes, stream>>>(mq, mk, mv, p);
+  attn_kernel<D><<<grid, C::kThreads, C::kSmemBytes, stream>>>(mq, mk, mv, p);
   return cudaGetLastError();
 }
 
 }  // namespace
+
+#ifdef GESR_TRACE
+extern "C" int gesr_debug_trace_copy(void* host) {
+  return static_cast<int>(cudaMemcpyFromSymbol(host, g_trace, sizeof(g_trace)));
+}
+#endif
 
 cudaError_t launch_build_units(const int64_t* cand_offsets, int64_t B, int2* units, int* count,
                                cudaStream_t stream) {
