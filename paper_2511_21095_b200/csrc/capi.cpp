@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -97,6 +98,16 @@ gesr_status make_out_map(CUtensorMap* map, void* base, uint64_t H, uint64_t M, u
   if (r != CUDA_SUCCESS)
     return fail(GESR_ERR_CUDA, "cuTensorMapEncodeTiled(%s) failed: %d", what, static_cast<int>(r));
   return GESR_OK;
+}
+
+// The CTA-pair attention kernel serves d = 128 unless GESR_ATTN_PAIR=0 (A/B switch for tests).
+bool pair_attention_enabled() {
+  static int cached = -1;
+  if (cached < 0) {
+    const char* v = getenv("GESR_ATTN_PAIR");
+    cached = (v != nullptr && v[0] == '0') ? 0 : 1;
+  }
+  return cached == 1;
 }
 
 bool valid_d(int32_t d) { return d == 32 || d == 64 || d == 128; }
@@ -276,6 +287,14 @@ gesr_status gesr_tasa_score(const void* T, int64_t total_C, int32_t D_in,
   if (s != GESR_OK) return s;
   s = make_map_2d(&mv, V_cache, static_cast<uint64_t>(H) * total_L, d, 128, box_cols, swz, "V");
   if (s != GESR_OK) return s;
+  if (d == 128 && pair_attention_enabled()) {
+    CUtensorMap mkh;
+    s = make_map_2d(&mkh, K_cache, static_cast<uint64_t>(H) * total_L, d, 64, 64, swz, "K half");
+    if (s != GESR_OK) return s;
+    e = gesr::launch_attn_pair(mq, mkh, mv, p, max_units(B, total_C), st);
+    if (e != cudaSuccess) return cuda_fail(e, "attn_pair_kernel launch");
+    return GESR_OK;
+  }
   e = gesr::launch_attn(d, mq, mk, mv, p, max_units(B, total_C), st);
   if (e != cudaSuccess) return cuda_fail(e, "attn_kernel launch");
   return GESR_OK;

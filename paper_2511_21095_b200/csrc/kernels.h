@@ -52,6 +52,10 @@ cudaError_t launch_build_units(const int64_t* cand_offsets, int64_t B, int2* uni
 cudaError_t launch_attn(int d, const CUtensorMap& map_q, const CUtensorMap& map_k,
                         const CUtensorMap& map_v, const AttnParams& p, int64_t max_units,
                         cudaStream_t stream);
+// d = 128: CTA-pair kernel (attn2.cu); K map box {64, 64}, Q / V maps box {64, 128}
+cudaError_t launch_attn_pair(const CUtensorMap& map_q, const CUtensorMap& map_kh,
+                             const CUtensorMap& map_vh, const AttnParams& p, int64_t max_units,
+                             cudaStream_t stream);
 cudaError_t launch_attn_empty(const AttnParams& p, int d, cudaStream_t stream);
 
 // ---------------------------------------------------------------- K-HMA (hma.cu)
