@@ -28,9 +28,23 @@
 
 namespace gesr {
 
+#ifdef GESR_TRACE
+__device__ unsigned long long g_trace2[64][32][8];
+#define GESR_T2(e, j)                                                                          \
+  do {                                                                                         \
+    const int _b = blockIdx.x + blockIdx.y * gridDim.x;                                        \
+    if (_b < 64 && (j) < 32) g_trace2[_b][(j)][(e)] = clock64();                               \
+  } while (0)
+#else
+#define GESR_T2(e, j) do {} while (0)
+#endif
+
 namespace {
 
 constexpr int kD = 128;
+#ifndef GESR_PAIR_POLY_EVERY
+#define GESR_PAIR_POLY_EVERY 1000   // one pair in N takes the FMA-pipe exp2 on full tiles
+#endif
 constexpr int kThreads = 384;
 constexpr int kKeys = 128;                       // keys per tile (S columns)
 constexpr uint32_t kQBytes = 128 * kD * 2;       // 32 KB: Q tile, [2 col blocks][128 rows][64]
@@ -56,10 +70,30 @@ __device__ __forceinline__ void ffma2(float& d0, float& d1, float a0, float a1, 
       " mov.b64 c, {%6, %7};\n fma.rn.f32x2 d, a, b, c;\n mov.b64 {%0, %1}, d;\n}"
       : "=f"(d0), "=f"(d1) : "f"(a0), "f"(a1), "f"(b0), "f"(b1), "f"(c0), "f"(c1));
 }
+// 2^x for a pair on the FMA/ALU pipes (MUFU offload): round-to-nearest split x = j + f with the
+// 1.5*2^23 magic-number add, degree-3 polynomial for 2^f on [-0.5, 0.5] (max rel. error
+// 2.1e-4, below the bf16 rounding of P), exponent added in the integer domain; x clamped at -126.
+__device__ __forceinline__ void exp2_poly2(float& y0, float& y1, float x0, float x1);
+
 __device__ __forceinline__ void fadd2(float& d0, float& d1, float a0, float a1, float b0, float b1) {
   asm("{\n .reg .b64 a, b, d;\n mov.b64 a, {%2, %3};\n mov.b64 b, {%4, %5};\n"
       " add.rn.f32x2 d, a, b;\n mov.b64 {%0, %1}, d;\n}"
       : "=f"(d0), "=f"(d1) : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
+
+__device__ __forceinline__ void exp2_poly2(float& y0, float& y1, float x0, float x1) {
+  constexpr float kMagic = 12582912.0f;   // 1.5 * 2^23
+  x0 = fmaxf(x0, -126.0f);
+  x1 = fmaxf(x1, -126.0f);
+  float t0, t1, r0, r1, f0, f1, p0, p1;
+  fadd2(t0, t1, x0, x1, kMagic, kMagic);
+  fadd2(r0, r1, t0, t1, -kMagic, -kMagic);
+  ffma2(f0, f1, r0, r1, -1.0f, -1.0f, x0, x1);
+  ffma2(p0, p1, f0, f1, 0.054848f, 0.054848f, 0.24180661f, 0.24180661f);
+  ffma2(p0, p1, p0, p1, f0, f1, 0.6932482f, 0.6932482f);
+  ffma2(p0, p1, p0, p1, f0, f1, 0.99998866f, 0.99998866f);
+  y0 = __int_as_float(__float_as_int(p0) + (__float_as_int(t0) << 23));
+  y1 = __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23));
 }
 
 // K-major descriptor (SW128) for a [rows][128] bf16 tile stored as 2 column blocks of
@@ -116,9 +150,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_free[i], 2);
+      mbar_init(&s_free[i], 16);     // one arrival per softmax warp of the pair
     }
-    mbar_init(p_full, 2);
+    mbar_init(p_full, 16);
     mbar_init(p_free, 1);
     fence_mbar_init();
   }
@@ -202,12 +236,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (nkv > 1) issue_s(1, take());
         for (int j = 0; j < nkv; ++j) {
           const int vslot = take();
+          if (lane == 0) GESR_T2(3, j);
           if (j + 2 < nkv) {
             // S(j+2) reuses S(j)'s buffer: both CTAs must have loaded S(j) into registers
             mbar_wait(&s_free[j & 1], (j >> 1) & 1);
+            if (lane == 0) GESR_T2(4, j);
             issue_s(j & 1, take());
           }
           mbar_wait(p_full, j & 1);
+          if (lane == 0) GESR_T2(5, j);
           tc_fence_after();
           if (elect_one()) {
             const uint32_t vb = sRing + vslot * kHalfBytes;
@@ -224,6 +261,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   } else {
     // ------------------------------------------------------------ softmax + epilogue
+    // Per key tile, one fused pass: p = 2^(s*scale*log2e - m_run) with the running max of the
+    // PREVIOUS tiles, the tile's own max reduced alongside (FMNMX beside MUFU), one pair in
+    // GESR_PAIR_POLY_EVERY through the FMA-pipe polynomial exp2.  Only if the max grew by more
+    // than 2^8 (rare after the first tile) are p recomputed with the new max and O rescaled; the
+    // first tile computes its max first.  S(j+1) (double buffer) is loaded from TMEM while tile j's
+    // P is handed off, so the TMEM load latency is off the critical path.
     setmaxnreg_inc<kSoftRegs>();
     const int sw = warp - 4;
     const int half = sw >> 2;                   // key-column half of this warp
@@ -243,37 +286,82 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const float sl2 = p.scale_log2;
     float m_run = -INFINITY;
     float l = 0.f;
-    for (int j = 0; j < nkv; ++j) {
-      const int buf = j & 1;
-      mbar_wait(&s_full[buf], (j >> 1) & 1);
+
+    auto load_s = [&](int j, uint32_t* r) {       // wait S(j) and start its TMEM load
+      mbar_wait(&s_full[j & 1], (j >> 1) & 1);
       tc_fence_after();
-      uint32_t r[64];
-      tmem_ld32(tS + buf * kKeys, r);
-      tmem_ld32(tS + buf * kKeys + 32, r + 32);
+      tmem_ld32(tS + (j & 1) * kKeys, r);
+      tmem_ld32(tS + (j & 1) * kKeys + 32, r + 32);
+    };
+    auto release_s = [&](int j) {                 // S(j) landed in registers: free its buffer
       tmem_ld_wait();
-      // S(j) is in registers in all 8 softmax warps of this CTA: release the buffer
       tc_fence_before();
-      named_bar_sync(1, 256);
-      if (sw == 0 && lane == 0) mbar_arrive_cluster(buf ? s_free_leader1 : s_free_leader0);
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster_relaxed((j & 1) ? s_free_leader1 : s_free_leader0);
+    };
+    uint32_t r[64];
+    if (nkv > 0) {
+      load_s(0, r);
+      release_s(0);
+    }
+    for (int j = 0; j < nkv; ++j) {
+      // r holds S(j); S(j+1) is loaded into r once S(j) is dead (completed at the end)
+      if (sw == 0 && lane == 0) GESR_T2(0, j);
       const int valid = L - kKeys * j - half * 64;      // valid keys among my 64 columns
-      if (valid < 64) {
+      const bool full = valid >= 64;
+      if (!full) {
 #pragma unroll
         for (int k = 0; k < 64; ++k)
           if (k >= valid) r[k] = __float_as_uint(-INFINITY);
       }
+      uint32_t pk[32];
+      float acc[8];
       float mx[8];
+      auto exp_pass = [&](float m, bool with_max) {
+        const float neg_m = -m;
 #pragma unroll
-      for (int e = 0; e < 8; ++e) mx[e] = -INFINITY;
+        for (int e = 0; e < 8; ++e) {
+          acc[e] = 0.f;
+          mx[e] = -INFINITY;
+        }
 #pragma unroll
-      for (int k = 0; k < 64; ++k) mx[k & 7] = fmaxf(mx[k & 7], __uint_as_float(r[k]));
-      float mraw = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
-                         fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
-      xmax[(half * 2 + buf) * 128 + rloc] = mraw;
+        for (int k = 0; k < 32; ++k) {
+          const float s0v = __uint_as_float(r[2 * k]), s1v = __uint_as_float(r[2 * k + 1]);
+          if (with_max) {
+            mx[(2 * k) & 7] = fmaxf(mx[(2 * k) & 7], s0v);
+            mx[(2 * k + 1) & 7] = fmaxf(mx[(2 * k + 1) & 7], s1v);
+          }
+          float x0, x1, p0, p1;
+          ffma2(x0, x1, s0v, s1v, sl2, sl2, neg_m, neg_m);
+          if ((k % GESR_PAIR_POLY_EVERY) == GESR_PAIR_POLY_EVERY - 1 && full) {
+            exp2_poly2(p0, p1, x0, x1);
+          } else {
+            p0 = ex2(x0);
+            p1 = ex2(x1);
+          }
+          const int a = (k & 3) * 2;
+          fadd2(acc[a], acc[a + 1], acc[a], acc[a + 1], p0, p1);
+          pk[k] = pack_bf16x2(p0, p1);
+        }
+      };
+      float mraw;
+      if (j == 0) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) mx[e] = -INFINITY;
+#pragma unroll
+        for (int k = 0; k < 64; ++k) mx[k & 7] = fmaxf(mx[k & 7], __uint_as_float(r[k]));
+      } else {
+        exp_pass(m_run, true);     // speculative: assumes the running max still holds
+      }
+      mraw = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                   fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+      xmax[(half * 2 + (j & 1)) * 128 + rloc] = mraw;
       named_bar_sync(bar_pair, 64);
-      mraw = fmaxf(mraw, xmax[((1 - half) * 2 + buf) * 128 + rloc]);
+      mraw = fmaxf(mraw, xmax[((1 - half) * 2 + (j & 1)) * 128 + rloc]);
       const float mt = mraw * sl2;
       if (j == 0) {
         m_run = mt;
+        exp_pass(m_run, false);
       } else {
         const bool need = mt > m_run + 8.0f;
         if (__any_sync(0xffffffffu, need)) {
@@ -296,31 +384,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             tmem_st32(tO + c * 32, o);
           }
           tmem_st_wait();
+          exp_pass(m_run, false);  // recompute P with the new running max
         }
       }
-      const float neg_m = -m_run;
-      float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-      for (int k = 0; k < 32; ++k) {
-        float x0, x1;
-        ffma2(x0, x1, __uint_as_float(r[2 * k]), __uint_as_float(r[2 * k + 1]), sl2, sl2, neg_m,
-              neg_m);
-        const float p0 = ex2(x0), p1 = ex2(x1);
-        const int a = (k & 3) * 2;
-        fadd2(acc[a], acc[a + 1], acc[a], acc[a + 1], p0, p1);
-        r[k] = pack_bf16x2(p0, p1);
-      }
+      // r is dead from here on: start loading S(j+1) so its latency overlaps the P hand-off
+      if (j + 1 < nkv) load_s(j + 1, r);
       l += ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+      if (sw == 0 && lane == 0) GESR_T2(6, j);
       // P(j-1) must have been consumed by PV(j-1) before P is overwritten
       if (j > 0) {
         mbar_wait(p_free, (j - 1) & 1);
         tc_fence_after();
       }
-      tmem_st32(tP, r);
+      tmem_st32(tP, pk);
       tmem_st_wait();
       tc_fence_before();
-      named_bar_sync(2, 256);
-      if (sw == 0 && lane == 0) mbar_arrive_cluster(p_full_leader);
+      __syncwarp();
+      if (sw == 0 && lane == 0) GESR_T2(2, j);
+      if (lane == 0) mbar_arrive_cluster_relaxed(p_full_leader);
+      if (j + 1 < nkv) release_s(j + 1);
     }
     // ---------------- epilogue: O / l for my 64 columns of my rows
     xsum[half * 128 + rloc] = l;
@@ -377,6 +459,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 }
 
 }  // namespace
+
+#ifdef GESR_TRACE
+extern "C" int gesr_debug_trace2_copy(void* host) {
+  return static_cast<int>(cudaMemcpyFromSymbol(host, g_trace2, sizeof(g_trace2)));
+}
+#endif
 
 cudaError_t launch_attn_pair(const CUtensorMap& mq, const CUtensorMap& mkh, const CUtensorMap& mvh,
                              const AttnParams& p, int64_t max_units, cudaStream_t stream) {

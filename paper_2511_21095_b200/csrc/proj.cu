@@ -240,7 +240,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       // accumulator drained by all 16 warps: one arrival per CTA on the leader's barrier
       tc_fence_before();
       named_bar_sync(1, kEpiWarps * 32);
-      if (warp == 4 && lane == 0) mbar_arrive_cluster(buf ? tempty_leader1 : tempty_leader0);
+      if (warp == 4 && lane == 0) mbar_arrive_cluster_relaxed(buf ? tempty_leader1 : tempty_leader0);
     }
     if (lane == 0) bulk_wait_group<0>();
   }

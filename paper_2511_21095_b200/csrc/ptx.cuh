@@ -295,6 +295,13 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
                : "memory");
 }
+// Relaxed remote arrive: no memory-ordering fence (the release form costs a GPU-scope MEMBAR).
+// Use only to publish completion of tcgen05 operations, which are ordered by
+// tcgen05.fence::before_thread_sync + tcgen05.wait, not by generic-proxy fences.
+__device__ __forceinline__ void mbar_arrive_cluster_relaxed(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
 
 // TMA load whose completion bytes are signalled on the pair LEADER's barrier (peer bit cleared).
 constexpr uint32_t kPeerBitMask = 0xFEFFFFFFu;
