@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(AttnCfg<D>::kThreads, 1)
       uint32_t phase = 0;
       for (int j = 0; j < nkv; ++j) {
         for (int which = 0; which < 2; ++which) {
-          mbar_wait(&kv_empty[stage], phase ^ 1);
+          mbar_wait_sleep(&kv_empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&kv_full[stage], C::kTileBytes);
           const CUtensorMap* m = which ? &map_v : &map_k;
           for (int cb = 0; cb < C::kColBlocks; ++cb)
@@ -232,10 +232,10 @@ __global__ void __launch_bounds__(AttnCfg<D>::kThreads, 1)
           mma_ts(tmem + 256 + i * D, tmem + i * 128 + ks * 8, v_desc<D>(vbase, ks), idesc_o,
                  (j > 0 || ks > 0) ? 1u : 0u);
       };
-      mbar_wait(q_full, 0);
+      mbar_wait_sleep(q_full, 0);
       // prologue: S_i for key tile 0
       int kslot = stage;
-      mbar_wait(&kv_full[kslot], phase);
+      mbar_wait_sleep(&kv_full[kslot], phase);
       tc_fence_after();
       if (++stage == C::kStages) { stage = 0; phase ^= 1; }
       if (elect_one()) {
@@ -252,18 +252,18 @@ __global__ void __launch_bounds__(AttnCfg<D>::kThreads, 1)
       for (int j = 0; j < nkv; ++j) {
         if (lane == 0) GESR_T(7, j);
         const int vslot = stage;
-        mbar_wait(&kv_full[vslot], phase);
+        mbar_wait_sleep(&kv_full[vslot], phase);
         if (++stage == C::kStages) { stage = 0; phase ^= 1; }
         const bool has_next = j + 1 < nkv;
         if (has_next) {
           kslot = stage;
-          mbar_wait(&kv_full[kslot], phase);
+          mbar_wait_sleep(&kv_full[kslot], phase);
           if (++stage == C::kStages) { stage = 0; phase ^= 1; }
         }
         const uint32_t vb = sKV + vslot * C::kTileBytes;
         const uint32_t kb = sKV + kslot * C::kTileBytes;
         // Q tile 0: O0 += P0 V_j, then S0 for the next key tile
-        mbar_wait(&p_full[0], j & 1);
+        mbar_wait_sleep(&p_full[0], j & 1);
         if (lane == 0) GESR_T(5, j);
         tc_fence_after();
         if (elect_one()) {
@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(AttnCfg<D>::kThreads, 1)
         }
         __syncwarp();
         if (nq == 2) {
-          mbar_wait(&p_full[1], j & 1);
+          mbar_wait_sleep(&p_full[1], j & 1);
           if (lane == 0) GESR_T(6, j);
           tc_fence_after();
           if (elect_one()) {
@@ -309,8 +309,8 @@ __global__ void __launch_bounds__(AttnCfg<D>::kThreads, 1)
     const int rloc = sub * 32 + lane;          // row within the Q tile
     const int row_in_unit = i * 128 + rloc;
     // [tile][half][buffer][row] partial maxima, [tile][half][row] partial sums
-    float* xmax = reinterpret_cast<float*>(smem + C::kXchOff);
-    float* xsum = xmax + 2 * 2 * 2 * 128;
+    const uint32_t xmax_s = smem_u32(smem + C::kXchOff);          // shared-space addresses
+    const uint32_t xsum_s = xmax_s + 2 * 2 * 2 * 128 * 4;
     const uint32_t bar_id = 1 + i * 4 + sub;   // named barrier of the kSplit warps of a row set
     if (i < nq) {
       const uint32_t lane_addr = (sub * 32) << 16;
@@ -321,7 +321,7 @@ __global__ void __launch_bounds__(AttnCfg<D>::kThreads, 1)
       float m_run = -INFINITY;
       float l = 0.f;
       for (int j = 0; j < nkv; ++j) {
-        mbar_wait(&s_full[i], j & 1);
+        mbar_wait_sleep(&s_full[i], j & 1);
         const bool tr = (sub == 0 && half == 0 && lane == 0);
         if (tr) GESR_T(i == 0 ? 0 : 3, j);
         tc_fence_after();
@@ -330,34 +330,74 @@ __global__ void __launch_bounds__(AttnCfg<D>::kThreads, 1)
         for (int c = 0; c < kCols / 32; ++c) tmem_ld32(tS + c * 32, r + c * 32);
         tmem_ld_wait();
         const int valid = L - kBlockKeys * j - half * kCols;   // valid keys in my columns
-        if (valid < kCols) {
+        const bool full = valid >= kCols;
+        if (!full) {
 #pragma unroll
           for (int k = 0; k < kCols; ++k)
             if (k >= valid) r[k] = __float_as_uint(-INFINITY);   // keys beyond L_b
         }
-        // row max of the raw scores (scale > 0 commutes with max); 8 independent chains
+        // One fused pass per tile: p = 2^(s*scale*log2e - m) with the running max m of the
+        // PREVIOUS tiles (speculative), the tile's own max reduced alongside (FMNMX beside
+        // MUFU).  Only if the max grew by > 2^8 (rare after the first tile) are p recomputed
+        // and O rescaled; the first tile reduces its max first.  Masked keys give exactly 0.
+        // P is packed in place into r[0 .. kCols/2): S stays intact in TMEM until P is stored
+        // over it, so the (rare) recompute reloads S from TMEM
+        uint32_t* pk = r;
+        float acc[8];
         float mx[8];
+        auto exp_pass = [&](float m, bool with_max) {
+          const float neg_m = -m;
 #pragma unroll
-        for (int e = 0; e < 8; ++e) mx[e] = -INFINITY;
+          for (int e = 0; e < 8; ++e) {
+            acc[e] = 0.f;
+            mx[e] = -INFINITY;
+          }
 #pragma unroll
-        for (int k = 0; k < kCols; ++k) mx[k & 7] = fmaxf(mx[k & 7], __uint_as_float(r[k]));
+          for (int k = 0; k < kCols / 2; ++k) {
+            const float s0v = __uint_as_float(r[2 * k]), s1v = __uint_as_float(r[2 * k + 1]);
+            if (with_max) {
+              mx[(2 * k) & 7] = fmaxf(mx[(2 * k) & 7], s0v);
+              mx[(2 * k + 1) & 7] = fmaxf(mx[(2 * k + 1) & 7], s1v);
+            }
+            float x0, x1, p0, p1;
+            ffma2(x0, x1, s0v, s1v, sl2, sl2, neg_m, neg_m);
+            if ((k % GESR_POLY_EVERY) == GESR_POLY_EVERY - 1 && full) {
+              exp2_poly2(p0, p1, x0, x1);
+            } else {
+              p0 = ex2(x0);
+              p1 = ex2(x1);
+            }
+            const int a = (k & 3) * 2;
+            fadd2(acc[a], acc[a + 1], acc[a], acc[a + 1], p0, p1);
+            pk[k] = pack_bf16x2(p0, p1);
+          }
+        };
+        if (j == 0) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) mx[e] = -INFINITY;
+#pragma unroll
+          for (int k = 0; k < kCols; ++k) mx[k & 7] = fmaxf(mx[k & 7], __uint_as_float(r[k]));
+        } else {
+          exp_pass(m_run, true);
+        }
         float mraw = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
                            fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
         if constexpr (kSplit == 2) {
-          float* xb = xmax + ((i * 2) * 2 + (j & 1)) * 128;   // [i][half][buf] base for half 0
-          xb[half * 2 * 128 + rloc] = mraw;
+          const uint32_t xb = xmax_s + (((i * 2) * 2 + (j & 1)) * 128 + rloc) * 4;   // [i][h][buf]
+          st_shared_f32(xb + half * 2 * 128 * 4, mraw);
           named_bar_sync(bar_id, 64);
-          mraw = fmaxf(mraw, xb[(1 - half) * 2 * 128 + rloc]);
+          mraw = fmaxf(mraw, ld_shared_f32(xb + (1 - half) * 2 * 128 * 4));
         }
         const float mt = mraw * sl2;
         if (tr && i == 0) GESR_T(1, j);
         if (j == 0) {
           m_run = mt;
+          exp_pass(m_run, false);
         } else {
           const bool need = mt > m_run + 8.0f;
           if (__any_sync(0xffffffffu, need)) {
             // O_i must hold P_{j-1} V_{j-1} before it is rescaled
-            mbar_wait(&o_done[i], (j - 1) & 1);
+            mbar_wait_sleep(&o_done[i], (j - 1) & 1);
             tc_fence_after();
             float alpha = 1.f;
             if (need) {
@@ -375,33 +415,21 @@ __global__ void __launch_bounds__(AttnCfg<D>::kThreads, 1)
               tmem_st32(tO + c * 32, o);
             }
             tmem_st_wait();
-          }
-        }
-        // p = 2^(s*scale*log2e - m): one FFMA2 per pair + exp2 (MUFU; on full tiles one pair in
-        // GESR_POLY_EVERY takes the FMA-pipe polynomial).  Masked keys give exactly 0.  Row sum
-        // in four packed accumulators; P packed to bf16 in place.
-        const float neg_m = -m_run;
-        float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        const bool full = valid >= kCols;
 #pragma unroll
-        for (int k = 0; k < kCols / 2; ++k) {
-          float x0, x1, p0, p1;
-          ffma2(x0, x1, __uint_as_float(r[2 * k]), __uint_as_float(r[2 * k + 1]), sl2, sl2, neg_m,
-                neg_m);
-          if ((k % GESR_POLY_EVERY) == GESR_POLY_EVERY - 1 && full) {
-            exp2_poly2(p0, p1, x0, x1);
-          } else {
-            p0 = ex2(x0);
-            p1 = ex2(x1);
+            for (int c = 0; c < kCols / 32; ++c) tmem_ld32(tS + c * 32, r + c * 32);
+            tmem_ld_wait();
+            if (!full) {
+#pragma unroll
+              for (int k = 0; k < kCols; ++k)
+                if (k >= valid) r[k] = __float_as_uint(-INFINITY);
+            }
+            exp_pass(m_run, false);   // recompute P with the new running max
           }
-          const int a = (k & 3) * 2;
-          fadd2(acc[a], acc[a + 1], acc[a], acc[a + 1], p0, p1);
-          r[k] = pack_bf16x2(p0, p1);
         }
         l += ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
 #pragma unroll
-        for (int c = 0; c < kCols / 64; ++c) tmem_st32(tP + c * 32, r + c * 32);
-        if constexpr (kCols / 2 % 32 != 0) tmem_st16(tP, r);
+        for (int c = 0; c < kCols / 64; ++c) tmem_st32(tP + c * 32, pk + c * 32);
+        if constexpr (kCols / 2 % 32 != 0) tmem_st16(tP, pk);
         tmem_st_wait();
         tc_fence_before();
         if (tr) GESR_T(i == 0 ? 2 : 4, j);
@@ -409,15 +437,15 @@ __global__ void __launch_bounds__(AttnCfg<D>::kThreads, 1)
       }
       // epilogue: O / l for my columns
       if constexpr (kSplit == 2) {
-        xsum[(i * 2 + half) * 128 + rloc] = l;
+        st_shared_f32(xsum_s + ((i * 2 + half) * 128 + rloc) * 4, l);
         named_bar_sync(bar_id, 64);
-        l += xsum[(i * 2 + (1 - half)) * 128 + rloc];
+        l += ld_shared_f32(xsum_s + ((i * 2 + (1 - half)) * 128 + rloc) * 4);
       }
       const bool row_ok = row_in_unit < rows_valid;
       const int64_t row = cbeg + row_in_unit;
       const int64_t HD = static_cast<int64_t>(p.H) * D;
       if (nkv > 0) {
-        mbar_wait(&o_done[i], (nkv - 1) & 1);
+        mbar_wait_sleep(&o_done[i], (nkv - 1) & 1);
         tc_fence_after();
       }
       const float inv_l = nkv > 0 ? 1.0f / l : 0.f;

@@ -182,7 +182,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         uint32_t phase = 0;
         // consumption order of the MMA issuer: K0, K1, then per j: V_j, K_{j+2}
         auto load_k = [&](int jj) {
-          mbar_wait(&kv_empty[stage], phase ^ 1);
+          mbar_wait_sleep(&kv_empty[stage], phase ^ 1);
           if (rank == 0) mbar_arrive_expect_tx(&kv_full[stage], 2 * kHalfBytes);
           uint8_t* dst = smem + kRingOff + stage * kHalfBytes;
           const int32_t row = krow + kKeys * jj + static_cast<int32_t>(rank) * 64;
@@ -191,7 +191,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         };
         auto load_v = [&](int jj) {
-          mbar_wait(&kv_empty[stage], phase ^ 1);
+          mbar_wait_sleep(&kv_empty[stage], phase ^ 1);
           if (rank == 0) mbar_arrive_expect_tx(&kv_full[stage], 2 * kHalfBytes);
           uint8_t* dst = smem + kRingOff + stage * kHalfBytes;
           tma_load_2d_pair(dst, &map_vh, &kv_full[stage], static_cast<int32_t>(rank) * 64,
@@ -214,7 +214,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         uint32_t phase = 0;
         auto take = [&]() {
           const int s = stage;
-          mbar_wait(&kv_full[s], phase);
+          mbar_wait_sleep(&kv_full[s], phase);
           if (++stage == kStages) { stage = 0; phase ^= 1; }
           return s;
         };
@@ -231,7 +231,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
           __syncwarp();
         };
-        mbar_wait(q_full, 0);
+        mbar_wait_sleep(q_full, 0);
         issue_s(0, take());
         if (nkv > 1) issue_s(1, take());
         for (int j = 0; j < nkv; ++j) {
@@ -239,11 +239,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if (lane == 0) GESR_T2(3, j);
           if (j + 2 < nkv) {
             // S(j+2) reuses S(j)'s buffer: both CTAs must have loaded S(j) into registers
-            mbar_wait(&s_free[j & 1], (j >> 1) & 1);
+            mbar_wait_sleep(&s_free[j & 1], (j >> 1) & 1);
             if (lane == 0) GESR_T2(4, j);
             issue_s(j & 1, take());
           }
-          mbar_wait(p_full, j & 1);
+          mbar_wait_sleep(p_full, j & 1);
           if (lane == 0) GESR_T2(5, j);
           tc_fence_after();
           if (elect_one()) {
@@ -288,7 +288,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     float l = 0.f;
 
     auto load_s = [&](int j, uint32_t* r) {       // wait S(j) and start its TMEM load
-      mbar_wait(&s_full[j & 1], (j >> 1) & 1);
+      mbar_wait_sleep(&s_full[j & 1], (j >> 1) & 1);
       tc_fence_after();
       tmem_ld32(tS + (j & 1) * kKeys, r);
       tmem_ld32(tS + (j & 1) * kKeys + 32, r + 32);
@@ -366,7 +366,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const bool need = mt > m_run + 8.0f;
         if (__any_sync(0xffffffffu, need)) {
           // O must hold PV(j-1) before it is rescaled
-          mbar_wait(p_free, (j - 1) & 1);
+          mbar_wait_sleep(p_free, (j - 1) & 1);
           tc_fence_after();
           float alpha = 1.f;
           if (need) {
@@ -393,7 +393,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       if (sw == 0 && lane == 0) GESR_T2(6, j);
       // P(j-1) must have been consumed by PV(j-1) before P is overwritten
       if (j > 0) {
-        mbar_wait(p_free, (j - 1) & 1);
+        mbar_wait_sleep(p_free, (j - 1) & 1);
         tc_fence_after();
       }
       tmem_st32(tP, pk);
@@ -412,7 +412,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int64_t row = cbeg + row_in_unit;
     const int64_t HD = static_cast<int64_t>(p.H) * kD;
     if (nkv > 0) {
-      mbar_wait(p_free, (nkv - 1) & 1);
+      mbar_wait_sleep(p_free, (nkv - 1) & 1);
       tc_fence_after();
     }
     const float inv_l = nkv > 0 ? 1.0f / l : 0.f;

@@ -127,7 +127,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int nb = ((n0 < p.n_split) ? n0 : n0 - p.n_split) + static_cast<int>(rank) * (BN / 2);
         const int ma = m_blk * 2 * kBM + static_cast<int>(rank) * kBM;
         for (int kb = 0; kb < num_kb; ++kb) {
-          mbar_wait(&empty_bar[stage], phase ^ 1);
+          mbar_wait_sleep(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = smem + stage * S::kStageBytes;
           uint8_t* sb = sa + kABytes;
           if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], 2 * S::kStageBytes);
@@ -147,11 +147,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       for (int tile = pair; tile < num_tiles; tile += npairs, ++local) {
         const uint32_t buf = local & 1;
         const uint32_t aphase = (local >> 1) & 1;
-        mbar_wait(&tempty_bar[buf], aphase ^ 1);
+        mbar_wait_sleep(&tempty_bar[buf], aphase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + buf * BN;
         for (int kb = 0; kb < num_kb; ++kb) {
-          mbar_wait(&full_bar[stage], phase);
+          mbar_wait_sleep(&full_bar[stage], phase);
           tc_fence_after();
           if (elect_one()) {
             const uint32_t sa = smem_u32(smem + stage * S::kStageBytes);
@@ -191,7 +191,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const uint32_t buf = local & 1;
       const uint32_t aphase = (local >> 1) & 1;
       const int row0 = m_blk * 2 * kBM + static_cast<int>(rank) * kBM + static_cast<int>(sub) * 32;
-      mbar_wait(&tfull_bar[buf], aphase);
+      mbar_wait_sleep(&tfull_bar[buf], aphase);
       tc_fence_after();
 #pragma unroll 1
       for (int c = c_begin; c < c_end; ++c) {

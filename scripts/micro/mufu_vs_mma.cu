@@ -1,0 +1,76 @@
+// Microbenchmark: does concurrent tcgen05.mma traffic slow the MUFU-bound softmax exp pass?
+// 8 warps run the exp pass (64 scores/thread); warp 8 optionally streams M=128 N=256 K=16 MMAs.
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "../../paper_2511_21095_b200/csrc/ptx.cuh"
+using namespace gesr;
+__device__ __forceinline__ uint32_t pack(float lo, float hi) { uint32_t r; asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo)); return r; }
+template <bool MMA>
+__global__ void __launch_bounds__(288, 1) k(uint32_t* out, int iters, float sl2, long long* clk) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint32_t tslot;
+  __shared__ uint64_t bar;
+  __shared__ int done;
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_mbar_init(); done = 0; }
+  if (warp == 8) { tmem_alloc(&tslot, 512); tmem_relinquish(); }
+  for (int i = threadIdx.x; i < 65536 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0;
+  tc_fence_before(); __syncthreads(); tc_fence_after();
+  const uint32_t tmem = tslot;
+  if (warp == 8) {
+    if (MMA) {
+      const uint32_t idesc = make_idesc_bf16(128, 256, 0, 0);
+      const uint32_t sa = smem_u32(smem), sb = sa + 16384;
+      uint32_t ph = 0;
+      while (atomicAdd(&done, 0) < 8) {
+        if (elect_one()) {
+          for (int i = 0; i < 64; ++i)
+            mma_ss(tmem, make_sdesc(sa + (i & 3) * 32, 16, 1024, kSwizzle128B),
+                   make_sdesc(sb + (i & 3) * 32, 16, 1024, kSwizzle128B), idesc, 1u);
+          mma_commit(&bar);
+        }
+        __syncwarp();
+        mbar_wait(&bar, ph); ph ^= 1;
+      }
+    }
+  } else {
+    uint32_t r[64];
+    for (int i = 0; i < 64; ++i) r[i] = __float_as_uint((threadIdx.x * 64 + i) * 1e-4f);
+    uint32_t sink = 0; float m = 0.5f;
+    long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+      uint32_t pk[32]; float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0}; const float nm = -m;
+#pragma unroll
+      for (int kk = 0; kk < 32; ++kk) {
+        const float x0 = fmaf(__uint_as_float(r[2 * kk]), sl2, nm), x1 = fmaf(__uint_as_float(r[2 * kk + 1]), sl2, nm);
+        const float p0 = ex2(x0), p1 = ex2(x1);
+        acc[(kk & 3) * 2] += p0; acc[(kk & 3) * 2 + 1] += p1;
+        pk[kk] = pack(p0, p1);
+      }
+      float l = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+      for (int kk = 0; kk < 32; ++kk) sink ^= pk[kk];
+      m += l * 1e-9f;
+    }
+    long long t1 = clock64();
+    if (sink == 0x1234567u) out[threadIdx.x] = sink;
+    if (threadIdx.x == 0) clk[blockIdx.x] = t1 - t0;
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) atomicAdd(&done, 1);
+  }
+  __syncthreads();
+  if (warp == 8) { tc_fence_after(); tmem_dealloc(tmem, 512); }
+}
+int main() {
+  uint32_t* d; cudaMalloc(&d, 4096); long long* c; cudaMalloc(&c, 4096 * 8);
+  int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  for (int v = 0; v < 2; ++v) {
+    auto kern = v ? k<true> : k<false>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+    kern<<<sms, 288, 65536>>>(d, 2000, 0.1f, c);
+    cudaError_t e = cudaDeviceSynchronize();
+    long long h[200]; cudaMemcpy(h, c, sms * 8, cudaMemcpyDeviceToHost);
+    printf("%s: %.1f clk per 64-score exp pass (err=%d)\n", v ? "with concurrent MMA" : "no MMA          ", double(h[0]) / 2000, (int)e);
+  }
+  return 0;
+}

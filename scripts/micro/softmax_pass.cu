@@ -24,6 +24,7 @@ __global__ void __launch_bounds__(256, 1) k(uint32_t* out, int iters, float sl2,
   for (int it = 0; it < iters; ++it) {
     uint32_t pk[32];
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    float mx[8] = {-1e30f, -1e30f, -1e30f, -1e30f, -1e30f, -1e30f, -1e30f, -1e30f};
     const float nm = -m;
 #pragma unroll
     for (int kk = 0; kk < 32; ++kk) {
@@ -31,13 +32,16 @@ __global__ void __launch_bounds__(256, 1) k(uint32_t* out, int iters, float sl2,
       ffma2(x0, x1, __uint_as_float(r[2 * kk]), __uint_as_float(r[2 * kk + 1]), sl2, sl2, nm, nm);
       const float p0 = ex2(x0), p1 = ex2(x1);
       const int a = (kk & 3) * 2;
-      if (VARIANT == 0) fadd2(acc[a], acc[a + 1], acc[a], acc[a + 1], p0, p1);
-      else { acc[a] += p0; acc[a + 1] += p1; }
+      fadd2(acc[a], acc[a + 1], acc[a], acc[a + 1], p0, p1);
+      if (VARIANT == 1) {
+        mx[(2 * kk) & 7] = fmaxf(mx[(2 * kk) & 7], __uint_as_float(r[2 * kk]));
+        mx[(2 * kk + 1) & 7] = fmaxf(mx[(2 * kk + 1) & 7], __uint_as_float(r[2 * kk + 1]));
+      }
       pk[kk] = pack(p0, p1);
     }
     float l = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
     for (int kk = 0; kk < 32; ++kk) sink ^= pk[kk];
-    m += l * 1e-9f;
+    m += l * 1e-9f + (mx[0] + mx[1] + mx[2] + mx[3] + mx[4] + mx[5] + mx[6] + mx[7]) * 1e-12f;
   }
   long long t1 = clock64();
   if (sink == 0x1234567u) out[threadIdx.x] = sink;
@@ -53,7 +57,7 @@ int main() {
     if (v == 0) k<0><<<sms, 256, 200000>>>(d, iters, 0.1f, c); else k<1><<<sms, 256, 200000>>>(d, iters, 0.1f, c);
     cudaDeviceSynchronize();
     long long h[200]; cudaMemcpy(h, c, sms * 8, cudaMemcpyDeviceToHost);
-    printf("variant %d: %.1f clk per 64-score exp pass (8 warps/SM: 2 per SMSP; MUFU bound 1024)\n", v, double(h[0]) / iters);
+    printf(v == 0 ? "exp pass      :" : "exp pass + max:"); printf(" variant %d: %.1f clk per 64-score exp pass (8 warps/SM: 2 per SMSP; MUFU bound 1024)\n", v, double(h[0]) / iters);
   }
   return 0;
 }
