@@ -31,11 +31,11 @@ namespace gesr {
 #ifdef GESR_TRACE
 // Debug-only timeline trace (build with -DGESR_TRACE): clock64 at pipeline events for the first
 // 64 CTAs and 32 key tiles.  Not part of the product library.
-__device__ unsigned long long g_trace[64][32][8];
+__device__ unsigned long long g_trace[64][64][8];
 #define GESR_T(e, j)                                                                           \
   do {                                                                                         \
     const int _b = blockIdx.x + blockIdx.y * gridDim.x;                                        \
-    if (_b < 64 && (j) < 32) g_trace[_b][(j)][(e)] = clock64();                                \
+    if (_b < 64 && (j) < 64) g_trace[_b][(j)][(e)] = clock64();                                \
   } while (0)
 #else
 #define GESR_T(e, j) do {} while (0)
@@ -130,29 +130,26 @@ __global__ void __launch_bounds__(AttnCfg<D>::kThreads, 1)
     attn_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
                 const __grid_constant__ CUtensorMap map_v, const AttnParams p) {
   using C = AttnCfg<D>;
-  const int u = blockIdx.x;
-  if (u >= __ldg(p.unit_count)) return;   // uniform for the whole CTA
-  const int h = blockIdx.y;
-  const int2 unit = p.units[u];
-  const int b = unit.x;
-  const int64_t s0 = p.seq_offsets[b];
-  const int L = static_cast<int>(p.seq_offsets[b + 1] - s0);
-  const int64_t cbeg = p.cand_offsets[b] + static_cast<int64_t>(unit.y) * kUnitRows;
-  const int64_t crem = p.cand_offsets[b + 1] - cbeg;
-  const int rows_valid = crem < kUnitRows ? static_cast<int>(crem) : kUnitRows;
-  const int nq = rows_valid > 128 ? 2 : 1;
-  const int nkv = (L + kBlockKeys - 1) / kBlockKeys;
+  // Persistent: CTA c processes work items w = c, c + G, ... of W = units x H, w -> (unit
+  // w % U, head w / U): neighbouring CTAs work on the pairs of the same (request, head) at the
+  // same time, so each K/V slab is fetched from HBM once and re-read from L2.  The next unit's
+  // Q load and first S MMA overlap the current unit's epilogue.
+  const int U = __ldg(p.unit_count);
+  const int W = U * p.H;
+  if (static_cast<int>(blockIdx.x) >= W) return;   // uniform for the whole CTA
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint64_t* q_full = reinterpret_cast<uint64_t*>(smem + C::kBarOff);
-  uint64_t* kv_full = q_full + 1;
+  uint64_t* q_empty = q_full + 1;
+  uint64_t* kv_full = q_empty + 1;
   uint64_t* kv_empty = kv_full + C::kStages;
   uint64_t* s_full = kv_empty + C::kStages;   // [2]
   uint64_t* p_full = s_full + 2;              // [2]
   uint64_t* o_done = p_full + 2;              // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
+  uint64_t* o_free = o_done + 2;              // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_free + 2);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -162,6 +159,7 @@ __global__ void __launch_bounds__(AttnCfg<D>::kThreads, 1)
     tma_prefetch_desc(&map_k);
     tma_prefetch_desc(&map_v);
     mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
     for (int s = 0; s < C::kStages; ++s) {
       mbar_init(&kv_full[s], 1);
       mbar_init(&kv_empty[s], 1);
@@ -170,6 +168,7 @@ __global__ void __launch_bounds__(AttnCfg<D>::kThreads, 1)
       mbar_init(&s_full[i], 1);
       mbar_init(&p_full[i], 128 * C::kSplit);
       mbar_init(&o_done[i], 1);
+      mbar_init(&o_free[i], 128 * C::kSplit);
     }
     fence_mbar_init();
   }
@@ -185,40 +184,76 @@ __global__ void __launch_bounds__(AttnCfg<D>::kThreads, 1)
   const uint32_t sQ = smem_u32(smem + C::kQOff);
   const uint32_t sKV = smem_u32(smem + C::kKVOff);
 
+  struct Work {
+    int h, L, rows_valid, nq, nkv;
+    int64_t s0, cbeg;
+  };
+  // the unit descriptor of work item w is one 16-byte load; it is fetched one item ahead and
+  // decoded only when used, so its latency overlaps the current unit
+  auto fetch = [&](int w) { return __ldg(p.units + (w % U)); };
+  auto decode = [&](int w, int4 d) {
+    Work x;
+    x.h = w / U;
+    x.s0 = d.x;
+    x.L = d.y;
+    x.cbeg = d.z;
+    x.rows_valid = d.w;
+    x.nq = x.rows_valid > 128 ? 2 : 1;
+    x.nkv = (x.L + kBlockKeys - 1) / kBlockKeys;
+    return x;
+  };
+
   // Register split (per SM sub-partition: one warp of each warpgroup): the control warpgroup
-  // drops to 88 registers so each softmax thread can hold its 128 scores and the packed P.
+  // drops registers so each softmax thread can hold its scores and the packed P.
   if (warp < 4) setmaxnreg_dec<C::kCtrlRegs>();
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
-    if (nkv > 0 && elect_one()) {
-      const int32_t qrow = static_cast<int32_t>(static_cast<int64_t>(h) * p.total_C + cbeg);
-      mbar_arrive_expect_tx(q_full, nq * C::kTileBytes);
-      for (int i = 0; i < nq; ++i)
-        for (int cb = 0; cb < C::kColBlocks; ++cb)
-          tma_load_2d(smem + C::kQOff + i * C::kTileBytes + cb * C::kBoxBytes, &map_q, q_full,
-                      cb * C::kBoxCols, qrow + 128 * i);
-      const int32_t krow = static_cast<int32_t>(static_cast<int64_t>(h) * p.total_L + s0);
+    if (elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int j = 0; j < nkv; ++j) {
-        for (int which = 0; which < 2; ++which) {
-          mbar_wait_sleep(&kv_empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&kv_full[stage], C::kTileBytes);
-          const CUtensorMap* m = which ? &map_v : &map_k;
+      int m = 0;                                 // units with key tiles so far
+      int4 nx = fetch(blockIdx.x);
+      for (int w = blockIdx.x; w < W; w += gridDim.x) {
+        const Work x = decode(w, nx);            // descriptor fetched one unit ahead
+        if (w + static_cast<int>(gridDim.x) < W) nx = fetch(w + gridDim.x);
+        if (x.nkv == 0) continue;
+        if (m > 0) mbar_wait_sleep(q_empty, (m - 1) & 1);   // previous unit's S MMAs done with Q
+        const int32_t qrow = static_cast<int32_t>(static_cast<int64_t>(x.h) * p.total_C + x.cbeg);
+        mbar_arrive_expect_tx(q_full, x.nq * C::kTileBytes);
+        for (int i = 0; i < x.nq; ++i)
           for (int cb = 0; cb < C::kColBlocks; ++cb)
-            tma_load_2d(smem + C::kKVOff + stage * C::kTileBytes + cb * C::kBoxBytes, m,
-                        &kv_full[stage], cb * C::kBoxCols, krow + kBlockKeys * j);
-          if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+            tma_load_2d(smem + C::kQOff + i * C::kTileBytes + cb * C::kBoxBytes, &map_q, q_full,
+                        cb * C::kBoxCols, qrow + 128 * i);
+        const int32_t krow = static_cast<int32_t>(static_cast<int64_t>(x.h) * p.total_L + x.s0);
+        for (int j = 0; j < x.nkv; ++j) {
+          for (int which = 0; which < 2; ++which) {
+            mbar_wait_sleep(&kv_empty[stage], phase ^ 1);
+            mbar_arrive_expect_tx(&kv_full[stage], C::kTileBytes);
+            const CUtensorMap* mp = which ? &map_v : &map_k;
+            for (int cb = 0; cb < C::kColBlocks; ++cb)
+              tma_load_2d(smem + C::kKVOff + stage * C::kTileBytes + cb * C::kBoxBytes, mp,
+                          &kv_full[stage], cb * C::kBoxCols, krow + kBlockKeys * j);
+            if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+          }
         }
+        ++m;
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    if (nkv > 0) {
-      const uint32_t idesc_s = make_idesc_bf16(128, kBlockKeys, 0, 0);
-      const uint32_t idesc_o = make_idesc_bf16(128, D, 0, 1);
-      int stage = 0;
-      uint32_t phase = 0;
+    const uint32_t idesc_s = make_idesc_bf16(128, kBlockKeys, 0, 0);
+    const uint32_t idesc_o = make_idesc_bf16(128, D, 0, 1);
+    int stage = 0;
+    uint32_t phase = 0;
+    int m = 0;                 // units with key tiles so far (q_full / q_empty phases)
+    int cnt[2] = {0, 0};       // key tiles processed per Q tile (s_full / p_full / o_done phases)
+    int act[2] = {0, 0};       // units with key tiles per Q tile (o_free phases)
+    int4 nx = fetch(blockIdx.x);
+    for (int w = blockIdx.x; w < W; w += gridDim.x) {
+      const Work x = decode(w, nx);              // descriptor fetched one unit ahead
+      if (w + static_cast<int>(gridDim.x) < W) nx = fetch(w + gridDim.x);
+      if (x.nkv == 0) continue;
+      const int nq = x.nq, nkv = x.nkv;
       auto issue_s = [&](int i, uint32_t kbase) {
         const uint32_t qbase = sQ + i * C::kTileBytes;
 #pragma unroll
@@ -232,8 +267,8 @@ __global__ void __launch_bounds__(AttnCfg<D>::kThreads, 1)
           mma_ts(tmem + 256 + i * D, tmem + i * 128 + ks * 8, v_desc<D>(vbase, ks), idesc_o,
                  (j > 0 || ks > 0) ? 1u : 0u);
       };
-      mbar_wait_sleep(q_full, 0);
-      // prologue: S_i for key tile 0
+      mbar_wait_sleep(q_full, m & 1);
+      // prologue: S_i for key tile 0 (S_i / P_i of the previous unit were consumed in order)
       int kslot = stage;
       mbar_wait_sleep(&kv_full[kslot], phase);
       tc_fence_after();
@@ -247,10 +282,10 @@ __global__ void __launch_bounds__(AttnCfg<D>::kThreads, 1)
           mma_commit(&s_full[1]);
         }
         mma_commit(&kv_empty[kslot]);
+        if (nkv == 1) mma_commit(q_empty);
       }
       __syncwarp();
       for (int j = 0; j < nkv; ++j) {
-        if (lane == 0) GESR_T(7, j);
         const int vslot = stage;
         mbar_wait_sleep(&kv_full[vslot], phase);
         if (++stage == C::kStages) { stage = 0; phase ^= 1; }
@@ -262,29 +297,19 @@ __global__ void __launch_bounds__(AttnCfg<D>::kThreads, 1)
         }
         const uint32_t vb = sKV + vslot * C::kTileBytes;
         const uint32_t kb = sKV + kslot * C::kTileBytes;
-        // Q tile 0: O0 += P0 V_j, then S0 for the next key tile
-        mbar_wait_sleep(&p_full[0], j & 1);
-        if (lane == 0) GESR_T(5, j);
-        tc_fence_after();
-        if (elect_one()) {
-          issue_pv(0, vb, j);
-          mma_commit(&o_done[0]);
-          if (has_next) {
-            issue_s(0, kb);
-            mma_commit(&s_full[0]);
-          }
-        }
-        __syncwarp();
-        if (nq == 2) {
-          mbar_wait_sleep(&p_full[1], j & 1);
-          if (lane == 0) GESR_T(6, j);
+        for (int i = 0; i < nq; ++i) {
+          // O_i += P_i V_j (the unit's first PV overwrites O_i: wait for the last epilogue),
+          // then S_i for the next key tile
+          if (j == 0 && act[i] > 0) mbar_wait_sleep(&o_free[i], (act[i] - 1) & 1);
+          mbar_wait_sleep(&p_full[i], (cnt[i] + j) & 1);
+          if (lane == 0) GESR_T(5 + i, cnt[i] + j);
           tc_fence_after();
           if (elect_one()) {
-            issue_pv(1, vb, j);
-            mma_commit(&o_done[1]);
+            issue_pv(i, vb, j);
+            mma_commit(&o_done[i]);
             if (has_next) {
-              issue_s(1, kb);
-              mma_commit(&s_full[1]);
+              issue_s(i, kb);
+              mma_commit(&s_full[i]);
             }
           }
           __syncwarp();
@@ -292,9 +317,15 @@ __global__ void __launch_bounds__(AttnCfg<D>::kThreads, 1)
         if (elect_one()) {
           mma_commit(&kv_empty[vslot]);
           if (has_next) mma_commit(&kv_empty[kslot]);
+          if (j + 2 == nkv) mma_commit(q_empty);     // the unit's last S MMAs were just issued
         }
         __syncwarp();
       }
+      for (int i = 0; i < nq; ++i) {
+        cnt[i] += nkv;
+        act[i] += 1;
+      }
+      ++m;
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ softmax + epilogue
@@ -312,18 +343,26 @@ __global__ void __launch_bounds__(AttnCfg<D>::kThreads, 1)
     const uint32_t xmax_s = smem_u32(smem + C::kXchOff);          // shared-space addresses
     const uint32_t xsum_s = xmax_s + 2 * 2 * 2 * 128 * 4;
     const uint32_t bar_id = 1 + i * 4 + sub;   // named barrier of the kSplit warps of a row set
-    if (i < nq) {
-      const uint32_t lane_addr = (sub * 32) << 16;
-      const uint32_t tS = tmem + lane_addr + i * 128 + half * kCols;
-      const uint32_t tP = tmem + lane_addr + i * 128 + half * (kCols / 2);
-      const uint32_t tO = tmem + lane_addr + 256 + i * D + half * kOCols;
-      const float sl2 = p.scale_log2;
+    const uint32_t lane_addr = (sub * 32) << 16;
+    const uint32_t tS = tmem + lane_addr + i * 128 + half * kCols;
+    const uint32_t tP = tmem + lane_addr + i * 128 + half * (kCols / 2);
+    const uint32_t tO = tmem + lane_addr + 256 + i * D + half * kOCols;
+    const float sl2 = p.scale_log2;
+    int cnt = 0;                                // key tiles processed by this Q tile so far
+    int4 nx = fetch(blockIdx.x);
+    for (int w = blockIdx.x; w < W; w += gridDim.x) {
+      const Work x = decode(w, nx);              // descriptor fetched one unit ahead
+      if (w + static_cast<int>(gridDim.x) < W) nx = fetch(w + gridDim.x);
+      if (i >= x.nq) continue;
+      const int L = x.L, nkv = x.nkv, rows_valid = x.rows_valid, h = x.h;
+      const int64_t cbeg = x.cbeg;
       float m_run = -INFINITY;
       float l = 0.f;
       for (int j = 0; j < nkv; ++j) {
-        mbar_wait_sleep(&s_full[i], j & 1);
+        const int gj = cnt + j;                 // global key-tile index of this Q tile
+        mbar_wait_sleep(&s_full[i], gj & 1);
         const bool tr = (sub == 0 && half == 0 && lane == 0);
-        if (tr) GESR_T(i == 0 ? 0 : 3, j);
+        if (tr) GESR_T(i == 0 ? 0 : 3, gj);
         tc_fence_after();
         uint32_t r[kCols];
 #pragma unroll
@@ -383,13 +422,13 @@ __global__ void __launch_bounds__(AttnCfg<D>::kThreads, 1)
         float mraw = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
                            fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
         if constexpr (kSplit == 2) {
-          const uint32_t xb = xmax_s + (((i * 2) * 2 + (j & 1)) * 128 + rloc) * 4;   // [i][h][buf]
+          const uint32_t xb = xmax_s + (((i * 2) * 2 + (gj & 1)) * 128 + rloc) * 4;   // [i][h][buf]
           st_shared_f32(xb + half * 2 * 128 * 4, mraw);
           named_bar_sync(bar_id, 64);
           mraw = fmaxf(mraw, ld_shared_f32(xb + (1 - half) * 2 * 128 * 4));
         }
         const float mt = mraw * sl2;
-        if (tr && i == 0) GESR_T(1, j);
+        if (tr && i == 0) GESR_T(1, gj);
         if (j == 0) {
           m_run = mt;
           exp_pass(m_run, false);
@@ -397,7 +436,7 @@ __global__ void __launch_bounds__(AttnCfg<D>::kThreads, 1)
           const bool need = mt > m_run + 8.0f;
           if (__any_sync(0xffffffffu, need)) {
             // O_i must hold P_{j-1} V_{j-1} before it is rescaled
-            mbar_wait_sleep(&o_done[i], (j - 1) & 1);
+            mbar_wait_sleep(&o_done[i], (gj - 1) & 1);
             tc_fence_after();
             float alpha = 1.f;
             if (need) {
@@ -432,7 +471,7 @@ __global__ void __launch_bounds__(AttnCfg<D>::kThreads, 1)
         if constexpr (kCols / 2 % 32 != 0) tmem_st16(tP, pk);
         tmem_st_wait();
         tc_fence_before();
-        if (tr) GESR_T(i == 0 ? 2 : 4, j);
+        if (tr) GESR_T(i == 0 ? 2 : 4, gj);
         mbar_arrive(&p_full[i]);
       }
       // epilogue: O / l for my columns
@@ -445,7 +484,7 @@ __global__ void __launch_bounds__(AttnCfg<D>::kThreads, 1)
       const int64_t row = cbeg + row_in_unit;
       const int64_t HD = static_cast<int64_t>(p.H) * D;
       if (nkv > 0) {
-        mbar_wait_sleep(&o_done[i], (nkv - 1) & 1);
+        mbar_wait_sleep(&o_done[i], (cnt + nkv - 1) & 1);
         tc_fence_after();
       }
       const float inv_l = nkv > 0 ? 1.0f / l : 0.f;
@@ -466,16 +505,15 @@ __global__ void __launch_bounds__(AttnCfg<D>::kThreads, 1)
 #pragma unroll
             for (int e = 0; e < 16; ++e)
               pk2[e] = pack_bf16x2(__uint_as_float(o[2 * e]) * inv_l, __uint_as_float(o[2 * e + 1]) * inv_l);
-            uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.O) + row * HD + col0 + c * 32);
-#pragma unroll
-            for (int v = 0; v < 4; ++v)
-              dst[v] = make_uint4(pk2[4 * v], pk2[4 * v + 1], pk2[4 * v + 2], pk2[4 * v + 3]);
+            __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(p.O) + row * HD + col0 + c * 32;
+            st_global_v8(dst, pk2);
+            st_global_v8(dst + 16, pk2 + 8);
           } else {
-            float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.O) + row * HD + col0 + c * 32);
+            float* dst = static_cast<float*>(p.O) + row * HD + col0 + c * 32;
 #pragma unroll
-            for (int v = 0; v < 8; ++v)
-              dst[v] = make_float4(__uint_as_float(o[4 * v]) * inv_l, __uint_as_float(o[4 * v + 1]) * inv_l,
-                                   __uint_as_float(o[4 * v + 2]) * inv_l, __uint_as_float(o[4 * v + 3]) * inv_l);
+            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * inv_l);
+#pragma unroll
+            for (int v = 0; v < 4; ++v) st_global_v8(dst + 8 * v, o + 8 * v);
           }
         }
       }
@@ -483,6 +521,13 @@ __global__ void __launch_bounds__(AttnCfg<D>::kThreads, 1)
         // m_run and log2(l) are in log2 units of the scaled score
         p.lse[row * p.H + h] = nkv > 0 ? (m_run + __log2f(l)) * 0.69314718055994530942f : -INFINITY;
       }
+      if (nkv > 0) {
+        // O_i drained: the next unit's first PV may overwrite it
+        if (i == 0 && sub == 0 && half == 0 && lane == 0) GESR_T(7, cnt + nkv - 1);
+        tc_fence_before();
+        mbar_arrive(&o_free[i]);
+      }
+      cnt += nkv;
     }
   }
 
@@ -494,8 +539,11 @@ __global__ void __launch_bounds__(AttnCfg<D>::kThreads, 1)
   }
 }
 
-__global__ void build_units_kernel(const int64_t* __restrict__ cand_offsets, int64_t B,
-                                   int2* __restrict__ units, int* __restrict__ count) {
+// Work list: one int4 per 256-candidate unit {first history row, L_b, first candidate row,
+// valid rows}, so the attention kernel decodes a unit with a single 16-byte load.
+__global__ void build_units_kernel(const int64_t* __restrict__ seq_offsets,
+                                   const int64_t* __restrict__ cand_offsets, int64_t B,
+                                   int4* __restrict__ units, int* __restrict__ count) {
   __shared__ int warp_sums[32];
   __shared__ int running;
   const int lane = threadIdx.x & 31;
@@ -506,8 +554,12 @@ __global__ void build_units_kernel(const int64_t* __restrict__ cand_offsets, int
   for (int64_t base = 0; base < B; base += blockDim.x) {
     const int64_t b = base + threadIdx.x;
     int n = 0;
+    int64_t c = 0, cb0 = 0, s0 = 0, L = 0;
     if (b < B) {
-      const int64_t c = cand_offsets[b + 1] - cand_offsets[b];
+      cb0 = cand_offsets[b];
+      c = cand_offsets[b + 1] - cb0;
+      s0 = seq_offsets[b];
+      L = seq_offsets[b + 1] - s0;
       n = static_cast<int>((c + kUnitRows - 1) / kUnitRows);
     }
     int x = n;
@@ -529,7 +581,12 @@ __global__ void build_units_kernel(const int64_t* __restrict__ cand_offsets, int
     }
     __syncthreads();
     const int excl = running + (x - n) + (w > 0 ? warp_sums[w - 1] : 0);
-    for (int k = 0; k < n; ++k) units[excl + k] = make_int2(static_cast<int>(b), k);
+    for (int k = 0; k < n; ++k) {
+      const int64_t rem = c - static_cast<int64_t>(k) * kUnitRows;
+      units[excl + k] = make_int4(static_cast<int>(s0), static_cast<int>(L),
+                                  static_cast<int>(cb0 + static_cast<int64_t>(k) * kUnitRows),
+                                  static_cast<int>(rem < kUnitRows ? rem : kUnitRows));
+    }
     __syncthreads();
     if (threadIdx.x == blockDim.x - 1) running = excl + n;
     __syncthreads();
@@ -560,7 +617,11 @@ cudaError_t launch_d(const CUtensorMap& mq, const CUtensorMap& mk, const CUtenso
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
-  dim3 grid(static_cast<unsigned>(max_units), static_cast<unsigned>(p.H));
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t work = max_units * p.H;
+  const unsigned grid = static_cast<unsigned>(work < sms ? work : sms);
   attn_kernel<D><<<grid, C::kThreads, C::kSmemBytes, stream>>>(mq, mk, mv, p);
   return cudaGetLastError();
 }
@@ -573,9 +634,9 @@ extern "C" int gesr_debug_trace_copy(void* host) {
 }
 #endif
 
-cudaError_t launch_build_units(const int64_t* cand_offsets, int64_t B, int2* units, int* count,
-                               cudaStream_t stream) {
-  build_units_kernel<<<1, 1024, 0, stream>>>(cand_offsets, B, units, count);
+cudaError_t launch_build_units(const int64_t* seq_offsets, const int64_t* cand_offsets, int64_t B,
+                               int4* units, int* count, cudaStream_t stream) {
+  build_units_kernel<<<1, 1024, 0, stream>>>(seq_offsets, cand_offsets, B, units, count);
   return cudaGetLastError();
 }
 

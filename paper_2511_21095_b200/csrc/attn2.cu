@@ -115,13 +115,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   if (u >= __ldg(p.unit_count)) return;   // uniform for the pair
   const uint32_t rank = cluster_ctarank();
   const int h = blockIdx.y;
-  const int2 unit = p.units[u];
-  const int b = unit.x;
-  const int64_t s0 = p.seq_offsets[b];
-  const int L = static_cast<int>(p.seq_offsets[b + 1] - s0);
-  const int64_t cbeg = p.cand_offsets[b] + static_cast<int64_t>(unit.y) * kUnitRows;
-  const int64_t crem = p.cand_offsets[b + 1] - cbeg;
-  const int rows_valid = crem < kUnitRows ? static_cast<int>(crem) : kUnitRows;
+  const int4 unit = p.units[u];
+  const int64_t s0 = unit.x;
+  const int L = unit.y;
+  const int64_t cbeg = unit.z;
+  const int rows_valid = unit.w;
   const int nkv = (L + kKeys - 1) / kKeys;
 
   extern __shared__ uint8_t smem_raw[];

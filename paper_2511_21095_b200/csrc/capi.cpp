@@ -129,7 +129,7 @@ int64_t max_units(int64_t B, int64_t total_C) {
   return B + (total_C + gesr::kUnitRows - 1) / gesr::kUnitRows;
 }
 size_t units_end(int64_t B, int64_t total_C) {
-  size_t e = 256 + static_cast<size_t>(max_units(B, total_C)) * sizeof(int2);
+  size_t e = 256 + static_cast<size_t>(max_units(B, total_C)) * sizeof(int4);
   return (e + 1023) & ~static_cast<size_t>(1023);
 }
 
@@ -269,12 +269,12 @@ gesr_status gesr_tasa_score(const void* T, int64_t total_C, int32_t D_in,
 
   uint8_t* ws = static_cast<uint8_t*>(workspace);
   int* count = reinterpret_cast<int*>(ws);
-  int2* units = reinterpret_cast<int2*>(ws + 256);
+  int4* units = reinterpret_cast<int4*>(ws + 256);
   void* Q = ws + units_end(B, total_C);
   p.units = units;
   p.unit_count = count;
 
-  cudaError_t e = gesr::launch_build_units(cand_offsets, B, units, count, st);
+  cudaError_t e = gesr::launch_build_units(seq_offsets, cand_offsets, B, units, count, st);
   if (e != cudaSuccess) return cuda_fail(e, "build_units launch");
   s = run_projection(T, total_C, D_in, W_q, nullptr, b_q, nullptr, H, d, act, Q, nullptr, st);
   if (s != GESR_OK) return s;

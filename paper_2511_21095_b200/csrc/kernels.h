@@ -34,7 +34,7 @@ cudaError_t launch_proj(const CUtensorMap& map_a, const CUtensorMap& map_b0,
 struct AttnParams {
   const int64_t* seq_offsets;
   const int64_t* cand_offsets;
-  const int2* units;       // (b, pair index) work list
+  const int4* units;       // work list: {first history row s0, L_b, first candidate row, rows}
   const int* unit_count;
   int64_t total_C;
   int64_t total_L;
@@ -47,7 +47,8 @@ struct AttnParams {
 
 constexpr int kUnitRows = 256;   // candidates per work unit (two 128-row Q tiles)
 
-cudaError_t launch_build_units(const int64_t* cand_offsets, int64_t B, int2* units, int* count,
+cudaError_t launch_build_units(const int64_t* seq_offsets, const int64_t* cand_offsets, int64_t B,
+                               int4* units, int* count,
                                cudaStream_t stream);
 cudaError_t launch_attn(int d, const CUtensorMap& map_q, const CUtensorMap& map_k,
                         const CUtensorMap& map_v, const AttnParams& p, int64_t max_units,
