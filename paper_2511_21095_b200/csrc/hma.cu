@@ -161,18 +161,32 @@ __global__ void __launch_bounds__(kThreads, 2)
   }
   __syncthreads();
 
-  // ---- 2. coalesced scan of the item-ID stream, 32 segments per warp step
+  // ---- 2. coalesced scan of the item-ID stream, 32 segments per warp step.  The next group's
+  //         offsets are fetched while the current group is processed, and all of a group's IDs
+  //         (up to kUnroll per lane) are loaded before the first lookup, so each warp keeps
+  //         ~2 KB of loads in flight.
+  constexpr int kUnroll = 16;
   unsigned short* own = s.owner[warp];
   for (int64_t c0 = first; c0 < ce; c0 += static_cast<int64_t>(gridDim.y) * kChunk) {
     const int64_t c1 = (c0 + kChunk < ce) ? c0 + kChunk : ce;
     const int64_t seg_begin = c0 * F, seg_end = c1 * F;
-    for (int64_t g = seg_begin + static_cast<int64_t>(warp) * 32; g < seg_end;
-         g += static_cast<int64_t>(kWarps) * 32) {
+    int64_t g = seg_begin + static_cast<int64_t>(warp) * 32;
+    int64_t off_cur = 0, end_cur = 0;
+    auto fetch_offsets = [&](int64_t gg, int64_t& o, int64_t& e) {
+      if (gg < seg_end) {
+        const int ns = (seg_end - gg) < 32 ? static_cast<int>(seg_end - gg) : 32;
+        o = __ldg(p.item_offsets + gg + (lane < ns ? lane : ns));
+        e = __ldg(p.item_offsets + gg + ns);
+      }
+    };
+    fetch_offsets(g, off_cur, end_cur);
+    for (; g < seg_end; g += static_cast<int64_t>(kWarps) * 32) {
       const int nseg = (seg_end - g) < 32 ? static_cast<int>(seg_end - g) : 32;
       // lane k holds the start offset of segment g+k; lanes nseg..31 hold the end offset
-      const int64_t my_off64 = p.item_offsets[g + (lane < nseg ? lane : nseg)];
+      const int64_t my_off64 = off_cur;
+      const int64_t end = end_cur;
+      fetch_offsets(g + static_cast<int64_t>(kWarps) * 32, off_cur, end_cur);   // prefetch next
       const int64_t start = __shfl_sync(0xffffffffu, my_off64, 0);
-      const int64_t end = p.item_offsets[g + nseg];   // same address for all lanes: broadcast
       const int my_off = static_cast<int>(my_off64 - start);
       const int nxt = __shfl_down_sync(0xffffffffu, my_off, 1);
       const int n_ids = static_cast<int>(end - start);
@@ -180,19 +194,20 @@ __global__ void __launch_bounds__(kThreads, 2)
       const int my_f = static_cast<int>(g - seg_begin + lane) % F;   // seg_begin % F == 0
       const int64_t* ids = p.item_ids + start;
       if (n_ids <= kOwnerCap) {
-        if (lane < nseg)
-          for (int q = my_off; q < my_end; ++q) own[q] = static_cast<unsigned short>(lane | (my_f << 5));
-        __syncwarp();
-        // 4 coalesced 256-byte loads in flight per warp before any lookup (latency hiding)
-        for (int base = 0; base < n_ids; base += 128) {
-          unsigned long long kk[4];
+        for (int base = 0; base < n_ids; base += kUnroll * 32) {
+          unsigned long long kk[kUnroll];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
+          for (int u = 0; u < kUnroll; ++u) {
             const int pos = base + u * 32 + lane;
             kk[u] = pos < n_ids ? static_cast<unsigned long long>(__ldg(ids + pos)) : 0ull;
           }
+          if (base == 0) {
+            if (lane < nseg)
+              for (int q = my_off; q < my_end; ++q) own[q] = static_cast<unsigned short>(lane | (my_f << 5));
+            __syncwarp();
+          }
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
+          for (int u = 0; u < kUnroll; ++u) {
             const int pos = base + u * 32 + lane;
             if (pos < n_ids) {
               const int o = own[pos];
