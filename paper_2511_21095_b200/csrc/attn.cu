@@ -44,6 +44,9 @@ __device__ unsigned long long g_trace[64][64][8];
 namespace {
 
 constexpr int kBlockKeys = 128;
+#ifndef GESR_ATTN_SPLIT
+#define GESR_ATTN_SPLIT 1      // softmax warps per TMEM lane quarter and Q tile (d >= 64); 2 measured slower
+#endif
 #ifndef GESR_POLY_EVERY
 #define GESR_POLY_EVERY 1000   // one pair in N takes the FMA-pipe exp2 (off: measured slower)
 #endif
@@ -60,7 +63,7 @@ struct AttnCfg {
   static constexpr int kStages = 4;
   // softmax warps per (Q tile, TMEM lane quarter): 2 for d >= 64 (each takes half of the 128
   // key columns of its 32 rows: more warps per sub-partition to hide latency), 1 for d = 32
-  static constexpr int kSplit = D >= 64 ? 2 : 1;
+  static constexpr int kSplit = D >= 64 ? GESR_ATTN_SPLIT : 1;
   static constexpr int kThreads = 128 + 2 * 128 * kSplit;
   // setmaxnreg budget: the CTA's register pool is (launch registers x threads), launch
   // registers = floor(65536 / threads / 8) * 8; the split must fit in that pool.

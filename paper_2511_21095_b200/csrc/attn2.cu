@@ -349,7 +349,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int k = 0; k < 64; ++k) mx[k & 7] = fmaxf(mx[k & 7], __uint_as_float(r[k]));
       } else {
+        if (sw == 0 && lane == 0) GESR_T2(1, j);
         exp_pass(m_run, true);     // speculative: assumes the running max still holds
+        if (sw == 0 && lane == 0) GESR_T2(7, j);
       }
       mraw = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
                    fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));

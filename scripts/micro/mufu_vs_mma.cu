@@ -14,8 +14,8 @@ __global__ void __launch_bounds__(288, 1) k(uint32_t* out, int iters, float sl2,
   __shared__ int done;
   const int warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_mbar_init(); done = 0; }
-  if (warp == 8) { tmem_alloc(&tslot, 512); tmem_relinquish(); }
-  for (int i = threadIdx.x; i < 65536 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0;
+  if (MMA && warp == 8) { tmem_alloc(&tslot, 512); tmem_relinquish(); }
+  for (int i = threadIdx.x; i < 200000 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0;
   tc_fence_before(); __syncthreads(); tc_fence_after();
   const uint32_t tmem = tslot;
   if (warp == 8) {
@@ -59,15 +59,15 @@ __global__ void __launch_bounds__(288, 1) k(uint32_t* out, int iters, float sl2,
     if ((threadIdx.x & 31) == 0) atomicAdd(&done, 1);
   }
   __syncthreads();
-  if (warp == 8) { tc_fence_after(); tmem_dealloc(tmem, 512); }
+  if (MMA && warp == 8) { tc_fence_after(); tmem_dealloc(tmem, 512); }
 }
 int main() {
   uint32_t* d; cudaMalloc(&d, 4096); long long* c; cudaMalloc(&c, 4096 * 8);
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   for (int v = 0; v < 2; ++v) {
     auto kern = v ? k<true> : k<false>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
-    kern<<<sms, 288, 65536>>>(d, 2000, 0.1f, c);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200000);
+    kern<<<sms, 288, 200000>>>(d, 2000, 0.1f, c);
     cudaError_t e = cudaDeviceSynchronize();
     long long h[200]; cudaMemcpy(h, c, sms * 8, cudaMemcpyDeviceToHost);
     printf("%s: %.1f clk per 64-score exp pass (err=%d)\n", v ? "with concurrent MMA" : "no MMA          ", double(h[0]) / 2000, (int)e);

@@ -16,7 +16,7 @@ for _ in range(3):
 torch.cuda.synchronize()
 buf = np.zeros((64, 32, 8), np.uint64)
 assert gb.lib().gesr_debug_trace2_copy(ctypes.c_void_p(buf.ctypes.data)) == 0
-names = ["s_ready", "s_freed", "p_done", "mma_step", "mma_sfree", "mma_pfull", "sm_exp_end", "sm_pfree"]
+names = ["s_ready", "exp_start", "p_done", "mma_step", "mma_sfree", "mma_pfull", "sm_exp_end", "exp_done"]
 for cta in (0, 1, 20, 21):
     t = buf[cta].astype(np.int64)
     base = t[0, 0] if t[0, 0] else t[0, 3]
@@ -25,3 +25,4 @@ for cta in (0, 1, 20, 21):
     for j in range(16):
         print(f"  {j:2d} " + " ".join(f"{int(t[j, e] - base) if t[j, e] else 0:10d}" for e in range(8)))
     print("  softmax period (s_ready diffs):", np.diff(t[:16, 0]).tolist())
+    print("  exp pass (exp_done - exp_start):", (t[1:16, 7] - t[1:16, 1]).tolist())
