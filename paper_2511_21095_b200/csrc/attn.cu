@@ -76,8 +76,13 @@ struct AttnCfg {
   static constexpr uint32_t kKVOff = 2 * kTileBytes;
   static constexpr uint32_t kBarOff = kKVOff + kStages * kTileBytes;
   static constexpr uint32_t kXchOff = kBarOff + 256;          // row-max / row-sum exchange
-  static constexpr uint32_t kXchBytes = 2 * 2 * 2 * 128 * 4 + 2 * 2 * 128 * 4;
-  static constexpr uint32_t kSmemBytes = kXchOff + kXchBytes + 1024;
+  static constexpr uint32_t kXchBytes = kSplit == 2 ? 2 * 2 * 2 * 128 * 4 + 2 * 2 * 128 * 4 : 0;
+  // bf16 O epilogue staging (kSplit == 1): two 2 KB boxes (32 rows x 32 columns, 64B swizzle)
+  // per softmax warp, drained by TMA tensor stores while the warp moves on to the next unit
+  static constexpr uint32_t kStgOff = (kXchOff + kXchBytes + 1023) / 1024 * 1024;   // swizzle atom aligned
+  static constexpr uint32_t kStgBytes = kSplit == 1 ? 8 * 2 * 2048 : 0;
+  static constexpr uint32_t kSmemBytes = kStgOff + kStgBytes + 1024;
+  static_assert(kSmemBytes <= 232448, "shared memory budget");
 };
 
 // K-major operand (Q or K tile) descriptor for the 16-element K step `ks`.
@@ -131,7 +136,8 @@ __device__ __forceinline__ void exp2_poly2(float& y0, float& y1, float x0, float
 template <int D>
 __global__ void __launch_bounds__(AttnCfg<D>::kThreads, 1)
     attn_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
-                const __grid_constant__ CUtensorMap map_v, const AttnParams p) {
+                const __grid_constant__ CUtensorMap map_v, const __grid_constant__ CUtensorMap map_o,
+                const AttnParams p) {
   using C = AttnCfg<D>;
   // Persistent: CTA c processes work items w = c, c + G, ... of W = units x H, w -> (unit
   // w % U, head w / U): neighbouring CTAs work on the pairs of the same (request, head) at the
@@ -161,6 +167,7 @@ __global__ void __launch_bounds__(AttnCfg<D>::kThreads, 1)
     tma_prefetch_desc(&map_q);
     tma_prefetch_desc(&map_k);
     tma_prefetch_desc(&map_v);
+    if (p.o_tma) tma_prefetch_desc(&map_o);
     mbar_init(q_full, 1);
     mbar_init(q_empty, 1);
     for (int s = 0; s < C::kStages; ++s) {
@@ -169,9 +176,9 @@ __global__ void __launch_bounds__(AttnCfg<D>::kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&p_full[i], 128 * C::kSplit);
+      mbar_init(&p_full[i], 4 * C::kSplit);    // one arrival per softmax warp
       mbar_init(&o_done[i], 1);
-      mbar_init(&o_free[i], 128 * C::kSplit);
+      mbar_init(&o_free[i], 4 * C::kSplit);
     }
     fence_mbar_init();
   }
@@ -342,6 +349,7 @@ __global__ void __launch_bounds__(AttnCfg<D>::kThreads, 1)
     const uint32_t sub = warp & 3;             // TMEM lane quarter
     const int rloc = sub * 32 + lane;          // row within the Q tile
     const int row_in_unit = i * 128 + rloc;
+    uint8_t* stg = smem + C::kStgOff + sw * 4096;   // used only when kSplit == 1
     // [tile][half][buffer][row] partial maxima, [tile][half][row] partial sums
     const uint32_t xmax_s = smem_u32(smem + C::kXchOff);          // shared-space addresses
     const uint32_t xsum_s = xmax_s + 2 * 2 * 2 * 128 * 4;
@@ -475,7 +483,8 @@ __global__ void __launch_bounds__(AttnCfg<D>::kThreads, 1)
         tmem_st_wait();
         tc_fence_before();
         if (tr) GESR_T(i == 0 ? 2 : 4, gj);
-        mbar_arrive(&p_full[i]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[i]);
       }
       // epilogue: O / l for my columns
       if constexpr (kSplit == 2) {
@@ -492,6 +501,10 @@ __global__ void __launch_bounds__(AttnCfg<D>::kThreads, 1)
       }
       const float inv_l = nkv > 0 ? 1.0f / l : 0.f;
       const int64_t col0 = static_cast<int64_t>(h) * D + half * kOCols;
+      // bf16 rows of a fully valid 32-row warp slab leave through the staging boxes and TMA
+      // tensor stores ([total_C, H, d] map, box 32 x 1 x 32); a ragged slab (the rows past it
+      // belong to the next request) stores its valid rows directly
+      const bool use_tma = kSplit == 1 && p.o_tma && i * 128 + static_cast<int>(sub) * 32 + 32 <= rows_valid;
 #pragma unroll 1
       for (int c = 0; c < kOCols / 32; ++c) {
         uint32_t o[32];
@@ -502,7 +515,27 @@ __global__ void __launch_bounds__(AttnCfg<D>::kThreads, 1)
 #pragma unroll
           for (int e = 0; e < 32; ++e) o[e] = 0u;
         }
-        if (row_ok) {
+        if (use_tma) {
+          uint32_t pk2[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e)
+            pk2[e] = pack_bf16x2(__uint_as_float(o[2 * e]) * inv_l, __uint_as_float(o[2 * e + 1]) * inv_l);
+          // this box must have been read by the store issued from it two chunks ago
+          if (lane == 0) bulk_wait_group_read<1>();
+          __syncwarp();
+          uint8_t* box = stg + (c & 1) * 2048;
+          uint8_t* rowp = box + lane * 64;
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            *reinterpret_cast<uint4*>(rowp + ((q ^ ((lane >> 1) & 3)) << 4)) =
+                make_uint4(pk2[4 * q], pk2[4 * q + 1], pk2[4 * q + 2], pk2[4 * q + 3]);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_3d(&map_o, box, c * 32, h, static_cast<int32_t>(cbeg + i * 128 + sub * 32));
+            bulk_commit_group();
+          }
+        } else if (row_ok) {
           if (p.o_bf16) {
             uint32_t pk2[16];
 #pragma unroll
@@ -528,10 +561,12 @@ __global__ void __launch_bounds__(AttnCfg<D>::kThreads, 1)
         // O_i drained: the next unit's first PV may overwrite it
         if (i == 0 && sub == 0 && half == 0 && lane == 0) GESR_T(7, cnt + nkv - 1);
         tc_fence_before();
-        mbar_arrive(&o_free[i]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&o_free[i]);
       }
       cnt += nkv;
     }
+    if (lane == 0) bulk_wait_group<0>();   // staging boxes stay allocated until read
   }
 
   tc_fence_before();
@@ -611,7 +646,8 @@ __global__ void attn_empty_kernel(AttnParams p, int D) {
 
 template <int D>
 cudaError_t launch_d(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
-                     const AttnParams& p, int64_t max_units, cudaStream_t stream) {
+                     const CUtensorMap& mo, const AttnParams& p, int64_t max_units,
+                     cudaStream_t stream) {
   using C = AttnCfg<D>;
   static bool attr_done = false;
   if (!attr_done) {
@@ -625,7 +661,7 @@ cudaError_t launch_d(const CUtensorMap& mq, const CUtensorMap& mk, const CUtenso
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t work = max_units * p.H;
   const unsigned grid = static_cast<unsigned>(work < sms ? work : sms);
-  attn_kernel<D><<<grid, C::kThreads, C::kSmemBytes, stream>>>(mq, mk, mv, p);
+  attn_kernel<D><<<grid, C::kThreads, C::kSmemBytes, stream>>>(mq, mk, mv, mo, p);
   return cudaGetLastError();
 }
 
@@ -644,11 +680,12 @@ cudaError_t launch_build_units(const int64_t* seq_offsets, const int64_t* cand_o
 }
 
 cudaError_t launch_attn(int d, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
-                        const AttnParams& p, int64_t max_units, cudaStream_t stream) {
+                        const CUtensorMap& mo, const AttnParams& p, int64_t max_units,
+                        cudaStream_t stream) {
   switch (d) {
-    case 32: return launch_d<32>(mq, mk, mv, p, max_units, stream);
-    case 64: return launch_d<64>(mq, mk, mv, p, max_units, stream);
-    case 128: return launch_d<128>(mq, mk, mv, p, max_units, stream);
+    case 32: return launch_d<32>(mq, mk, mv, mo, p, max_units, stream);
+    case 64: return launch_d<64>(mq, mk, mv, mo, p, max_units, stream);
+    case 128: return launch_d<128>(mq, mk, mv, mo, p, max_units, stream);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -111,6 +111,23 @@ bool pair_attention_enabled() {
   return cached == 1;
 }
 
+// bf16 attention output O [total_C, H*d] viewed as [total_C, H, d] for the epilogue's TMA
+// tensor stores: box {32 columns, 1 head, 32 rows}, 64B swizzle (the staging box layout)
+gesr_status make_o_map(CUtensorMap* map, void* base, uint64_t rows, uint64_t H, uint64_t d) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return fail(GESR_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+  cuuint64_t dims[3] = {d, H, rows};
+  cuuint64_t strides[2] = {d * 2, H * d * 2};
+  cuuint32_t box[3] = {32, 1, 32};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, base, dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                   CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(GESR_ERR_CUDA, "cuTensorMapEncodeTiled(O) failed: %d", static_cast<int>(r));
+  return GESR_OK;
+}
+
 bool valid_d(int32_t d) { return d == 32 || d == 64 || d == 128; }
 
 gesr_status check_common(int32_t D_in, int32_t H, int32_t d, int32_t act) {
@@ -288,15 +305,22 @@ gesr_status gesr_tasa_score(const void* T, int64_t total_C, int32_t D_in,
   if (s != GESR_OK) return s;
   s = make_map_2d(&mv, V_cache, static_cast<uint64_t>(H) * total_L, d, 128, box_cols, swz, "V");
   if (s != GESR_OK) return s;
+  CUtensorMap mo;
+  std::memset(&mo, 0, sizeof(mo));
+  if (p.o_bf16 && total_C > 0 && total_C < (int64_t{1} << 31)) {
+    s = make_o_map(&mo, O, static_cast<uint64_t>(total_C), H, d);
+    if (s != GESR_OK) return s;
+    p.o_tma = 1;
+  }
   if (d == 128 && pair_attention_enabled()) {
     CUtensorMap mkh;
     s = make_map_2d(&mkh, K_cache, static_cast<uint64_t>(H) * total_L, d, 64, 64, swz, "K half");
     if (s != GESR_OK) return s;
-    e = gesr::launch_attn_pair(mq, mkh, mv, p, max_units(B, total_C), st);
+    e = gesr::launch_attn_pair(mq, mkh, mv, mo, p, max_units(B, total_C), st);
     if (e != cudaSuccess) return cuda_fail(e, "attn_pair_kernel launch");
     return GESR_OK;
   }
-  e = gesr::launch_attn(d, mq, mk, mv, p, max_units(B, total_C), st);
+  e = gesr::launch_attn(d, mq, mk, mv, mo, p, max_units(B, total_C), st);
   if (e != cudaSuccess) return cuda_fail(e, "attn_kernel launch");
   return GESR_OK;
 }

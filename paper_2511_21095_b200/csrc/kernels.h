@@ -42,6 +42,7 @@ struct AttnParams {
   float scale_log2;        // scale * log2(e)
   void* O;                 // [total_C, H*d]
   int o_bf16;
+  int o_tma;               // bf16 O through the map_o TMA tensor stores (1-CTA kernel)
   float* lse;              // [total_C, H] or null
 };
 
@@ -50,13 +51,15 @@ constexpr int kUnitRows = 256;   // candidates per work unit (two 128-row Q tile
 cudaError_t launch_build_units(const int64_t* seq_offsets, const int64_t* cand_offsets, int64_t B,
                                int4* units, int* count,
                                cudaStream_t stream);
+// map_o: bf16 O as [total_C, H, d] (box {32, 1, 32}, 64B swizzle), used when p.o_tma
 cudaError_t launch_attn(int d, const CUtensorMap& map_q, const CUtensorMap& map_k,
-                        const CUtensorMap& map_v, const AttnParams& p, int64_t max_units,
+                        const CUtensorMap& map_v, const CUtensorMap& map_o, const AttnParams& p,
+                        int64_t max_units,
                         cudaStream_t stream);
 // d = 128: CTA-pair kernel (attn2.cu); K map box {64, 64}, Q / V maps box {64, 128}
 cudaError_t launch_attn_pair(const CUtensorMap& map_q, const CUtensorMap& map_kh,
-                             const CUtensorMap& map_vh, const AttnParams& p, int64_t max_units,
-                             cudaStream_t stream);
+                             const CUtensorMap& map_vh, const CUtensorMap& map_o,
+                             const AttnParams& p, int64_t max_units, cudaStream_t stream);
 cudaError_t launch_attn_empty(const AttnParams& p, int d, cudaStream_t stream);
 
 // ---------------------------------------------------------------- K-HMA (hma.cu)
