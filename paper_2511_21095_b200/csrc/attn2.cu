@@ -13,18 +13,20 @@
 //     each CTA's TMEM, each CTA stages HALF of each V tile -- 64 of the 128 d-columns), so each
 //     SM moves half of the 1-CTA kernel's K/V bytes per row;
 //   * the key tiles of a unit are dealt alternately to two softmax warpgroups: A takes the even
-//     tiles, B the odd ones.  Each has its own S buffer (P aliased into it), its own O
-//     accumulator and its own running max / sum; the two partial softmaxes are merged in the
-//     epilogue (O = (O_A 2^(m_A-m) + O_B 2^(m_B-m)) / (l_A 2^(m_A-m) + l_B 2^(m_B-m))).  While
-//     warpgroup A works on tile j, the tensor pipe runs PV(j-1) and S(j+1) for B: the chain of
-//     one warpgroup spans two tiles, and each sub-partition always has a softmax warp with work;
+//     tiles, B the odd ones.  Each has its own S buffer in TMEM, its own P buffer in SHARED
+//     memory, its own O accumulator and its own running max / sum; the two partial softmaxes are
+//     merged in the epilogue (O = (O_A 2^(m_A-m) + O_B 2^(m_B-m)) / (l_A 2^(m_A-m) + l_B 2^(m_B-m))).
+//     With P out of TMEM, a warpgroup frees its S buffer as soon as it has loaded S into
+//     registers (s_free), so S(j+2) is computed while the softmax of tile j runs: no MMA sits
+//     between two softmax passes of a warpgroup, and PV (SS form, A = P from smem) runs beside;
 //   * TMEM per CTA (512 columns): S_A [0,128), S_B [128,256), O_A [256,384), O_B [384,512);
 //   * persistent: pair c takes work items c, c + G, ... (w -> unit w % U, head w / U), the next
 //     unit's Q load and first S MMAs overlap the current unit's epilogue, and full 32-row output
-//     slabs leave through TMA tensor stores.
-// Warp roles per CTA: warp 0 TMA producer (both CTAs), warp 1 TMEM allocator + MMA issuer (leader
-// only), warps 2-3 idle, warps 4-7 softmax A, warps 8-11 softmax B (warp w reads TMEM lane
-// quarter w % 4: thread = candidate row, all 128 key columns of its tile).
+//     slabs leave through TMA tensor stores (staged in the warp's own rows of its P buffer).
+// Warp roles per CTA: warp 0 Q/K producer and warp 2 V producer (both CTAs), warp 1 TMEM
+// allocator + S MMA issuer and warp 3 PV MMA issuer (leader only), warps 4-7 softmax A, warps
+// 8-11 softmax B (warp w reads TMEM lane quarter w % 4: thread = candidate row, all 128 key
+// columns of its tile), warps 12-15 epilogue.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -40,31 +42,64 @@ __device__ unsigned long long g_trace2[64][64][8];
     const int _b = blockIdx.x;                                                                 \
     if (_b < 64 && (j) < 64) g_trace2[_b][(j)][(e)] = clock64();                               \
   } while (0)
+__device__ unsigned long long g_trace3[64][16][8];   // per unit: control-warp events
+__device__ unsigned long long g_trace4[64][16][16];  // per unit: epilogue chunk loads done
+#define GESR_T4(e, u)                                                                          \
+  do {                                                                                         \
+    const int _b = blockIdx.x;                                                                 \
+    if (_b < 64 && (u) < 16) g_trace4[_b][(u)][(e)] = clock64();                               \
+  } while (0)
+#define GESR_T3(e, u)                                                                          \
+  do {                                                                                         \
+    const int _b = blockIdx.x;                                                                 \
+    if (_b < 64 && (u) < 16) g_trace3[_b][(u)][(e)] = clock64();                               \
+  } while (0)
 #else
 #define GESR_T2(e, j) do {} while (0)
+#define GESR_T3(e, u) do {} while (0)
+#define GESR_T4(e, u) do {} while (0)
 #endif
 
 namespace {
 
+#ifndef GESR_PAIR_SUM_LIMIT
+#define GESR_PAIR_SUM_LIMIT 4096.0f   // tile row sums above this take the exact-max path
+#endif
+// mbarrier waits: 1 = try_wait spin loop, 0 = try_wait with a suspend-time hint
+#ifndef GESR_PAIR_GATE
+#define GESR_PAIR_GATE 1      // a unit's first exp pass waits for the epilogue's TMEM reads
+#endif
+#ifndef GESR_PAIR_SPIN
+#define GESR_PAIR_SPIN 0
+#endif
+__device__ __forceinline__ void pwait(uint64_t* bar, uint32_t parity) {
+  if (GESR_PAIR_SPIN) mbar_wait(bar, parity); else mbar_wait_sleep(bar, parity);
+}
 constexpr int kD = 128;
 constexpr int kKeys = 128;                       // keys per tile (S columns)
-constexpr int kThreads = 384;
+constexpr int kThreads = 512;
 constexpr uint32_t kQBytes = 128 * kD * 2;       // 32 KB: Q tile, [2 col blocks][128 rows][64]
 constexpr uint32_t kHalfBytes = 16384;           // K half [2][64 keys][64] or V half [128][64]
-constexpr int kStages = 9;
+constexpr int kKStages = 2;                     // K-half ring
+constexpr int kVStages = 3;                     // V-half ring
+constexpr int kStages = kKStages + kVStages;
 constexpr uint32_t kQOff = 0;
-constexpr uint32_t kRingOff = kQBytes;
-constexpr uint32_t kStgOff = kRingOff + kStages * kHalfBytes;      // 2 x 2 KB boxes per softmax warp
-constexpr uint32_t kBarOff = kStgOff + 8 * 4096;
+constexpr uint32_t kPOff = kQBytes;                                  // P_A, P_B: [2 atoms][128][128 B]
+constexpr uint32_t kPBytes = 128 * kKeys * 2;                        // 32 KB
+constexpr uint32_t kRingOff = kPOff + 2 * kPBytes;
+constexpr uint32_t kStgOff = kRingOff + kStages * kHalfBytes;        // 4 x 2 KB boxes per epilogue warp
+constexpr uint32_t kBarOff = kStgOff + 4 * 8192;
 constexpr uint32_t kXchOff = kBarOff + 256;                          // [unit parity][WG][m, l][row]
 constexpr uint32_t kSmemBytes = kXchOff + 2 * 2 * 2 * 128 * 4 + 1024;
 static_assert(kSmemBytes <= 232448, "shared memory budget");
-// register split: launch registers 168 x 384 threads; control warps 88, softmax warps 208
-constexpr int kCtrlRegs = 88;
-constexpr int kSoftRegs = 208;
-static_assert(128 * kCtrlRegs + 256 * kSoftRegs <= 168 * kThreads, "setmaxnreg pool");
+// register split (setmaxnreg per warpgroup; launch registers 128 x 512 threads): control 56,
+// softmax 184, epilogue 88
+constexpr int kCtrlRegs = 56;
+constexpr int kSoftRegs = 184;
+constexpr int kEpiRegs = 88;
+static_assert(128 * kCtrlRegs + 256 * kSoftRegs + 128 * kEpiRegs <= 128 * kThreads, "setmaxnreg pool");
 // TMEM columns
-constexpr uint32_t kTS = 0;          // S_A at 0, S_B at 128 (P_x aliases the first 64 columns)
+constexpr uint32_t kTS = 0;          // S_A at 0, S_B at 128
 constexpr uint32_t kTO = 256;        // O_A at 256, O_B at 384
 
 __device__ __forceinline__ void ffma2(float& d0, float& d1, float a0, float a1, float b0, float b1,
@@ -72,6 +107,11 @@ __device__ __forceinline__ void ffma2(float& d0, float& d1, float a0, float a1, 
   asm("{\n .reg .b64 a, b, c, d;\n mov.b64 a, {%2, %3};\n mov.b64 b, {%4, %5};\n"
       " mov.b64 c, {%6, %7};\n fma.rn.f32x2 d, a, b, c;\n mov.b64 {%0, %1}, d;\n}"
       : "=f"(d0), "=f"(d1) : "f"(a0), "f"(a1), "f"(b0), "f"(b1), "f"(c0), "f"(c1));
+}
+__device__ __forceinline__ void fmul2(float& d0, float& d1, float a0, float a1, float b0, float b1) {
+  asm("{\n .reg .b64 a, b, d;\n mov.b64 a, {%2, %3};\n mov.b64 b, {%4, %5};\n"
+      " mul.rn.f32x2 d, a, b;\n mov.b64 {%0, %1}, d;\n}"
+      : "=f"(d0), "=f"(d1) : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
 }
 __device__ __forceinline__ void fadd2(float& d0, float& d1, float a0, float a1, float b0, float b1) {
   asm("{\n .reg .b64 a, b, d;\n mov.b64 a, {%2, %3};\n mov.b64 b, {%4, %5};\n"
@@ -112,13 +152,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                                              ~uintptr_t(1023));
   uint64_t* q_full = reinterpret_cast<uint64_t*>(smem + kBarOff);   // leader's used
   uint64_t* q_empty = q_full + 1;                 // each CTA
-  uint64_t* kv_full = q_empty + 1;                // [kStages]  (leader's used)
+  uint64_t* kv_full = q_empty + 1;                // [kStages]  K ring, then V ring (leader's used)
   uint64_t* kv_empty = kv_full + kStages;         // [kStages]  (each CTA)
   uint64_t* s_full = kv_empty + kStages;          // [2]        (each CTA)
-  uint64_t* p_full = s_full + 2;                  // [2]        (leader; 8 warps of the pair)
-  uint64_t* o_done = p_full + 2;                  //            (each CTA)
-  uint64_t* o_free = o_done + 1;                  //            (leader; 16 warps of the pair)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_free + 1);
+  uint64_t* s_free = s_full + 2;                  // [2]        (leader; 8 warps of the pair)
+  uint64_t* p_full = s_free + 2;                  // [2]        (leader; 8 warps of the pair)
+  uint64_t* p_free = p_full + 2;                  // [2]        (each CTA)
+  uint64_t* o_done = p_free + 2;                  //            (each CTA)
+  uint64_t* o_free = o_done + 1;                  //            (leader; 8 epilogue warps of the pair)
+  uint64_t* ml_full = o_free + 1;                 //            (each CTA; its 8 softmax warps)
+  uint64_t* o_read = ml_full + 1;                 //            (each CTA; its 4 epilogue warps)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_read + 1);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -136,10 +180,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
+      mbar_init(&s_free[i], 8);
       mbar_init(&p_full[i], 8);
+      mbar_init(&p_free[i], 1);
     }
     mbar_init(o_done, 1);
-    mbar_init(o_free, 16);
+    mbar_init(o_free, 8);
+    mbar_init(ml_full, 8);
+    mbar_init(o_read, 4);
     fence_mbar_init();
   }
   if (warp == 1) {
@@ -152,6 +200,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const uint32_t tmem = *tmem_slot;
   const uint32_t sQ = smem_u32(smem + kQOff);
   const uint32_t sRing = smem_u32(smem + kRingOff);
+  const uint32_t sP = smem_u32(smem + kPOff);
 
   // the unit descriptor of work item w is one 16-byte load, fetched one item ahead
   auto fetch = [&](int w) { return __ldg(p.units + (w % U)); };
@@ -166,68 +215,114 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     return x;
   };
 
+  // The key tiles of all work items of this pair form one stream (units without keys skipped):
+  // the producer and the MMA issuer walk it with TileStream cursors, so the next unit's first
+  // S MMAs are issued while the current unit's last PVs wait for their P (no bubble at unit
+  // boundaries).  Stream order of the MMA issuer: S(0), S(1), S(2), then per step S(g+3) and
+  // PV(g); the producer loads K(g) / V(g) in exactly that order.
+  struct Tile {
+    Work x;
+    int t, m;       // tile index in its unit, ordinal of its unit among units with keys
+  };
+  struct TileStream {
+    int w, t, m;
+    Work x;
+    int4 nx;
+  };
+  auto stream_init = [&](TileStream& st) {
+    st.w = pair;
+    st.t = 0;
+    st.m = -1;
+    st.x.nkv = 0;
+    st.nx = pair < W ? fetch(pair) : make_int4(0, 0, 0, 0);
+  };
+  auto stream_next = [&](TileStream& st, Tile& out) -> bool {
+    while (st.t >= st.x.nkv) {
+      if (st.w >= W) return false;
+      st.x = decode(st.w, st.nx);
+      st.w += npairs;
+      if (st.w < W) st.nx = fetch(st.w);
+      st.t = 0;
+      if (st.x.nkv > 0) ++st.m;
+    }
+    out.x = st.x;
+    out.t = st.t++;
+    out.m = st.m;
+    return true;
+  };
+
   if (warp < 4) {
     setmaxnreg_dec<kCtrlRegs>();
+    // Four independent control streams over the tile stream (each blocks only on its own
+    // resources): warp 0 loads Q and the K halves, warp 2 the V halves (both CTAs); in the
+    // leader, warp 1 issues the S MMAs and warp 3 the PV MMAs.  S(g) needs its K half, its
+    // unit's Q and the s_free of its buffer's previous S; PV(g) its V half and p_full(g).
+    auto krow_of = [&](const Tile& tl) {
+      return static_cast<int32_t>(static_cast<int64_t>(tl.x.h) * p.total_L + tl.x.s0) + kKeys * tl.t;
+    };
+    TileStream st;
+    stream_init(st);
+    Tile tl;
     if (warp == 0) {
-      // ---------------------------------------------------------- TMA producer (both CTAs)
+      // ---------------------------------------------------------- Q + K producer (both CTAs)
       if (elect_one()) {
-        int stage = 0;
-        uint32_t phase = 0;
-        int m = 0;                                 // units with key tiles so far
-        auto load_k = [&](int32_t krow, int jj) {
-          mbar_wait_sleep(&kv_empty[stage], phase ^ 1);
-          if (rank == 0) mbar_arrive_expect_tx(&kv_full[stage], 2 * kHalfBytes);
-          uint8_t* dst = smem + kRingOff + stage * kHalfBytes;
-          const int32_t row = krow + kKeys * jj + static_cast<int32_t>(rank) * 64;
-          tma_load_2d_pair(dst, &map_kh, &kv_full[stage], 0, row);
-          tma_load_2d_pair(dst + 8192, &map_kh, &kv_full[stage], 64, row);
-          if (++stage == kStages) { stage = 0; phase ^= 1; }
-        };
-        auto load_v = [&](int32_t krow, int jj) {
-          mbar_wait_sleep(&kv_empty[stage], phase ^ 1);
-          if (rank == 0) mbar_arrive_expect_tx(&kv_full[stage], 2 * kHalfBytes);
-          uint8_t* dst = smem + kRingOff + stage * kHalfBytes;
-          tma_load_2d_pair(dst, &map_vh, &kv_full[stage], static_cast<int32_t>(rank) * 64,
-                           krow + kKeys * jj);
-          if (++stage == kStages) { stage = 0; phase ^= 1; }
-        };
-        int4 nx = fetch(pair);
-        for (int w = pair; w < W; w += npairs) {
-          const Work x = decode(w, nx);
-          if (w + npairs < W) nx = fetch(w + npairs);
-          if (x.nkv == 0) continue;
-          if (m > 0) mbar_wait_sleep(q_empty, (m - 1) & 1);   // previous unit's S MMAs done with Q
-          const int32_t qrow = static_cast<int32_t>(static_cast<int64_t>(x.h) * p.total_C + x.cbeg) +
-                               static_cast<int32_t>(rank) * 128;
-          if (rank == 0) mbar_arrive_expect_tx(q_full, 2 * kQBytes);
-          tma_load_2d_pair(smem + kQOff, &map_q, q_full, 0, qrow);
-          tma_load_2d_pair(smem + kQOff + kQBytes / 2, &map_q, q_full, 64, qrow);
-          const int32_t krow = static_cast<int32_t>(static_cast<int64_t>(x.h) * p.total_L + x.s0);
-          // consumption order of the MMA issuer: K0, K1, then per j: V_j, K_{j+2}
-          load_k(krow, 0);
-          if (x.nkv > 1) load_k(krow, 1);
-          for (int j = 0; j < x.nkv; ++j) {
-            load_v(krow, j);
-            if (j + 2 < x.nkv) load_k(krow, j + 2);
+        int kst = 0;
+        uint32_t kph = 0;
+        while (stream_next(st, tl)) {
+          if (tl.t == 0) {
+            // the unit's Q: the previous unit's S MMAs must be done with the single Q buffer
+            if (tl.m > 0) pwait(q_empty, (tl.m - 1) & 1);
+            GESR_T3(3, tl.m);
+            const int32_t qrow = static_cast<int32_t>(static_cast<int64_t>(tl.x.h) * p.total_C + tl.x.cbeg) +
+                                 static_cast<int32_t>(rank) * 128;
+            if (rank == 0) mbar_arrive_expect_tx(q_full, 2 * kQBytes);
+            tma_load_2d_pair(smem + kQOff, &map_q, q_full, 0, qrow);
+            tma_load_2d_pair(smem + kQOff + kQBytes / 2, &map_q, q_full, 64, qrow);
           }
-          ++m;
+          const int slot = kst;
+          pwait(&kv_empty[slot], kph ^ 1);
+          if (rank == 0) mbar_arrive_expect_tx(&kv_full[slot], 2 * kHalfBytes);
+          uint8_t* dst = smem + kRingOff + slot * kHalfBytes;
+          const int32_t row = krow_of(tl) + static_cast<int32_t>(rank) * 64;
+          tma_load_2d_pair(dst, &map_kh, &kv_full[slot], 0, row);
+          tma_load_2d_pair(dst + 8192, &map_kh, &kv_full[slot], 64, row);
+          if (++kst == kKStages) { kst = 0; kph ^= 1; }
+        }
+      }
+    } else if (warp == 2) {
+      // ---------------------------------------------------------- V producer (both CTAs)
+      if (elect_one()) {
+        int vst = 0;
+        uint32_t vph = 0;
+        while (stream_next(st, tl)) {
+          const int slot = kKStages + vst;
+          pwait(&kv_empty[slot], vph ^ 1);
+          if (rank == 0) mbar_arrive_expect_tx(&kv_full[slot], 2 * kHalfBytes);
+          uint8_t* dst = smem + kRingOff + slot * kHalfBytes;
+          tma_load_2d_pair(dst, &map_vh, &kv_full[slot], static_cast<int32_t>(rank) * 64, krow_of(tl));
+          if (++vst == kVStages) { vst = 0; vph ^= 1; }
         }
       }
     } else if (warp == 1 && rank == 0) {
-      // ---------------------------------------------------------- MMA issuer (leader only)
+      // ---------------------------------------------------------- S MMA issuer (leader only)
       const uint32_t idesc_s = make_idesc_bf16(256, kKeys, 0, 0);
-      const uint32_t idesc_o = make_idesc_bf16(256, kD, 0, 1);
-      int stage = 0;
-      uint32_t phase = 0;
-      int m = 0;                                   // units with key tiles so far
-      uint32_t pc0 = 0, pc1 = 0;                   // p_full phases of A / B
-      auto take = [&]() {
-        const int s = stage;
-        mbar_wait_sleep(&kv_full[s], phase);
-        if (++stage == kStages) { stage = 0; phase ^= 1; }
-        return s;
-      };
-      auto issue_s = [&](int buf, int slot, bool last) {
+      int kst = 0;
+      uint32_t kph = 0;
+      uint32_t sn0 = 0, sn1 = 0;                   // S issued into buffer A / B so far
+      while (stream_next(st, tl)) {
+        const int buf = tl.t & 1;
+        if (tl.t == 0) {
+          pwait(q_full, tl.m & 1);                 // the unit's Q tile (both CTAs)
+          if (lane == 0) GESR_T3(0, tl.m);
+        }
+        // the buffer's previous S must have been loaded by its warpgroup (both CTAs)
+        const uint32_t sn = buf ? sn1 : sn0;
+        if (sn > 0) pwait(&s_free[buf], (sn - 1) & 1);
+        if (buf) ++sn1; else ++sn0;
+        const int slot = kst;
+        pwait(&kv_full[slot], kph);
+        if (++kst == kKStages) { kst = 0; kph ^= 1; }
+        if (lane == 0) GESR_T2(7, tl.m * 16 + tl.t);
         const uint32_t kb = sRing + slot * kHalfBytes;
         tc_fence_after();
         if (elect_one()) {
@@ -237,154 +332,167 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         idesc_s, ks > 0 ? 1u : 0u);
           mma_commit_pair_mc(&s_full[buf], 0x3);
           mma_commit_pair_mc(&kv_empty[slot], 0x3);
-          if (last) mma_commit_pair_mc(q_empty, 0x3);   // the unit's last S: Q may be reloaded
+          // the unit's last S: its Q buffer may be reloaded
+          if (tl.t == tl.x.nkv - 1) mma_commit_pair_mc(q_empty, 0x3);
         }
         __syncwarp();
-      };
-      int4 nx = fetch(pair);
-      for (int w = pair; w < W; w += npairs) {
-        const Work x = decode(w, nx);
-        if (w + npairs < W) nx = fetch(w + npairs);
-        const int nkv = x.nkv;
-        if (nkv == 0) continue;
-        mbar_wait_sleep(q_full, m & 1);
-        issue_s(0, take(), nkv == 1);
-        if (nkv > 1) issue_s(1, take(), nkv == 2);
-        for (int j = 0; j < nkv; ++j) {
-          const int xb = j & 1;
-          const int vslot = take();
-          // the unit's first PV overwrites O_A: the previous unit's epilogue must be done
-          if (j == 0 && m > 0) mbar_wait_sleep(o_free, (m - 1) & 1);
-          mbar_wait_sleep(&p_full[xb], (xb ? pc1 : pc0) & 1);
-          if (xb) ++pc1; else ++pc0;
-          if (lane == 0) GESR_T2(4 + xb, m * 16 + j);
-          tc_fence_after();
-          if (elect_one()) {
-            const uint32_t vb = sRing + vslot * kHalfBytes;
-#pragma unroll
-            for (int ks = 0; ks < kKeys / 16; ++ks)
-              mma_ts_pair(tmem + kTO + xb * kD, tmem + kTS + xb * kKeys + ks * 8, vdesc(vb, ks),
-                          idesc_o, (j >= 2 || ks > 0) ? 1u : 0u);
-            mma_commit_pair_mc(&kv_empty[vslot], 0x3);
-            if (j == nkv - 1) mma_commit_pair_mc(o_done, 0x3);
-          }
-          __syncwarp();
-          // S(j+2) reuses S(j)'s buffer: P(j) is read by the PV just issued (in order)
-          if (j + 2 < nkv) issue_s(xb, take(), j + 2 == nkv - 1);
+      }
+    } else if (warp == 3 && rank == 0) {
+      // ---------------------------------------------------------- PV MMA issuer (leader only)
+      const uint32_t idesc_o = make_idesc_bf16(256, kD, 0, 1);
+      int vst = 0;
+      uint32_t vph = 0;
+      uint32_t pn0 = 0, pn1 = 0;                   // PV issued from P_A / P_B so far
+      while (stream_next(st, tl)) {
+        const int xb = tl.t & 1;
+        const int vslot = kKStages + vst;
+        pwait(&kv_full[vslot], vph);
+        if (++vst == kVStages) { vst = 0; vph ^= 1; }
+        if (tl.t == 0 && tl.m > 0) {
+          // the unit's first PV overwrites O_A: the previous unit's epilogue must have read O
+          pwait(o_free, (tl.m - 1) & 1);
+          if (lane == 0) GESR_T3(1, tl.m);
         }
-        ++m;
+        const uint32_t pn = xb ? pn1 : pn0;
+        pwait(&p_full[xb], pn & 1);
+        if (xb) ++pn1; else ++pn0;
+        if (lane == 0) GESR_T2(6, tl.m * 16 + tl.t);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t vb = sRing + vslot * kHalfBytes;
+          const uint32_t pb = sP + xb * kPBytes;
+#pragma unroll
+          for (int ks = 0; ks < kKeys / 16; ++ks)
+            mma_ss_pair(tmem + kTO + xb * kD, kdesc(pb, kPBytes / 2, ks), vdesc(vb, ks), idesc_o,
+                        (tl.t >= 2 || ks > 0) ? 1u : 0u);
+          mma_commit_pair_mc(&p_free[xb], 0x3);
+          mma_commit_pair_mc(&kv_empty[vslot], 0x3);
+          if (tl.t == tl.x.nkv - 1) mma_commit_pair_mc(o_done, 0x3);
+        }
+        __syncwarp();
+        if (tl.t == tl.x.nkv - 1 && lane == 0) GESR_T3(2, tl.m);
       }
     }
-  } else {
-    // ------------------------------------------------------------ softmax + epilogue
+  } else if (warp < 12) {
+    // ------------------------------------------------------------ softmax
     setmaxnreg_inc<kSoftRegs>();
     const int g = (static_cast<int>(warp) - 4) >> 2;   // warpgroup: 0 = A (even tiles), 1 = B
     const uint32_t sub = warp & 3;                       // TMEM lane quarter
     const int rloc = static_cast<int>(sub) * 32 + static_cast<int>(lane);
-    const int row_in_unit = static_cast<int>(rank) * 128 + rloc;
     const uint32_t lane_addr = (sub * 32) << 16;
     const uint32_t tS = tmem + lane_addr + kTS + g * kKeys;
     const uint32_t tO = tmem + lane_addr + kTO;          // O_A; O_B at + kD
     const uint32_t tOg = tO + g * kD;
+    const uint32_t s_free_leader = mapa_shared(smem_u32(&s_free[g]), 0);
     const uint32_t p_full_leader = mapa_shared(smem_u32(&p_full[g]), 0);
-    const uint32_t o_free_leader = mapa_shared(smem_u32(o_free), 0);
     const uint32_t xch = smem_u32(smem + kXchOff);
-    uint8_t* stg = smem + kStgOff + (warp - 4) * 4096;
+    // P_g: K-major SW128, [2 atoms of 64 keys][128 rows][128 B]; row rloc's 16-byte chunk c of
+    // atom a sits at a * 16 KB + rloc * 128 + ((c ^ (rloc & 7)) << 4)
+    const uint32_t prow = smem_u32(smem + kPOff + g * kPBytes) + rloc * 128;
     const float sl2 = p.scale_log2;
-    const int64_t HD = static_cast<int64_t>(p.H) * kD;
     int sc = 0;                                          // S tiles consumed by this warpgroup
+    // MUFU token: the exp passes of the two warps of a sub-partition (A and B, same lane
+    // quarter) alternate in tile order, so one's exp pass overlaps the other's TMEM loads, P
+    // stores and waits instead of both running them at the same time.  Named barriers 5 + sub
+    // ("A may exp") and 9 + sub ("B may exp"), 64 threads each (one bar.sync + one bar.arrive).
+    const uint32_t tok_mine = (g == 0 ? 5u : 9u) + sub;
+    const uint32_t tok_other = (g == 0 ? 9u : 5u) + sub;
+    bool prev_last_b = false;                            // previous unit's last tile was B's
     int m = 0;                                           // units with key tiles so far
     int4 nx = fetch(pair);
     for (int w = pair; w < W; w += npairs) {
       const Work x = decode(w, nx);
       if (w + npairs < W) nx = fetch(w + npairs);
-      const int L = x.L, nkv = x.nkv, h = x.h;
-      const bool row_ok = row_in_unit < x.rows_valid;
-      const int64_t row = x.cbeg + row_in_unit;
-      const int64_t col0 = static_cast<int64_t>(h) * kD + g * 64;   // my 64 output columns
-      if (nkv == 0) {
-        // L_b = 0: no keys, O = 0 and lse = -inf
-        if (row_ok) {
-          if (p.o_bf16) {
-            uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.O) + row * HD + col0);
-#pragma unroll
-            for (int v = 0; v < 8; ++v) dst[v] = make_uint4(0u, 0u, 0u, 0u);
-          } else {
-            float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.O) + row * HD + col0);
-#pragma unroll
-            for (int v = 0; v < 16; ++v) dst[v] = make_float4(0.f, 0.f, 0.f, 0.f);
-          }
-          if (g == 0 && p.lse != nullptr) p.lse[row * p.H + h] = -INFINITY;
-        }
-        continue;
-      }
+      const int L = x.L, nkv = x.nkv;
+      if (nkv == 0) continue;                          // the epilogue warps write O = 0
       float m_run = -INFINITY;
       float l = 0.f;
       for (int j = g; j < nkv; j += 2) {
-        mbar_wait_sleep(&s_full[g], sc & 1);
+        pwait(&s_full[g], sc & 1);
         ++sc;
         const bool tr = (sub == 0 && lane == 0);
-        if (tr) GESR_T2(g, m * 16 + j);
+        const bool trd = tr;
+        if (trd) GESR_T2(0, m * 16 + j);
         tc_fence_after();
         uint32_t r[kKeys];
 #pragma unroll
         for (int c = 0; c < 4; ++c) tmem_ld32(tS + c * 32, r + c * 32);
         tmem_ld_wait();
+        if (trd) GESR_T2(1, m * 16 + j);
         const int valid = L - kKeys * j;
-        const bool full = valid >= kKeys;
-        if (!full) {
+        if (valid < kKeys) {
 #pragma unroll
           for (int k = 0; k < kKeys; ++k)
             if (k >= valid) r[k] = __float_as_uint(-INFINITY);   // keys beyond L_b
         }
-        // One fused pass per tile: p = 2^(s*scale*log2e - m) with the running max m of this
-        // warpgroup's PREVIOUS tiles (speculative), the tile's own max reduced alongside.  Only
-        // if the max grew by > 2^8 are p recomputed (from S, still in TMEM) and O_g rescaled;
-        // the first tile reduces its max first.  P is packed in place into r[0, 64).
-        uint32_t* pk = r;
-        float acc[8];
-        float mx[8];
-        auto exp_pass = [&](float mm, bool with_max) {
-          const float neg_m = -mm;
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            acc[e] = 0.f;
-            mx[e] = -INFINITY;
-          }
-#pragma unroll
-          for (int k = 0; k < kKeys / 2; ++k) {
-            const float s0v = __uint_as_float(r[2 * k]), s1v = __uint_as_float(r[2 * k + 1]);
-            if (with_max) {
-              mx[(2 * k) & 7] = fmaxf(mx[(2 * k) & 7], s0v);
-              mx[(2 * k + 1) & 7] = fmaxf(mx[(2 * k + 1) & 7], s1v);
-            }
-            float x0, x1;
-            ffma2(x0, x1, s0v, s1v, sl2, sl2, neg_m, neg_m);
-            const float p0 = ex2(x0), p1 = ex2(x1);
-            const int a = (k & 3) * 2;
-            fadd2(acc[a], acc[a + 1], acc[a], acc[a + 1], p0, p1);
-            pk[k] = pack_bf16x2(p0, p1);
-          }
-        };
-        const bool first = j == g;
-        if (first) {
+        // S is in registers: the buffer may take S(j+2)
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster_relaxed(s_free_leader);
+        if (trd) GESR_T2(2, m * 16 + j);
+        // Row max.  Min/max instructions share the issue path of MUFU (scripts/micro/
+        // exp_interf.cu: a max pass on the other warp of a sub-partition slows an exp pass from
+        // 1.17k to 2k cycles), so only a warpgroup's first tile of a unit reduces its exact max.
+        // Later tiles use the running max m_run speculatively and test the tile's row sum
+        // instead: sum <= 2^12 implies every p <= 2^12 (so l <= 2^23 and O stays far from fp32
+        // overflow).  Only rows over it reduce their exact max, and if that exceeds m_run by > 8
+        // (log2 units, the lazy-rescale bound) O_g is rescaled and p recomputed from S, still
+        // in registers.
+        auto row_max = [&]() {
+          float mx[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e) mx[e] = -INFINITY;
 #pragma unroll
           for (int k = 0; k < kKeys; ++k) mx[k & 7] = fmaxf(mx[k & 7], __uint_as_float(r[k]));
-        } else {
-          exp_pass(m_run, true);
-        }
-        const float mraw = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
-                                 fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
-        const float mt = mraw * sl2;
-        if (first) {
-          m_run = mt;
-          exp_pass(m_run, false);
-        } else {
+          return fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                       fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) * sl2;
+        };
+        if (j == g) m_run = row_max();
+        // P_g must have been read by PV(j-2) (long done, normally) before the exp pass writes it
+        if (sc > 1) pwait(&p_free[g], (sc - 2) & 1);
+        float acc[8];
+        // p = 2^(s*scale*log2e - m_run), packed to bf16 pairs and stored to P_g 16 bytes at a time
+        auto exp_pass = [&]() {
+          const float neg_m = -m_run;
+#pragma unroll
+          for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+#pragma unroll
+          for (int q = 0; q < kKeys / 8; ++q) {
+            uint32_t pw[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int k = q * 4 + u;
+              float x0, x1;
+              ffma2(x0, x1, __uint_as_float(r[2 * k]), __uint_as_float(r[2 * k + 1]), sl2, sl2,
+                    neg_m, neg_m);
+              const float p0 = ex2(x0), p1 = ex2(x1);
+              const int a = (k & 3) * 2;
+              fadd2(acc[a], acc[a + 1], acc[a], acc[a + 1], p0, p1);
+              pw[u] = pack_bf16x2(p0, p1);
+            }
+            st_shared_v4(prow + (q >> 3) * (kPBytes / 2) + (((q & 7) ^ (rloc & 7)) << 4), pw[0], pw[1],
+                         pw[2], pw[3]);
+          }
+        };
+        // A unit's first exp pass waits until the epilogue warps have read the previous unit's
+        // O out of TMEM: their TMEM loads and smem stores then do not queue behind this
+        // warpgroup's MUFU stream, and the unit's first PV is not held up by a slow epilogue.
+        if (GESR_PAIR_GATE && j == g && m > 0) pwait(o_read, (m - 1) & 1);
+        // masked keys give exactly 0
+        if (j > 0 || prev_last_b) named_bar_sync(tok_mine, 64);   // tile j-1's exp pass is done
+        if (trd) GESR_T2(4, m * 16 + j);
+        exp_pass();
+        // hand the token to tile j+1's warpgroup (the next unit starts with A)
+        if (j + 1 < nkv || (g == 1 && w + npairs < W)) named_bar_arrive(tok_other, 64);
+        float tsum = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+        if (j != g && __any_sync(0xffffffffu, !(tsum <= GESR_PAIR_SUM_LIMIT))) {
+          float mt = m_run;
+          if (!(tsum <= GESR_PAIR_SUM_LIMIT)) mt = row_max();
           const bool need = mt > m_run + 8.0f;
           if (__any_sync(0xffffffffu, need)) {
-            // O_g holds PV(j-2): S_g(j) was issued after it and has completed
+            // O_g must hold PV(j-2) before it is rescaled
+            pwait(&p_free[g], (sc - 2) & 1);
+            tc_fence_after();
             float alpha = 1.f;
             if (need) {
               alpha = ex2(m_run - mt);
@@ -401,98 +509,177 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               tmem_st32(tOg + c * 32, o);
             }
             tmem_st_wait();
-#pragma unroll
-            for (int c = 0; c < 4; ++c) tmem_ld32(tS + c * 32, r + c * 32);
-            tmem_ld_wait();
-            if (!full) {
-#pragma unroll
-              for (int k = 0; k < kKeys; ++k)
-                if (k >= valid) r[k] = __float_as_uint(-INFINITY);
-            }
-            exp_pass(m_run, false);   // recompute P with the new running max
+            tc_fence_before();
+            exp_pass();   // recompute p with the new running max
+            tsum = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
           }
         }
-        l += ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
-        tmem_st32(tS, pk);
-        tmem_st32(tS + 32, pk + 32);
-        tmem_st_wait();
-        tc_fence_before();
+        l += tsum;
+        if (trd) GESR_T2(3, m * 16 + j);
+        fence_proxy_async_smem();
         __syncwarp();
-        if (tr) GESR_T2(2 + g, m * 16 + j);
+        if (trd) GESR_T2(5, m * 16 + j);
         if (lane == 0) mbar_arrive_cluster_relaxed(p_full_leader);
       }
-      // ---------------- epilogue: merge the two partial softmaxes of my rows, O for my columns
+      prev_last_b = ((nkv - 1) & 1) == 1;
+      // publish this warpgroup's running max / sum of my rows for the epilogue warps
       const uint32_t xb = xch + ((m & 1) * 2 * 2 * 128) * 4;      // [WG][m, l][row]
       st_shared_f32(xb + ((g * 2 + 0) * 128 + rloc) * 4, m_run);
       st_shared_f32(xb + ((g * 2 + 1) * 128 + rloc) * 4, l);
-      named_bar_sync(1 + sub, 64);                        // warp sub of A and of B
-      const float m_o = ld_shared_f32(xb + (((1 - g) * 2 + 0) * 128 + rloc) * 4);
-      const float l_o = ld_shared_f32(xb + (((1 - g) * 2 + 1) * 128 + rloc) * 4);
-      const float mA = g == 0 ? m_run : m_o, lA = g == 0 ? l : l_o;
-      const float mB = g == 0 ? m_o : m_run, lB = g == 0 ? l_o : l;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(ml_full);
+      ++m;
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue (warps 12-15)
+    // Merges the two partial softmaxes of a unit while the softmax warpgroups already work on
+    // the next one: O = (O_A 2^(m_A-m) + O_B 2^(m_B-m)) / (l_A 2^(m_A-m) + l_B 2^(m_B-m)).
+    // bf16 output: the warp's 32 rows x 128 columns are merged 16 columns at a time into four
+    // 2 KB staging boxes (32 rows x 32 columns, 64B swizzle); TMEM is released as soon as the
+    // last columns are read, then full 32-row slabs leave with TMA tensor stores (a ragged slab
+    // stores its valid rows from the boxes).  fp32 output: direct stores.
+    setmaxnreg_dec<kEpiRegs>();
+    const uint32_t sub = warp & 3;
+    const int rloc = static_cast<int>(sub) * 32 + static_cast<int>(lane);
+    const int row_in_unit = static_cast<int>(rank) * 128 + rloc;
+    const uint32_t tO = tmem + ((sub * 32) << 16) + kTO;   // O_A; O_B at + kD
+    const uint32_t o_free_leader = mapa_shared(smem_u32(o_free), 0);
+    const uint32_t xch = smem_u32(smem + kXchOff);
+    uint8_t* stg = smem + kStgOff + sub * 8192;
+    const uint32_t stg_s = smem_u32(stg);
+    const int64_t HD = static_cast<int64_t>(p.H) * kD;
+    int m = 0;
+    int4 nx = fetch(pair);
+    for (int w = pair; w < W; w += npairs) {
+      const Work x = decode(w, nx);
+      if (w + npairs < W) nx = fetch(w + npairs);
+      const int nkv = x.nkv, h = x.h;
+      const bool row_ok = row_in_unit < x.rows_valid;
+      const int64_t row = x.cbeg + row_in_unit;
+      if (nkv == 0) {
+        // L_b = 0: no keys, O = 0 and lse = -inf
+        if (row_ok) {
+          if (p.o_bf16) {
+            uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.O) + row * HD + h * kD);
+#pragma unroll
+            for (int v = 0; v < 16; ++v) dst[v] = make_uint4(0u, 0u, 0u, 0u);
+          } else {
+            float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.O) + row * HD + h * kD);
+#pragma unroll
+            for (int v = 0; v < 32; ++v) dst[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+          if (p.lse != nullptr) p.lse[row * p.H + h] = -INFINITY;
+        }
+        continue;
+      }
+      pwait(ml_full, m & 1);
+      if (sub == 0 && lane == 0) GESR_T3(5, m);
+      const uint32_t xb = xch + ((m & 1) * 2 * 2 * 128) * 4;
+      const float mA = ld_shared_f32(xb + (0 * 128 + rloc) * 4);
+      const float lA = ld_shared_f32(xb + (1 * 128 + rloc) * 4);
       const bool hasB = nkv > 1;
+      const float mB = hasB ? ld_shared_f32(xb + (2 * 128 + rloc) * 4) : -INFINITY;
+      const float lB = hasB ? ld_shared_f32(xb + (3 * 128 + rloc) * 4) : 0.f;
       const float mm = hasB ? fmaxf(mA, mB) : mA;
       const float wA = ex2(mA - mm);
       const float wB = hasB ? ex2(mB - mm) : 0.f;
       const float lsum = lA * wA + lB * wB;
       const float inv = 1.0f / lsum;
       const float fA = wA * inv, fB = wB * inv;
-      mbar_wait_sleep(o_done, m & 1);
+      // the previous unit's TMA stores must have read the staging boxes
+      if (lane == 0) bulk_wait_group_read<0>();
+      __syncwarp();
+      pwait(o_done, m & 1);
+      if (sub == 0 && lane == 0) GESR_T3(6, m);
       tc_fence_after();
-      const bool use_tma = p.o_tma && static_cast<int>(rank) * 128 + static_cast<int>(sub) * 32 + 32 <= x.rows_valid;
+      // 32 columns per TMEM round trip (four x16 loads, one wait), merged with packed FMAs
 #pragma unroll 1
-      for (int cc = 0; cc < 2; ++cc) {
-        const int c = g * 2 + cc;                        // 32-column chunk of O
+      for (int c = 0; c < kD / 32; ++c) {
         uint32_t oa[32], ob[32];
-        tmem_ld32(tO + c * 32, oa);
-        if (hasB) tmem_ld32(tO + kD + c * 32, ob);
+        tmem_ld16(tO + c * 32, oa);
+        tmem_ld16(tO + c * 32 + 16, oa + 16);
+        if (hasB) {
+          tmem_ld16(tO + kD + c * 32, ob);
+          tmem_ld16(tO + kD + c * 32 + 16, ob + 16);
+        }
         tmem_ld_wait();
-        float v[32];
-#pragma unroll
-        for (int e = 0; e < 32; ++e)
-          v[e] = hasB ? __uint_as_float(oa[e]) * fA + __uint_as_float(ob[e]) * fB
-                      : __uint_as_float(oa[e]) * fA;
-        if (use_tma) {
-          uint32_t pk2[16];
-#pragma unroll
-          for (int e = 0; e < 16; ++e) pk2[e] = pack_bf16x2(v[2 * e], v[2 * e + 1]);
-          if (lane == 0) bulk_wait_group_read<1>();       // box (cc) read by its previous store
+        if (sub == 0 && lane == 0) GESR_T4(c, m);
+        if (c == kD / 32 - 1) {
+          // O_A / O_B drained: the next unit's first PV may overwrite them
+          tc_fence_before();
           __syncwarp();
-          uint8_t* box = stg + cc * 2048;
-          uint8_t* rowp = box + lane * 64;
+          if (lane == 0) {
+            mbar_arrive_cluster_relaxed(o_free_leader);
+            mbar_arrive(o_read);
+          }
+          if (sub == 0 && lane == 0) GESR_T3(7, m);
+        }
+        // v = O_A fA + O_B fB, in place in oa
+        if (hasB) {
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
-            *reinterpret_cast<uint4*>(rowp + ((q ^ ((lane >> 1) & 3)) << 4)) =
-                make_uint4(pk2[4 * q], pk2[4 * q + 1], pk2[4 * q + 2], pk2[4 * q + 3]);
+          for (int e = 0; e < 32; e += 2) {
+            float t0, t1, y0, y1;
+            fmul2(t0, t1, __uint_as_float(ob[e]), __uint_as_float(ob[e + 1]), fB, fB);
+            ffma2(y0, y1, __uint_as_float(oa[e]), __uint_as_float(oa[e + 1]), fA, fA, t0, t1);
+            oa[e] = __float_as_uint(y0);
+            oa[e + 1] = __float_as_uint(y1);
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < 32; e += 2) {
+            float y0, y1;
+            fmul2(y0, y1, __uint_as_float(oa[e]), __uint_as_float(oa[e + 1]), fA, fA);
+            oa[e] = __float_as_uint(y0);
+            oa[e + 1] = __float_as_uint(y1);
+          }
+        }
+        if (p.o_bf16) {
+          // box c (32 rows x 32 columns): 16-byte chunk qq of row `lane` (64B swizzle)
+          const uint32_t rowp = stg_s + c * 2048 + lane * 64;
+#pragma unroll
+          for (int qq = 0; qq < 4; ++qq) {
+            const int e = qq * 8;
+            st_shared_v4(rowp + ((qq ^ ((lane >> 1) & 3)) << 4),
+                         pack_bf16x2(__uint_as_float(oa[e]), __uint_as_float(oa[e + 1])),
+                         pack_bf16x2(__uint_as_float(oa[e + 2]), __uint_as_float(oa[e + 3])),
+                         pack_bf16x2(__uint_as_float(oa[e + 4]), __uint_as_float(oa[e + 5])),
+                         pack_bf16x2(__uint_as_float(oa[e + 6]), __uint_as_float(oa[e + 7])));
+          }
+          if (sub == 0 && lane == 0) GESR_T4(8 + c, m);
+        } else if (row_ok) {
+          float* dst = static_cast<float*>(p.O) + row * HD + h * kD + c * 32;
+#pragma unroll
+          for (int vv = 0; vv < 4; ++vv) st_global_v8(dst + 8 * vv, oa + 8 * vv);
+        }
+      }
+      if (p.o_bf16) {
+        const int row0 = static_cast<int>(rank) * 128 + static_cast<int>(sub) * 32;
+        if (p.o_tma && row0 + 32 <= x.rows_valid) {
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            tma_store_3d(&map_o, box, c * 32, h,
-                         static_cast<int32_t>(x.cbeg + static_cast<int>(rank) * 128 + static_cast<int>(sub) * 32));
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+              tma_store_3d(&map_o, stg + b * 2048, b * 32, h, static_cast<int32_t>(x.cbeg + row0));
             bulk_commit_group();
           }
-        } else if (row_ok) {
-          if (p.o_bf16) {
-            uint32_t pk2[16];
+        } else {
+          __syncwarp();
+          if (row_ok) {
+            // ragged slab: copy my row out of the boxes (un-swizzle) with 16-byte stores
+            uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.O) + row * HD + h * kD);
 #pragma unroll
-            for (int e = 0; e < 16; ++e) pk2[e] = pack_bf16x2(v[2 * e], v[2 * e + 1]);
-            __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(p.O) + row * HD + static_cast<int64_t>(h) * kD + c * 32;
-            st_global_v8(dst, pk2);
-            st_global_v8(dst + 16, pk2 + 8);
-          } else {
-            float* dst = static_cast<float*>(p.O) + row * HD + static_cast<int64_t>(h) * kD + c * 32;
+            for (int b = 0; b < 4; ++b)
 #pragma unroll
-            for (int vv = 0; vv < 4; ++vv) st_global_v8(dst + 8 * vv, reinterpret_cast<const uint32_t*>(v) + 8 * vv);
+              for (int qq = 0; qq < 4; ++qq)
+                dst[b * 4 + qq] = *reinterpret_cast<const uint4*>(
+                    stg + b * 2048 + lane * 64 + ((qq ^ ((lane >> 1) & 3)) << 4));
           }
+          __syncwarp();
         }
       }
-      if (g == 0 && row_ok && p.lse != nullptr)
+      if (row_ok && p.lse != nullptr)
         p.lse[row * p.H + h] = (mm + __log2f(lsum)) * 0.69314718055994530942f;
-      // O_A / O_B drained: the next unit's first PV may overwrite them
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster_relaxed(o_free_leader);
-      if (sub == 0 && lane == 0) GESR_T2(6 + g, m * 16 + nkv - 1);
       ++m;
     }
     if (lane == 0) bulk_wait_group<0>();   // staging boxes stay allocated until read
@@ -511,6 +698,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #ifdef GESR_TRACE
 extern "C" int gesr_debug_trace2_copy(void* host) {
   return static_cast<int>(cudaMemcpyFromSymbol(host, g_trace2, sizeof(g_trace2)));
+}
+extern "C" int gesr_debug_trace4_copy(void* host) {
+  return static_cast<int>(cudaMemcpyFromSymbol(host, g_trace4, sizeof(g_trace4)));
+}
+extern "C" int gesr_debug_trace3_copy(void* host) {
+  return static_cast<int>(cudaMemcpyFromSymbol(host, g_trace3, sizeof(g_trace3)));
 }
 #endif
 

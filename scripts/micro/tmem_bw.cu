@@ -3,6 +3,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cuda_runtime.h>
+#include "ptx.cuh"
 
 __device__ __forceinline__ void ld32(uint32_t a, uint32_t* r) {
   asm volatile(
@@ -24,6 +25,60 @@ __device__ __forceinline__ void st32(uint32_t a, const uint32_t* r) {
       "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]),
       "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]),
       "r"(r[29]), "r"(r[30]), "r"(r[31]));
+}
+
+template <int MODE>
+__global__ void k(uint32_t* out, unsigned long long* clk, int iters);
+
+// tcgen05.ld (x16, like the attention epilogue) latency + throughput from warps 4.., with and
+// without a concurrent MMA stream (SS M=128 N=128 K=16 into columns 256..383) from warp 0.
+template <int WITH_MMA>
+__global__ void k_mma(unsigned long long* clk, int iters) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint32_t slot;
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ volatile int stop;
+  const int warp = threadIdx.x / 32;
+  if (warp == 0) { gesr::tmem_alloc(&slot, 512); gesr::tmem_relinquish(); }
+  if (threadIdx.x == 0) { gesr::mbar_init(&bar, 1); gesr::fence_mbar_init(); stop = 0; }
+  gesr::tc_fence_before();
+  __syncthreads();
+  gesr::tc_fence_after();
+  const uint32_t tmem = slot;
+  if (warp == 0) {
+    if (WITH_MMA && threadIdx.x == 0) {
+      const uint32_t sa = gesr::smem_u32(smem), sb = gesr::smem_u32(smem + 32768);
+      const uint32_t idesc = gesr::make_idesc_bf16(128, 128, 0, 0);
+      int n = 0;
+      while (!stop && n < 200000) {
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks)
+          gesr::mma_ss(tmem + 256, gesr::make_sdesc(sa + (ks / 4) * 16384 + (ks % 4) * 32, 16, 1024, 2),
+                       gesr::make_sdesc(sb + (ks / 4) * 16384 + (ks % 4) * 32, 16, 1024, 2), idesc, 1u);
+        ++n;
+        if ((n & 15) == 0) { gesr::mma_commit(&bar); gesr::mbar_wait(&bar, ((n >> 4) - 1) & 1); }
+      }
+    }
+  } else if (warp >= 4) {
+    const uint32_t taddr = tmem + (((warp & 3) * 32) << 16) + ((warp / 4) - 1) * 64;
+    uint32_t a[16], b[16], acc = 0;
+    const unsigned long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+      gesr::tmem_ld16(taddr + (it & 1) * 16, a);
+      gesr::tmem_ld16(taddr + 32 + (it & 1) * 16, b);
+      gesr::tmem_ld_wait();
+      acc += a[0] ^ b[15] ^ a[7];
+    }
+    const unsigned long long t1 = clock64();
+    if (threadIdx.x == 128) clk[blockIdx.x] = t1 - t0;
+    if (acc == 0x1234567u) clk[1000] = acc;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) stop = 1;
+  gesr::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) { gesr::tc_fence_after(); gesr::tmem_dealloc(tmem, 512); }
 }
 
 template <int MODE>
@@ -89,6 +144,21 @@ int main() {
       double bytes = double(warps) * 32 * iters * (mode == 0 ? 128 : 64) * 4;
       printf("%s warps=%2d  %.1f B/clk/SM  (%s)\n", mode == 0 ? "tcgen05.ld" : "tcgen05.st", warps,
              bytes / double(h[0]), cudaGetErrorString(e));
+    }
+  }
+  unsigned long long* c2;
+  cudaMalloc(&c2, 2048 * 8);
+  for (int mma = 0; mma < 2; ++mma) {
+    for (int warps : {1, 4}) {
+      const int iters = 2000;
+      const int threads = (4 + warps) * 32;
+      if (mma) { cudaFuncSetAttribute(k_mma<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024); k_mma<1><<<148, threads, 80 * 1024>>>(c2, iters); }
+      else { cudaFuncSetAttribute(k_mma<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024); k_mma<0><<<148, threads, 80 * 1024>>>(c2, iters); }
+      cudaError_t e = cudaDeviceSynchronize();
+      unsigned long long h;
+      cudaMemcpy(&h, c2, 8, cudaMemcpyDeviceToHost);
+      printf("2 x tcgen05.ld x16 + wait, %d loader warp(s)%s: %.0f clk per iteration (%s)\n", warps,
+             mma ? ", MMA stream running" : "", double(h) / iters, cudaGetErrorString(e));
     }
   }
   return 0;

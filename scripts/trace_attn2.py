@@ -1,5 +1,5 @@
 """Debug: timeline of the persistent CTA-pair attention pipeline (-DGESR_TRACE build via GESR_LIB,
-GESR_ATTN_PAIR=1).  Rows are global key tiles (unit * 16 + j) of a CTA."""
+GESR_ATTN_PAIR=1).  Rows are global key tiles (unit * 16 + j); softmax events of warpgroup A."""
 import ctypes, os, sys
 import numpy as np
 import torch
@@ -17,16 +17,37 @@ for _ in range(3):
 torch.cuda.synchronize()
 buf = np.zeros((64, 64, 8), np.uint64)
 assert gb.lib().gesr_debug_trace2_copy(ctypes.c_void_p(buf.ctypes.data)) == 0
-names = ["sA_ready", "sB_ready", "pA_done", "pB_done", "mma_pA", "mma_pB", "epiA_end", "epiB_end"]
+names = ["s_ready", "s_loaded", "s_freed", "exp_done", "token", "p_done", "mma_pv", "mma_s"]
 for cta in (0, 1, 10):
     t = buf[cta].astype(np.int64)
-    base = t[0, 0] if t[0, 0] else t[0, 4]
-    print(f"CTA {cta}: clk relative to sA_ready[0]")
+    base = t[0, 0]
+    print(f"CTA {cta}: clk relative to s_ready[0] (even tiles: warpgroup A, odd: B)")
     print("   g " + " ".join(f"{n:>10s}" for n in names))
-    for g in range(48):
+    for g in range(40):
         print(f"  {g:2d} " + " ".join(f"{int(t[g, e] - base) if t[g, e] else 0:10d}" for e in range(8)))
-    sa = t[:48, 0][::2]
-    print("  A period per 2 tiles:", np.diff(sa[sa > 0]).tolist())
-    print("  softmax A (s->p):", (t[:48:2, 2] - t[:48:2, 0]).tolist())
-    print("  softmax B (s->p):", (t[1:48:2, 3] - t[1:48:2, 1]).tolist())
-    print("  A pdone->mma:", (t[:48:2, 4] - t[:48:2, 2]).tolist())
+    for par in (0, 1):
+      ev = t[par:40:2]
+      ev = ev[ev[:, 0] > 0]
+      print("  warpgroup", "AB"[par])
+      for a, b, nm in [(0, 1, "ld"), (1, 2, "sfree"), (2, 4, "tokwait"), (4, 3, "exp"), (3, 5, "fence"), (5, 0, "->next s")]:
+        if nm == "->next s":
+            d = ev[1:, 0] - ev[:-1, 5]
+        else:
+            d = ev[:, b] - ev[:, a]
+        print(f"    {nm:9s}", d.tolist())
+buf3 = np.zeros((64, 16, 8), np.uint64)
+assert gb.lib().gesr_debug_trace3_copy(ctypes.c_void_p(buf3.ctypes.data)) == 0
+names3 = ["q_full_ok", "o_free_ok", "lastPV_iss", "Qload_iss", "K0_iss", "ml_full", "o_done", "o_free_arr"]
+for cta in (0, 1):
+    t = buf3[cta].astype(np.int64)
+    base = buf[cta, 0, 0].astype(np.int64)
+    print(f"CTA {cta} per-unit control events (clk rel. to s_ready[0])")
+    print("   u " + " ".join(f"{n:>10s}" for n in names3))
+    for u in range(5):
+        print(f"  {u:2d} " + " ".join(f"{int(t[u, e] - base) if t[u, e] else 0:10d}" for e in range(8)))
+buf4 = np.zeros((64, 16, 16), np.uint64)
+assert gb.lib().gesr_debug_trace4_copy(ctypes.c_void_p(buf4.ctypes.data)) == 0
+t4 = buf4[0].astype(np.int64)
+for u in range(3):
+    print(f"unit {u} epilogue chunk loads (clk after o_done):", (t4[u, :4] - buf3[0, u, 6].astype(np.int64)).tolist())
+    print(f"unit {u} epilogue chunk stores (clk after o_done):", (t4[u, 8:12] - buf3[0, u, 6].astype(np.int64)).tolist())
