@@ -62,13 +62,16 @@ __device__ unsigned long long g_trace4[64][16][16];  // per unit: epilogue chunk
 
 namespace {
 
+#ifndef GESR_PAIR_STS_AFTER
+#define GESR_PAIR_STS_AFTER 0   // experiment: P packed in place, stored after the exp loop (no rescale)
+#endif
+#ifndef GESR_PAIR_POLY_EVERY
+#define GESR_PAIR_POLY_EVERY 1000   // one pair in N takes the FMA-pipe exp2 on full tiles (1000: off)
+#endif
 #ifndef GESR_PAIR_SUM_LIMIT
 #define GESR_PAIR_SUM_LIMIT 4096.0f   // tile row sums above this take the exact-max path
 #endif
 // mbarrier waits: 1 = try_wait spin loop, 0 = try_wait with a suspend-time hint
-#ifndef GESR_PAIR_GATE
-#define GESR_PAIR_GATE 1      // a unit's first exp pass waits for the epilogue's TMEM reads
-#endif
 #ifndef GESR_PAIR_SPIN
 #define GESR_PAIR_SPIN 0
 #endif
@@ -90,7 +93,8 @@ constexpr uint32_t kRingOff = kPOff + 2 * kPBytes;
 constexpr uint32_t kStgOff = kRingOff + kStages * kHalfBytes;        // 4 x 2 KB boxes per epilogue warp
 constexpr uint32_t kBarOff = kStgOff + 4 * 8192;
 constexpr uint32_t kXchOff = kBarOff + 256;                          // [unit parity][WG][m, l][row]
-constexpr uint32_t kSmemBytes = kXchOff + 2 * 2 * 2 * 128 * 4 + 1024;
+constexpr uint32_t kMshOff = kXchOff + 2 * 2 * 2 * 128 * 4;          // shared running max [row]
+constexpr uint32_t kSmemBytes = kMshOff + 128 * 4 + 1024;
 static_assert(kSmemBytes <= 232448, "shared memory budget");
 // register split (setmaxnreg per warpgroup; launch registers 128 x 512 threads): control 56,
 // softmax 184, epilogue 88
@@ -100,7 +104,7 @@ constexpr int kEpiRegs = 88;
 static_assert(128 * kCtrlRegs + 256 * kSoftRegs + 128 * kEpiRegs <= 128 * kThreads, "setmaxnreg pool");
 // TMEM columns
 constexpr uint32_t kTS = 0;          // S_A at 0, S_B at 128
-constexpr uint32_t kTO = 256;        // O_A at 256, O_B at 384
+constexpr uint32_t kTO = 256;        // O of even units at 256, of odd units at 384
 
 __device__ __forceinline__ void ffma2(float& d0, float& d1, float a0, float a1, float b0, float b1,
                                       float c0, float c1) {
@@ -113,10 +117,31 @@ __device__ __forceinline__ void fmul2(float& d0, float& d1, float a0, float a1, 
       " mul.rn.f32x2 d, a, b;\n mov.b64 {%0, %1}, d;\n}"
       : "=f"(d0), "=f"(d1) : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
 }
+// 2^x for a pair on the FMA pipe only (no MUFU, no min/max): x clamped to [-126, 126] with a
+// saturating FFMA, split x = j + f with the 1.5*2^23 magic add, degree-3 polynomial for 2^f on
+// [-0.5, 0.5] (max rel. error 2.1e-4, below the bf16 rounding of P), exponent added with an
+// IMAD.  Used for one pair in GESR_PAIR_POLY_EVERY on full tiles.
+__device__ __forceinline__ void exp2_fma2(float& y0, float& y1, float x0, float x1);
 __device__ __forceinline__ void fadd2(float& d0, float& d1, float a0, float a1, float b0, float b1) {
   asm("{\n .reg .b64 a, b, d;\n mov.b64 a, {%2, %3};\n mov.b64 b, {%4, %5};\n"
       " add.rn.f32x2 d, a, b;\n mov.b64 {%0, %1}, d;\n}"
       : "=f"(d0), "=f"(d1) : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
+
+__device__ __forceinline__ void exp2_fma2(float& y0, float& y1, float x0, float x1) {
+  float u0, u1;
+  asm("fma.rn.sat.f32 %0, %1, %2, %3;" : "=f"(u0) : "f"(x0), "f"(1.0f / 252.0f), "f"(0.5f));
+  asm("fma.rn.sat.f32 %0, %1, %2, %3;" : "=f"(u1) : "f"(x1), "f"(1.0f / 252.0f), "f"(0.5f));
+  constexpr float kMagic = 12582912.0f;   // 1.5 * 2^23
+  float t0, t1, s0, s1, f0, f1, p0, p1;
+  ffma2(t0, t1, u0, u1, 252.0f, 252.0f, kMagic - 126.0f, kMagic - 126.0f);   // round(x') in low bits
+  fadd2(s0, s1, -t0, -t1, kMagic - 126.0f, kMagic - 126.0f);                   // -126 - round(x')
+  ffma2(f0, f1, u0, u1, 252.0f, 252.0f, s0, s1);                                // f = x' - round(x')
+  ffma2(p0, p1, f0, f1, 0.054848f, 0.054848f, 0.24180661f, 0.24180661f);
+  ffma2(p0, p1, p0, p1, f0, f1, 0.6932482f, 0.6932482f);
+  ffma2(p0, p1, p0, p1, f0, f1, 0.99998866f, 0.99998866f);
+  y0 = __int_as_float(__float_as_int(t0) * (1 << 23) + __float_as_int(p0));
+  y1 = __int_as_float(__float_as_int(t1) * (1 << 23) + __float_as_int(p1));
 }
 
 // K-major descriptor (SW128) for a [rows][128] bf16 tile stored as 2 column blocks of
@@ -158,11 +183,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t* s_free = s_full + 2;                  // [2]        (leader; 8 warps of the pair)
   uint64_t* p_full = s_free + 2;                  // [2]        (leader; 8 warps of the pair)
   uint64_t* p_free = p_full + 2;                  // [2]        (each CTA)
-  uint64_t* o_done = p_free + 2;                  //            (each CTA)
-  uint64_t* o_free = o_done + 1;                  //            (leader; 8 epilogue warps of the pair)
-  uint64_t* ml_full = o_free + 1;                 //            (each CTA; its 8 softmax warps)
-  uint64_t* o_read = ml_full + 1;                 //            (each CTA; its 4 epilogue warps)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_read + 1);
+  uint64_t* o_done = p_free + 2;                  // [2]        (each CTA; per O buffer)
+  uint64_t* o_free = o_done + 2;                  // [2]        (leader; 8 epilogue warps of the pair)
+  uint64_t* ml_full = o_free + 2;                 //            (each CTA; its 8 softmax warps)
+  uint64_t* pv_done = ml_full + 1;                //            (each CTA; one phase per PV)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 1);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -184,10 +209,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_init(&p_full[i], 8);
       mbar_init(&p_free[i], 1);
     }
-    mbar_init(o_done, 1);
-    mbar_init(o_free, 8);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&o_done[i], 1);
+      mbar_init(&o_free[i], 8);
+    }
     mbar_init(ml_full, 8);
-    mbar_init(o_read, 4);
+    mbar_init(pv_done, 1);
     fence_mbar_init();
   }
   if (warp == 1) {
@@ -348,9 +375,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int vslot = kKStages + vst;
         pwait(&kv_full[vslot], vph);
         if (++vst == kVStages) { vst = 0; vph ^= 1; }
-        if (tl.t == 0 && tl.m > 0) {
-          // the unit's first PV overwrites O_A: the previous unit's epilogue must have read O
-          pwait(o_free, (tl.m - 1) & 1);
+        const int ob = tl.m & 1;                     // O buffer of this unit
+        if (tl.t == 0 && tl.m >= 2) {
+          // the unit's first PV overwrites its O buffer: unit m-2's epilogue must have read it
+          pwait(&o_free[ob], ((tl.m >> 1) - 1) & 1);
           if (lane == 0) GESR_T3(1, tl.m);
         }
         const uint32_t pn = xb ? pn1 : pn0;
@@ -363,11 +391,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const uint32_t pb = sP + xb * kPBytes;
 #pragma unroll
           for (int ks = 0; ks < kKeys / 16; ++ks)
-            mma_ss_pair(tmem + kTO + xb * kD, kdesc(pb, kPBytes / 2, ks), vdesc(vb, ks), idesc_o,
-                        (tl.t >= 2 || ks > 0) ? 1u : 0u);
+            mma_ss_pair(tmem + kTO + ob * kD, kdesc(pb, kPBytes / 2, ks), vdesc(vb, ks), idesc_o,
+                        (tl.t > 0 || ks > 0) ? 1u : 0u);
           mma_commit_pair_mc(&p_free[xb], 0x3);
           mma_commit_pair_mc(&kv_empty[vslot], 0x3);
-          if (tl.t == tl.x.nkv - 1) mma_commit_pair_mc(o_done, 0x3);
+          mma_commit_pair_mc(pv_done, 0x3);
+          if (tl.t == tl.x.nkv - 1) mma_commit_pair_mc(&o_done[ob], 0x3);
         }
         __syncwarp();
         if (tl.t == tl.x.nkv - 1 && lane == 0) GESR_T3(2, tl.m);
@@ -375,17 +404,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   } else if (warp < 12) {
     // ------------------------------------------------------------ softmax
+    // Both warpgroups accumulate into ONE O per unit (double-buffered across units in TMEM, so
+    // the epilogue of unit u overlaps unit u+1) with ONE running max per row, m_sh (shared
+    // memory).  The MUFU token orders the tiles' exp passes A(0), B(1), A(2), ...; m_sh is
+    // written only by the token holder and read after taking the token, so every P(j) is
+    // computed against the max O is scaled to when PV(j) lands.  Raising m_sh (rare: a tile
+    // whose row sum exceeds 2^12 and whose exact max exceeds m_sh by > 8, log2 units) waits for
+    // PV(j-1) and rescales O first.  Each warpgroup keeps its own row sum l relative to the
+    // m_sh it last used (m_loc) and rescales it when it finds m_sh raised.
     setmaxnreg_inc<kSoftRegs>();
     const int g = (static_cast<int>(warp) - 4) >> 2;   // warpgroup: 0 = A (even tiles), 1 = B
     const uint32_t sub = warp & 3;                       // TMEM lane quarter
     const int rloc = static_cast<int>(sub) * 32 + static_cast<int>(lane);
     const uint32_t lane_addr = (sub * 32) << 16;
     const uint32_t tS = tmem + lane_addr + kTS + g * kKeys;
-    const uint32_t tO = tmem + lane_addr + kTO;          // O_A; O_B at + kD
-    const uint32_t tOg = tO + g * kD;
     const uint32_t s_free_leader = mapa_shared(smem_u32(&s_free[g]), 0);
     const uint32_t p_full_leader = mapa_shared(smem_u32(&p_full[g]), 0);
     const uint32_t xch = smem_u32(smem + kXchOff);
+    const uint32_t msh = smem_u32(smem + kMshOff) + rloc * 4;
     // P_g: K-major SW128, [2 atoms of 64 keys][128 rows][128 B]; row rloc's 16-byte chunk c of
     // atom a sits at a * 16 KB + rloc * 128 + ((c ^ (rloc & 7)) << 4)
     const uint32_t prow = smem_u32(smem + kPOff + g * kPBytes) + rloc * 128;
@@ -399,13 +435,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const uint32_t tok_other = (g == 0 ? 9u : 5u) + sub;
     bool prev_last_b = false;                            // previous unit's last tile was B's
     int m = 0;                                           // units with key tiles so far
+    int gbase = 0;                                       // stream index of the unit's tile 0
     int4 nx = fetch(pair);
     for (int w = pair; w < W; w += npairs) {
       const Work x = decode(w, nx);
       if (w + npairs < W) nx = fetch(w + npairs);
       const int L = x.L, nkv = x.nkv;
       if (nkv == 0) continue;                          // the epilogue warps write O = 0
-      float m_run = -INFINITY;
+      const uint32_t tO = tmem + lane_addr + kTO + (m & 1) * kD;   // this unit's O
+      float m_loc = -INFINITY;
       float l = 0.f;
       for (int j = g; j < nkv; j += 2) {
         pwait(&s_full[g], sc & 1);
@@ -420,7 +458,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         tmem_ld_wait();
         if (trd) GESR_T2(1, m * 16 + j);
         const int valid = L - kKeys * j;
-        if (valid < kKeys) {
+        const bool full = valid >= kKeys;
+        if (!full) {
 #pragma unroll
           for (int k = 0; k < kKeys; ++k)
             if (k >= valid) r[k] = __float_as_uint(-INFINITY);   // keys beyond L_b
@@ -432,12 +471,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (trd) GESR_T2(2, m * 16 + j);
         // Row max.  Min/max instructions share the issue path of MUFU (scripts/micro/
         // exp_interf.cu: a max pass on the other warp of a sub-partition slows an exp pass from
-        // 1.17k to 2k cycles), so only a warpgroup's first tile of a unit reduces its exact max.
-        // Later tiles use the running max m_run speculatively and test the tile's row sum
-        // instead: sum <= 2^12 implies every p <= 2^12 (so l <= 2^23 and O stays far from fp32
-        // overflow).  Only rows over it reduce their exact max, and if that exceeds m_run by > 8
-        // (log2 units, the lazy-rescale bound) O_g is rescaled and p recomputed from S, still
-        // in registers.
+        // 1.17k to 2k cycles), so only the unit's tile 0 reduces its exact max; later tiles
+        // use m_sh speculatively and test the tile's row sum instead: sum <= 2^12 implies every
+        // p <= 2^12 (so l <= 2^23, O far from fp32 overflow).  Only rows over it reduce their
+        // exact max, and only if that exceeds m_sh by > 8 is m_sh raised.  (Each code path
+        // below appears once: the softmax loop must stay small in the instruction cache.)
         auto row_max = [&]() {
           float mx[8];
 #pragma unroll
@@ -445,15 +483,56 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int k = 0; k < kKeys; ++k) mx[k & 7] = fmaxf(mx[k & 7], __uint_as_float(r[k]));
           return fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
-                       fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) * sl2;
+                       fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
         };
-        if (j == g) m_run = row_max();
+        const bool first_b = j > 0 && m_loc == -INFINITY;   // B's first tile of the unit
+        if (j == 0) m_loc = row_max() * sl2;
+        // x = s*scale*log2e - m in place, before the token (FMA pipe, overlaps the other
+        // warpgroup's exp pass); B's first tile takes m = 0 and is shifted once m_sh is known
+        {
+          const float neg_m = first_b ? 0.f : -m_loc;
+#pragma unroll
+          for (int k = 0; k < kKeys / 2; ++k) {
+            float x0, x1;
+            ffma2(x0, x1, __uint_as_float(r[2 * k]), __uint_as_float(r[2 * k + 1]), sl2, sl2,
+                  neg_m, neg_m);
+            r[2 * k] = __float_as_uint(x0);
+            r[2 * k + 1] = __float_as_uint(x1);
+          }
+        }
         // P_g must have been read by PV(j-2) (long done, normally) before the exp pass writes it
         if (sc > 1) pwait(&p_free[g], (sc - 2) & 1);
+        if (j > 0 || prev_last_b) named_bar_sync(tok_mine, 64);   // tile j-1's exp pass is done
+        if (trd) GESR_T2(4, m * 16 + j);
+        float d = 0.f;                                   // shift of x still to apply
+        if (j == 0) {
+          st_shared_f32(msh, m_loc);                     // the unit's first max
+        } else {
+          const float ms = ld_shared_f32(msh);
+          if (first_b) {
+            d = ms;
+            m_loc = ms;
+          } else {
+            d = fmaxf(ms - m_loc, 0.f);                  // m_sh raised since my last tile
+            l *= ex2(-d);
+            m_loc += d;
+          }
+        }
         float acc[8];
-        // p = 2^(s*scale*log2e - m_run), packed to bf16 pairs and stored to P_g 16 bytes at a time
-        auto exp_pass = [&]() {
-          const float neg_m = -m_run;
+        float tsum;
+#pragma unroll 1
+        for (int pass = 0;; ++pass) {
+          if (__any_sync(0xffffffffu, d != 0.f)) {
+#pragma unroll
+            for (int k = 0; k < kKeys / 2; ++k) {
+              float x0, x1;
+              fadd2(x0, x1, __uint_as_float(r[2 * k]), __uint_as_float(r[2 * k + 1]), -d, -d);
+              r[2 * k] = __float_as_uint(x0);
+              r[2 * k + 1] = __float_as_uint(x1);
+            }
+          }
+          // p = 2^x, packed to bf16 pairs and stored to P_g 16 bytes at a time; masked keys
+          // give exactly 0
 #pragma unroll
           for (int e = 0; e < 8; ++e) acc[e] = 0.f;
 #pragma unroll
@@ -462,88 +541,91 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
               const int k = q * 4 + u;
-              float x0, x1;
-              ffma2(x0, x1, __uint_as_float(r[2 * k]), __uint_as_float(r[2 * k + 1]), sl2, sl2,
-                    neg_m, neg_m);
-              const float p0 = ex2(x0), p1 = ex2(x1);
+              float p0, p1;
+              if ((k % GESR_PAIR_POLY_EVERY) == GESR_PAIR_POLY_EVERY - 1 && full) {
+                exp2_fma2(p0, p1, __uint_as_float(r[2 * k]), __uint_as_float(r[2 * k + 1]));
+              } else {
+                p0 = ex2(__uint_as_float(r[2 * k]));
+                p1 = ex2(__uint_as_float(r[2 * k + 1]));
+              }
               const int a = (k & 3) * 2;
               fadd2(acc[a], acc[a + 1], acc[a], acc[a + 1], p0, p1);
               pw[u] = pack_bf16x2(p0, p1);
+              if (GESR_PAIR_STS_AFTER) r[k] = pw[u];
             }
-            st_shared_v4(prow + (q >> 3) * (kPBytes / 2) + (((q & 7) ^ (rloc & 7)) << 4), pw[0], pw[1],
-                         pw[2], pw[3]);
+            if (!GESR_PAIR_STS_AFTER)
+              st_shared_v4(prow + (q >> 3) * (kPBytes / 2) + (((q & 7) ^ (rloc & 7)) << 4), pw[0], pw[1],
+                           pw[2], pw[3]);
           }
-        };
-        // A unit's first exp pass waits until the epilogue warps have read the previous unit's
-        // O out of TMEM: their TMEM loads and smem stores then do not queue behind this
-        // warpgroup's MUFU stream, and the unit's first PV is not held up by a slow epilogue.
-        if (GESR_PAIR_GATE && j == g && m > 0) pwait(o_read, (m - 1) & 1);
-        // masked keys give exactly 0
-        if (j > 0 || prev_last_b) named_bar_sync(tok_mine, 64);   // tile j-1's exp pass is done
-        if (trd) GESR_T2(4, m * 16 + j);
-        exp_pass();
+          if (GESR_PAIR_STS_AFTER) {
+#pragma unroll
+            for (int q = 0; q < kKeys / 8; ++q)
+              st_shared_v4(prow + (q >> 3) * (kPBytes / 2) + (((q & 7) ^ (rloc & 7)) << 4), r[4 * q],
+                           r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
+          }
+          if (trd && pass == 0) GESR_T2(3, m * 16 + j);
+          tsum = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+          const bool over = !(tsum <= GESR_PAIR_SUM_LIMIT);
+          if (pass == 1 || j == 0 || GESR_PAIR_STS_AFTER || !__any_sync(0xffffffffu, over)) break;
+          const float dx = over ? row_max() : 0.f;       // exact max above m_loc (x units)
+          const bool need = dx > 8.0f;
+          if (!__any_sync(0xffffffffu, need)) break;
+          // raise m_sh: O must hold PV(j-1) (the other warpgroup's last tile) before it is
+          // rescaled; no later PV can land before this warpgroup's p_full(j)
+          pwait(pv_done, (gbase + j - 1) & 1);
+          tc_fence_after();
+          d = need ? dx : 0.f;
+          const float alpha = ex2(-d);
+          if (need) {
+            m_loc += d;
+            l *= alpha;
+            st_shared_f32(msh, m_loc);
+          }
+#pragma unroll 1
+          for (int c = 0; c < 4; ++c) {
+            uint32_t o[32];
+            tmem_ld32(tO + c * 32, o);
+            tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+            tmem_st32(tO + c * 32, o);
+          }
+          tmem_st_wait();
+          tc_fence_before();
+        }
         // hand the token to tile j+1's warpgroup (the next unit starts with A)
         if (j + 1 < nkv || (g == 1 && w + npairs < W)) named_bar_arrive(tok_other, 64);
-        float tsum = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
-        if (j != g && __any_sync(0xffffffffu, !(tsum <= GESR_PAIR_SUM_LIMIT))) {
-          float mt = m_run;
-          if (!(tsum <= GESR_PAIR_SUM_LIMIT)) mt = row_max();
-          const bool need = mt > m_run + 8.0f;
-          if (__any_sync(0xffffffffu, need)) {
-            // O_g must hold PV(j-2) before it is rescaled
-            pwait(&p_free[g], (sc - 2) & 1);
-            tc_fence_after();
-            float alpha = 1.f;
-            if (need) {
-              alpha = ex2(m_run - mt);
-              m_run = mt;
-              l *= alpha;
-            }
-#pragma unroll 1
-            for (int c = 0; c < 4; ++c) {
-              uint32_t o[32];
-              tmem_ld32(tOg + c * 32, o);
-              tmem_ld_wait();
-#pragma unroll
-              for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-              tmem_st32(tOg + c * 32, o);
-            }
-            tmem_st_wait();
-            tc_fence_before();
-            exp_pass();   // recompute p with the new running max
-            tsum = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
-          }
-        }
         l += tsum;
-        if (trd) GESR_T2(3, m * 16 + j);
         fence_proxy_async_smem();
         __syncwarp();
         if (trd) GESR_T2(5, m * 16 + j);
         if (lane == 0) mbar_arrive_cluster_relaxed(p_full_leader);
       }
       prev_last_b = ((nkv - 1) & 1) == 1;
-      // publish this warpgroup's running max / sum of my rows for the epilogue warps
+      // publish this warpgroup's max / sum of my rows for the epilogue warps
       const uint32_t xb = xch + ((m & 1) * 2 * 2 * 128) * 4;      // [WG][m, l][row]
-      st_shared_f32(xb + ((g * 2 + 0) * 128 + rloc) * 4, m_run);
+      st_shared_f32(xb + ((g * 2 + 0) * 128 + rloc) * 4, m_loc);
       st_shared_f32(xb + ((g * 2 + 1) * 128 + rloc) * 4, l);
       __syncwarp();
       if (lane == 0) mbar_arrive(ml_full);
+      gbase += nkv;
       ++m;
     }
   } else {
     // ------------------------------------------------------------ epilogue (warps 12-15)
-    // Merges the two partial softmaxes of a unit while the softmax warpgroups already work on
-    // the next one: O = (O_A 2^(m_A-m) + O_B 2^(m_B-m)) / (l_A 2^(m_A-m) + l_B 2^(m_B-m)).
-    // bf16 output: the warp's 32 rows x 128 columns are merged 16 columns at a time into four
-    // 2 KB staging boxes (32 rows x 32 columns, 64B swizzle); TMEM is released as soon as the
-    // last columns are read, then full 32-row slabs leave with TMA tensor stores (a ragged slab
-    // stores its valid rows from the boxes).  fp32 output: direct stores.
+    // Normalises a unit's O (one accumulator, both warpgroups' PVs) while the softmax
+    // warpgroups already work on the next unit: O / (l_A 2^(m_A-m) + l_B 2^(m_B-m)).  bf16
+    // output: the warp's 32 rows x 128 columns go through four 2 KB staging boxes (32 rows x 32
+    // columns, 64B swizzle), the O buffer is released as soon as it is read, then full 32-row
+    // slabs leave with TMA tensor stores (a ragged slab stores its valid rows from the boxes).
+    // fp32 output: direct stores.
     setmaxnreg_dec<kEpiRegs>();
     const uint32_t sub = warp & 3;
     const int rloc = static_cast<int>(sub) * 32 + static_cast<int>(lane);
     const int row_in_unit = static_cast<int>(rank) * 128 + rloc;
-    const uint32_t tO = tmem + ((sub * 32) << 16) + kTO;   // O_A; O_B at + kD
-    const uint32_t o_free_leader = mapa_shared(smem_u32(o_free), 0);
+    const uint32_t tO0 = tmem + ((sub * 32) << 16) + kTO;   // O buffer 0; buffer 1 at + kD
+    const uint32_t o_free_leader0 = mapa_shared(smem_u32(&o_free[0]), 0);
+    const uint32_t o_free_leader1 = mapa_shared(smem_u32(&o_free[1]), 0);
     const uint32_t xch = smem_u32(smem + kXchOff);
     uint8_t* stg = smem + kStgOff + sub * 8192;
     const uint32_t stg_s = smem_u32(stg);
@@ -580,58 +662,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const bool hasB = nkv > 1;
       const float mB = hasB ? ld_shared_f32(xb + (2 * 128 + rloc) * 4) : -INFINITY;
       const float lB = hasB ? ld_shared_f32(xb + (3 * 128 + rloc) * 4) : 0.f;
-      const float mm = hasB ? fmaxf(mA, mB) : mA;
-      const float wA = ex2(mA - mm);
-      const float wB = hasB ? ex2(mB - mm) : 0.f;
-      const float lsum = lA * wA + lB * wB;
+      const float mm = hasB ? fmaxf(mA, mB) : mA;      // = the final shared max O is scaled to
+      const float lsum = lA * ex2(mA - mm) + (hasB ? lB * ex2(mB - mm) : 0.f);
       const float inv = 1.0f / lsum;
-      const float fA = wA * inv, fB = wB * inv;
       // the previous unit's TMA stores must have read the staging boxes
       if (lane == 0) bulk_wait_group_read<0>();
       __syncwarp();
-      pwait(o_done, m & 1);
+      const int ob = m & 1;
+      pwait(&o_done[ob], (m >> 1) & 1);
       if (sub == 0 && lane == 0) GESR_T3(6, m);
       tc_fence_after();
-      // 32 columns per TMEM round trip (four x16 loads, one wait), merged with packed FMAs
+      const uint32_t tO = tO0 + ob * kD;
 #pragma unroll 1
       for (int c = 0; c < kD / 32; ++c) {
-        uint32_t oa[32], ob[32];
-        tmem_ld16(tO + c * 32, oa);
-        tmem_ld16(tO + c * 32 + 16, oa + 16);
-        if (hasB) {
-          tmem_ld16(tO + kD + c * 32, ob);
-          tmem_ld16(tO + kD + c * 32 + 16, ob + 16);
-        }
+        uint32_t o[32];
+        tmem_ld32(tO + c * 32, o);
         tmem_ld_wait();
         if (sub == 0 && lane == 0) GESR_T4(c, m);
         if (c == kD / 32 - 1) {
-          // O_A / O_B drained: the next unit's first PV may overwrite them
+          // O drained: unit m+2's first PV may overwrite it
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) {
-            mbar_arrive_cluster_relaxed(o_free_leader);
-            mbar_arrive(o_read);
-          }
+          if (lane == 0) mbar_arrive_cluster_relaxed(ob ? o_free_leader1 : o_free_leader0);
           if (sub == 0 && lane == 0) GESR_T3(7, m);
         }
-        // v = O_A fA + O_B fB, in place in oa
-        if (hasB) {
 #pragma unroll
-          for (int e = 0; e < 32; e += 2) {
-            float t0, t1, y0, y1;
-            fmul2(t0, t1, __uint_as_float(ob[e]), __uint_as_float(ob[e + 1]), fB, fB);
-            ffma2(y0, y1, __uint_as_float(oa[e]), __uint_as_float(oa[e + 1]), fA, fA, t0, t1);
-            oa[e] = __float_as_uint(y0);
-            oa[e + 1] = __float_as_uint(y1);
-          }
-        } else {
-#pragma unroll
-          for (int e = 0; e < 32; e += 2) {
-            float y0, y1;
-            fmul2(y0, y1, __uint_as_float(oa[e]), __uint_as_float(oa[e + 1]), fA, fA);
-            oa[e] = __float_as_uint(y0);
-            oa[e + 1] = __float_as_uint(y1);
-          }
+        for (int e = 0; e < 32; e += 2) {
+          float y0, y1;
+          fmul2(y0, y1, __uint_as_float(o[e]), __uint_as_float(o[e + 1]), inv, inv);
+          o[e] = __float_as_uint(y0);
+          o[e + 1] = __float_as_uint(y1);
         }
         if (p.o_bf16) {
           // box c (32 rows x 32 columns): 16-byte chunk qq of row `lane` (64B swizzle)
@@ -640,16 +700,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           for (int qq = 0; qq < 4; ++qq) {
             const int e = qq * 8;
             st_shared_v4(rowp + ((qq ^ ((lane >> 1) & 3)) << 4),
-                         pack_bf16x2(__uint_as_float(oa[e]), __uint_as_float(oa[e + 1])),
-                         pack_bf16x2(__uint_as_float(oa[e + 2]), __uint_as_float(oa[e + 3])),
-                         pack_bf16x2(__uint_as_float(oa[e + 4]), __uint_as_float(oa[e + 5])),
-                         pack_bf16x2(__uint_as_float(oa[e + 6]), __uint_as_float(oa[e + 7])));
+                         pack_bf16x2(__uint_as_float(o[e]), __uint_as_float(o[e + 1])),
+                         pack_bf16x2(__uint_as_float(o[e + 2]), __uint_as_float(o[e + 3])),
+                         pack_bf16x2(__uint_as_float(o[e + 4]), __uint_as_float(o[e + 5])),
+                         pack_bf16x2(__uint_as_float(o[e + 6]), __uint_as_float(o[e + 7])));
           }
           if (sub == 0 && lane == 0) GESR_T4(8 + c, m);
         } else if (row_ok) {
           float* dst = static_cast<float*>(p.O) + row * HD + h * kD + c * 32;
 #pragma unroll
-          for (int vv = 0; vv < 4; ++vv) st_global_v8(dst + 8 * vv, oa + 8 * vv);
+          for (int vv = 0; vv < 4; ++vv) st_global_v8(dst + 8 * vv, o + 8 * vv);
         }
       }
       if (p.o_bf16) {

@@ -43,8 +43,10 @@ template <int MODE>
 __global__ void __launch_bounds__(256, 1) k(uint32_t* out, int iters, float sl2, long long* clk) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint32_t slot;
+  __shared__ __align__(8) uint64_t mbar_s;
   const int warp = threadIdx.x / 32;
   if (warp == 0) { tmem_alloc(&slot, 512); tmem_relinquish(); }
+  if (threadIdx.x == 0) { mbar_init(&mbar_s, 1); fence_mbar_init(); }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -53,47 +55,61 @@ __global__ void __launch_bounds__(256, 1) k(uint32_t* out, int iters, float sl2,
   for (int i = 0; i < 128; ++i) r[i] = __float_as_uint((threadIdx.x * 128 + i) * 1e-5f);
   uint32_t sink = 0;
   if (warp < 4 && MODE >= 8) {
-    // the kernel's exp pass: p packed to bf16 pairs and stored 16 bytes at a time (swizzled)
+    // the kernel's exp pass variants (one warp per SMSP, other warps idle)
     float m = 0.5f;
     const uint32_t prow = smem_u32(smem) + threadIdx.x * 128;
+    const uint32_t taddr = tmem + (((warp & 3) * 32) << 16);
+    uint32_t sink2 = 0;
     const long long t0 = clock64();
     for (int it = 0; it < iters; ++it) {
       float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      const float nm = -m;
+      uint32_t x[128];
 #pragma unroll
-      for (int q = 0; q < 16; ++q) {
-        uint32_t pw[4];
+      for (int i = 0; i < 128; ++i) x[i] = r[i];
+      if (MODE == 13 || MODE == 14) {
+        // pack in place into x[0..63], then store after the loop
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int kk = q * 4 + u;
-          float x0, x1;
-          ffma2(x0, x1, __uint_as_float(r[2 * kk]), __uint_as_float(r[2 * kk + 1]), sl2, sl2, nm, nm);
-          float p0, p1;
-          if (MODE >= 10 && MODE <= 12 && (kk % (MODE - 8)) == 0) {
-            exp2_fma2(p0, p1, x0, x1);
-          } else {
-            p0 = ex2(x0);
-            p1 = ex2(x1);
-          }
+        for (int kk = 0; kk < 64; ++kk) {
+          const float p0 = ex2(__uint_as_float(x[2 * kk]) - m), p1 = ex2(__uint_as_float(x[2 * kk + 1]) - m);
           const int a = (kk & 3) * 2;
           fadd2(acc[a], acc[a + 1], acc[a], acc[a + 1], p0, p1);
-          pw[u] = pack_bf16x2(p0, p1);
-          if (MODE == 13) r[kk] = pw[u];
+          x[kk] = pack_bf16x2(p0, p1);
         }
-        if (MODE != 13) st_shared_v4(prow + (q >> 3) * 16384 + (((q & 7) ^ (threadIdx.x & 7)) << 4), pw[0], pw[1], pw[2], pw[3]);
+        if (MODE == 13) {
+#pragma unroll
+          for (int q = 0; q < 16; ++q)
+            st_shared_v4(prow + (q >> 3) * 16384 + (((q & 7) ^ (threadIdx.x & 7)) << 4), x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]);
+        } else {
+          tmem_st32(taddr, x);
+          tmem_st32(taddr + 32, x + 32);
+          tmem_st_wait();
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          uint32_t pw[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int kk = q * 4 + u;
+            float p0, p1;
+            if (MODE >= 10 && MODE <= 12 && (kk % (MODE - 8)) == 0) {
+              exp2_fma2(p0, p1, __uint_as_float(x[2 * kk]) - m, __uint_as_float(x[2 * kk + 1]) - m);
+            } else {
+              p0 = ex2(__uint_as_float(x[2 * kk]) - m);
+              p1 = ex2(__uint_as_float(x[2 * kk + 1]) - m);
+            }
+            const int a = (kk & 3) * 2;
+            fadd2(acc[a], acc[a + 1], acc[a], acc[a + 1], p0, p1);
+            pw[u] = pack_bf16x2(p0, p1);
+          }
+          st_shared_v4(prow + (q >> 3) * 16384 + (((q & 7) ^ (threadIdx.x & 7)) << 4), pw[0], pw[1], pw[2], pw[3]);
+        }
       }
+      sink2 += x[0] ^ x[5];
       m += (((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]))) * 1e-9f;
-      if (MODE == 13) {
-#pragma unroll
-        for (int q = 0; q < 16; ++q)
-          st_shared_v4(prow + (q >> 3) * 16384 + (((q & 7) ^ (threadIdx.x & 7)) << 4), r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
-#pragma unroll
-        for (int i = 0; i < 64; ++i) r[i] = r[i + 64] ^ (r[i] & 1u);
-      }
-      r[it & 127] ^= 1;
     }
     const long long t1 = clock64();
-    for (int i = 0; i < 128; ++i) sink ^= r[i];
+    sink ^= sink2;
     if (threadIdx.x == 0) clk[blockIdx.x] = t1 - t0;
   } else if (warp < 4) {
     float m = 0.5f;
@@ -178,6 +194,19 @@ __global__ void __launch_bounds__(256, 1) k(uint32_t* out, int iters, float sl2,
         const long long w0 = clock64();
         while (clock64() - w0 < 1200) {}
         sink += r[it & 127];
+      } else if (MODE == 15) {  // tcgen05 MMA stream (SS M=128 N=128 K=16) into columns 256..383
+        if (threadIdx.x == 128) {
+          const uint32_t sa = smem_u32(smem), sb = smem_u32(smem + 16384);
+          const uint32_t idesc = make_idesc_bf16(128, 128, 0, 0);
+#pragma unroll 1
+          for (int rep = 0; rep < 64; ++rep)
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks)
+              mma_ss(tmem + 256, make_sdesc(sa + ks * 32, 16, 1024, 2), make_sdesc(sb + ks * 32, 16, 1024, 2), idesc, 1u);
+          mma_commit(&mbar_s);
+          mbar_wait(&mbar_s, it & 1);
+        }
+        __syncwarp();
       } else if (MODE == 3) {  // 16 x st.shared.v4
 #pragma unroll
         for (int c = 0; c < 16; ++c) st_shared_v4(srow + ((c * 16) & 127) + (c / 8) * 16384, r[c], r[c + 1], r[c + 2], sink);
@@ -197,12 +226,12 @@ int main() {
   long long* c;
   cudaMalloc(&d, 4096);
   cudaMalloc(&c, 4096 * 8);
-  const char* names[14] = {"alone", "+FMNMX max pass", "+tcgen05.ld x128", "+16 STS.128 + proxy fence",
+  const char* names[16] = {"alone", "+FMNMX max pass", "+tcgen05.ld x128", "+16 STS.128 + proxy fence",
                           "+3-input max.f32", "+IMNMX on bits", "+max.bf16x2", "+FFMA stream",
                           "kernel loop (STS inside), alone", "kernel loop + ld/1.2k clk",
                           "kernel loop, poly 1 in 2", "kernel loop, poly 1 in 3", "kernel loop, poly 1 in 4",
-                          "pack in place, 16 STS after loop"};
-  for (int mode = 0; mode < 14; ++mode) {
+                          "pack in place, 16 STS after loop", "pack in place, 2 tcgen05.st after", "kernel loop + MMA stream (other warp)"};
+  for (int mode = 0; mode < 16; ++mode) {
     const int iters = 400;
     auto launch = [&] {
       if (mode == 0) k<0><<<148, 256, 40000>>>(d, iters, 0.1f, c);
@@ -219,6 +248,8 @@ int main() {
       if (mode == 11) k<11><<<148, 256, 40000>>>(d, iters, 0.1f, c);
       if (mode == 12) k<12><<<148, 256, 40000>>>(d, iters, 0.1f, c);
       if (mode == 13) k<13><<<148, 256, 40000>>>(d, iters, 0.1f, c);
+      if (mode == 14) k<14><<<148, 256, 40000>>>(d, iters, 0.1f, c);
+      if (mode == 15) k<15><<<148, 256, 40000>>>(d, iters, 0.1f, c);
     };
     launch();
     cudaError_t e = cudaDeviceSynchronize();

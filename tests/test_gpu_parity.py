@@ -271,6 +271,36 @@ def test_large_scores_no_overflow():
     assert O.abs().max() <= Vmax * 1.01
 
 
+@pytest.mark.parametrize("d", [128, 64])
+def test_growing_scores_raise_running_max(d):
+    # Key tiles whose scores grow tile by tile (x(1 + 3t)) and, at the end of request 0, jump by
+    # far more than 128 (log2 units) over everything before: exercises the lazy-rescale slow
+    # paths (running max raised, O rescaled, P recomputed after an overflowing speculative exp)
+    H, D_in = 2, 128
+    Ls, Cs = [1024, 700, 129], [150, 37, 260]
+    bt = _custom(Ls, Cs, H=H, d=d, D_in=D_in, cfg_id=300 + d)
+    K, V = oracle.kv_project(bt.U, bt.W_k, bt.W_v, H, d, act=1)
+    so = bt.seq_offsets.numpy()
+    f = np.ones(K.shape[1])
+    for b in range(len(Ls)):
+        t = np.arange(Ls[b]) // 128
+        f[so[b]:so[b + 1]] = 1.0 + 3.0 * t
+    f[so[0] + 1000:so[0] + 1024] = 60.0
+    f[so[2] + 128] = 80.0                       # a lone huge key in a 1-key tail tile
+    Kb = torch.from_numpy(K * f[None, :, None]).to(torch.bfloat16)
+    Vb = torch.from_numpy(V).to(torch.bfloat16)
+    # Q rounded to bf16 as the kernel's Q is (R8): with keys scaled x60-80 the
+    # 2^-9 rounding of Q alone moves scores by ~0.3
+    O_or, lse_or = oracle.tasa_score(bt.T, bt.cand_offsets, bt.W_q, Kb.double().numpy(),
+                                     Vb.double().numpy(), bt.seq_offsets, H, d, round_q_bf16=True)
+    g = bt.to(_cuda())
+    O, lse = gb.tasa_score(g.T, g.cand_offsets, g.W_q, Kb.to(_cuda()), Vb.to(_cuda()),
+                           g.seq_offsets, H, d, 1)
+    torch.cuda.synchronize()
+    _attn_tol(O.float().cpu().numpy(), O_or, f"growing scores d={d}")
+    assert np.abs(lse.cpu().numpy() - lse_or).max() < 5e-2
+
+
 # ----------------------------------------------------------------------------- HMA
 
 def _hma_gpu(bt, F, cap=0):
