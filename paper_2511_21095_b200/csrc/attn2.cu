@@ -1,32 +1,31 @@
-// attn2.cu -- K-ATTN for d = 128 on a CTA PAIR (tcgen05 cta_group::2), persistent, with two
-// softmax warpgroups that take alternate key tiles.
+// attn2.cu -- K-ATTN for d = 128 (the default for d = 128): CTA PAIR (tcgen05 cta_group::2),
+// persistent, two softmax warpgroups taking alternate key tiles.
 //
 // Same contract as attn.cu (PAPER.md:341 mask rules (1)-(2): each candidate attends to all L_b
 // history keys of its own request and to no other candidate; softmax per DESIGN.md R1).
 //
-// Why (profiles/r1_attn_trace.txt): in the 1-CTA kernel the softmax of a Q tile
-// and its MMAs form one dependency chain (softmax(j) -> PV(j) -> S(j+1) -> softmax(j+1)), so a
-// 128-key tile of two Q tiles takes ~3.8k cycles against ~2k of tensor work.  Here:
+// Why (profiles/): in the 1-CTA kernel the softmax of a Q tile and its MMAs form
+// one dependency chain (softmax(j) -> PV(j) -> S(j+1) -> softmax(j+1)) and every unit ends in
+// an epilogue bubble.  Here:
 //   * a cluster of 2 CTAs works on one unit (request b, head h, 256 candidates); CTA r owns
 //     candidate rows [128 r, 128 r + 128).  The leader issues M=256 MMAs for the pair: S = Q K^T
-//     (SS; each CTA stages its Q tile and HALF of each K tile -- 64 keys), O += P V (TS; P from
-//     each CTA's TMEM, each CTA stages HALF of each V tile -- 64 of the 128 d-columns), so each
-//     SM moves half of the 1-CTA kernel's K/V bytes per row;
-//   * the key tiles of a unit are dealt alternately to two softmax warpgroups: A takes the even
-//     tiles, B the odd ones.  Each has its own S buffer in TMEM, its own P buffer in SHARED
-//     memory, its own O accumulator and its own running max / sum; the two partial softmaxes are
-//     merged in the epilogue (O = (O_A 2^(m_A-m) + O_B 2^(m_B-m)) / (l_A 2^(m_A-m) + l_B 2^(m_B-m))).
-//     With P out of TMEM, a warpgroup frees its S buffer as soon as it has loaded S into
-//     registers (s_free), so S(j+2) is computed while the softmax of tile j runs: no MMA sits
-//     between two softmax passes of a warpgroup, and PV (SS form, A = P from smem) runs beside;
-//   * TMEM per CTA (512 columns): S_A [0,128), S_B [128,256), O_A [256,384), O_B [384,512);
-//   * persistent: pair c takes work items c, c + G, ... (w -> unit w % U, head w / U), the next
-//     unit's Q load and first S MMAs overlap the current unit's epilogue, and full 32-row output
-//     slabs leave through TMA tensor stores (staged in the warp's own rows of its P buffer).
-// Warp roles per CTA: warp 0 Q/K producer and warp 2 V producer (both CTAs), warp 1 TMEM
-// allocator + S MMA issuer and warp 3 PV MMA issuer (leader only), warps 4-7 softmax A, warps
-// 8-11 softmax B (warp w reads TMEM lane quarter w % 4: thread = candidate row, all 128 key
-// columns of its tile), warps 12-15 epilogue.
+//     (SS; each CTA stages its Q tile and HALF of each K tile -- 64 keys) and O += P V (SS; P
+//     from each CTA's shared memory, each CTA stages HALF of each V tile -- 64 d-columns);
+//   * P lives in shared memory, so a warpgroup frees its S buffer (TMEM) as soon as S is in
+//     registers and S(j+2) is computed during the softmax of tile j: no MMA sits between two
+//     softmax passes of a warpgroup;
+//   * key tiles alternate between softmax warpgroups A (even) and B (odd); a named-barrier
+//     "MUFU token" per sub-partition orders their exp passes A(0), B(1), A(2), ... so one's exp
+//     pass overlaps the other's TMEM load, x pass and P hand-off.  Both accumulate into ONE O per
+//     unit with ONE running max per row (m_sh in shared memory, written only by the token
+//     holder); the row max is exact only for tile 0, later tiles test the tile's row sum and
+//     take the slow path (exact max, raise m_sh, rescale O, recompute P) only when needed;
+//   * TMEM per CTA (512 columns): S_A [0,128), S_B [128,256), O of even units [256,384), O of
+//     odd units [384,512): a unit's epilogue (warps 12-15) overlaps the next unit entirely;
+//   * persistent: pair c takes work items c, c + G, ... (w -> unit w % U, head w / U); the key
+//     tiles of all its work items form one stream, walked independently by the Q/K producer,
+//     the V producer, the S-MMA issuer and the PV-MMA issuer; full 32-row output slabs leave
+//     through TMA tensor stores.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -75,9 +74,21 @@ namespace {
 #ifndef GESR_PAIR_SPIN
 #define GESR_PAIR_SPIN 0
 #endif
-__device__ __forceinline__ void pwait(uint64_t* bar, uint32_t parity) {
-  if (GESR_PAIR_SPIN) mbar_wait(bar, parity); else mbar_wait_sleep(bar, parity);
+// ctx (call site * 2^20 + unit * 2^8 + tile) is only reported if the wait times out
+__device__ __forceinline__ void pwait(uint64_t* bar, uint32_t parity, uint32_t ctx = 0) {
+  const uint32_t a = smem_u32(bar);
+  if (mbar_try_wait_hint(a, parity, GESR_PAIR_SPIN ? 0u : 1000000u)) return;
+  const long long t0 = clock64();
+  while (!mbar_try_wait_hint(a, parity, GESR_PAIR_SPIN ? 0u : 1000000u)) {
+    if (clock64() - t0 > 40000000000LL) {
+      if ((threadIdx.x & 31) == 0)
+        printf("gesr: attn_pair mbarrier timeout block %d warp %d smem 0x%x parity %u site %u unit %u tile %u\n",
+               blockIdx.x, threadIdx.x / 32, a, parity, ctx >> 20, (ctx >> 8) & 0xfff, ctx & 0xff);
+      __trap();
+    }
+  }
 }
+#define CTX(site, u, t) ((static_cast<uint32_t>(site) << 20) | ((static_cast<uint32_t>(u) & 0xfff) << 8) | (static_cast<uint32_t>(t) & 0xff))
 constexpr int kD = 128;
 constexpr int kKeys = 128;                       // keys per tile (S columns)
 constexpr int kThreads = 512;
@@ -92,8 +103,8 @@ constexpr uint32_t kPBytes = 128 * kKeys * 2;                        // 32 KB
 constexpr uint32_t kRingOff = kPOff + 2 * kPBytes;
 constexpr uint32_t kStgOff = kRingOff + kStages * kHalfBytes;        // 4 x 2 KB boxes per epilogue warp
 constexpr uint32_t kBarOff = kStgOff + 4 * 8192;
-constexpr uint32_t kXchOff = kBarOff + 256;                          // [unit parity][WG][m, l][row]
-constexpr uint32_t kMshOff = kXchOff + 2 * 2 * 2 * 128 * 4;          // shared running max [row]
+constexpr uint32_t kXchOff = kBarOff + 256;                          // [unit % 4][WG][m, l][row]
+constexpr uint32_t kMshOff = kXchOff + 4 * 2 * 2 * 128 * 4;          // shared running max [row]
 constexpr uint32_t kSmemBytes = kMshOff + 128 * 4 + 1024;
 static_assert(kSmemBytes <= 232448, "shared memory budget");
 // register split (setmaxnreg per warpgroup; launch registers 128 x 512 threads): control 56,
@@ -185,8 +196,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t* p_free = p_full + 2;                  // [2]        (each CTA)
   uint64_t* o_done = p_free + 2;                  // [2]        (each CTA; per O buffer)
   uint64_t* o_free = o_done + 2;                  // [2]        (leader; 8 epilogue warps of the pair)
-  uint64_t* ml_full = o_free + 2;                 //            (each CTA; its 8 softmax warps)
-  uint64_t* pv_done = ml_full + 1;                //            (each CTA; one phase per PV)
+  // per unit % 4: the softmax may publish units m+1 and m+2 (short units need no PV of their
+  // own before their last tile) while an epilogue warp still waits for unit m; four barriers
+  // (and four m / l slots) keep every waiter within one phase of its barrier
+  uint64_t* ml_full = o_free + 2;                 // [4]        (each CTA; its 8 softmax warps)
+  uint64_t* pv_done = ml_full + 4;                //            (each CTA; one phase per PV)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 1);
 
   const uint32_t warp = warp_id();
@@ -213,7 +227,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_init(&o_done[i], 1);
       mbar_init(&o_free[i], 8);
     }
-    mbar_init(ml_full, 8);
+    for (int i = 0; i < 4; ++i) mbar_init(&ml_full[i], 8);
     mbar_init(pv_done, 1);
     fence_mbar_init();
   }
@@ -298,7 +312,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         while (stream_next(st, tl)) {
           if (tl.t == 0) {
             // the unit's Q: the previous unit's S MMAs must be done with the single Q buffer
-            if (tl.m > 0) pwait(q_empty, (tl.m - 1) & 1);
+            if (tl.m > 0) pwait(q_empty, (tl.m - 1) & 1, CTX(1, tl.m, tl.t));
             GESR_T3(3, tl.m);
             const int32_t qrow = static_cast<int32_t>(static_cast<int64_t>(tl.x.h) * p.total_C + tl.x.cbeg) +
                                  static_cast<int32_t>(rank) * 128;
@@ -307,7 +321,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             tma_load_2d_pair(smem + kQOff + kQBytes / 2, &map_q, q_full, 64, qrow);
           }
           const int slot = kst;
-          pwait(&kv_empty[slot], kph ^ 1);
+          pwait(&kv_empty[slot], kph ^ 1, CTX(2, tl.m, tl.t));
           if (rank == 0) mbar_arrive_expect_tx(&kv_full[slot], 2 * kHalfBytes);
           uint8_t* dst = smem + kRingOff + slot * kHalfBytes;
           const int32_t row = krow_of(tl) + static_cast<int32_t>(rank) * 64;
@@ -323,7 +337,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         uint32_t vph = 0;
         while (stream_next(st, tl)) {
           const int slot = kKStages + vst;
-          pwait(&kv_empty[slot], vph ^ 1);
+          pwait(&kv_empty[slot], vph ^ 1, CTX(3, tl.m, tl.t));
           if (rank == 0) mbar_arrive_expect_tx(&kv_full[slot], 2 * kHalfBytes);
           uint8_t* dst = smem + kRingOff + slot * kHalfBytes;
           tma_load_2d_pair(dst, &map_vh, &kv_full[slot], static_cast<int32_t>(rank) * 64, krow_of(tl));
@@ -339,15 +353,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       while (stream_next(st, tl)) {
         const int buf = tl.t & 1;
         if (tl.t == 0) {
-          pwait(q_full, tl.m & 1);                 // the unit's Q tile (both CTAs)
+          pwait(q_full, tl.m & 1, CTX(4, tl.m, tl.t));   // the unit's Q tile (both CTAs)
           if (lane == 0) GESR_T3(0, tl.m);
         }
         // the buffer's previous S must have been loaded by its warpgroup (both CTAs)
         const uint32_t sn = buf ? sn1 : sn0;
-        if (sn > 0) pwait(&s_free[buf], (sn - 1) & 1);
+        if (sn > 0) pwait(&s_free[buf], (sn - 1) & 1, CTX(5, tl.m, tl.t));
         if (buf) ++sn1; else ++sn0;
         const int slot = kst;
-        pwait(&kv_full[slot], kph);
+        pwait(&kv_full[slot], kph, CTX(6, tl.m, tl.t));
         if (++kst == kKStages) { kst = 0; kph ^= 1; }
         if (lane == 0) GESR_T2(7, tl.m * 16 + tl.t);
         const uint32_t kb = sRing + slot * kHalfBytes;
@@ -373,16 +387,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       while (stream_next(st, tl)) {
         const int xb = tl.t & 1;
         const int vslot = kKStages + vst;
-        pwait(&kv_full[vslot], vph);
+        pwait(&kv_full[vslot], vph, CTX(7, tl.m, tl.t));
         if (++vst == kVStages) { vst = 0; vph ^= 1; }
         const int ob = tl.m & 1;                     // O buffer of this unit
         if (tl.t == 0 && tl.m >= 2) {
           // the unit's first PV overwrites its O buffer: unit m-2's epilogue must have read it
-          pwait(&o_free[ob], ((tl.m >> 1) - 1) & 1);
+          pwait(&o_free[ob], ((tl.m >> 1) - 1) & 1, CTX(8, tl.m, tl.t));
           if (lane == 0) GESR_T3(1, tl.m);
         }
         const uint32_t pn = xb ? pn1 : pn0;
-        pwait(&p_full[xb], pn & 1);
+        pwait(&p_full[xb], pn & 1, CTX(9, tl.m, tl.t));
         if (xb) ++pn1; else ++pn0;
         if (lane == 0) GESR_T2(6, tl.m * 16 + tl.t);
         tc_fence_after();
@@ -446,7 +460,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       float m_loc = -INFINITY;
       float l = 0.f;
       for (int j = g; j < nkv; j += 2) {
-        pwait(&s_full[g], sc & 1);
+        pwait(&s_full[g], sc & 1, CTX(10, m, j));
         ++sc;
         const bool tr = (sub == 0 && lane == 0);
         const bool trd = tr;
@@ -501,7 +515,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
         }
         // P_g must have been read by PV(j-2) (long done, normally) before the exp pass writes it
-        if (sc > 1) pwait(&p_free[g], (sc - 2) & 1);
+        if (sc > 1) pwait(&p_free[g], (sc - 2) & 1, CTX(11, m, j));
         if (j > 0 || prev_last_b) named_bar_sync(tok_mine, 64);   // tile j-1's exp pass is done
         if (trd) GESR_T2(4, m * 16 + j);
         float d = 0.f;                                   // shift of x still to apply
@@ -572,7 +586,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if (!__any_sync(0xffffffffu, need)) break;
           // raise m_sh: O must hold PV(j-1) (the other warpgroup's last tile) before it is
           // rescaled; no later PV can land before this warpgroup's p_full(j)
-          pwait(pv_done, (gbase + j - 1) & 1);
+          pwait(pv_done, (gbase + j - 1) & 1, CTX(12, m, j));
           tc_fence_after();
           d = need ? dx : 0.f;
           const float alpha = ex2(-d);
@@ -603,11 +617,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
       prev_last_b = ((nkv - 1) & 1) == 1;
       // publish this warpgroup's max / sum of my rows for the epilogue warps
-      const uint32_t xb = xch + ((m & 1) * 2 * 2 * 128) * 4;      // [WG][m, l][row]
+      const uint32_t xb = xch + ((m & 3) * 2 * 2 * 128) * 4;      // [WG][m, l][row]
       st_shared_f32(xb + ((g * 2 + 0) * 128 + rloc) * 4, m_loc);
       st_shared_f32(xb + ((g * 2 + 1) * 128 + rloc) * 4, l);
       __syncwarp();
-      if (lane == 0) mbar_arrive(ml_full);
+      if (lane == 0) mbar_arrive(&ml_full[m & 3]);
       gbase += nkv;
       ++m;
     }
@@ -654,9 +668,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         continue;
       }
-      pwait(ml_full, m & 1);
+      pwait(&ml_full[m & 3], (m >> 2) & 1, CTX(13, m, 0));
       if (sub == 0 && lane == 0) GESR_T3(5, m);
-      const uint32_t xb = xch + ((m & 1) * 2 * 2 * 128) * 4;
+      const uint32_t xb = xch + ((m & 3) * 2 * 2 * 128) * 4;
       const float mA = ld_shared_f32(xb + (0 * 128 + rloc) * 4);
       const float lA = ld_shared_f32(xb + (1 * 128 + rloc) * 4);
       const bool hasB = nkv > 1;
@@ -669,7 +683,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       if (lane == 0) bulk_wait_group_read<0>();
       __syncwarp();
       const int ob = m & 1;
-      pwait(&o_done[ob], (m >> 1) & 1);
+      pwait(&o_done[ob], (m >> 1) & 1, CTX(14, m, 0));
       if (sub == 0 && lane == 0) GESR_T3(6, m);
       tc_fence_after();
       const uint32_t tO = tO0 + ob * kD;

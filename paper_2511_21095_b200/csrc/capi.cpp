@@ -100,13 +100,13 @@ gesr_status make_out_map(CUtensorMap* map, void* base, uint64_t H, uint64_t M, u
   return GESR_OK;
 }
 
-// The CTA-pair attention kernel (attn2.cu) is opt-in with GESR_ATTN_PAIR=1 for d = 128: it is
-// correct but currently slower than the 1-CTA kernel at the headline (DESIGN.md tuning log).
+// d = 128 runs the CTA-pair attention kernel (attn2.cu); GESR_ATTN_PAIR=0 selects the 1-CTA
+// kernel instead (equal at the headline, slower on jagged / chunked workloads: DESIGN.md s10).
 bool pair_attention_enabled() {
   static int cached = -1;
   if (cached < 0) {
     const char* v = getenv("GESR_ATTN_PAIR");
-    cached = (v != nullptr && v[0] == '1') ? 1 : 0;
+    cached = (v != nullptr && v[0] == '0') ? 0 : 1;
   }
   return cached == 1;
 }

@@ -70,7 +70,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const long long t0 = clock64();
   while (!mbar_try_wait(a, parity)) {
     if (clock64() - t0 > 40000000000LL) {
-      printf("gesr: mbarrier timeout block %d thread %d\n", blockIdx.x, threadIdx.x);
+      if ((threadIdx.x & 31) == 0)
+        printf("gesr: mbarrier timeout block %d thread %d smem 0x%x parity %u\n", blockIdx.x,
+               threadIdx.x, a, parity);
       __trap();
     }
   }
@@ -97,7 +99,9 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
   const long long t0 = clock64();
   while (!mbar_try_wait_hint(a, parity, 1000000u)) {
     if (clock64() - t0 > 40000000000LL) {
-      printf("gesr: mbarrier timeout block %d thread %d\n", blockIdx.x, threadIdx.x);
+      if ((threadIdx.x & 31) == 0)
+        printf("gesr: mbarrier timeout block %d thread %d smem 0x%x parity %u\n", blockIdx.x,
+               threadIdx.x, a, parity);
       __trap();
     }
   }

@@ -301,6 +301,25 @@ def test_growing_scores_raise_running_max(d):
     assert np.abs(lse.cpu().numpy() - lse_or).max() < 5e-2
 
 
+def test_one_cta_kernel_d128_subprocess():
+    # d = 128 runs the CTA-pair kernel by default; the 1-CTA kernel (GESR_ATTN_PAIR=0, read once
+    # per process) keeps its own parity check on ragged shapes and bf16 output
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import importlib.util, sys; sys.path.insert(0, '.'); "
+        "spec = importlib.util.spec_from_file_location('tgp', 'tests/test_gpu_parity.py'); "
+        "t = importlib.util.module_from_spec(spec); spec.loader.exec_module(t); "
+        "t.test_tasa_ragged_edges(128, 2, 256); t.test_tasa_bf16_output(); "
+        "t.test_growing_scores_raise_running_max(128); print('one-cta ok')")
+    env = dict(os.environ, GESR_ATTN_PAIR="0")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0 and "one-cta ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+
+
 # ----------------------------------------------------------------------------- HMA
 
 def _hma_gpu(bt, F, cap=0):
