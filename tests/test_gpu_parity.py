@@ -399,3 +399,26 @@ def test_headline_full_size_sampled():
     want = oracle.hma_count(sub.user_ids, sub.user_offsets, sub.item_ids, sub.item_offsets,
                             sub.cand_offsets, cfg.F)
     assert np.array_equal(counts[torch.as_tensor(rows, device=dev)].cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("name", ["3", "4", "5"])
+def test_config_full_size_sampled(name):
+    """BASELINE configs 3 (jagged L <= 2048), 4 (L=4096 cache reused over 8 candidate chunks of
+    512) and 5 (8192 requests, L log-uniform 32-4096, C 100-2000) run in full through
+    score_step; sampled requests checked against the oracle (attention tolerance, HMA exact)."""
+    dev = _cuda()
+    cfg = configs.get(name)
+    bt = inputs.make_batch(cfg, device=dev)
+    bufs = gb.StepBuffers(bt, want_lse=True)
+    O, counts = gb.score_step(bt, bufs, chunk=cfg.chunk)
+    torch.cuda.synchronize()
+    sample = sorted({0, cfg.B // 3, cfg.B // 2, cfg.B - 1})
+    sub = inputs.make_batch(cfg, requests=sample)
+    _, _, O_or, _ = _run_oracle_attn(sub)
+    co = bt.cand_offsets.cpu().numpy()
+    rows = np.concatenate([np.arange(co[b], co[b + 1]) for b in sample])
+    _attn_tol(O[torch.as_tensor(rows, device=dev)].cpu().numpy(), O_or, f"config {name} sampled")
+    want = oracle.hma_count(sub.user_ids, sub.user_offsets, sub.item_ids, sub.item_offsets,
+                            sub.cand_offsets, cfg.F)
+    assert np.array_equal(counts[torch.as_tensor(rows, device=dev)].cpu().numpy(), want)
+
