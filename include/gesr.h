@@ -99,10 +99,16 @@ size_t gesr_tasa_workspace_bytes(int64_t B, int64_t total_C, int32_t H, int32_t 
  *              one cache, e.g. candidate chunks of the same users).
  *   seq_offsets int64 [B+1] (device) into the cache rows.
  *   scale      score scale; <= 0 selects 1/sqrt(d) (reading R4).
- *   kv_splits  0 = auto, >= 1 forced.  This version computes every row in a single pass over
- *              its history (splits = 1); values > 1 return GESR_ERR_UNSUPPORTED.  Each output
- *              row depends only on its own candidate and its user's K/V: results are
- *              bit-identical across chunking, batch composition and GPU count (reading R9).
+ *   kv_splits  split-L: each (256-candidate unit, head) is cut into kv_splits ranges of key
+ *              tiles computed independently and merged (weights l_s 2^(m_s - max m), summed in
+ *              split order) -- occupancy for few-request calls such as one user's candidate
+ *              chunks (BASELINE config 4).  0 = auto (splits only when there are fewer than 74
+ *              (unit, head) items; the choice depends on B, total_C, total_L, H, so results
+ *              are NOT batch-invariant), 1 = unsplit, 2..64 forced.  Splits need d = 128 (the
+ *              CTA-pair kernel): d < 128 with kv_splits > 1 returns GESR_ERR_UNSUPPORTED, auto
+ *              runs unsplit.  For a fixed kv_splits >= 1 each output row depends only on its
+ *              own candidate and its user's K/V: results are bit-identical across chunking,
+ *              batch composition and GPU count (reading R9).  kv_splits > 64 is invalid.
  *   flags      0, or GESR_TASA_SELF_KEY (unsupported in this version).
  *   O          [total_C, H*d] fp32 or bf16 (o_dtype): O[t][h*d+j] = sum_i p_i V[h][r_i][j] with
  *              p = softmax_i(scale * q_h . K[h][r_i]) over the request's L_b history rows.

@@ -204,8 +204,11 @@ def score_step(batch, bufs: StepBuffers, act: int = GESR_ACT_SILU, cap: int = 0,
         # config 4: the same user's cache reused across candidate chunks (one call per chunk)
         for c0 in range(0, batch.total_C, chunk):
             c1 = min(batch.total_C, c0 + chunk)
-            co = bufs.__dict__.setdefault(
-                f"_co_{c0}", torch.tensor([0, c1 - c0], dtype=torch.int64, device=batch.T.device))
+            key = f"_co_{c0}"            # chunk offsets built once (no copies in graph capture)
+            if key not in bufs.__dict__:
+                bufs.__dict__[key] = torch.tensor([0, c1 - c0], dtype=torch.int64,
+                                                  device=batch.T.device)
+            co = bufs.__dict__[key]
             tasa_score(batch.T[c0:c1], co, batch.W_q, bufs.K, bufs.V, batch.seq_offsets, cfg.H,
                        cfg.d, act, O=bufs.O[c0:c1],
                        lse=None if bufs.lse is None else bufs.lse[c0:c1],

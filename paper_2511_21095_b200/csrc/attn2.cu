@@ -167,7 +167,8 @@ __device__ __forceinline__ uint64_t vdesc(uint32_t base, int ks) {
 }
 
 struct Work {
-  int h, L, rows_valid, nkv;
+  int h, L, rows_valid, nkv;      // nkv: key tiles of this work item (its split's range)
+  int t0, split;                  // first key tile of the range, split index
   int64_t s0, cbeg;
 };
 
@@ -177,7 +178,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                      const __grid_constant__ CUtensorMap map_vh,
                      const __grid_constant__ CUtensorMap map_o, const AttnParams p) {
   const int U = __ldg(p.unit_count);
-  const int W = U * p.H;
+  const int S = p.splits;
+  const int W = U * p.H * S;
   const int pair = static_cast<int>(blockIdx.x >> 1);
   const int npairs = static_cast<int>(gridDim.x >> 1);
   if (pair >= W) return;                          // uniform for the pair
@@ -245,14 +247,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
   // the unit descriptor of work item w is one 16-byte load, fetched one item ahead
   auto fetch = [&](int w) { return __ldg(p.units + (w % U)); };
+  // w -> (unit w % U, split (w / U) % S, head w / (U S)): neighbouring pairs share a head
   auto decode = [&](int w, int4 d) {
     Work x;
-    x.h = w / U;
+    const int rest = w / U;
+    x.split = rest % S;
+    x.h = rest / S;
     x.s0 = d.x;
     x.L = d.y;
     x.cbeg = d.z;
     x.rows_valid = d.w;
-    x.nkv = (x.L + kKeys - 1) / kKeys;
+    const int n = (x.L + kKeys - 1) / kKeys;
+    x.t0 = static_cast<int>(static_cast<int64_t>(x.split) * n / S);
+    x.nkv = static_cast<int>(static_cast<int64_t>(x.split + 1) * n / S) - x.t0;
     return x;
   };
 
@@ -299,7 +306,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     // leader, warp 1 issues the S MMAs and warp 3 the PV MMAs.  S(g) needs its K half, its
     // unit's Q and the s_free of its buffer's previous S; PV(g) its V half and p_full(g).
     auto krow_of = [&](const Tile& tl) {
-      return static_cast<int32_t>(static_cast<int64_t>(tl.x.h) * p.total_L + tl.x.s0) + kKeys * tl.t;
+      return static_cast<int32_t>(static_cast<int64_t>(tl.x.h) * p.total_L + tl.x.s0) +
+             kKeys * (tl.x.t0 + tl.t);
     };
     TileStream st;
     stream_init(st);
@@ -471,7 +479,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         for (int c = 0; c < 4; ++c) tmem_ld32(tS + c * 32, r + c * 32);
         tmem_ld_wait();
         if (trd) GESR_T2(1, m * 16 + j);
-        const int valid = L - kKeys * j;
+        const int valid = L - kKeys * (x.t0 + j);
         const bool full = valid >= kKeys;
         if (!full) {
 #pragma unroll
@@ -652,9 +660,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const int nkv = x.nkv, h = x.h;
       const bool row_ok = row_in_unit < x.rows_valid;
       const int64_t row = x.cbeg + row_in_unit;
+      const bool split_out = S > 1;                     // write split-L partials, not O
       if (nkv == 0) {
-        // L_b = 0: no keys, O = 0 and lse = -inf
-        if (row_ok) {
+        // L_b = 0 (or an empty split range): no keys, O = 0 and lse = -inf
+        if (row_ok && split_out) {
+          p.part_ml[(static_cast<int64_t>(x.split) * p.total_C + row) * p.H + h] =
+              make_float2(-INFINITY, 0.f);
+        } else if (row_ok) {
           if (p.o_bf16) {
             uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.O) + row * HD + h * kD);
 #pragma unroll
@@ -707,7 +719,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           o[e] = __float_as_uint(y0);
           o[e + 1] = __float_as_uint(y1);
         }
-        if (p.o_bf16) {
+        if (split_out) {
+          if (row_ok) {
+            float* dst = p.part_o + ((static_cast<int64_t>(x.split) * p.total_C + row) * p.H + h) * kD + c * 32;
+#pragma unroll
+            for (int vv = 0; vv < 4; ++vv) st_global_v8(dst + 8 * vv, o + 8 * vv);
+          }
+        } else if (p.o_bf16) {
           // box c (32 rows x 32 columns): 16-byte chunk qq of row `lane` (64B swizzle)
           const uint32_t rowp = stg_s + c * 2048 + lane * 64;
 #pragma unroll
@@ -726,7 +744,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           for (int vv = 0; vv < 4; ++vv) st_global_v8(dst + 8 * vv, o + 8 * vv);
         }
       }
-      if (p.o_bf16) {
+      if (split_out) {
+        if (row_ok)
+          p.part_ml[(static_cast<int64_t>(x.split) * p.total_C + row) * p.H + h] = make_float2(mm, lsum);
+      } else if (p.o_bf16) {
         const int row0 = static_cast<int>(rank) * 128 + static_cast<int>(sub) * 32;
         if (p.o_tma && row0 + 32 <= x.rows_valid) {
           fence_proxy_async_smem();
@@ -752,7 +773,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           __syncwarp();
         }
       }
-      if (row_ok && p.lse != nullptr)
+      if (!split_out && row_ok && p.lse != nullptr)
         p.lse[row * p.H + h] = (mm + __log2f(lsum)) * 0.69314718055994530942f;
       ++m;
     }
@@ -767,7 +788,49 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   }
 }
 
+// Split-L merge (one CTA of d threads per (candidate, head)): the s-th partial holds
+// O_s / l_s and (m_s, l_s) with m in log2 units of the scaled score; O = sum_s w_s (O_s / l_s) /
+// sum_s w_s with w_s = l_s 2^(m_s - max_s m_s), summed in split order (deterministic).
+__global__ void __launch_bounds__(128) attn_combine_kernel(const AttnParams p, int d) {
+  const int64_t rh = blockIdx.x;                   // row * H + h
+  const int64_t row = rh / p.H;
+  const int h = static_cast<int>(rh % p.H);
+  const int j = threadIdx.x;
+  const int S = p.splits;
+  const int64_t stride = p.total_C * p.H;
+  float mmax = -INFINITY;
+  for (int s = 0; s < S; ++s) {
+    const float2 ml = p.part_ml[s * stride + rh];
+    if (ml.y > 0.f) mmax = fmaxf(mmax, ml.x);
+  }
+  float wsum = 0.f, acc = 0.f;
+  for (int s = 0; s < S; ++s) {
+    const float2 ml = p.part_ml[s * stride + rh];
+    if (ml.y > 0.f) {
+      const float w = ml.y * exp2f(ml.x - mmax);
+      wsum += w;
+      if (j < d) acc += w * p.part_o[(s * stride + rh) * d + j];
+    }
+  }
+  const float v = wsum > 0.f ? acc / wsum : 0.f;
+  if (j < d) {
+    if (p.o_bf16)
+      static_cast<__nv_bfloat16*>(p.O)[row * p.H * d + h * d + j] = __float2bfloat16_rn(v);
+    else
+      static_cast<float*>(p.O)[row * p.H * d + h * d + j] = v;
+  }
+  if (j == 0 && p.lse != nullptr)
+    p.lse[rh] = wsum > 0.f ? (mmax + log2f(wsum)) * 0.69314718055994530942f : -INFINITY;
+}
+
 }  // namespace
+
+cudaError_t launch_attn_combine(const AttnParams& p, int d, cudaStream_t stream) {
+  const int64_t n = p.total_C * p.H;
+  if (n == 0) return cudaSuccess;
+  attn_combine_kernel<<<static_cast<unsigned>(n), 128, 0, stream>>>(p, d);
+  return cudaGetLastError();
+}
 
 #ifdef GESR_TRACE
 extern "C" int gesr_debug_trace2_copy(void* host) {
@@ -811,7 +874,7 @@ cudaError_t launch_attn_pair(const CUtensorMap& mq, const CUtensorMap& mkh, cons
     }
     max_pairs = clusters;
   }
-  const int64_t work = max_units * p.H;
+  const int64_t work = max_units * p.H * p.splits;
   const unsigned pairs = static_cast<unsigned>(work < max_pairs ? work : max_pairs);
   attn_pair_kernel<<<2 * pairs, kThreads, kSmemBytes, stream>>>(mq, mkh, mvh, mo, p);
   return cudaGetLastError();

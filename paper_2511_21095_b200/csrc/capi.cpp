@@ -224,11 +224,50 @@ gesr_status gesr_kv_project(const void* U, int64_t total_L, int32_t D_in, const 
                         static_cast<cudaStream_t>(stream));
 }
 
+// Split-L (d = 128, pair kernel): a forced kv_splits = s > 1 cuts every (unit, head) into s
+// ranges of key tiles; auto (0) splits only when there are fewer (unit, head) work items than
+// CTA pairs (kAutoSplitItems), into enough ranges to cover them, by up to kMaxAutoSplits and
+// keeping >= 2 key tiles per split on average.
+constexpr int64_t kAutoSplitItems = 74;
+constexpr int kMaxAutoSplits = 16;
+constexpr int kMaxSplits = 64;
+
+int pick_splits(int64_t B, int64_t total_C, int64_t total_L, int32_t H, int32_t d,
+                int32_t kv_splits) {
+  if (d != 128 || !pair_attention_enabled()) return 1;
+  if (kv_splits >= 1) return kv_splits;
+  const int64_t items = max_units(B, total_C) * H;
+  if (items >= kAutoSplitItems || B == 0) return 1;
+  const int64_t tiles = (total_L / B + 127) / 128;             // mean key tiles per request
+  int64_t s = (kAutoSplitItems + items - 1) / items;
+  if (s > tiles / 2) s = tiles / 2;
+  if (s > kMaxAutoSplits) s = kMaxAutoSplits;
+  return s < 1 ? 1 : static_cast<int>(s);
+}
+
+// [splits, total_C, H] float2 (m, l), then (256-aligned) [splits, total_C, H, d] fp32
+size_t split_ml_bytes(int64_t total_C, int32_t H, int splits) {
+  return (static_cast<size_t>(splits) * total_C * H * 8 + 255) & ~static_cast<size_t>(255);
+}
+size_t split_bytes(int64_t total_C, int32_t H, int32_t d, int splits) {
+  if (splits <= 1) return 0;
+  return split_ml_bytes(total_C, H, splits) + static_cast<size_t>(splits) * total_C * H * d * 4;
+}
+
 size_t gesr_tasa_workspace_bytes(int64_t B, int64_t total_C, int32_t H, int32_t d,
                                  int32_t kv_splits) {
-  (void)kv_splits;
-  if (B < 0 || total_C < 0 || H < 1 || !valid_d(d)) return 0;
-  return units_end(B, total_C) + static_cast<size_t>(total_C) * H * d * 2;
+  if (B < 0 || total_C < 0 || H < 1 || !valid_d(d) || kv_splits < 0 || kv_splits > kMaxSplits)
+    return 0;
+  size_t part = 0;
+  if (d == 128) {
+    if (kv_splits > 1) {
+      part = split_bytes(total_C, H, d, kv_splits);
+    } else if (kv_splits == 0 && max_units(B, total_C) * H < kAutoSplitItems) {
+      part = split_bytes(total_C, H, d, kMaxAutoSplits);      // bound for any auto choice
+    }
+  }
+  const size_t q_end = units_end(B, total_C) + static_cast<size_t>(total_C) * H * d * 2;
+  return ((q_end + 255) & ~static_cast<size_t>(255)) + part;
 }
 
 gesr_status gesr_tasa_score(const void* T, int64_t total_C, int32_t D_in,
@@ -247,8 +286,10 @@ gesr_status gesr_tasa_score(const void* T, int64_t total_C, int32_t D_in,
     return fail(GESR_ERR_INVALID_ARG, "H*total rows exceed the 2^31 TMA coordinate range");
   if (o_dtype != GESR_OUT_F32 && o_dtype != GESR_OUT_BF16)
     return fail(GESR_ERR_INVALID_ARG, "o_dtype=%d is not a gesr_out_dtype", o_dtype);
-  if (kv_splits < 0) return fail(GESR_ERR_INVALID_ARG, "kv_splits=%d < 0", kv_splits);
-  if (kv_splits > 1) return fail(GESR_ERR_UNSUPPORTED, "kv_splits > 1 not supported in this version");
+  if (kv_splits < 0 || kv_splits > kMaxSplits)
+    return fail(GESR_ERR_INVALID_ARG, "kv_splits=%d outside [0, %d]", kv_splits, kMaxSplits);
+  if (kv_splits > 1 && (d != 128 || !pair_attention_enabled()))
+    return fail(GESR_ERR_UNSUPPORTED, "kv_splits > 1 needs d = 128 (CTA-pair attention kernel)");
   if (flags & GESR_TASA_SELF_KEY)
     return fail(GESR_ERR_UNSUPPORTED, "GESR_TASA_SELF_KEY not supported in this version");
   if (flags & ~GESR_TASA_SELF_KEY) return fail(GESR_ERR_INVALID_ARG, "unknown flags 0x%x", flags);
@@ -279,6 +320,7 @@ gesr_status gesr_tasa_score(const void* T, int64_t total_C, int32_t D_in,
   p.O = O;
   p.o_bf16 = o_dtype == GESR_OUT_BF16;
   p.lse = lse;
+  p.splits = 1;
   if (total_L == 0) {
     cudaError_t e = gesr::launch_attn_empty(p, d, st);
     return e == cudaSuccess ? GESR_OK : cuda_fail(e, "attn_empty launch");
@@ -290,6 +332,13 @@ gesr_status gesr_tasa_score(const void* T, int64_t total_C, int32_t D_in,
   void* Q = ws + units_end(B, total_C);
   p.units = units;
   p.unit_count = count;
+  p.splits = pick_splits(B, total_C, total_L, H, d, kv_splits);
+  if (p.splits > 1) {
+    const size_t q_end = units_end(B, total_C) + static_cast<size_t>(total_C) * H * d * 2;
+    uint8_t* part = ws + ((q_end + 255) & ~static_cast<size_t>(255));
+    p.part_ml = reinterpret_cast<float2*>(part);
+    p.part_o = reinterpret_cast<float*>(part + split_ml_bytes(total_C, H, p.splits));
+  }
 
   cudaError_t e = gesr::launch_build_units(seq_offsets, cand_offsets, B, units, count, st);
   if (e != cudaSuccess) return cuda_fail(e, "build_units launch");
@@ -318,6 +367,10 @@ gesr_status gesr_tasa_score(const void* T, int64_t total_C, int32_t D_in,
     if (s != GESR_OK) return s;
     e = gesr::launch_attn_pair(mq, mkh, mv, mo, p, max_units(B, total_C), st);
     if (e != cudaSuccess) return cuda_fail(e, "attn_pair_kernel launch");
+    if (p.splits > 1) {
+      e = gesr::launch_attn_combine(p, d, st);
+      if (e != cudaSuccess) return cuda_fail(e, "attn_combine_kernel launch");
+    }
     return GESR_OK;
   }
   e = gesr::launch_attn(d, mq, mk, mv, mo, p, max_units(B, total_C), st);

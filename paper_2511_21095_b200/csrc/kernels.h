@@ -42,8 +42,14 @@ struct AttnParams {
   float scale_log2;        // scale * log2(e)
   void* O;                 // [total_C, H*d]
   int o_bf16;
-  int o_tma;               // bf16 O through the map_o TMA tensor stores (1-CTA kernel)
+  int o_tma;               // bf16 O through the map_o TMA tensor stores
   float* lse;              // [total_C, H] or null
+  // split-L (pair kernel): each (unit, head) is cut into `splits` ranges of key tiles; with
+  // splits > 1 the kernel writes per-split partials (O_s / l_s fp32 and (m_s, l_s), m in log2
+  // units) that launch_attn_combine merges into O / lse
+  int splits;
+  float* part_o;           // [splits, total_C, H, d]
+  float2* part_ml;         // [splits, total_C, H]
 };
 
 constexpr int kUnitRows = 256;   // candidates per work unit (two 128-row Q tiles)
@@ -60,6 +66,8 @@ cudaError_t launch_attn(int d, const CUtensorMap& map_q, const CUtensorMap& map_
 cudaError_t launch_attn_pair(const CUtensorMap& map_q, const CUtensorMap& map_kh,
                              const CUtensorMap& map_vh, const CUtensorMap& map_o,
                              const AttnParams& p, int64_t max_units, cudaStream_t stream);
+// merges split-L partials: O = sum_s w_s O_s / sum_s w_s, w_s = l_s 2^(m_s - max m)
+cudaError_t launch_attn_combine(const AttnParams& p, int d, cudaStream_t stream);
 cudaError_t launch_attn_empty(const AttnParams& p, int d, cudaStream_t stream);
 
 // ---------------------------------------------------------------- K-HMA (hma.cu)

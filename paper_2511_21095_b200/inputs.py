@@ -18,6 +18,7 @@ Recipe:
 """
 from __future__ import annotations
 
+import functools
 import math
 from dataclasses import dataclass
 from typing import Optional, Sequence
@@ -181,11 +182,12 @@ class Batch:
     def B(self) -> int:
         return int(self.requests.numel())
 
-    @property
+    # cached on first use (a device read): later uses, e.g. inside CUDA-graph capture, do not sync
+    @functools.cached_property
     def total_L(self) -> int:
         return int(self.seq_offsets[-1].item())
 
-    @property
+    @functools.cached_property
     def total_C(self) -> int:
         return int(self.cand_offsets[-1].item())
 

@@ -84,8 +84,9 @@ def test_tasa_validation(L):
     assert tasa(L, B=-1) == gb.GESR_ERR_INVALID_ARG
     assert tasa(L, flags=gb.GESR_TASA_SELF_KEY) == gb.GESR_ERR_UNSUPPORTED
     assert tasa(L, flags=0x8) == gb.GESR_ERR_INVALID_ARG
-    assert tasa(L, splits=4) == gb.GESR_ERR_UNSUPPORTED
+    assert tasa(L, splits=4) == gb.GESR_ERR_UNSUPPORTED       # split-L needs d = 128
     assert tasa(L, splits=-1) == gb.GESR_ERR_INVALID_ARG
+    assert tasa(L, splits=65, d=128) == gb.GESR_ERR_INVALID_ARG
     assert tasa(L, T=None) == gb.GESR_ERR_INVALID_ARG
     assert tasa(L, O=MIS) == gb.GESR_ERR_INVALID_ARG
     assert tasa(L, ws=P(0x10010)) == gb.GESR_ERR_INVALID_ARG   # workspace must be 256-aligned
@@ -100,6 +101,11 @@ def test_workspace_size(L):
     assert n >= 1024000 * 4 * 128 * 2 and n < 1024000 * 4 * 128 * 2 + (1 << 20)
     assert gb.tasa_workspace_bytes(-1, 10, 4, 128) == 0
     assert gb.tasa_workspace_bytes(1, 10, 4, 100) == 0
+    # split-L partials: [s, C, H] (m, l) + [s, C, H, d] fp32 on top of the unsplit workspace
+    base = gb.tasa_workspace_bytes(1, 512, 4, 128, 1)
+    assert gb.tasa_workspace_bytes(1, 512, 4, 128, 8) >= base + 8 * 512 * 4 * 130 * 4
+    assert gb.tasa_workspace_bytes(1, 512, 4, 128, 0) >= base + 16 * 512 * 4 * 130 * 4  # auto bound
+    assert gb.tasa_workspace_bytes(1, 512, 4, 128, 65) == 0
 
 
 def hma(L, ui=FAKE, uo=FAKE, ii=FAKE, io=FAKE, co=FAKE, B=2, C=5, F=3, cap=0, counts=FAKE):

@@ -301,6 +301,67 @@ def test_growing_scores_raise_running_max(d):
     assert np.abs(lse.cpu().numpy() - lse_or).max() < 5e-2
 
 
+@pytest.mark.parametrize("splits", [2, 3, 8])
+def test_split_l_parity(splits):
+    # forced split-L (d = 128): ranges of key tiles computed apart and merged; L < 128 * splits
+    # leaves empty splits, L = 0 gives O = 0 / lse = -inf
+    Ls = [0, 1, 127, 129, 300, 700, 1030, 5]
+    Cs = [3, 40, 128, 129, 256, 257, 130, 2]
+    bt = _custom(Ls, Cs, H=2, d=128, D_in=256, cfg_id=400 + splits)
+    K, V, O_or, lse_or = _run_oracle_attn(bt)
+    g = bt.to(_cuda())
+    Kg, Vg = gb.kv_project(g.U, g.W_k, g.W_v, 2, 128, 1)
+    O, lse = gb.tasa_score(g.T, g.cand_offsets, g.W_q, Kg, Vg, g.seq_offsets, 2, 128, 1,
+                           kv_splits=splits)
+    torch.cuda.synchronize()
+    _attn_tol(O.cpu().numpy(), O_or, f"split-L {splits}")
+    lse = lse.cpu().numpy()
+    fin = np.isfinite(lse_or)
+    assert np.array_equal(fin, np.isfinite(lse))
+    assert np.abs(lse[fin] - lse_or[fin]).max() < 2e-2
+    assert np.all(O.cpu().numpy()[:3] == 0)
+
+
+def test_split_l_batch_invariance_exact():
+    # a fixed kv_splits is batch-invariant: config 4 style chunks of one cache == one call
+    cfg = configs.get("4").with_(L=("fixed", 1500), C=("fixed", 700))
+    bt = inputs.make_batch(cfg, hma=False)
+    g = bt.to(_cuda())
+    K, V = gb.kv_project(g.U, g.W_k, g.W_v, cfg.H, cfg.d, 1)
+    O1, l1 = gb.tasa_score(g.T, g.cand_offsets, g.W_q, K, V, g.seq_offsets, cfg.H, cfg.d,
+                           kv_splits=6)
+    parts = []
+    for c0 in range(0, 700, 256):
+        c1 = min(700, c0 + 256)
+        co = torch.tensor([0, c1 - c0], dtype=torch.int64, device="cuda")
+        parts.append(gb.tasa_score(g.T[c0:c1].contiguous(), co, g.W_q, K, V, g.seq_offsets,
+                                   cfg.H, cfg.d, kv_splits=6)[0])
+    torch.cuda.synchronize()
+    assert torch.equal(O1, torch.cat(parts))
+
+
+@pytest.mark.parametrize("name", ["1", "4"])
+def test_cuda_graph_capture_identical(name):
+    # the C-ABI calls are capturable (no host sync, no allocation): a captured step replays to
+    # the eager step's exact outputs (configs 1 and 4 are measured under graphs)
+    cfg = configs.get(name)
+    bt = inputs.make_batch(cfg, device=_cuda())
+    bufs = gb.StepBuffers(bt, out_dtype=torch.bfloat16)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        gb.score_step(bt, bufs, chunk=cfg.chunk, stream=s)
+        torch.cuda.synchronize()
+        O_ref, c_ref = bufs.O.clone(), bufs.counts.clone()
+        bufs.O.zero_()
+        bufs.counts.zero_()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            gb.score_step(bt, bufs, chunk=cfg.chunk, stream=s)
+        g.replay()
+        torch.cuda.synchronize()
+    assert torch.equal(bufs.O, O_ref) and torch.equal(bufs.counts, c_ref)
+
+
 def test_one_cta_kernel_d128_subprocess():
     # d = 128 runs the CTA-pair kernel by default; the 1-CTA kernel (GESR_ATTN_PAIR=0, read once
     # per process) keeps its own parity check on ragged shapes and bf16 output
