@@ -74,16 +74,22 @@ namespace {
 #ifndef GESR_PAIR_SPIN
 #define GESR_PAIR_SPIN 0
 #endif
-// ctx (call site * 2^20 + unit * 2^8 + tile) is only reported if the wait times out
+// A wait that exceeds ~20 s traps.  Builds with -DGESR_DEBUG_WAITS also print the call site
+// (ctx = site * 2^20 + unit * 2^8 + tile) first; the default build has no call in the wait
+// loops (a call site there makes ptxas keep the softmax's registers in local memory).
 __device__ __forceinline__ void pwait(uint64_t* bar, uint32_t parity, uint32_t ctx = 0) {
   const uint32_t a = smem_u32(bar);
   if (mbar_try_wait_hint(a, parity, GESR_PAIR_SPIN ? 0u : 1000000u)) return;
   const long long t0 = clock64();
   while (!mbar_try_wait_hint(a, parity, GESR_PAIR_SPIN ? 0u : 1000000u)) {
     if (clock64() - t0 > 40000000000LL) {
+#ifdef GESR_DEBUG_WAITS
       if ((threadIdx.x & 31) == 0)
         printf("gesr: attn_pair mbarrier timeout block %d warp %d smem 0x%x parity %u site %u unit %u tile %u\n",
                blockIdx.x, threadIdx.x / 32, a, parity, ctx >> 20, (ctx >> 8) & 0xfff, ctx & 0xff);
+#else
+      (void)ctx;
+#endif
       __trap();
     }
   }
@@ -103,7 +109,7 @@ constexpr uint32_t kPBytes = 128 * kKeys * 2;                        // 32 KB
 constexpr uint32_t kRingOff = kPOff + 2 * kPBytes;
 constexpr uint32_t kStgOff = kRingOff + kStages * kHalfBytes;        // 4 x 2 KB boxes per epilogue warp
 constexpr uint32_t kBarOff = kStgOff + 4 * 8192;
-constexpr uint32_t kXchOff = kBarOff + 256;                          // [unit % 4][WG][m, l][row]
+constexpr uint32_t kXchOff = kBarOff + 512;                          // [unit % 4][WG][m, l][row]
 constexpr uint32_t kMshOff = kXchOff + 4 * 2 * 2 * 128 * 4;          // shared running max [row]
 constexpr uint32_t kSmemBytes = kMshOff + 128 * 4 + 1024;
 static_assert(kSmemBytes <= 232448, "shared memory budget");
@@ -202,8 +208,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   // own before their last tile) while an epilogue warp still waits for unit m; four barriers
   // (and four m / l slots) keep every waiter within one phase of its barrier
   uint64_t* ml_full = o_free + 2;                 // [4]        (each CTA; its 8 softmax warps)
-  uint64_t* pv_done = ml_full + 4;                //            (each CTA; one phase per PV)
+  // slot u % 4 reused by unit u + 4 only after the epilogue read it (a warpgroup with no tile
+  // in a run of 1-tile units would otherwise publish 4+ units ahead)
+  uint64_t* ml_empty = ml_full + 4;               // [4]        (each CTA; its 4 epilogue warps)
+  uint64_t* pv_done = ml_empty + 4;               //            (each CTA; one phase per PV)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 1);
+  static_assert((2 + 2 * kStages + 2 * 6 + 8 + 1) * 8 + 4 <= kXchOff - kBarOff, "barrier area");
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -229,7 +239,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_init(&o_done[i], 1);
       mbar_init(&o_free[i], 8);
     }
-    for (int i = 0; i < 4; ++i) mbar_init(&ml_full[i], 8);
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(&ml_full[i], 8);
+      mbar_init(&ml_empty[i], 4);
+    }
     mbar_init(pv_done, 1);
     fence_mbar_init();
   }
@@ -251,15 +264,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   auto decode = [&](int w, int4 d) {
     Work x;
     const int rest = w / U;
-    x.split = rest % S;
-    x.h = rest / S;
     x.s0 = d.x;
     x.L = d.y;
     x.cbeg = d.z;
     x.rows_valid = d.w;
     const int n = (x.L + kKeys - 1) / kKeys;
-    x.t0 = static_cast<int>(static_cast<int64_t>(x.split) * n / S);
-    x.nkv = static_cast<int>(static_cast<int64_t>(x.split + 1) * n / S) - x.t0;
+    if (S == 1) {
+      x.split = 0;
+      x.h = rest;
+      x.t0 = 0;
+      x.nkv = n;
+    } else {
+      x.split = rest % S;
+      x.h = rest / S;
+      x.t0 = x.split * n / S;              // n <= 2^24, S <= 64: no int32 overflow
+      x.nkv = (x.split + 1) * n / S - x.t0;
+    }
     return x;
   };
 
@@ -462,7 +482,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     for (int w = pair; w < W; w += npairs) {
       const Work x = decode(w, nx);
       if (w + npairs < W) nx = fetch(w + npairs);
-      const int L = x.L, nkv = x.nkv;
+      const int nkv = x.nkv;
+      const int L = x.L - kKeys * x.t0;                // keys from this work item's first tile
       if (nkv == 0) continue;                          // the epilogue warps write O = 0
       const uint32_t tO = tmem + lane_addr + kTO + (m & 1) * kD;   // this unit's O
       float m_loc = -INFINITY;
@@ -479,7 +500,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         for (int c = 0; c < 4; ++c) tmem_ld32(tS + c * 32, r + c * 32);
         tmem_ld_wait();
         if (trd) GESR_T2(1, m * 16 + j);
-        const int valid = L - kKeys * (x.t0 + j);
+        const int valid = L - kKeys * j;
         const bool full = valid >= kKeys;
         if (!full) {
 #pragma unroll
@@ -625,6 +646,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
       prev_last_b = ((nkv - 1) & 1) == 1;
       // publish this warpgroup's max / sum of my rows for the epilogue warps
+      if (m >= 4) pwait(&ml_empty[m & 3], ((m >> 2) - 1) & 1, CTX(15, m, 0));
       const uint32_t xb = xch + ((m & 3) * 2 * 2 * 128) * 4;      // [WG][m, l][row]
       st_shared_f32(xb + ((g * 2 + 0) * 128 + rloc) * 4, m_loc);
       st_shared_f32(xb + ((g * 2 + 1) * 128 + rloc) * 4, l);
@@ -688,6 +710,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const bool hasB = nkv > 1;
       const float mB = hasB ? ld_shared_f32(xb + (2 * 128 + rloc) * 4) : -INFINITY;
       const float lB = hasB ? ld_shared_f32(xb + (3 * 128 + rloc) * 4) : 0.f;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ml_empty[m & 3]);     // m / l slot read
       const float mm = hasB ? fmaxf(mA, mB) : mA;      // = the final shared max O is scaled to
       const float lsum = lA * ex2(mA - mm) + (hasB ? lB * ex2(mB - mm) : 0.f);
       const float inv = 1.0f / lsum;

@@ -62,6 +62,20 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
   return ok != 0;
 }
 
+// Timeout report: printed only in -DGESR_DEBUG_WAITS builds (a printf call inside a wait loop
+// makes ptxas spill the caller's live registers around it).
+__device__ __forceinline__ void mbar_timeout(uint32_t a, uint32_t parity) {
+#ifdef GESR_DEBUG_WAITS
+  if ((threadIdx.x & 31) == 0)
+    printf("gesr: mbarrier timeout block %d thread %d smem 0x%x parity %u\n", blockIdx.x,
+           threadIdx.x, a, parity);
+#else
+  (void)a;
+  (void)parity;
+#endif
+  __trap();
+}
+
 // Wait until the phase with the given parity has completed.  A wait that exceeds ~20 s traps
 // (turns a protocol bug into a launch error instead of a hung GPU).
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
@@ -69,12 +83,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   if (mbar_try_wait(a, parity)) return;
   const long long t0 = clock64();
   while (!mbar_try_wait(a, parity)) {
-    if (clock64() - t0 > 40000000000LL) {
-      if ((threadIdx.x & 31) == 0)
-        printf("gesr: mbarrier timeout block %d thread %d smem 0x%x parity %u\n", blockIdx.x,
-               threadIdx.x, a, parity);
-      __trap();
-    }
+    if (clock64() - t0 > 40000000000LL) mbar_timeout(a, parity);
   }
 }
 
@@ -98,12 +107,7 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
   if (mbar_try_wait_hint(a, parity, 1000000u)) return;
   const long long t0 = clock64();
   while (!mbar_try_wait_hint(a, parity, 1000000u)) {
-    if (clock64() - t0 > 40000000000LL) {
-      if ((threadIdx.x & 31) == 0)
-        printf("gesr: mbarrier timeout block %d thread %d smem 0x%x parity %u\n", blockIdx.x,
-               threadIdx.x, a, parity);
-      __trap();
-    }
+    if (clock64() - t0 > 40000000000LL) mbar_timeout(a, parity);
   }
 }
 
