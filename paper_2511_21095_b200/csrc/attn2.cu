@@ -9,19 +9,22 @@
 // an epilogue bubble.  Here:
 //   * a cluster of 2 CTAs works on one unit (request b, head h, 256 candidates); CTA r owns
 //     candidate rows [128 r, 128 r + 128).  The leader issues M=256 MMAs for the pair: S = Q K^T
-//     (SS; each CTA stages its Q tile and HALF of each K tile -- 64 keys) and O += P V (SS; P
-//     from each CTA's shared memory, each CTA stages HALF of each V tile -- 64 d-columns);
-//   * P lives in shared memory, so a warpgroup frees its S buffer (TMEM) as soon as S is in
-//     registers and S(j+2) is computed during the softmax of tile j: no MMA sits between two
-//     softmax passes of a warpgroup;
+//     (SS; each CTA stages its Q tile and HALF of each K tile -- 64 keys) and O += P V (TS; P
+//     from each CTA's TMEM, each CTA stages HALF of each V tile -- 64 d-columns);
+//   * ONE S buffer in TMEM serves both warpgroups and P lives in its own TMEM columns, so a
+//     warpgroup releases S as soon as S is in registers and S(j+1) is computed during the
+//     softmax of tile j: no MMA sits between two softmax passes; PV is a TS MMA (A = P from
+//     TMEM), so the tensor core reads only Q, K and V from shared memory (P in shared memory
+//     cost ~6 %: its stores stalled behind the tensor core's operand reads);
 //   * key tiles alternate between softmax warpgroups A (even) and B (odd); a named-barrier
 //     "MUFU token" per sub-partition orders their exp passes A(0), B(1), A(2), ... so one's exp
 //     pass overlaps the other's TMEM load, x pass and P hand-off.  Both accumulate into ONE O per
 //     unit with ONE running max per row (m_sh in shared memory, written only by the token
 //     holder); the row max is exact only for tile 0, later tiles test the tile's row sum and
 //     take the slow path (exact max, raise m_sh, rescale O, recompute P) only when needed;
-//   * TMEM per CTA (512 columns): S_A [0,128), S_B [128,256), O of even units [256,384), O of
-//     odd units [384,512): a unit's epilogue (warps 12-15) overlaps the next unit entirely;
+//   * TMEM per CTA (512 columns): S [0,128), P_A [128,192), P_B [192,256), O of even units
+//     [256,384), O of odd units [384,512): a unit's epilogue (warps 12-15) overlaps the next
+//     unit entirely;
 //   * persistent: pair c takes work items c, c + G, ... (w -> unit w % U, head w / U); the key
 //     tiles of all its work items form one stream, walked independently by the Q/K producer,
 //     the V producer, the S-MMA issuer and the PV-MMA issuer; full 32-row output slabs leave
@@ -61,9 +64,6 @@ __device__ unsigned long long g_trace4[64][16][16];  // per unit: epilogue chunk
 
 namespace {
 
-#ifndef GESR_PAIR_STS_AFTER
-#define GESR_PAIR_STS_AFTER 0   // experiment: P packed in place, stored after the exp loop (no rescale)
-#endif
 #ifndef GESR_PAIR_POLY_EVERY
 #define GESR_PAIR_POLY_EVERY 1000   // one pair in N takes the FMA-pipe exp2 on full tiles (1000: off)
 #endif
@@ -100,13 +100,11 @@ constexpr int kKeys = 128;                       // keys per tile (S columns)
 constexpr int kThreads = 512;
 constexpr uint32_t kQBytes = 128 * kD * 2;       // 32 KB: Q tile, [2 col blocks][128 rows][64]
 constexpr uint32_t kHalfBytes = 16384;           // K half [2][64 keys][64] or V half [128][64]
-constexpr int kKStages = 2;                     // K-half ring
-constexpr int kVStages = 3;                     // V-half ring
+constexpr int kKStages = 4;                     // K-half ring
+constexpr int kVStages = 5;                     // V-half ring
 constexpr int kStages = kKStages + kVStages;
 constexpr uint32_t kQOff = 0;
-constexpr uint32_t kPOff = kQBytes;                                  // P_A, P_B: [2 atoms][128][128 B]
-constexpr uint32_t kPBytes = 128 * kKeys * 2;                        // 32 KB
-constexpr uint32_t kRingOff = kPOff + 2 * kPBytes;
+constexpr uint32_t kRingOff = kQBytes;
 constexpr uint32_t kStgOff = kRingOff + kStages * kHalfBytes;        // 4 x 2 KB boxes per epilogue warp
 constexpr uint32_t kBarOff = kStgOff + 4 * 8192;
 constexpr uint32_t kXchOff = kBarOff + 512;                          // [unit % 4][WG][m, l][row]
@@ -120,7 +118,8 @@ constexpr int kSoftRegs = 184;
 constexpr int kEpiRegs = 88;
 static_assert(128 * kCtrlRegs + 256 * kSoftRegs + 128 * kEpiRegs <= 128 * kThreads, "setmaxnreg pool");
 // TMEM columns
-constexpr uint32_t kTS = 0;          // S_A at 0, S_B at 128
+constexpr uint32_t kTS = 0;          // S: one buffer, alternately A's and B's tiles
+constexpr uint32_t kTP = 128;        // P_A at 128, P_B at 192 (bf16 pairs, 64 columns each)
 constexpr uint32_t kTO = 256;        // O of even units at 256, of odd units at 384
 
 __device__ __forceinline__ void ffma2(float& d0, float& d1, float a0, float a1, float b0, float b1,
@@ -199,7 +198,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t* kv_full = q_empty + 1;                // [kStages]  K ring, then V ring (leader's used)
   uint64_t* kv_empty = kv_full + kStages;         // [kStages]  (each CTA)
   uint64_t* s_full = kv_empty + kStages;          // [2]        (each CTA)
-  uint64_t* s_free = s_full + 2;                  // [2]        (leader; 8 warps of the pair)
+  uint64_t* s_free = s_full + 2;                  //            (leader; 4 warps x 2 CTAs per S)
   uint64_t* p_full = s_free + 2;                  // [2]        (leader; 8 warps of the pair)
   uint64_t* p_free = p_full + 2;                  // [2]        (each CTA)
   uint64_t* o_done = p_free + 2;                  // [2]        (each CTA; per O buffer)
@@ -231,7 +230,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_free[i], 8);
+      mbar_init(&s_free[i], 8);                  // [1] unused
       mbar_init(&p_full[i], 8);
       mbar_init(&p_free[i], 1);
     }
@@ -256,7 +255,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const uint32_t tmem = *tmem_slot;
   const uint32_t sQ = smem_u32(smem + kQOff);
   const uint32_t sRing = smem_u32(smem + kRingOff);
-  const uint32_t sP = smem_u32(smem + kPOff);
 
   // the unit descriptor of work item w is one 16-byte load, fetched one item ahead
   auto fetch = [&](int w) { return __ldg(p.units + (w % U)); };
@@ -377,17 +375,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const uint32_t idesc_s = make_idesc_bf16(256, kKeys, 0, 0);
       int kst = 0;
       uint32_t kph = 0;
-      uint32_t sn0 = 0, sn1 = 0;                   // S issued into buffer A / B so far
+      uint32_t sn0 = 0;                            // S issued so far
       while (stream_next(st, tl)) {
         const int buf = tl.t & 1;
         if (tl.t == 0) {
           pwait(q_full, tl.m & 1, CTX(4, tl.m, tl.t));   // the unit's Q tile (both CTAs)
           if (lane == 0) GESR_T3(0, tl.m);
         }
-        // the buffer's previous S must have been loaded by its warpgroup (both CTAs)
-        const uint32_t sn = buf ? sn1 : sn0;
-        if (sn > 0) pwait(&s_free[buf], (sn - 1) & 1, CTX(5, tl.m, tl.t));
-        if (buf) ++sn1; else ++sn0;
+        // the single S buffer's previous S must have been loaded into registers (both CTAs)
+        if (sn0 > 0) pwait(s_free, (sn0 - 1) & 1, CTX(5, tl.m, tl.t));
+        ++sn0;
         const int slot = kst;
         pwait(&kv_full[slot], kph, CTX(6, tl.m, tl.t));
         if (++kst == kKStages) { kst = 0; kph ^= 1; }
@@ -397,8 +394,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (elect_one()) {
 #pragma unroll
           for (int ks = 0; ks < kD / 16; ++ks)
-            mma_ss_pair(tmem + kTS + buf * kKeys, kdesc(sQ, kQBytes / 2, ks), kdesc(kb, 8192, ks),
-                        idesc_s, ks > 0 ? 1u : 0u);
+            mma_ss_pair(tmem + kTS, kdesc(sQ, kQBytes / 2, ks), kdesc(kb, 8192, ks), idesc_s,
+                        ks > 0 ? 1u : 0u);
           mma_commit_pair_mc(&s_full[buf], 0x3);
           mma_commit_pair_mc(&kv_empty[slot], 0x3);
           // the unit's last S: its Q buffer may be reloaded
@@ -430,11 +427,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         tc_fence_after();
         if (elect_one()) {
           const uint32_t vb = sRing + vslot * kHalfBytes;
-          const uint32_t pb = sP + xb * kPBytes;
 #pragma unroll
           for (int ks = 0; ks < kKeys / 16; ++ks)
-            mma_ss_pair(tmem + kTO + ob * kD, kdesc(pb, kPBytes / 2, ks), vdesc(vb, ks), idesc_o,
-                        (tl.t > 0 || ks > 0) ? 1u : 0u);
+            mma_ts_pair(tmem + kTO + ob * kD, tmem + kTP + xb * (kKeys / 2) + ks * 8, vdesc(vb, ks),
+                        idesc_o, (tl.t > 0 || ks > 0) ? 1u : 0u);
           mma_commit_pair_mc(&p_free[xb], 0x3);
           mma_commit_pair_mc(&kv_empty[vslot], 0x3);
           mma_commit_pair_mc(pv_done, 0x3);
@@ -459,14 +455,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const uint32_t sub = warp & 3;                       // TMEM lane quarter
     const int rloc = static_cast<int>(sub) * 32 + static_cast<int>(lane);
     const uint32_t lane_addr = (sub * 32) << 16;
-    const uint32_t tS = tmem + lane_addr + kTS + g * kKeys;
-    const uint32_t s_free_leader = mapa_shared(smem_u32(&s_free[g]), 0);
+    const uint32_t tS = tmem + lane_addr + kTS;
+    const uint32_t tP = tmem + lane_addr + kTP + g * (kKeys / 2);
+    const uint32_t s_free_leader = mapa_shared(smem_u32(s_free), 0);
     const uint32_t p_full_leader = mapa_shared(smem_u32(&p_full[g]), 0);
     const uint32_t xch = smem_u32(smem + kXchOff);
     const uint32_t msh = smem_u32(smem + kMshOff) + rloc * 4;
-    // P_g: K-major SW128, [2 atoms of 64 keys][128 rows][128 B]; row rloc's 16-byte chunk c of
-    // atom a sits at a * 16 KB + rloc * 128 + ((c ^ (rloc & 7)) << 4)
-    const uint32_t prow = smem_u32(smem + kPOff + g * kPBytes) + rloc * 128;
     const float sl2 = p.scale_log2;
     int sc = 0;                                          // S tiles consumed by this warpgroup
     // MUFU token: the exp passes of the two warps of a sub-partition (A and B, same lane
@@ -574,16 +568,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               r[2 * k + 1] = __float_as_uint(x1);
             }
           }
-          // p = 2^x, packed to bf16 pairs and stored to P_g 16 bytes at a time; masked keys
-          // give exactly 0
+          // p = 2^x, packed to bf16 pairs and stored to P_g (TMEM) 32 columns at a time;
+          // masked keys give exactly 0
 #pragma unroll
           for (int e = 0; e < 8; ++e) acc[e] = 0.f;
 #pragma unroll
-          for (int q = 0; q < kKeys / 8; ++q) {
-            uint32_t pw[4];
+          for (int hh = 0; hh < 2; ++hh) {
+            uint32_t pk[32];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const int k = q * 4 + u;
+            for (int u = 0; u < 32; ++u) {
+              const int k = hh * 32 + u;
               float p0, p1;
               if ((k % GESR_PAIR_POLY_EVERY) == GESR_PAIR_POLY_EVERY - 1 && full) {
                 exp2_fma2(p0, p1, __uint_as_float(r[2 * k]), __uint_as_float(r[2 * k + 1]));
@@ -593,23 +587,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               }
               const int a = (k & 3) * 2;
               fadd2(acc[a], acc[a + 1], acc[a], acc[a + 1], p0, p1);
-              pw[u] = pack_bf16x2(p0, p1);
-              if (GESR_PAIR_STS_AFTER) r[k] = pw[u];
+              pk[u] = pack_bf16x2(p0, p1);
             }
-            if (!GESR_PAIR_STS_AFTER)
-              st_shared_v4(prow + (q >> 3) * (kPBytes / 2) + (((q & 7) ^ (rloc & 7)) << 4), pw[0], pw[1],
-                           pw[2], pw[3]);
-          }
-          if (GESR_PAIR_STS_AFTER) {
-#pragma unroll
-            for (int q = 0; q < kKeys / 8; ++q)
-              st_shared_v4(prow + (q >> 3) * (kPBytes / 2) + (((q & 7) ^ (rloc & 7)) << 4), r[4 * q],
-                           r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
+            tmem_st32(tP + hh * 32, pk);
           }
           if (trd && pass == 0) GESR_T2(3, m * 16 + j);
           tsum = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
           const bool over = !(tsum <= GESR_PAIR_SUM_LIMIT);
-          if (pass == 1 || j == 0 || GESR_PAIR_STS_AFTER || !__any_sync(0xffffffffu, over)) break;
+          if (pass == 1 || j == 0 || !__any_sync(0xffffffffu, over)) break;
           const float dx = over ? row_max() : 0.f;       // exact max above m_loc (x units)
           const bool need = dx > 8.0f;
           if (!__any_sync(0xffffffffu, need)) break;
@@ -639,7 +624,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         // hand the token to tile j+1's warpgroup (the next unit starts with A)
         if (j + 1 < nkv || (g == 1 && w + npairs < W)) named_bar_arrive(tok_other, 64);
         l += tsum;
-        fence_proxy_async_smem();
+        tmem_st_wait();                                  // P_g in TMEM before PV(j) reads it
+        tc_fence_before();
         __syncwarp();
         if (trd) GESR_T2(5, m * 16 + j);
         if (lane == 0) mbar_arrive_cluster_relaxed(p_full_leader);

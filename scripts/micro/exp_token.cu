@@ -21,7 +21,7 @@ __device__ __forceinline__ void fadd2(float& d0, float& d1, float a0, float a1, 
 }
 
 template <int WORK>
-__global__ void __launch_bounds__(256, 1) k(long long* clk, int iters, float sl2) {
+__global__ void __launch_bounds__(288, 1) k(long long* clk, int iters, float sl2) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint32_t slot;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -30,6 +30,30 @@ __global__ void __launch_bounds__(256, 1) k(long long* clk, int iters, float sl2
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = slot;
+  if (warp == 8) {
+    // WORK >= 2: a tcgen05 MMA stream (SS M=128 N=128 K=16, operands in smem at 96 KB+) for the
+    // duration, as the attention kernel's tensor pipe runs beside its softmax
+    if (WORK >= 2 && lane == 0) {
+      const uint32_t sa = smem_u32(smem + 98304), sb = smem_u32(smem + 98304 + 32768);
+      const uint32_t idesc = make_idesc_bf16(128, 128, 0, 0);
+      __shared__ __align__(8) uint64_t mb;
+      mbar_init(&mb, 1);
+      fence_mbar_init();
+      for (int rep = 0; rep < iters * 4; ++rep) {
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks)
+          mma_ss(tmem + 384, make_sdesc(sa + (ks / 4) * 16384 + (ks % 4) * 32, 16, 1024, 2),
+                 make_sdesc(sb + (ks / 4) * 16384 + (ks % 4) * 32, 16, 1024, 2), idesc, 1u);
+        mma_commit(&mb);
+        mbar_wait(&mb, rep & 1);
+      }
+    }
+    __syncwarp();
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) { tc_fence_after(); tmem_dealloc(tmem, 512); }
+    return;
+  }
   const int g = warp / 4, sub = warp & 3;
   const uint32_t tS = tmem + ((sub * 32) << 16) + g * 128;
   const uint32_t prow = smem_u32(smem) + g * 32768 + (sub * 32 + lane) * 128;
@@ -90,15 +114,17 @@ __global__ void __launch_bounds__(256, 1) k(long long* clk, int iters, float sl2
 int main() {
   long long* c;
   cudaMalloc(&c, 4096 * 8);
-  for (int work = 0; work < 2; ++work) {
+  for (int work = 0; work < 3; ++work) {
     const int iters = 300;
     cudaEvent_t a, b;
     cudaEventCreate(&a); cudaEventCreate(&b);
     auto launch = [&] {
-      if (work) k<1><<<148, 256, 70000>>>(c, iters, 0.1f); else k<0><<<148, 256, 70000>>>(c, iters, 0.1f);
+      if (work == 2) k<2><<<148, 288, 200000>>>(c, iters, 0.1f);
+      else if (work) k<1><<<148, 288, 200000>>>(c, iters, 0.1f); else k<0><<<148, 288, 200000>>>(c, iters, 0.1f);
     };
-    cudaFuncSetAttribute(k<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 70000);
-    cudaFuncSetAttribute(k<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 70000);
+    cudaFuncSetAttribute(k<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200000);
+    cudaFuncSetAttribute(k<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200000);
+    cudaFuncSetAttribute(k<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200000);
     launch();
     cudaDeviceSynchronize();
     cudaEventRecord(a);
@@ -112,7 +138,7 @@ int main() {
     int clkr;
     cudaDeviceGetAttribute(&clkr, cudaDevAttrClockRate, 0);
     printf("token-alternating exp passes, %s: exp window %lld clk; period per tile %.0f clk (at max clock) (%s)\n",
-           work ? "with S load + x pass between" : "no other work", h,
+           work == 2 ? "S load + x pass + MMA stream" : work ? "with S load + x pass between" : "no other work", h,
            ms * 1e-3 * clkr * 1e3 / (2.0 * iters), cudaGetErrorString(e));
   }
   return 0;
