@@ -109,7 +109,8 @@ size_t gesr_tasa_workspace_bytes(int64_t B, int64_t total_C, int32_t H, int32_t 
  *              runs unsplit.  For a fixed kv_splits >= 1 each output row depends only on its
  *              own candidate and its user's K/V: results are bit-identical across chunking,
  *              batch composition and GPU count (reading R9).  kv_splits > 64 is invalid.
- *   flags      0, or GESR_TASA_SELF_KEY (unsupported in this version).
+ *   flags      0.  GESR_TASA_SELF_KEY needs the candidates' own keys / values: it returns
+ *              GESR_ERR_UNSUPPORTED here; use gesr_tasa_score_self.
  *   O          [total_C, H*d] fp32 or bf16 (o_dtype): O[t][h*d+j] = sum_i p_i V[h][r_i][j] with
  *              p = softmax_i(scale * q_h . K[h][r_i]) over the request's L_b history rows.
  *              L_b = 0 gives an all-zero row (reading R6).
@@ -129,6 +130,27 @@ gesr_status gesr_tasa_score(const void* T, int64_t total_C, int32_t D_in,
                             float* lse,
                             void* workspace, size_t workspace_bytes,
                             void* stream);
+
+/* gesr_tasa_score_self -- gesr_tasa_score with the candidate SELF KEY: each candidate also
+ * attends to its own key (the diagonal SPEC.md's mask keeps; DESIGN.md
+ * reading R2 -- SURVEY s8(f) f1, the first piece of the full STU candidate row):
+ *   O[t][h] = (sum_i e^{s_i} V[h][r_i] + e^{s_t} V_self[h][t]) / (sum_i e^{s_i} + e^{s_t}),
+ *   s_i = scale q_h . K[h][r_i],  s_t = scale q_h . K_self[h][t]
+ * over the request's history rows r_i; lse includes s_t.  L_b = 0 gives O = V_self, lse = s_t.
+ *   K_self, V_self  bf16 [H, total_C, d]: the candidates' own keys / values, i.e.
+ *              gesr_kv_project applied to T (U := T, total_L := total_C) with W_k, W_v.
+ * All other arguments, the workspace size and the error behaviour are those of
+ * gesr_tasa_score; the merge runs after the history attention on the same stream. */
+gesr_status gesr_tasa_score_self(const void* T, int64_t total_C, int32_t D_in,
+                                 const int64_t* cand_offsets,
+                                 const void* W_q, const float* b_q, int32_t act,
+                                 const void* K_cache, const void* V_cache,
+                                 const int64_t* seq_offsets, int64_t B, int64_t total_L,
+                                 int32_t H, int32_t d, float scale, int32_t kv_splits,
+                                 const void* K_self, const void* V_self,
+                                 void* O, int32_t o_dtype, float* lse,
+                                 void* workspace, size_t workspace_bytes,
+                                 void* stream);
 
 /* gesr_hma_count -- HMA per-field match counts.
  *   user_ids / user_offsets  int64 CSR: segment b*F+f is request b's user-side ID list of

@@ -64,6 +64,10 @@ def lib():
     L.gesr_tasa_score.argtypes = [_vp, _i64, _i32, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _i64, _i64,
                                   _i32, _i32, ctypes.c_float, _i32, ctypes.c_uint32, _vp, _i32,
                                   _vp, _vp, ctypes.c_size_t, _vp]
+    L.gesr_tasa_score_self.restype = ctypes.c_int
+    L.gesr_tasa_score_self.argtypes = [_vp, _i64, _i32, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _i64,
+                                       _i64, _i32, _i32, ctypes.c_float, _i32, _vp, _vp, _vp,
+                                       _i32, _vp, _vp, ctypes.c_size_t, _vp]
     L.gesr_hma_count.restype = ctypes.c_int
     L.gesr_hma_count.argtypes = [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _i32, _i32, _vp, _vp]
     _lib = L
@@ -130,9 +134,12 @@ def tasa_workspace_bytes(B: int, total_C: int, H: int, d: int, kv_splits: int = 
 def tasa_score(T, cand_offsets, W_q, K_cache, V_cache, seq_offsets, H: int, d: int,
                act: int = GESR_ACT_SILU, b_q=None, scale: float = 0.0, kv_splits: int = 0,
                flags: int = 0, out_dtype=torch.float32, want_lse: bool = True, O=None, lse=None,
-               workspace=None, stream=None):
-    """O [total_C, H*d] (fp32|bf16), lse fp32 [total_C, H] (gesr_tasa_score)."""
-    _dev(T, cand_offsets, W_q, K_cache, V_cache, seq_offsets, b_q, O, lse, workspace)
+               workspace=None, stream=None, K_self=None, V_self=None):
+    """O [total_C, H*d] (fp32|bf16), lse fp32 [total_C, H] (gesr_tasa_score; with K_self /
+    V_self -- the candidates' own keys / values [H, total_C, d] from kv_project(T, ...) --
+    gesr_tasa_score_self: each candidate also attends to its own key)."""
+    _dev(T, cand_offsets, W_q, K_cache, V_cache, seq_offsets, b_q, O, lse, workspace, K_self,
+         V_self)
     total_C, D_in = T.shape
     B = cand_offsets.numel() - 1
     total_L = K_cache.shape[1]
@@ -144,6 +151,14 @@ def tasa_score(T, cand_offsets, W_q, K_cache, V_cache, seq_offsets, H: int, d: i
     if workspace is None:
         nbytes = tasa_workspace_bytes(B, total_C, H, d, kv_splits)
         workspace = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=T.device)
+    if K_self is not None or V_self is not None:
+        _check(lib().gesr_tasa_score_self(_ptr(T), total_C, D_in, _ptr(cand_offsets), _ptr(W_q),
+                                          _ptr(b_q), act, _ptr(K_cache), _ptr(V_cache),
+                                          _ptr(seq_offsets), B, total_L, H, d, float(scale),
+                                          kv_splits, _ptr(K_self), _ptr(V_self), _ptr(O),
+                                          o_dtype, _ptr(lse), _ptr(workspace), workspace.numel(),
+                                          _stream(stream)))
+        return O, lse
     _check(lib().gesr_tasa_score(_ptr(T), total_C, D_in, _ptr(cand_offsets), _ptr(W_q),
                                  _ptr(b_q), act, _ptr(K_cache), _ptr(V_cache), _ptr(seq_offsets),
                                  B, total_L, H, d, float(scale), kv_splits, flags, _ptr(O),

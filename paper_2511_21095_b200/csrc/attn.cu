@@ -632,6 +632,47 @@ __global__ void build_units_kernel(const int64_t* __restrict__ seq_offsets,
   if (threadIdx.x == 0) *count = running;
 }
 
+// Self key (the candidate diagonal of the [U, T] mask; R2): one
+// warp per (candidate, head).  The history attention left O = sum_i p_i v_i / sum_i p_i and
+// lse = log sum_i e^{s_i}; the candidate's own score s = scale q.k_self joins as one more key:
+// O' = (O e^{lse - M} + v_self e^{s - M}) / (e^{lse - M} + e^{s - M}), M = max(lse, s),
+// lse' = M + log(...).  L_b = 0 (lse = -inf) gives O' = v_self, lse' = s.
+__global__ void __launch_bounds__(256) attn_self_merge_kernel(const AttnParams p,
+                                                              const __nv_bfloat16* __restrict__ Q,
+                                                              const __nv_bfloat16* __restrict__ Ks,
+                                                              const __nv_bfloat16* __restrict__ Vs,
+                                                              int d, float scale) {
+  const int64_t item = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (item >= p.total_C * p.H) return;
+  const int64_t row = item / p.H;
+  const int h = static_cast<int>(item % p.H);
+  const int64_t kv = (static_cast<int64_t>(h) * p.total_C + row) * d;   // [H, total_C, d]
+  const int64_t o0 = row * p.H * d + static_cast<int64_t>(h) * d;
+  float dot = 0.f;
+  for (int j = lane; j < d; j += 32)
+    dot += __bfloat162float(Q[kv + j]) * __bfloat162float(Ks[kv + j]);
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+  const float s = dot * scale;
+  const float l0 = p.lse[item];
+  const float M = fmaxf(l0, s);
+  const float w0 = (l0 == -INFINITY) ? 0.f : expf(l0 - M);
+  const float w1 = expf(s - M);
+  const float inv = 1.0f / (w0 + w1);
+  for (int j = lane; j < d; j += 32) {
+    const float v = __bfloat162float(Vs[kv + j]);
+    if (p.o_bf16) {
+      __nv_bfloat16* O = static_cast<__nv_bfloat16*>(p.O);
+      O[o0 + j] = __float2bfloat16_rn((__bfloat162float(O[o0 + j]) * w0 + v * w1) * inv);
+    } else {
+      float* O = static_cast<float*>(p.O);
+      O[o0 + j] = (O[o0 + j] * w0 + v * w1) * inv;
+    }
+  }
+  if (lane == 0) p.lse[item] = M + logf(w0 + w1);
+}
+
 // total_L == 0: every candidate has an empty history -> O = 0, lse = -inf (R6)
 __global__ void attn_empty_kernel(AttnParams p, int D) {
   const int64_t HD = static_cast<int64_t>(p.H) * D;
@@ -688,6 +729,16 @@ cudaError_t launch_attn(int d, const CUtensorMap& mq, const CUtensorMap& mk, con
     case 128: return launch_d<128>(mq, mk, mv, mo, p, max_units, stream);
     default: return cudaErrorInvalidValue;
   }
+}
+
+cudaError_t launch_attn_self_merge(const AttnParams& p, const void* Q, const void* K_self,
+                                   const void* V_self, int d, float scale, cudaStream_t stream) {
+  const int64_t n = p.total_C * p.H;
+  if (n == 0) return cudaSuccess;
+  attn_self_merge_kernel<<<static_cast<unsigned>((n + 7) / 8), 256, 0, stream>>>(
+      p, static_cast<const __nv_bfloat16*>(Q), static_cast<const __nv_bfloat16*>(K_self),
+      static_cast<const __nv_bfloat16*>(V_self), d, scale);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_attn_empty(const AttnParams& p, int d, cudaStream_t stream) {

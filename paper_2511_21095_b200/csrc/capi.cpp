@@ -267,16 +267,19 @@ size_t gesr_tasa_workspace_bytes(int64_t B, int64_t total_C, int32_t H, int32_t 
     }
   }
   const size_t q_end = units_end(B, total_C) + static_cast<size_t>(total_C) * H * d * 2;
-  return ((q_end + 255) & ~static_cast<size_t>(255)) + part;
+  const size_t lse_scratch = (static_cast<size_t>(total_C) * H * 4 + 255) & ~static_cast<size_t>(255);
+  return ((q_end + 255) & ~static_cast<size_t>(255)) + part + lse_scratch;
 }
 
-gesr_status gesr_tasa_score(const void* T, int64_t total_C, int32_t D_in,
-                            const int64_t* cand_offsets, const void* W_q, const float* b_q,
-                            int32_t act, const void* K_cache, const void* V_cache,
-                            const int64_t* seq_offsets, int64_t B, int64_t total_L, int32_t H,
-                            int32_t d, float scale, int32_t kv_splits, uint32_t flags, void* O,
-                            int32_t o_dtype, float* lse, void* workspace,
-                            size_t workspace_bytes, void* stream) {
+// Shared body of gesr_tasa_score and gesr_tasa_score_self (K_self / V_self non-null: the
+// candidate's own key/value is merged into each row after the history attention).
+static gesr_status tasa_impl(const void* T, int64_t total_C, int32_t D_in, const int64_t* cand_offsets,
+                      const void* W_q, const float* b_q, int32_t act, const void* K_cache,
+                      const void* V_cache, const int64_t* seq_offsets, int64_t B, int64_t total_L,
+                      int32_t H, int32_t d, float scale, int32_t kv_splits, uint32_t flags,
+                      const void* K_self, const void* V_self, void* O, int32_t o_dtype,
+                      float* lse, void* workspace, size_t workspace_bytes, void* stream) {
+  const bool self = K_self != nullptr || V_self != nullptr;
   gesr_status s = check_common(D_in, H, d, act);
   if (s != GESR_OK) return s;
   if (B < 0 || total_C < 0 || total_L < 0)
@@ -290,14 +293,17 @@ gesr_status gesr_tasa_score(const void* T, int64_t total_C, int32_t D_in,
     return fail(GESR_ERR_INVALID_ARG, "kv_splits=%d outside [0, %d]", kv_splits, kMaxSplits);
   if (kv_splits > 1 && (d != 128 || !pair_attention_enabled()))
     return fail(GESR_ERR_UNSUPPORTED, "kv_splits > 1 needs d = 128 (CTA-pair attention kernel)");
-  if (flags & GESR_TASA_SELF_KEY)
-    return fail(GESR_ERR_UNSUPPORTED, "GESR_TASA_SELF_KEY not supported in this version");
+  if ((flags & GESR_TASA_SELF_KEY) && !self)
+    return fail(GESR_ERR_UNSUPPORTED,
+                "GESR_TASA_SELF_KEY needs the candidates' own K/V: use gesr_tasa_score_self");
   if (flags & ~GESR_TASA_SELF_KEY) return fail(GESR_ERR_INVALID_ARG, "unknown flags 0x%x", flags);
   if (total_C == 0 || B == 0) return GESR_OK;
   if (!T || !cand_offsets || !W_q || !seq_offsets || !O || !workspace)
     return fail(GESR_ERR_INVALID_ARG, "null required pointer");
   if (total_L > 0 && (!K_cache || !V_cache))
     return fail(GESR_ERR_INVALID_ARG, "null K/V cache with total_L > 0");
+  if (self && (!K_self || !V_self || !aligned16(K_self) || !aligned16(V_self)))
+    return fail(GESR_ERR_INVALID_ARG, "K_self and V_self must both be given and 16-byte aligned");
   if (!aligned16(T) || !aligned16(W_q) || !aligned16(K_cache) || !aligned16(V_cache) ||
       !aligned16(O) || !aligned16(b_q) || !aligned16(lse) ||
       (reinterpret_cast<uintptr_t>(workspace) & 255u) != 0 ||
@@ -319,27 +325,42 @@ gesr_status gesr_tasa_score(const void* T, int64_t total_C, int32_t D_in,
   p.scale_log2 = sc * 1.4426950408889634f;
   p.O = O;
   p.o_bf16 = o_dtype == GESR_OUT_BF16;
-  p.lse = lse;
   p.splits = 1;
-  if (total_L == 0) {
-    cudaError_t e = gesr::launch_attn_empty(p, d, st);
-    return e == cudaSuccess ? GESR_OK : cuda_fail(e, "attn_empty launch");
-  }
-
   uint8_t* ws = static_cast<uint8_t*>(workspace);
   int* count = reinterpret_cast<int*>(ws);
   int4* units = reinterpret_cast<int4*>(ws + 256);
   void* Q = ws + units_end(B, total_C);
+  const size_t q_end = units_end(B, total_C) + static_cast<size_t>(total_C) * H * d * 2;
+  uint8_t* part = ws + ((q_end + 255) & ~static_cast<size_t>(255));
+  // the self-key merge needs the history lse: a scratch row set when the caller wants none
+  float* lse_scratch = reinterpret_cast<float*>(
+      part + split_bytes(total_C, H, d,
+                         d == 128 ? (kv_splits > 1 ? kv_splits
+                                     : (kv_splits == 0 && max_units(B, total_C) * H < kAutoSplitItems
+                                            ? kMaxAutoSplits : 1))
+                                  : 1));
+  p.lse = (self && lse == nullptr) ? lse_scratch : lse;
+  auto self_merge = [&]() -> gesr_status {
+    if (!self) return GESR_OK;
+    cudaError_t e2 = gesr::launch_attn_self_merge(p, Q, K_self, V_self, d, sc, st);
+    return e2 == cudaSuccess ? GESR_OK : cuda_fail(e2, "attn_self_merge launch");
+  };
+  if (total_L == 0) {
+    cudaError_t e = gesr::launch_attn_empty(p, d, st);
+    if (e != cudaSuccess) return cuda_fail(e, "attn_empty launch");
+    if (!self) return GESR_OK;
+    s = run_projection(T, total_C, D_in, W_q, nullptr, b_q, nullptr, H, d, act, Q, nullptr, st);
+    if (s != GESR_OK) return s;
+    return self_merge();
+  }
+
   p.units = units;
   p.unit_count = count;
   p.splits = pick_splits(B, total_C, total_L, H, d, kv_splits);
   if (p.splits > 1) {
-    const size_t q_end = units_end(B, total_C) + static_cast<size_t>(total_C) * H * d * 2;
-    uint8_t* part = ws + ((q_end + 255) & ~static_cast<size_t>(255));
     p.part_ml = reinterpret_cast<float2*>(part);
     p.part_o = reinterpret_cast<float*>(part + split_ml_bytes(total_C, H, p.splits));
   }
-
   cudaError_t e = gesr::launch_build_units(seq_offsets, cand_offsets, B, units, count, st);
   if (e != cudaSuccess) return cuda_fail(e, "build_units launch");
   s = run_projection(T, total_C, D_in, W_q, nullptr, b_q, nullptr, H, d, act, Q, nullptr, st);
@@ -371,11 +392,38 @@ gesr_status gesr_tasa_score(const void* T, int64_t total_C, int32_t D_in,
       e = gesr::launch_attn_combine(p, d, st);
       if (e != cudaSuccess) return cuda_fail(e, "attn_combine_kernel launch");
     }
-    return GESR_OK;
+    return self_merge();
   }
   e = gesr::launch_attn(d, mq, mk, mv, mo, p, max_units(B, total_C), st);
   if (e != cudaSuccess) return cuda_fail(e, "attn_kernel launch");
-  return GESR_OK;
+  return self_merge();
+}
+
+gesr_status gesr_tasa_score(const void* T, int64_t total_C, int32_t D_in,
+                            const int64_t* cand_offsets, const void* W_q, const float* b_q,
+                            int32_t act, const void* K_cache, const void* V_cache,
+                            const int64_t* seq_offsets, int64_t B, int64_t total_L, int32_t H,
+                            int32_t d, float scale, int32_t kv_splits, uint32_t flags, void* O,
+                            int32_t o_dtype, float* lse, void* workspace,
+                            size_t workspace_bytes, void* stream) {
+  return tasa_impl(T, total_C, D_in, cand_offsets, W_q, b_q, act, K_cache, V_cache, seq_offsets,
+                   B, total_L, H, d, scale, kv_splits, flags, nullptr, nullptr, O, o_dtype, lse,
+                   workspace, workspace_bytes, stream);
+}
+
+gesr_status gesr_tasa_score_self(const void* T, int64_t total_C, int32_t D_in,
+                                 const int64_t* cand_offsets, const void* W_q, const float* b_q,
+                                 int32_t act, const void* K_cache, const void* V_cache,
+                                 const int64_t* seq_offsets, int64_t B, int64_t total_L,
+                                 int32_t H, int32_t d, float scale, int32_t kv_splits,
+                                 const void* K_self, const void* V_self, void* O,
+                                 int32_t o_dtype, float* lse, void* workspace,
+                                 size_t workspace_bytes, void* stream) {
+  if (!K_self || !V_self)
+    return fail(GESR_ERR_INVALID_ARG, "gesr_tasa_score_self needs K_self and V_self");
+  return tasa_impl(T, total_C, D_in, cand_offsets, W_q, b_q, act, K_cache, V_cache, seq_offsets,
+                   B, total_L, H, d, scale, kv_splits, GESR_TASA_SELF_KEY, K_self, V_self, O,
+                   o_dtype, lse, workspace, workspace_bytes, stream);
 }
 
 gesr_status gesr_hma_count(const int64_t* user_ids, const int64_t* user_offsets,

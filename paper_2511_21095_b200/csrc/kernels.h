@@ -66,6 +66,10 @@ cudaError_t launch_attn(int d, const CUtensorMap& map_q, const CUtensorMap& map_
 cudaError_t launch_attn_pair(const CUtensorMap& map_q, const CUtensorMap& map_kh,
                              const CUtensorMap& map_vh, const CUtensorMap& map_o,
                              const AttnParams& p, int64_t max_units, cudaStream_t stream);
+// candidate self key (GESR_TASA_SELF_KEY): merges each row's own key / value into O and lse
+// (p.lse must be set): s = scale q.k_self, O' = (O e^lse + v_self e^s) / (e^lse + e^s)
+cudaError_t launch_attn_self_merge(const AttnParams& p, const void* Q, const void* K_self,
+                                   const void* V_self, int d, float scale, cudaStream_t stream);
 // merges split-L partials: O = sum_s w_s O_s / sum_s w_s, w_s = l_s 2^(m_s - max m)
 cudaError_t launch_attn_combine(const AttnParams& p, int d, cudaStream_t stream);
 cudaError_t launch_attn_empty(const AttnParams& p, int d, cudaStream_t stream);

@@ -95,10 +95,20 @@ def test_tasa_validation(L):
     assert tasa(L, B=0) == gb.GESR_OK
 
 
+def test_tasa_self_validation(L):
+    def self_(Ks=FAKE, Vs=FAKE, d=64):
+        return L.gesr_tasa_score_self(FAKE, 10, 64, FAKE, FAKE, None, 1, FAKE, FAKE, FAKE, 2, 10,
+                                      2, d, 0.0, 0, Ks, Vs, FAKE, 0, None, FAKE, 1 << 30, None)
+    assert self_(Ks=None) == gb.GESR_ERR_INVALID_ARG
+    assert self_(Vs=MIS) == gb.GESR_ERR_INVALID_ARG
+    assert self_(d=96) == gb.GESR_ERR_INVALID_ARG
+
+
 def test_workspace_size(L):
     n = gb.tasa_workspace_bytes(1024, 1024000, 4, 128)
-    # units list + Q [H, total_C, d] bf16
-    assert n >= 1024000 * 4 * 128 * 2 and n < 1024000 * 4 * 128 * 2 + (1 << 20)
+    # units list + Q [H, total_C, d] bf16 + an lse scratch [total_C, H] fp32 (self-key merge)
+    base = 1024000 * 4 * 128 * 2 + 1024000 * 4 * 4
+    assert n >= base and n < base + (1 << 20)
     assert gb.tasa_workspace_bytes(-1, 10, 4, 128) == 0
     assert gb.tasa_workspace_bytes(1, 10, 4, 100) == 0
     # split-L partials: [s, C, H] (m, l) + [s, C, H, d] fp32 on top of the unsplit workspace

@@ -362,6 +362,29 @@ def test_cuda_graph_capture_identical(name):
     assert torch.equal(bufs.O, O_ref) and torch.equal(bufs.counts, c_ref)
 
 
+@pytest.mark.parametrize("d,H,D_in", [(128, 2, 256), (64, 2, 128), (32, 1, 64)])
+def test_self_key_parity(d, H, D_in):
+    # gesr_tasa_score_self: the candidate also attends to its own key (SPEC.md's mask diagonal)
+    # vs the brute-force oracle over the full [U; T] mask with self_key=True; L_b = 0 included
+    Ls, Cs = [0, 1, 130, 300, 7], [3, 5, 140, 129, 2]
+    bt = _custom(Ls, Cs, H=H, d=d, D_in=D_in, cfg_id=500 + d)
+    g = bt.to(_cuda())
+    K, V = gb.kv_project(g.U, g.W_k, g.W_v, H, d, 1)
+    Ks, Vs = gb.kv_project(g.T, g.W_k, g.W_v, H, d, 1)
+    for odt in (torch.float32, torch.bfloat16):
+        O, lse = gb.tasa_score(g.T, g.cand_offsets, g.W_q, K, V, g.seq_offsets, H, d, 1,
+                               out_dtype=odt, K_self=Ks, V_self=Vs)
+        torch.cuda.synchronize()
+        O, lse = O.float().cpu().numpy(), lse.cpu().numpy()
+        so, co = bt.seq_offsets.numpy(), bt.cand_offsets.numpy()
+        for b in range(len(Ls)):
+            O_or, lse_or = oracle.full_masked_attention(bt.U[so[b]:so[b + 1]], bt.T[co[b]:co[b + 1]],
+                                                        bt.W_q, bt.W_k, bt.W_v, H, d,
+                                                        self_key=True)
+            _attn_tol(O[co[b]:co[b + 1]], O_or, f"self key d={d} request {b}")
+            assert np.abs(lse[co[b]:co[b + 1]] - lse_or).max() < 2e-2
+
+
 def test_one_cta_kernel_d128_subprocess():
     # d = 128 runs the CTA-pair kernel by default; the 1-CTA kernel (GESR_ATTN_PAIR=0, read once
     # per process) keeps its own parity check on ragged shapes and bf16 output
