@@ -171,6 +171,26 @@ gesr_status gesr_hma_count(const int64_t* user_ids, const int64_t* user_offsets,
                            int32_t cap, int32_t* counts,
                            void* stream);
 
+/* gesr_hma_count_embed -- gesr_hma_count fused with the HMA offset-embedding lookup
+ * (PAPER.md:314-318 s3.4.1 "e = E(c + o*M)"): for candidate t and field
+ * (feature pair) f, with c = min(count, M),
+ *   emb[t][f*D_h .. (f+1)*D_h) = E[c + f*(M+1)][0 .. D_h)
+ * i.e. Concat(e_1, ..., e_F), the input of T_match = MLP(Concat(...)) (the MLP is
+ * a dense layer outside this call).  The row stride is M+1, not the paper's literal M: c takes
+ * M+1 values 0..M, so stride M would make c = M of pair f collide with c = 0 of pair f+1
+ * (reading R14).
+ *   M          cap, >= 1 (the offset needs a bounded count).
+ *   counts     int32 [total_C, F] capped counts (written, as gesr_hma_count with cap = M).
+ *   E          bf16 [F*(M+1), D_h] embedding table; D_h a multiple of 8 in [8, 4096].
+ *   emb        bf16 [total_C, F*D_h] (written).  E and emb 16-byte aligned.
+ * Bit-exact (a gather of table rows).  Other arguments and errors as gesr_hma_count. */
+gesr_status gesr_hma_count_embed(const int64_t* user_ids, const int64_t* user_offsets,
+                                 const int64_t* item_ids, const int64_t* item_offsets,
+                                 const int64_t* cand_offsets, int64_t B, int64_t total_C,
+                                 int32_t F, int32_t M, int32_t* counts,
+                                 const void* E, int32_t D_h, void* emb,
+                                 void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -16,6 +16,9 @@ blocking/fusion), each citing the passage it follows:
 * :func:`build_mask` -- the mask itself.  PAPER.md:341.
 * :func:`hma_count` / :func:`hma_count_hash` -- HMA raw (optionally capped) match counts, two
   independent algorithms.  PAPER.md:308-312 (s3.4.1).
+* :func:`offset_index` / :func:`hma_offset_embed` -- HMA embedding with feature-pair offsets,
+  e = E(c + o(M+1)), concatenated over pairs.
+  (stride M+1: DESIGN.md reading R14).  Plain numpy.
 
 Parity pins: see tests/test_oracle_*.py.  Every function here is pinned.
 """
@@ -252,3 +255,30 @@ def hma_count_hash(user_ids, user_offsets, item_ids, item_offsets, cand_offsets,
                               _p(io, _c_i64p), _p(co, _c_i64p), B, total_C, F, cap,
                               _p(counts, _c_i32p))
     return counts
+
+
+def offset_index(c: int, o: int, M: int) -> int:
+    """Row of the offset-encoded embedding table for count c of feature pair o.
+
+    PAPER.md:314-316 writes e = E(c + o*M); c = min(count, M) takes the M+1 values 0..M, so the
+    stride is M+1 (reading R14): rows of distinct pairs never collide.
+    """
+    if not (0 <= c <= M):
+        raise ValueError(f"count {c} outside [0, {M}]")
+    return c + o * (M + 1)
+
+
+def hma_offset_embed(counts, E, M: int) -> np.ndarray:
+    """Concat(e_1, ..., e_F) per candidate: [total_C, F*D_h] from capped
+    counts [total_C, F] and the table E [F*(M+1), D_h], one lookup per (candidate, pair)."""
+    counts = np.asarray(counts)
+    E = np.asarray(E)
+    total_C, F = counts.shape
+    D_h = E.shape[1]
+    assert E.shape[0] == F * (M + 1)
+    out = np.zeros((total_C, F * D_h), E.dtype)
+    for t in range(total_C):
+        for o in range(F):
+            out[t, o * D_h:(o + 1) * D_h] = E[offset_index(int(counts[t, o]), o, M)]
+    return out
+

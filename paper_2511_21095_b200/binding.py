@@ -70,6 +70,9 @@ def lib():
                                        _i32, _vp, _vp, ctypes.c_size_t, _vp]
     L.gesr_hma_count.restype = ctypes.c_int
     L.gesr_hma_count.argtypes = [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _i32, _i32, _vp, _vp]
+    L.gesr_hma_count_embed.restype = ctypes.c_int
+    L.gesr_hma_count_embed.argtypes = [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _i32, _i32, _vp, _vp,
+                                       _i32, _vp, _vp]
     _lib = L
     return L
 
@@ -179,6 +182,24 @@ def hma_count(user_ids, user_offsets, item_ids, item_offsets, cand_offsets, F: i
                                 _ptr(item_offsets), _ptr(cand_offsets), B, total_C, F, cap,
                                 _ptr(counts), _stream(stream)))
     return counts
+
+
+def hma_count_embed(user_ids, user_offsets, item_ids, item_offsets, cand_offsets, F: int, M: int,
+                    E, counts=None, emb=None, stream=None):
+    """(counts int32 [total_C, F] capped at M, emb bf16 [total_C, F*D_h]) with
+    emb[t][f] = E[min(c, M) + f (M+1)] (gesr_hma_count_embed; E bf16 [F (M+1), D_h])."""
+    _dev(user_ids, user_offsets, item_ids, item_offsets, cand_offsets, counts, E, emb)
+    B = cand_offsets.numel() - 1
+    total_C = (item_offsets.numel() - 1) // F if F > 0 else 0
+    D_h = E.shape[1]
+    if counts is None:
+        counts = torch.empty((total_C, F), dtype=torch.int32, device=cand_offsets.device)
+    if emb is None:
+        emb = torch.empty((total_C, F * D_h), dtype=torch.bfloat16, device=cand_offsets.device)
+    _check(lib().gesr_hma_count_embed(_ptr(user_ids), _ptr(user_offsets), _ptr(item_ids),
+                                      _ptr(item_offsets), _ptr(cand_offsets), B, total_C, F, M,
+                                      _ptr(counts), _ptr(E), D_h, _ptr(emb), _stream(stream)))
+    return counts, emb
 
 
 class StepBuffers:

@@ -426,14 +426,22 @@ gesr_status gesr_tasa_score_self(const void* T, int64_t total_C, int32_t D_in,
                    o_dtype, lse, workspace, workspace_bytes, stream);
 }
 
-gesr_status gesr_hma_count(const int64_t* user_ids, const int64_t* user_offsets,
+static gesr_status hma_impl(const int64_t* user_ids, const int64_t* user_offsets,
                            const int64_t* item_ids, const int64_t* item_offsets,
                            const int64_t* cand_offsets, int64_t B, int64_t total_C, int32_t F,
-                           int32_t cap, int32_t* counts, void* stream) {
+                           int32_t cap, int32_t* counts, const void* E, int32_t D_h, void* emb,
+                           void* stream) {
   if (B < 0 || total_C < 0 || F < 0)
     return fail(GESR_ERR_INVALID_ARG, "B, total_C, F must be >= 0");
   if (F > 256) return fail(GESR_ERR_INVALID_ARG, "F=%d > 256 fields", F);
   if (B > 2147483647LL) return fail(GESR_ERR_INVALID_ARG, "B too large");
+  if (E != nullptr) {
+    if (cap < 1) return fail(GESR_ERR_INVALID_ARG, "the offset embedding needs cap M >= 1");
+    if (D_h < 8 || D_h % 8 != 0 || D_h > 4096)
+      return fail(GESR_ERR_INVALID_ARG, "D_h=%d must be a multiple of 8 in [8, 4096]", D_h);
+    if (!emb) return fail(GESR_ERR_INVALID_ARG, "null embedding output");
+    if (!aligned16(E) || !aligned16(emb)) return fail(GESR_ERR_INVALID_ARG, "misaligned pointer");
+  }
   if (B == 0 || total_C == 0 || F == 0) return GESR_OK;
   if (!user_offsets || !item_offsets || !cand_offsets || !counts)
     return fail(GESR_ERR_INVALID_ARG, "null required pointer");
@@ -453,8 +461,29 @@ gesr_status gesr_hma_count(const int64_t* user_ids, const int64_t* user_offsets,
   p.F = F;
   p.cap = cap;
   p.counts = counts;
+  p.E = static_cast<const uint4*>(E);
+  p.dh_chunks = E ? D_h / 8 : 0;
+  p.emb = static_cast<uint4*>(emb);
   cudaError_t e = gesr::launch_hma(p, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? GESR_OK : cuda_fail(e, "hma_kernel launch");
+}
+
+gesr_status gesr_hma_count(const int64_t* user_ids, const int64_t* user_offsets,
+                           const int64_t* item_ids, const int64_t* item_offsets,
+                           const int64_t* cand_offsets, int64_t B, int64_t total_C, int32_t F,
+                           int32_t cap, int32_t* counts, void* stream) {
+  return hma_impl(user_ids, user_offsets, item_ids, item_offsets, cand_offsets, B, total_C, F,
+                  cap, counts, nullptr, 0, nullptr, stream);
+}
+
+gesr_status gesr_hma_count_embed(const int64_t* user_ids, const int64_t* user_offsets,
+                                 const int64_t* item_ids, const int64_t* item_offsets,
+                                 const int64_t* cand_offsets, int64_t B, int64_t total_C,
+                                 int32_t F, int32_t M, int32_t* counts, const void* E,
+                                 int32_t D_h, void* emb, void* stream) {
+  if (!E) return fail(GESR_ERR_INVALID_ARG, "null embedding table");
+  return hma_impl(user_ids, user_offsets, item_ids, item_offsets, cand_offsets, B, total_C, F, M,
+                  counts, E, D_h, emb, stream);
 }
 
 }  // extern "C"

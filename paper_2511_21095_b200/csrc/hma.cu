@@ -239,6 +239,15 @@ __global__ void __launch_bounds__(kThreads, 2)
         int c = s.warp_cnt[warp][lane];
         if (p.cap > 0 && c > p.cap) c = p.cap;
         p.counts[g + lane] = c;
+        if (p.E != nullptr) {
+          // offset embedding (stride cap + 1: DESIGN.md R14): segment
+          // g + lane = (candidate t, field f) owns out[t][f D_h, (f + 1) D_h) -- contiguous
+          const int f = static_cast<int>(g - seg_begin + lane) % F;
+          const int64_t rowE = static_cast<int64_t>(c) + static_cast<int64_t>(f) * (p.cap + 1);
+          const uint4* src = p.E + rowE * p.dh_chunks;
+          uint4* dst = p.emb + (g + lane) * p.dh_chunks;
+          for (int q = 0; q < p.dh_chunks; ++q) dst[q] = __ldg(src + q);
+        }
       }
       s.warp_cnt[warp][lane] = 0;
       __syncwarp();

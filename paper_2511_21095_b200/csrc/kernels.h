@@ -86,6 +86,10 @@ struct HmaParams {
   int F;
   int cap;
   int32_t* counts;
+  // optional offset embedding: emb[t][f] = E[min(c, cap) + f (cap + 1)], D_h bf16
+  const uint4* E;          // [F (cap + 1), D_h] bf16 rows, 16-byte chunks; null = counts only
+  int dh_chunks;           // D_h / 8
+  uint4* emb;              // [total_C, F D_h] bf16
 };
 
 cudaError_t launch_hma(const HmaParams& p, cudaStream_t stream);

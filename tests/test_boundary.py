@@ -137,3 +137,15 @@ def test_binding_rejects_cpu_tensors(L):
     U = torch.zeros(4, 64, dtype=torch.bfloat16)
     with pytest.raises(gb.GesrError):
         gb.kv_project(U, U, U, 1, 64)
+
+
+def test_hma_embed_validation(L):
+    def emb(E=FAKE, M=16, D_h=8, out=FAKE):
+        return L.gesr_hma_count_embed(FAKE, FAKE, FAKE, FAKE, FAKE, 2, 5, 3, M, FAKE, E, D_h, out,
+                                      None)
+    assert emb(E=None) == gb.GESR_ERR_INVALID_ARG
+    assert emb(M=0) == gb.GESR_ERR_INVALID_ARG
+    assert emb(D_h=12) == gb.GESR_ERR_INVALID_ARG
+    assert emb(out=None) == gb.GESR_ERR_INVALID_ARG
+    assert emb(out=MIS) == gb.GESR_ERR_INVALID_ARG
+

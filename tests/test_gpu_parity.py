@@ -454,6 +454,28 @@ def test_hma_edge_ids_and_empty():
     assert want[0, 0] == 2   # sentinel-valued ID counted
 
 
+@pytest.mark.parametrize("name,M,D_h", [("2", 16, 8), ("3", 4, 64), ("1", 1, 16)])
+def test_hma_offset_embed_exact(name, M, D_h):
+    # fused counting + offset-embedding gather: counts and the concatenated rows
+    # bit-exact against the oracle's counts (cap M) and its plain-numpy gather
+    cfg = configs.get(name)
+    if cfg.B > 64:
+        cfg = cfg.with_(B=64)
+    bt = inputs.make_batch(cfg, attention=False)
+    g = torch.Generator().manual_seed(11)
+    E = torch.randn(cfg.F * (M + 1), D_h, generator=g).to(torch.bfloat16)
+    dev = _cuda()
+    c, e = gb.hma_count_embed(bt.user_ids.to(dev), bt.user_offsets.to(dev), bt.item_ids.to(dev),
+                              bt.item_offsets.to(dev), bt.cand_offsets.to(dev), cfg.F, M,
+                              E.to(dev))
+    torch.cuda.synchronize()
+    want_c = oracle.hma_count(bt.user_ids, bt.user_offsets, bt.item_ids, bt.item_offsets,
+                              bt.cand_offsets, cfg.F, M)
+    assert np.array_equal(c.cpu().numpy(), want_c)
+    want_e = oracle.hma_offset_embed(want_c, E.view(torch.int16).numpy(), M)
+    assert np.array_equal(e.view(torch.int16).cpu().numpy(), want_e)
+
+
 def test_hma_headline_subset():
     cfg = configs.get("3h")
     sub = list(range(0, 1024, 97))

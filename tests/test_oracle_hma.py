@@ -173,3 +173,46 @@ def test_generator_lists_are_duplicate_free_and_counts_spread():
     c2 = _python_counts(ui, uo, ii, io, bt.cand_offsets.numpy(), F, 0)
     np.testing.assert_array_equal(c, c2)
     assert c.max() >= 4 and (c == 0).any()
+
+
+# ---------------------------------------------------------------- offset embedding (f2)
+
+def _offset_examples():
+    path = os.path.join(os.path.dirname(__file__), "golden", "hma_offset_examples.txt")
+    rows = []
+    for ln in open(path):
+        if ln.startswith("#") or not ln.strip():
+            continue
+        c, o, M, want, _ = [x.strip() for x in ln.split("|")]
+        rows.append((int(c), int(o), int(M), int(want)))
+    return rows
+
+
+def test_offset_index_spec_examples():
+    for c, o, M, want in _offset_examples():
+        assert oracle.offset_index(c, o, M) == want
+
+
+def test_offset_index_exhaustive_collision_free():
+    # SPEC.md:232 "exhaustive (c,o) grid for P=3, M=4 -> all indices distinct and in range"
+    P, M = 3, 4
+    idx = [oracle.offset_index(c, o, M) for o in range(P) for c in range(M + 1)]
+    assert sorted(idx) == list(range(P * (M + 1)))
+    with pytest.raises(ValueError):
+        oracle.offset_index(M + 1, 0, M)
+
+
+def test_offset_embed_against_one_hot_matmul():
+    # the gather equals the one-hot row selection onehot(c + o (M+1)) @ E, built here from the
+    # counts without offset_index; pair order is the concatenation order
+    rng = np.random.default_rng(7)
+    F, M, D_h, C = 3, 5, 8, 11
+    counts = rng.integers(0, M + 1, size=(C, F))
+    E = rng.standard_normal((F * (M + 1), D_h))
+    got = oracle.hma_offset_embed(counts, E, M)
+    for t in range(C):
+        for o in range(F):
+            onehot = np.zeros(F * (M + 1))
+            onehot[o * (M + 1) + counts[t, o]] = 1.0
+            assert np.array_equal(got[t, o * D_h:(o + 1) * D_h], onehot @ E)
+
