@@ -101,18 +101,6 @@ __device__ __forceinline__ uint64_t v_desc(uint32_t base, int ks) {
   return make_sdesc(base + ks * 16 * C::kRowBytes, C::kBoxBytes, C::kSBO, C::kLayout);
 }
 
-// Packed fp32x2 arithmetic (sm_100 FFMA2 / FADD2: two lanes' worth of FP32 work per issue slot).
-__device__ __forceinline__ void ffma2(float& d0, float& d1, float a0, float a1, float b0, float b1,
-                                      float c0, float c1) {
-  asm("{\n .reg .b64 a, b, c, d;\n mov.b64 a, {%2, %3};\n mov.b64 b, {%4, %5};\n"
-      " mov.b64 c, {%6, %7};\n fma.rn.f32x2 d, a, b, c;\n mov.b64 {%0, %1}, d;\n}"
-      : "=f"(d0), "=f"(d1) : "f"(a0), "f"(a1), "f"(b0), "f"(b1), "f"(c0), "f"(c1));
-}
-__device__ __forceinline__ void fadd2(float& d0, float& d1, float a0, float a1, float b0, float b1) {
-  asm("{\n .reg .b64 a, b, d;\n mov.b64 a, {%2, %3};\n mov.b64 b, {%4, %5};\n"
-      " add.rn.f32x2 d, a, b;\n mov.b64 {%0, %1}, d;\n}"
-      : "=f"(d0), "=f"(d1) : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
-}
 
 // 2^x for a pair on the FMA/ALU pipes (FA4-style MUFU offload): round-to-nearest split
 // x = j + f (f in [-0.5, 0.5]) with the 1.5*2^23 magic-number add, degree-3 polynomial for 2^f

@@ -122,27 +122,11 @@ constexpr uint32_t kTS = 0;          // S: one buffer, alternately A's and B's t
 constexpr uint32_t kTP = 128;        // P_A at 128, P_B at 192 (bf16 pairs, 64 columns each)
 constexpr uint32_t kTO = 256;        // O of even units at 256, of odd units at 384
 
-__device__ __forceinline__ void ffma2(float& d0, float& d1, float a0, float a1, float b0, float b1,
-                                      float c0, float c1) {
-  asm("{\n .reg .b64 a, b, c, d;\n mov.b64 a, {%2, %3};\n mov.b64 b, {%4, %5};\n"
-      " mov.b64 c, {%6, %7};\n fma.rn.f32x2 d, a, b, c;\n mov.b64 {%0, %1}, d;\n}"
-      : "=f"(d0), "=f"(d1) : "f"(a0), "f"(a1), "f"(b0), "f"(b1), "f"(c0), "f"(c1));
-}
-__device__ __forceinline__ void fmul2(float& d0, float& d1, float a0, float a1, float b0, float b1) {
-  asm("{\n .reg .b64 a, b, d;\n mov.b64 a, {%2, %3};\n mov.b64 b, {%4, %5};\n"
-      " mul.rn.f32x2 d, a, b;\n mov.b64 {%0, %1}, d;\n}"
-      : "=f"(d0), "=f"(d1) : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
-}
 // 2^x for a pair on the FMA pipe only (no MUFU, no min/max): x clamped to [-126, 126] with a
 // saturating FFMA, split x = j + f with the 1.5*2^23 magic add, degree-3 polynomial for 2^f on
 // [-0.5, 0.5] (max rel. error 2.1e-4, below the bf16 rounding of P), exponent added with an
 // IMAD.  Used for one pair in GESR_PAIR_POLY_EVERY on full tiles.
 __device__ __forceinline__ void exp2_fma2(float& y0, float& y1, float x0, float x1);
-__device__ __forceinline__ void fadd2(float& d0, float& d1, float a0, float a1, float b0, float b1) {
-  asm("{\n .reg .b64 a, b, d;\n mov.b64 a, {%2, %3};\n mov.b64 b, {%4, %5};\n"
-      " add.rn.f32x2 d, a, b;\n mov.b64 {%0, %1}, d;\n}"
-      : "=f"(d0), "=f"(d1) : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
-}
 
 __device__ __forceinline__ void exp2_fma2(float& y0, float& y1, float x0, float x1) {
   float u0, u1;

@@ -18,6 +18,7 @@ struct ProjParams {
   int act;            // 0 identity, 1 SiLU
   int num_m_blocks;
   int num_n_blocks;
+  int m_major;        // set by launch_proj: tile order (see ProjTiles in proj.cu)
   const float* bias0;
   const float* bias1;
   __nv_bfloat16* out0;   // [H, M, d]

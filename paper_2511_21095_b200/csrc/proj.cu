@@ -16,12 +16,18 @@
 //             K=16, into a double-buffered TMEM accumulator (2*BN columns in each CTA);
 //             commits multicast to both CTAs' barriers.
 //   warp 2    TMEM allocator (cta_group::2).
-//   warps 4-11 epilogue (both CTAs): tcgen05.ld 32x32b (thread = output row), release of the
-//             accumulator (one arrival per CTA on the leader's TMEM-empty barrier), bias + act
-//             in fp32, RNE to bf16, swizzled 16-byte smem stores, TMA tensor stores into the
-//             head-major [H, M, d] output.  (Direct per-thread 16-byte global stores touched
-//             32 rows per instruction and capped the kernel at ~35% tensor-pipe.)
-// The epilogue of tile i overlaps the MMAs of tile i+1.
+//   warps 4-19 epilogue (both CTAs): tcgen05.ld 32x32b (thread = output row), bias + act in
+//             fp32 (packed FFMA2 SiLU, one MUFU op per element), RNE to bf16, swizzled 16-byte
+//             st.shared into a per-warp staging box, TMA tensor stores into the head-major
+//             [H, M, d] output; each warp releases its share of the accumulator with its own
+//             arrival on the leader's TMEM-empty barrier (no CTA-wide barrier: the slowest
+//             warp no longer holds the others).  (Direct per-thread 16-byte global stores
+//             touched 32 rows per instruction and capped the kernel at ~35% tensor-pipe.)
+// The epilogue of tile i overlaps the MMAs of tile i+1.  Tile order is m-major for large M
+// (ProjTiles): a pair takes all n-blocks of one 256-row block back to back, so X is read from
+// HBM exactly once (ncu: 2.16 GB DRAM reads for the 2.15 GB U, against 3.0 GB interleaved).
+#include <cstdlib>
+
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -37,14 +43,15 @@ constexpr int kBK = 64;              // 64 bf16 = 128 bytes = one 128B-swizzle r
 constexpr int kEpiWarps = 16;        // 4 per SM sub-partition: latency hiding by TLP
 constexpr int kThreads = (4 + kEpiWarps) * 32;
 constexpr uint32_t kABytes = kBM * kBK * 2;   // 16 KB
+constexpr int kBoxes = 1;   // staging boxes per epilogue warp (2 measured slower: one fewer stage)
 
 template <int BN>
 struct ProjSmem {
   static constexpr uint32_t kBBytes = (BN / 2) * kBK * 2;
   static constexpr uint32_t kStageBytes = kABytes + kBBytes;
-  // epilogue staging: one 2 KB box (32 rows x 32 columns, 64B swizzle) per epilogue warp
+  // epilogue staging: kBoxes 2 KB boxes (32 rows x 32 columns, 64B swizzle) per epilogue warp
   static constexpr int kChunks = BN / 32;
-  static constexpr uint32_t kStagingBytes = kEpiWarps * 2048;
+  static constexpr uint32_t kStagingBytes = kEpiWarps * 2048 * kBoxes;
   static constexpr int kStages = (224 * 1024 - kStagingBytes) / kStageBytes > 8
                                      ? 8 : (224 * 1024 - kStagingBytes) / kStageBytes;
   static constexpr uint32_t kTmemCols = (2 * BN) < 32 ? 32 : 2 * BN;
@@ -54,18 +61,66 @@ struct ProjSmem {
   static_assert(kBytes <= 232448, "shared memory budget");
 };
 
-// SiLU(x) = x / (1 + 2^(-x log2 e)) with ONE MUFU op per element: exp2 on the MUFU pipe, the
-// reciprocal on the FMA pipe (bit-trick seed, two Newton steps: rel. error < 2.5e-4, far
-// below the bf16 rounding of the result).  The exponent is clamped at 126 so y stays finite:
-// x < -87 gives |result| < 2^-119 (true value smaller still); x -> +inf: y = 1, result x.  (Two MUFU ops per element made the epilogue MUFU-bound at
-// exactly the MMA time per tile.)
-__device__ __forceinline__ float silu_fast(float x) {
-  const float y = 1.0f + ex2(fminf(x * -1.4426950408889634f, 126.0f));   // keep y finite
-  float r = __int_as_float(0x7EF311C7 - __float_as_int(y));
-  r = r * fmaf(-y, r, 2.0f);
-  r = r * fmaf(-y, r, 2.0f);
-  return x * r;
+// SiLU(x) = x / (1 + 2^(-x log2 e)) for a PAIR of values, with ONE MUFU op per element and the
+// rest as packed fp32x2 FMA-pipe work (FFMA2/FMUL2/FADD2: half the issue slots of scalar code;
+// the epilogue is issue-bound at the MMA time per tile).  The exponent z = -x log2 e is clamped
+// to [-126, 126] by a saturating FFMA (u = sat(x * -log2e/252 + 1/2), z = 252u - 126; no FMNMX,
+// which slows a concurrent MUFU stream) so y = 1 + 2^z stays finite; x < -87 then gives
+// |result| < 2^-119 (true value smaller still) and large x gives x.  1/y: bit-trick seed and two
+// Newton steps on the FMA pipe (rel. error < 2.5e-4, far below the bf16 rounding of the result;
+// a MUFU reciprocal made the epilogue MUFU-bound at exactly the MMA time per tile).
+__device__ __forceinline__ void silu2(float& x0, float& x1) {
+  constexpr float kC = -1.4426950408889634f / 252.0f;
+  float u0, u1;
+  asm("fma.rn.sat.f32 %0, %1, %2, %3;" : "=f"(u0) : "f"(x0), "f"(kC), "f"(0.5f));
+  asm("fma.rn.sat.f32 %0, %1, %2, %3;" : "=f"(u1) : "f"(x1), "f"(kC), "f"(0.5f));
+  float z0, z1;
+  ffma2(z0, z1, u0, u1, 252.0f, 252.0f, -126.0f, -126.0f);
+  const float e0 = ex2(z0), e1 = ex2(z1);
+  float ny0, ny1;                                  // -y = -(1 + e)
+  ffma2(ny0, ny1, e0, e1, -1.0f, -1.0f, -1.0f, -1.0f);
+  // seed 1/y = 0x7EF311C7 - bits(y), and bits(-y) = bits(y) + 2^31
+  float r0 = __uint_as_float(0xFEF311C7u - __float_as_uint(ny0));
+  float r1 = __uint_as_float(0xFEF311C7u - __float_as_uint(ny1));
+  float t0, t1;
+#pragma unroll
+  for (int it = 0; it < 2; ++it) {                 // r <- r (2 - y r)
+    ffma2(t0, t1, ny0, ny1, r0, r1, 2.0f, 2.0f);
+    fmul2(r0, r1, r0, r1, t0, t1);
+  }
+  fmul2(x0, x1, x0, x1, r0, r1);
 }
+
+// Tile order of one pair.  m-major (large M): the pair walks all n-blocks of its 256-row block
+// back to back, so the X rows are fetched from HBM once and re-read from L2 while hot;
+// interleaved (few row blocks): tiles dealt round-robin so every pair has work.
+struct ProjTiles {
+  int pair, npairs, nm, nn;
+  bool m_major;
+  __device__ __forceinline__ int count() const {
+    if (m_major) return pair < nm ? ((nm - 1 - pair) / npairs + 1) * nn : 0;
+    const int tiles = nm * nn;
+    return pair < tiles ? (tiles - 1 - pair) / npairs + 1 : 0;
+  }
+};
+// Walks one pair's tiles in ProjTiles order without a division per step.
+struct TileCursor {
+  int m, n, dm, dn, nn, npairs;
+  bool m_major;
+  __device__ __forceinline__ explicit TileCursor(const ProjTiles& t)
+      : nn(t.nn), npairs(t.npairs), m_major(t.m_major) {
+    if (m_major) { m = t.pair; n = 0; dm = 0; dn = 1; }
+    else { m = t.pair / t.nn; n = t.pair % t.nn; dm = t.npairs / t.nn; dn = t.npairs % t.nn; }
+  }
+  __device__ __forceinline__ void next() {
+    if (m_major) {
+      if (++n == nn) { n = 0; m += npairs; }
+    } else {
+      n += dn; m += dm;
+      if (n >= nn) { n -= nn; ++m; }
+    }
+  }
+};
 
 template <int BN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
@@ -87,7 +142,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const uint32_t rank = cluster_ctarank();          // 0 = leader of the pair
   const int pair = blockIdx.x >> 1;
   const int npairs = gridDim.x >> 1;
-  const int num_tiles = p.num_m_blocks * p.num_n_blocks;   // 256-row blocks x BN blocks
+  const ProjTiles tiles{pair, npairs, p.num_m_blocks, p.num_n_blocks, p.m_major != 0};
+  const int my_tiles = tiles.count();
   const int num_kb = (p.K + kBK - 1) / kBK;
 
   if (warp == 0 && lane == 0) {
@@ -100,7 +156,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull_bar[b], 1);
-      mbar_init(&tempty_bar[b], 2);     // one arrival per CTA of the pair
+      mbar_init(&tempty_bar[b], 2 * kEpiWarps);   // one arrival per epilogue warp of the pair
     }
     fence_mbar_init();
   }
@@ -118,9 +174,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       // ---------------- TMA producer (both CTAs)
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = pair; tile < num_tiles; tile += npairs) {
-        const int m_blk = tile / p.num_n_blocks;
-        const int n_blk = tile % p.num_n_blocks;
+      TileCursor cur(tiles);
+      for (int i = 0; i < my_tiles; ++i, cur.next()) {
+        const int m_blk = cur.m, n_blk = cur.n;
         const int n0 = n_blk * BN;
         // B comes from map_b0 for columns < n_split, else map_b1 (W_k / W_v stacked along N)
         const CUtensorMap* mb = (n0 < p.n_split) ? &map_b0 : &map_b1;
@@ -144,7 +200,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
-      for (int tile = pair; tile < num_tiles; tile += npairs, ++local) {
+      for (; local < my_tiles; ++local) {
         const uint32_t buf = local & 1;
         const uint32_t aphase = (local >> 1) & 1;
         mbar_wait_sleep(&tempty_bar[buf], aphase ^ 1);
@@ -181,30 +237,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     constexpr int kPer = S::kChunks >= 4 ? S::kChunks / 4 : 1;
     const int c_begin = part * kPer;
     const int c_end = c_begin + kPer <= S::kChunks ? c_begin + kPer : S::kChunks;
-    uint8_t* box = smem + S::kStagingOffset + (warp - 4) * 2048;
+    const uint32_t box_base = smem_u32(smem + S::kStagingOffset + (warp - 4) * 2048 * kBoxes);
+    uint32_t bi = 0;
     const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty_bar[0]), 0);
     const uint32_t tempty_leader1 = mapa_shared(smem_u32(&tempty_bar[1]), 0);
     int local = 0;
-    for (int tile = pair; tile < num_tiles; tile += npairs, ++local) {
-      const int m_blk = tile / p.num_n_blocks;
-      const int n_blk = tile % p.num_n_blocks;
+    const int dshift = __ffs(p.d) - 1;              // d is 32, 64 or 128
+    TileCursor cur(tiles);
+    for (; local < my_tiles; ++local, cur.next()) {
+      const int m_blk = cur.m, n_blk = cur.n;
       const uint32_t buf = local & 1;
       const uint32_t aphase = (local >> 1) & 1;
       const int row0 = m_blk * 2 * kBM + static_cast<int>(rank) * kBM + static_cast<int>(sub) * 32;
       mbar_wait_sleep(&tfull_bar[buf], aphase);
       tc_fence_after();
+      const uint32_t tm_row = tmem_base + ((sub * 32) << 16) + buf * BN;
 #pragma unroll 1
       for (int c = c_begin; c < c_end; ++c) {
         uint32_t r[32];
-        tmem_ld32(tmem_base + ((sub * 32) << 16) + buf * BN + c * 32, r);
-        tmem_ld_wait();
+        tmem_ld32(tm_row + c * 32, r);
+        tmem_ld_wait_regs32(r);
+        float v[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
         const int n0 = n_blk * BN + c * 32;   // chunk lies within one head (d >= 32)
         const int which = n0 >= p.n_split ? 1 : 0;
         const int within = n0 - which * p.n_split;
         const float* bias = which ? p.bias1 : p.bias0;
-        float v[32];
-#pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
         if (bias != nullptr) {
           const float4* b4 = reinterpret_cast<const float4*>(bias + within);
 #pragma unroll
@@ -215,32 +274,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         if (p.act == 1) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = silu_fast(v[i]);
+          for (int i = 0; i < 32; i += 2) silu2(v[i], v[i + 1]);
         }
         uint32_t packed[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) packed[i] = pack_bf16x2(v[2 * i], v[2 * i + 1]);
-        // the staging box must have been read by this warp's previous TMA store
-        if (lane == 0) bulk_wait_group_read<0>();
+        // the staging box must have been read by this warp's TMA store kBoxes chunks ago
+        if (lane == 0) bulk_wait_group_read<kBoxes - 1>();
         __syncwarp();
+        const uint32_t box_s = box_base + (kBoxes > 1 ? (bi & 1) * 2048 : 0);
+        uint8_t* box = smem + S::kStagingOffset + (warp - 4) * 2048 * kBoxes +
+                       (kBoxes > 1 ? (bi & 1) * 2048 : 0);
+        ++bi;
         // 64B swizzle: 16-byte chunk q of row `lane` goes to slot q ^ ((lane >> 1) & 3)
-        uint8_t* rowp = box + lane * 64;
+        const uint32_t rowp = box_s + lane * 64;
 #pragma unroll
         for (int q = 0; q < 4; ++q)
-          *reinterpret_cast<uint4*>(rowp + ((q ^ ((lane >> 1) & 3)) << 4)) =
-              make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
+          st_shared_v4(rowp + ((q ^ ((lane >> 1) & 3)) << 4), packed[4 * q], packed[4 * q + 1],
+                       packed[4 * q + 2], packed[4 * q + 3]);
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-          const int h = within / p.d;
-          tma_store_3d(which ? &map_o1 : &map_o0, box, within - h * p.d, row0, h);
+          const int h = within >> dshift;
+          tma_store_3d(which ? &map_o1 : &map_o0, box, within - (h << dshift), row0, h);
           bulk_commit_group();
         }
       }
-      // accumulator drained by all 16 warps: one arrival per CTA on the leader's barrier
+      // this warp's part of the accumulator is drained
       tc_fence_before();
-      named_bar_sync(1, kEpiWarps * 32);
-      if (warp == 4 && lane == 0) mbar_arrive_cluster_relaxed(buf ? tempty_leader1 : tempty_leader0);
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster_relaxed(buf ? tempty_leader1 : tempty_leader0);
     }
     if (lane == 0) bulk_wait_group<0>();
   }
@@ -265,9 +328,14 @@ cudaError_t launch_bn(const CUtensorMap& ma, const CUtensorMap& mb0, const CUten
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
-  const int tiles = p.num_m_blocks * p.num_n_blocks;
-  const int pairs = tiles < num_sms / 2 ? tiles : num_sms / 2;
-  proj_kernel<BN><<<2 * pairs, kThreads, S::kBytes, stream>>>(ma, mb0, mb1, mo0, mo1, p);
+  ProjParams q = p;
+  q.m_major = p.num_m_blocks >= num_sms / 2 ? 1 : 0;
+  static const char* order_env = getenv("GESR_PROJ_ORDER");   // A/B override: 0 / 1
+  if (order_env != nullptr && (order_env[0] == '0' || order_env[0] == '1'))
+    q.m_major = order_env[0] - '0';
+  const int work = q.m_major ? p.num_m_blocks : p.num_m_blocks * p.num_n_blocks;
+  const int pairs = work < num_sms / 2 ? work : num_sms / 2;
+  proj_kernel<BN><<<2 * pairs, kThreads, S::kBytes, stream>>>(ma, mb0, mb1, mo0, mo1, q);
   return cudaGetLastError();
 }
 

@@ -56,12 +56,18 @@ def main():
                                       bt.item_offsets, bt.cand_offsets, cfg.F, 0,
                                       counts=bufs.counts), args.iters)
     step = timeit(lambda: gb.score_step(bt, bufs, chunk=cfg.chunk), args.iters)
+
+    def serial():   # the three calls back to back on one stream (no overlap)
+        gb.hma_count(bt.user_ids, bt.user_offsets, bt.item_ids, bt.item_offsets,
+                     bt.cand_offsets, cfg.F, 0, counts=bufs.counts)
+        gb.score_step(bt, bufs, chunk=cfg.chunk, hma=False)
+    step_serial = timeit(serial, args.iters)
     print(json.dumps({
         "config": args.config, "kv_ms": kv, "kv_tflops": cnt["kv_flop"] / kv / 1e9,
         "tasa_ms": tasa, "tasa_tflops": cnt["tasa_flop"] / tasa / 1e9,
         "hma_ms": hma, "hma_gbs": cnt["hma_bytes"] / hma / 1e6,
         "step_ms": step, "cand_per_s": cnt["candidates"] / step * 1e3,
-        "serial_sum_ms": kv + tasa + hma}))
+        "serial_sum_ms": kv + tasa + hma, "step_serial_ms": step_serial}))
 
 
 if __name__ == "__main__":
