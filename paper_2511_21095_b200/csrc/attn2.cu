@@ -19,9 +19,12 @@
 //   * key tiles alternate between softmax warpgroups A (even) and B (odd); a named-barrier
 //     "MUFU token" per sub-partition orders their exp passes A(0), B(1), A(2), ... so one's exp
 //     pass overlaps the other's TMEM load, x pass and P hand-off.  Both accumulate into ONE O per
-//     unit with ONE running max per row (m_sh in shared memory, written only by the token
-//     holder); the row max is exact only for tile 0, later tiles test the tile's row sum and
-//     take the slow path (exact max, raise m_sh, rescale O, recompute P) only when needed;
+//     unit with ONE running max per row (m_sh in shared memory, decided tile by tile in order);
+//     the row max is exact only for tile 0, later tiles test the tile's row sum and take the
+//     slow path (exact max, raise m_sh, rescale O, recompute P) only when needed.  A pass starts
+//     right after the token with the warpgroup's own max, the token is handed on as soon as the
+//     last MUFU op is issued, and the previous tile's decision is checked after the pass (a rare
+//     raise recomputes): nothing but MUFU work sits between two exp passes;
 //   * TMEM per CTA (512 columns): S [0,128), P_A [128,192), P_B [192,256), O of even units
 //     [256,384), O of odd units [384,512): a unit's epilogue (warps 12-15) overlaps the next
 //     unit entirely;
@@ -64,8 +67,8 @@ __device__ unsigned long long g_trace4[64][16][16];  // per unit: epilogue chunk
 
 namespace {
 
-#ifndef GESR_PAIR_POLY_EVERY
-#define GESR_PAIR_POLY_EVERY 1000   // one pair in N takes the FMA-pipe exp2 on full tiles (1000: off)
+#ifndef GESR_PAIR_EPI_SLEEP
+#define GESR_PAIR_EPI_SLEEP 500   // ns per retry of the epilogue's unit-long waits
 #endif
 #ifndef GESR_PAIR_SUM_LIMIT
 #define GESR_PAIR_SUM_LIMIT 4096.0f   // tile row sums above this take the exact-max path
@@ -77,12 +80,19 @@ namespace {
 // A wait that exceeds ~20 s traps.  Builds with -DGESR_DEBUG_WAITS also print the call site
 // (ctx = site * 2^20 + unit * 2^8 + tile) first; the default build has no call in the wait
 // loops (a call site there makes ptxas keep the softmax's registers in local memory).
-__device__ __forceinline__ void pwait(uint64_t* bar, uint32_t parity, uint32_t ctx = 0) {
+// The retry loop is kept to a few instructions (a try_wait that suspends the warp in hardware,
+// an iteration counter instead of a clock read and 64-bit compare): waiting warps share their
+// sub-partition with an exp warp, and ncu showed the epilogue warps' unit-long waits spinning
+// ~370 times per unit through ~10 integer instructions each.  `sleep_ns` > 0 adds a nanosleep
+// per retry for waits that are long by construction (the epilogue waits a whole unit).
+__device__ __forceinline__ void pwait(uint64_t* bar, uint32_t parity, uint32_t ctx = 0,
+                                      uint32_t sleep_ns = 0) {
   const uint32_t a = smem_u32(bar);
   if (mbar_try_wait_hint(a, parity, GESR_PAIR_SPIN ? 0u : 1000000u)) return;
-  const long long t0 = clock64();
+  uint32_t n = 0;
   while (!mbar_try_wait_hint(a, parity, GESR_PAIR_SPIN ? 0u : 1000000u)) {
-    if (clock64() - t0 > 40000000000LL) {
+    if (sleep_ns) __nanosleep(sleep_ns);
+    if (++n == (1u << 28)) {
 #ifdef GESR_DEBUG_WAITS
       if ((threadIdx.x & 31) == 0)
         printf("gesr: attn_pair mbarrier timeout block %d warp %d smem 0x%x parity %u site %u unit %u tile %u\n",
@@ -108,8 +118,8 @@ constexpr uint32_t kRingOff = kQBytes;
 constexpr uint32_t kStgOff = kRingOff + kStages * kHalfBytes;        // 4 x 2 KB boxes per epilogue warp
 constexpr uint32_t kBarOff = kStgOff + 4 * 8192;
 constexpr uint32_t kXchOff = kBarOff + 512;                          // [unit % 4][WG][m, l][row]
-constexpr uint32_t kMshOff = kXchOff + 4 * 2 * 2 * 128 * 4;          // shared running max [row]
-constexpr uint32_t kSmemBytes = kMshOff + 128 * 4 + 1024;
+constexpr uint32_t kMshOff = kXchOff + 4 * 2 * 2 * 128 * 4;          // [row] {running max, tile}
+constexpr uint32_t kSmemBytes = kMshOff + 128 * 8 + 1024;
 static_assert(kSmemBytes <= 232448, "shared memory budget");
 // register split (setmaxnreg per warpgroup; launch registers 128 x 512 threads): control 56,
 // softmax 184, epilogue 88
@@ -121,28 +131,6 @@ static_assert(128 * kCtrlRegs + 256 * kSoftRegs + 128 * kEpiRegs <= 128 * kThrea
 constexpr uint32_t kTS = 0;          // S: one buffer, alternately A's and B's tiles
 constexpr uint32_t kTP = 128;        // P_A at 128, P_B at 192 (bf16 pairs, 64 columns each)
 constexpr uint32_t kTO = 256;        // O of even units at 256, of odd units at 384
-
-// 2^x for a pair on the FMA pipe only (no MUFU, no min/max): x clamped to [-126, 126] with a
-// saturating FFMA, split x = j + f with the 1.5*2^23 magic add, degree-3 polynomial for 2^f on
-// [-0.5, 0.5] (max rel. error 2.1e-4, below the bf16 rounding of P), exponent added with an
-// IMAD.  Used for one pair in GESR_PAIR_POLY_EVERY on full tiles.
-__device__ __forceinline__ void exp2_fma2(float& y0, float& y1, float x0, float x1);
-
-__device__ __forceinline__ void exp2_fma2(float& y0, float& y1, float x0, float x1) {
-  float u0, u1;
-  asm("fma.rn.sat.f32 %0, %1, %2, %3;" : "=f"(u0) : "f"(x0), "f"(1.0f / 252.0f), "f"(0.5f));
-  asm("fma.rn.sat.f32 %0, %1, %2, %3;" : "=f"(u1) : "f"(x1), "f"(1.0f / 252.0f), "f"(0.5f));
-  constexpr float kMagic = 12582912.0f;   // 1.5 * 2^23
-  float t0, t1, s0, s1, f0, f1, p0, p1;
-  ffma2(t0, t1, u0, u1, 252.0f, 252.0f, kMagic - 126.0f, kMagic - 126.0f);   // round(x') in low bits
-  fadd2(s0, s1, -t0, -t1, kMagic - 126.0f, kMagic - 126.0f);                   // -126 - round(x')
-  ffma2(f0, f1, u0, u1, 252.0f, 252.0f, s0, s1);                                // f = x' - round(x')
-  ffma2(p0, p1, f0, f1, 0.054848f, 0.054848f, 0.24180661f, 0.24180661f);
-  ffma2(p0, p1, p0, p1, f0, f1, 0.6932482f, 0.6932482f);
-  ffma2(p0, p1, p0, p1, f0, f1, 0.99998866f, 0.99998866f);
-  y0 = __int_as_float(__float_as_int(t0) * (1 << 23) + __float_as_int(p0));
-  y1 = __int_as_float(__float_as_int(t1) * (1 << 23) + __float_as_int(p1));
-}
 
 // K-major descriptor (SW128) for a [rows][128] bf16 tile stored as 2 column blocks of
 // `block_bytes` each, at K step ks (16 elements).
@@ -233,6 +221,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     tmem_alloc_pair(tmem_slot, 512);
     tmem_relinquish_pair();
   }
+  if (threadIdx.x < 128) {        // running-max words: no tile decided yet
+    const uint32_t w = smem_u32(smem + kMshOff) + threadIdx.x * 8;
+    asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(w), "r"(0u), "r"(0xFFFFFFFFu) : "memory");
+  }
   tc_fence_before();
   cluster_sync();
   tc_fence_after();
@@ -242,7 +234,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
   // the unit descriptor of work item w is one 16-byte load, fetched one item ahead
   auto fetch = [&](int w) { return __ldg(p.units + (w % U)); };
-  // w -> (unit w % U, split (w / U) % S, head w / (U S)): neighbouring pairs share a head
+  // w -> (unit w % U, split (w / U) % S, head w / (U S)): neighbouring pairs share a head and
+  // run the units of one request at the same time (K/V shared in L2; measured: a pair taking
+  // a contiguous block of items, units of a request back to back, read 11% MORE from HBM)
   auto decode = [&](int w, int4 d) {
     Work x;
     const int rest = w / U;
@@ -428,12 +422,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     // ------------------------------------------------------------ softmax
     // Both warpgroups accumulate into ONE O per unit (double-buffered across units in TMEM, so
     // the epilogue of unit u overlaps unit u+1) with ONE running max per row, m_sh (shared
-    // memory).  The MUFU token orders the tiles' exp passes A(0), B(1), A(2), ...; m_sh is
-    // written only by the token holder and read after taking the token, so every P(j) is
-    // computed against the max O is scaled to when PV(j) lands.  Raising m_sh (rare: a tile
-    // whose row sum exceeds 2^12 and whose exact max exceeds m_sh by > 8, log2 units) waits for
-    // PV(j-1) and rescales O first.  Each warpgroup keeps its own row sum l relative to the
-    // m_sh it last used (m_loc) and rescales it when it finds m_sh raised.
+    // memory, one {m, tile} word per row).  The MUFU token orders the tiles' exp passes A(0),
+    // B(1), A(2), ...; each tile publishes its decided max in tile order, and a tile's P is
+    // final only once it has been computed against the max decided by the tile before it
+    // (checked after the first pass, recomputed in the rare case it was raised), so every P(j)
+    // matches the max O is scaled to when PV(j) lands.  Raising m_sh (rare: a tile whose row sum
+    // exceeds 2^12 and whose exact max exceeds m_sh by > 8, log2 units) waits for PV(j-1) and
+    // rescales O first.  Each warpgroup keeps its own row sum l relative to the max it last
+    // used (m_loc) and rescales it when it finds m_sh raised.
     setmaxnreg_inc<kSoftRegs>();
     const int g = (static_cast<int>(warp) - 4) >> 2;   // warpgroup: 0 = A (even tiles), 1 = B
     const uint32_t sub = warp & 3;                       // TMEM lane quarter
@@ -444,7 +440,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const uint32_t s_free_leader = mapa_shared(smem_u32(s_free), 0);
     const uint32_t p_full_leader = mapa_shared(smem_u32(&p_full[g]), 0);
     const uint32_t xch = smem_u32(smem + kXchOff);
-    const uint32_t msh = smem_u32(smem + kMshOff) + rloc * 4;
+    const uint32_t msh = smem_u32(smem + kMshOff) + rloc * 8;
+    // {m, tile} of this row: the running max as decided by CTA-wide key tile `tile` (tiles
+    // decide in order; one 8-byte store / load, so the pair is always consistent)
+    auto publish_m = [&](float mv, int tile) {
+      asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(msh), "r"(__float_as_uint(mv)),
+                   "r"(static_cast<uint32_t>(tile)) : "memory");
+    };
+    auto wait_m = [&](int tile) {      // the running max once tile `tile` has decided
+      uint32_t mv, tv;
+      do {
+        asm volatile("ld.volatile.shared.v2.u32 {%0, %1}, [%2];" : "=r"(mv), "=r"(tv) : "r"(msh) : "memory");
+      } while (static_cast<int>(tv) < tile);
+      return __uint_as_float(mv);
+    };
     const float sl2 = p.scale_log2;
     int sc = 0;                                          // S tiles consumed by this warpgroup
     // MUFU token: the exp passes of the two warps of a sub-partition (A and B, same lane
@@ -476,8 +485,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         uint32_t r[kKeys];
 #pragma unroll
         for (int c = 0; c < 4; ++c) tmem_ld32(tS + c * 32, r + c * 32);
-        tmem_ld_wait();
+        tmem_ld_wait_regs32(r);
+        tmem_ld_wait_regs32(r + 32);
+        tmem_ld_wait_regs32(r + 64);
+        tmem_ld_wait_regs32(r + 96);
+#ifndef GESR_TRACE_LOOP
         if (trd) GESR_T2(1, m * 16 + j);
+#endif
         const int valid = L - kKeys * j;
         const bool full = valid >= kKeys;
         if (!full) {
@@ -489,7 +503,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster_relaxed(s_free_leader);
+#ifndef GESR_TRACE_LOOP
         if (trd) GESR_T2(2, m * 16 + j);
+#endif
         // Row max.  Min/max instructions share the issue path of MUFU (scripts/micro/
         // exp_interf.cu: a max pass on the other warp of a sub-partition slows an exp pass from
         // 1.17k to 2k cycles), so only the unit's tile 0 reduces its exact max; later tiles
@@ -506,12 +522,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           return fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
                        fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
         };
+        const int gidx = gbase + j;                      // CTA-wide key tile index
         const bool first_b = j > 0 && m_loc == -INFINITY;   // B's first tile of the unit
         if (j == 0) m_loc = row_max() * sl2;
+        // B's first tile takes the max tile 0 decided (published right after tile 0's pass, so
+        // this wait, off the token path, is short and once per unit)
+        if (first_b) m_loc = wait_m(gidx - 1);
+        // the token release condition, kept out of the post-token path
+        const bool pass_token = j + 1 < nkv || (g == 1 && w + npairs < W);
         // x = s*scale*log2e - m in place, before the token (FMA pipe, overlaps the other
-        // warpgroup's exp pass); B's first tile takes m = 0 and is shifted once m_sh is known
+        // warpgroup's exp pass)
         {
-          const float neg_m = first_b ? 0.f : -m_loc;
+          const float neg_m = -m_loc;
 #pragma unroll
           for (int k = 0; k < kKeys / 2; ++k) {
             float x0, x1;
@@ -525,50 +547,46 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (sc > 1) pwait(&p_free[g], (sc - 2) & 1, CTX(11, m, j));
         if (j > 0 || prev_last_b) named_bar_sync(tok_mine, 64);   // tile j-1's exp pass is done
         if (trd) GESR_T2(4, m * 16 + j);
-        float d = 0.f;                                   // shift of x still to apply
-        if (j == 0) {
-          st_shared_f32(msh, m_loc);                     // the unit's first max
-        } else {
-          const float ms = ld_shared_f32(msh);
-          if (first_b) {
-            d = ms;
-            m_loc = ms;
-          } else {
-            d = fmaxf(ms - m_loc, 0.f);                  // m_sh raised since my last tile
-            l *= ex2(-d);
-            m_loc += d;
+        // The exp pass starts right after the token with this warpgroup's own m_loc; the previous
+        // tile's decision (its sum test may raise the running max) is checked after the pass,
+        // off the token's critical path, and the rare raise recomputes the tile.  The token is
+        // released as soon as the first pass's MUFU work is issued.
+        auto shift = [&](float d) {                      // x -= d (lanes with d = 0 unchanged)
+#pragma unroll
+          for (int k = 0; k < kKeys / 2; ++k) {
+            float x0, x1;
+            fadd2(x0, x1, __uint_as_float(r[2 * k]), __uint_as_float(r[2 * k + 1]), -d, -d);
+            r[2 * k] = __float_as_uint(x0);
+            r[2 * k + 1] = __float_as_uint(x1);
           }
-        }
+        };
+        bool checked_prev = (j == 0) || first_b;
+        bool raised = false;
         float acc[8];
         float tsum;
 #pragma unroll 1
         for (int pass = 0;; ++pass) {
-          if (__any_sync(0xffffffffu, d != 0.f)) {
-#pragma unroll
-            for (int k = 0; k < kKeys / 2; ++k) {
-              float x0, x1;
-              fadd2(x0, x1, __uint_as_float(r[2 * k]), __uint_as_float(r[2 * k + 1]), -d, -d);
-              r[2 * k] = __float_as_uint(x0);
-              r[2 * k + 1] = __float_as_uint(x1);
-            }
-          }
           // p = 2^x, packed to bf16 pairs and stored to P_g (TMEM) 32 columns at a time;
           // masked keys give exactly 0
 #pragma unroll
           for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+#ifdef GESR_TRACE_LOOP
+          if (trd && pass == 0) GESR_T2(1, m * 16 + j);
+#endif
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
+#ifdef GESR_TRACE_LOOP
+            if (trd && pass == 0 && hh == 1) GESR_T2(2, m * 16 + j);
+#endif
             uint32_t pk[32];
 #pragma unroll
             for (int u = 0; u < 32; ++u) {
               const int k = hh * 32 + u;
-              float p0, p1;
-              if ((k % GESR_PAIR_POLY_EVERY) == GESR_PAIR_POLY_EVERY - 1 && full) {
-                exp2_fma2(p0, p1, __uint_as_float(r[2 * k]), __uint_as_float(r[2 * k + 1]));
-              } else {
-                p0 = ex2(__uint_as_float(r[2 * k]));
-                p1 = ex2(__uint_as_float(r[2 * k + 1]));
-              }
+              const float p0 = ex2(__uint_as_float(r[2 * k]));
+              const float p1 = ex2(__uint_as_float(r[2 * k + 1]));
+              // hand the token to tile j+1's warpgroup (the next unit starts with A) as soon as
+              // the first pass's last MUFU op is issued
+              if (hh == 1 && u == 31 && pass == 0 && pass_token) named_bar_arrive(tok_other, 64);
               const int a = (k & 3) * 2;
               fadd2(acc[a], acc[a + 1], acc[a], acc[a + 1], p0, p1);
               pk[u] = pack_bf16x2(p0, p1);
@@ -577,36 +595,51 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
           if (trd && pass == 0) GESR_T2(3, m * 16 + j);
           tsum = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+          if (!checked_prev) {
+            // the previous tile (other warpgroup) may have raised the running max after this
+            // pass started: rescale l and recompute against it
+            checked_prev = true;
+            const float ms = wait_m(gidx - 1);
+            const float d = fmaxf(ms - m_loc, 0.f);
+            if (__any_sync(0xffffffffu, d != 0.f)) {
+              l *= ex2(-d);
+              m_loc += d;
+              shift(d);
+              continue;
+            }
+          }
+          if (raised || j == 0) break;
           const bool over = !(tsum <= GESR_PAIR_SUM_LIMIT);
-          if (pass == 1 || j == 0 || !__any_sync(0xffffffffu, over)) break;
+          if (!__any_sync(0xffffffffu, over)) break;
           const float dx = over ? row_max() : 0.f;       // exact max above m_loc (x units)
           const bool need = dx > 8.0f;
           if (!__any_sync(0xffffffffu, need)) break;
-          // raise m_sh: O must hold PV(j-1) (the other warpgroup's last tile) before it is
-          // rescaled; no later PV can land before this warpgroup's p_full(j)
+          // raise the running max: O must hold PV(j-1) (the other warpgroup's last tile) before
+          // it is rescaled; no later PV can land before this warpgroup's p_full(j)
           pwait(pv_done, (gbase + j - 1) & 1, CTX(12, m, j));
           tc_fence_after();
-          d = need ? dx : 0.f;
+          const float d = need ? dx : 0.f;
           const float alpha = ex2(-d);
-          if (need) {
-            m_loc += d;
-            l *= alpha;
-            st_shared_f32(msh, m_loc);
-          }
+          m_loc += d;
+          l *= alpha;
 #pragma unroll 1
           for (int c = 0; c < 4; ++c) {
             uint32_t o[32];
             tmem_ld32(tO + c * 32, o);
-            tmem_ld_wait();
+            tmem_ld_wait_regs32(o);
 #pragma unroll
             for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
             tmem_st32(tO + c * 32, o);
           }
           tmem_st_wait();
           tc_fence_before();
+          shift(d);
+          raised = true;
         }
-        // hand the token to tile j+1's warpgroup (the next unit starts with A)
-        if (j + 1 < nkv || (g == 1 && w + npairs < W)) named_bar_arrive(tok_other, 64);
+        // this tile's decision; tile 0 of a unit first lets the previous tile's decision land
+        // (one word per row, written in tile order)
+        if (j == 0 && gidx > 0) (void)wait_m(gidx - 1);
+        publish_m(m_loc, gidx);
         l += tsum;
         tmem_st_wait();                                  // P_g in TMEM before PV(j) reads it
         tc_fence_before();
@@ -672,7 +705,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         continue;
       }
-      pwait(&ml_full[m & 3], (m >> 2) & 1, CTX(13, m, 0));
+      pwait(&ml_full[m & 3], (m >> 2) & 1, CTX(13, m, 0), GESR_PAIR_EPI_SLEEP);
       if (sub == 0 && lane == 0) GESR_T3(5, m);
       const uint32_t xb = xch + ((m & 3) * 2 * 2 * 128) * 4;
       const float mA = ld_shared_f32(xb + (0 * 128 + rloc) * 4);
@@ -689,7 +722,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       if (lane == 0) bulk_wait_group_read<0>();
       __syncwarp();
       const int ob = m & 1;
-      pwait(&o_done[ob], (m >> 1) & 1, CTX(14, m, 0));
+      pwait(&o_done[ob], (m >> 1) & 1, CTX(14, m, 0), GESR_PAIR_EPI_SLEEP);
       if (sub == 0 && lane == 0) GESR_T3(6, m);
       tc_fence_after();
       const uint32_t tO = tO0 + ob * kD;

@@ -357,6 +357,7 @@ static gesr_status tasa_impl(const void* T, int64_t total_C, int32_t D_in, const
   p.units = units;
   p.unit_count = count;
   p.splits = pick_splits(B, total_C, total_L, H, d, kv_splits);
+
   if (p.splits > 1) {
     p.part_ml = reinterpret_cast<float2*>(part);
     p.part_o = reinterpret_cast<float*>(part + split_ml_bytes(total_C, H, p.splits));
