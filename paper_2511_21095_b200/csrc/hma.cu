@@ -9,11 +9,12 @@
 //
 // B200 design (HBM-bound on the item-ID stream, ~8.5 int64 IDs per (candidate, field)):
 //   grid (B, Y): CTA (b, y) owns request b and candidate chunks y, y+Y, ... of kChunk rows.
-//   1. The request's F user lists go into per-field hash tables in shared memory: buckets of
-//      4 slots holding a 32-bit fingerprint, the 64-bit key and its multiplicity.  Insertion is
-//      parallel (64-bit atomicCAS, linear probing over bucket-aligned slots; the one sentinel
-//      key value INT64_MIN is counted on the side); load factor <= 1/4, so a miss -- the common
-//      case -- is one 16-byte fingerprint read and four compares, uniform across the warp.
+//   1. The request's F user lists go into per-field open-addressing tables in shared memory:
+//      64-bit keys (INT64_MIN marks an empty slot; that one ID value is counted on the side)
+//      with their multiplicities in a parallel array.  Insertion is parallel (64-bit atomicCAS,
+//      linear probing); the home slot is the even slot of a multiplicative hash of the key's
+//      two 32-bit halves, and at load factor <= 1/4 a lookup almost always ends within that
+//      slot pair: ONE 16-byte shared load and two 64-bit compares, no fingerprint indirection.
 //      Fields whose tables do not fit the pool fall back to a direct scan of global memory.
 //   2. Each warp takes 32 consecutive (candidate, field) segments of the CSR item stream.
 //      Lane k writes its segment id into a per-warp owner map (one uint16 per ID position),
@@ -32,42 +33,47 @@ namespace {
 constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
 constexpr int kChunk = 256;               // candidates per CTA chunk
-constexpr int kPoolBuckets = 1024;        // 4-slot buckets per CTA (64 KB)
+constexpr int kPoolSlots = 4096;          // table slots per CTA (32 KB keys + 16 KB counts)
 constexpr int kMaxFields = 256;
 constexpr int kOwnerCap = 512;            // IDs per 32-segment group handled with the owner map
-constexpr unsigned long long kSentinel = 0x8000000000000000ull;   // INT64_MIN
-constexpr unsigned long long kGold = 0x9E3779B97F4A7C15ull;
+constexpr unsigned long long kSentinel = 0x8000000000000000ull;   // INT64_MIN: empty slot
+constexpr uint32_t kMul = 0x9E3779B1u;
 
 struct HmaSmem {
-  uint4 fp[kPoolBuckets];                         // 4 fingerprints per bucket (0 = empty)
-  unsigned long long key[kPoolBuckets * 4];
-  int cnt[kPoolBuckets * 4];
-  int tab_off[kMaxFields];                        // first bucket of field f, -1 = global scan
-  int tab_mask[kMaxFields];                       // buckets - 1
+  unsigned long long key[kPoolSlots];             // kSentinel = empty
+  int cnt[kPoolSlots];
+  int2 tab[kMaxFields];                           // {first slot, hash shift}; first < 0: global
   int sent_cnt[kMaxFields];                       // multiplicity of INT64_MIN
   long long uoff[kMaxFields + 1];                 // this request's user_offsets (F+1)
   int warp_cnt[kWarps][32];
-  unsigned short owner[kWarps][kOwnerCap];
+  // owner word of each ID position of a warp's 32-segment group: segment lane (bits 0-4), the
+  // field's hash shift (5-9), its first table slot (10-21), the field (22-29)
+  uint32_t owner[kWarps][kOwnerCap];
+  int any_global;                                 // some field scans global memory instead
 };
+
+// Home slot pair of a key in a table of 2^(32 - shift) slot pairs (top bits of a
+// multiplicative hash of the folded key).
+__device__ __forceinline__ uint32_t home_pair(unsigned long long key, int shift) {
+  const uint32_t h = (static_cast<uint32_t>(key) ^ static_cast<uint32_t>(key >> 32)) * kMul;
+  return h >> shift;
+}
 
 __device__ __forceinline__ int lookup(const HmaSmem& s, const HmaParams& p, int f,
                                       unsigned long long key) {
-  const int off = s.tab_off[f];
-  if (off >= 0) {
-    if (key == kSentinel) return s.sent_cnt[f];
-    const unsigned long long hk = key * kGold;
-    const uint32_t mask = static_cast<uint32_t>(s.tab_mask[f]);
-    uint32_t bkt = static_cast<uint32_t>(hk >> 32) & mask;
-    const uint32_t fpv = static_cast<uint32_t>(hk) | 1u;
+  if (key == kSentinel) return s.sent_cnt[f];
+  const int2 t = s.tab[f];
+  if (t.x >= 0) {
+    const uint32_t pmask = 0xFFFFFFFFu >> t.y;
+    uint32_t pr = home_pair(key, t.y);
     while (true) {
-      const uint4 f4 = s.fp[off + bkt];
-      const int base = (off + bkt) * 4;
-      if (f4.x == fpv && s.key[base + 0] == key) return s.cnt[base + 0];
-      if (f4.y == fpv && s.key[base + 1] == key) return s.cnt[base + 1];
-      if (f4.z == fpv && s.key[base + 2] == key) return s.cnt[base + 2];
-      if (f4.w == fpv && s.key[base + 3] == key) return s.cnt[base + 3];
-      if (f4.w == 0u) return 0;        // slots fill in probe order: an empty slot ends it
-      bkt = (bkt + 1) & mask;
+      const int sl = t.x + 2 * static_cast<int>(pr);
+      const ulonglong2 kk = *reinterpret_cast<const ulonglong2*>(&s.key[sl]);
+      if (kk.x == key) return s.cnt[sl];
+      if (kk.x == kSentinel) return 0;               // slots fill in probe order
+      if (kk.y == key) return s.cnt[sl + 1];
+      if (kk.y == kSentinel) return 0;
+      pr = (pr + 1) & pmask;
     }
   }
   // global fallback: direct scan of the user list
@@ -96,22 +102,22 @@ __global__ void __launch_bounds__(kThreads, 2)
   __syncthreads();
   if (tid == 0) {
     int used = 0;
+    s.any_global = 0;
     for (int f = 0; f < F; ++f) {
       const long long n = s.uoff[f + 1] - s.uoff[f];
-      int nb = 2;
-      while (nb < n && nb < kPoolBuckets) nb <<= 1;     // >= n buckets: load factor <= 1/4
-      if (n <= nb && used + nb <= kPoolBuckets) {
-        s.tab_off[f] = used;
-        s.tab_mask[f] = nb - 1;
-        used += nb;
+      int ns = 4, shift = 31;                         // >= 4n slots: load factor <= 1/4
+      while (ns < 4 * n && ns < kPoolSlots) { ns <<= 1; --shift; }
+      if (4 * n <= ns && used + ns <= kPoolSlots) {
+        s.tab[f] = make_int2(used, shift);           // ns / 2 = 2^(32 - shift) slot pairs
+        used += ns;
       } else {
-        s.tab_off[f] = -1;
-        s.tab_mask[f] = 0;
+        s.tab[f] = make_int2(-1, 0);
+        s.any_global = 1;
       }
       s.sent_cnt[f] = 0;
     }
   }
-  for (int i = tid; i < kPoolBuckets * 4; i += kThreads) {
+  for (int i = tid; i < kPoolSlots; i += kThreads) {
     s.key[i] = kSentinel;
     s.cnt[i] = 0;
   }
@@ -128,45 +134,34 @@ __global__ void __launch_bounds__(kThreads, 2)
         if (s.uoff[mid] <= pos) lo = mid; else hi = mid - 1;
       }
       const int f = lo;
-      const int off = s.tab_off[f];
-      if (off < 0) continue;
+      const int2 t = s.tab[f];
+      if (t.x < 0) continue;
       const unsigned long long key = static_cast<unsigned long long>(__ldg(p.user_ids + pos));
       if (key == kSentinel) {
         atomicAdd(&s.sent_cnt[f], 1);
         continue;
       }
-      const uint32_t nslots = static_cast<uint32_t>(s.tab_mask[f] + 1) * 4;
-      uint32_t slot = (static_cast<uint32_t>((key * kGold) >> 32) &
-                       static_cast<uint32_t>(s.tab_mask[f])) * 4;
+      const uint32_t smask = (0xFFFFFFFFu >> t.y) * 2 + 1;   // slots - 1
+      uint32_t slot = home_pair(key, t.y) * 2;
       while (true) {
-        const unsigned long long prev = atomicCAS(&s.key[off * 4 + slot], kSentinel, key);
+        const unsigned long long prev = atomicCAS(&s.key[t.x + slot], kSentinel, key);
         if (prev == kSentinel || prev == key) {
-          atomicAdd(&s.cnt[off * 4 + slot], 1);
+          atomicAdd(&s.cnt[t.x + slot], 1);
           break;
         }
-        slot = (slot + 1 == nslots) ? 0 : slot + 1;
+        slot = (slot + 1) & smask;
       }
     }
-  }
-  __syncthreads();
-  // fingerprints of the occupied slots
-  for (int bk = tid; bk < kPoolBuckets; bk += kThreads) {
-    uint32_t v[4];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const unsigned long long k = s.key[bk * 4 + e];
-      v[e] = (k == kSentinel) ? 0u : (static_cast<uint32_t>(k * kGold) | 1u);
-    }
-    s.fp[bk] = make_uint4(v[0], v[1], v[2], v[3]);
   }
   __syncthreads();
 
   // ---- 2. coalesced scan of the item-ID stream, 32 segments per warp step.  The next group's
   //         offsets are fetched while the current group is processed, and all of a group's IDs
-  //         (up to kUnroll per lane) are loaded before the first lookup, so each warp keeps
-  //         ~2 KB of loads in flight.
-  constexpr int kUnroll = 16;
-  unsigned short* own = s.owner[warp];
+  //         (kUnroll per lane) are loaded before the first lookup, so each warp keeps ~2 KB of
+  //         loads in flight.
+  constexpr int kUnroll = 8;
+  constexpr int kBatch = 4;
+  uint32_t* own = s.owner[warp];
   for (int64_t c0 = first; c0 < ce; c0 += static_cast<int64_t>(gridDim.y) * kChunk) {
     const int64_t c1 = (c0 + kChunk < ce) ? c0 + kChunk : ce;
     const int64_t seg_begin = c0 * F, seg_end = c1 * F;
@@ -193,7 +188,11 @@ __global__ void __launch_bounds__(kThreads, 2)
       const int my_end = lane + 1 < nseg ? nxt : n_ids;
       const int my_f = static_cast<int>(g - seg_begin + lane) % F;   // seg_begin % F == 0
       const int64_t* ids = p.item_ids + start;
-      if (n_ids <= kOwnerCap) {
+      if (n_ids <= kOwnerCap && !s.any_global) {
+        // owner words of this group's ID positions (one table-info read per segment)
+        const int2 t = s.tab[my_f];
+        const uint32_t ow = static_cast<uint32_t>(lane) | (static_cast<uint32_t>(t.y) << 5) |
+                            (static_cast<uint32_t>(t.x) << 10) | (static_cast<uint32_t>(my_f) << 22);
         for (int base = 0; base < n_ids; base += kUnroll * 32) {
           unsigned long long kk[kUnroll];
 #pragma unroll
@@ -203,16 +202,85 @@ __global__ void __launch_bounds__(kThreads, 2)
           }
           if (base == 0) {
             if (lane < nseg)
-              for (int q = my_off; q < my_end; ++q) own[q] = static_cast<unsigned short>(lane | (my_f << 5));
+              for (int q = my_off; q < my_end; ++q) own[q] = ow;
             __syncwarp();
           }
+          // batches of kBatch positions in straight-line code, so their shared-memory reads
+          // overlap: owner word -> home slot pair -> one 16-byte key read -> compare; a
+          // position not settled by its home pair (rare at load factor 1/4) probes on after
+          // the batch
+#pragma unroll
+          for (int u0 = 0; u0 < kUnroll; u0 += kBatch) {
+            if (base + u0 * 32 >= n_ids) break;          // warp-uniform
+            uint32_t o[kBatch];
+            int sl[kBatch], c[kBatch];
+            bool open[kBatch];
+#pragma unroll
+            for (int v = 0; v < kBatch; ++v) {
+              const int pos = base + (u0 + v) * 32 + lane;
+              o[v] = pos < n_ids ? own[pos] : 0u;
+            }
+#pragma unroll
+            for (int v = 0; v < kBatch; ++v) {
+              const unsigned long long key = kk[u0 + v];
+              const int pos = base + (u0 + v) * 32 + lane;
+              const int shift = static_cast<int>((o[v] >> 5) & 31u);
+              sl[v] = static_cast<int>((o[v] >> 10) & 4095u) + 2 * static_cast<int>(home_pair(key, shift));
+              const ulonglong2 kv = *reinterpret_cast<const ulonglong2*>(&s.key[sl[v]]);
+              const bool m0 = kv.x == key, m1 = kv.y == key;
+              c[v] = (m0 || m1) ? s.cnt[sl[v] + (m0 ? 0 : 1)] : 0;
+              open[v] = !(m0 || m1 || kv.x == kSentinel || kv.y == kSentinel);
+              if (key == kSentinel) {                        // the empty marker's own ID value
+                c[v] = s.sent_cnt[o[v] >> 22];
+                open[v] = false;
+              }
+              if (pos >= n_ids) { c[v] = 0; open[v] = false; }
+            }
+            bool any_open = false;
+#pragma unroll
+            for (int v = 0; v < kBatch; ++v) any_open |= open[v];
+            if (__any_sync(0xffffffffu, any_open)) {
+#pragma unroll
+              for (int v = 0; v < kBatch; ++v) {
+                if (open[v]) {
+                  const uint32_t smask = (0xFFFFFFFFu >> ((o[v] >> 5) & 31u)) * 2 + 1;
+                  const int off = static_cast<int>((o[v] >> 10) & 4095u);
+                  int q = (sl[v] - off + 2) & static_cast<int>(smask);
+                  while (true) {
+                    const unsigned long long kq = s.key[off + q];
+                    if (kq == kk[u0 + v]) { c[v] = s.cnt[off + q]; break; }
+                    if (kq == kSentinel) break;
+                    q = (q + 1) & static_cast<int>(smask);
+                  }
+                }
+              }
+            }
+#pragma unroll
+            for (int v = 0; v < kBatch; ++v)
+              if (c[v] != 0) atomicAdd(&s.warp_cnt[warp][o[v] & 31u], c[v]);
+          }
+        }
+      } else if (n_ids <= kOwnerCap) {
+        for (int base = 0; base < n_ids; base += kUnroll * 32) {
+          unsigned long long kk[kUnroll];
 #pragma unroll
           for (int u = 0; u < kUnroll; ++u) {
             const int pos = base + u * 32 + lane;
+            kk[u] = pos < n_ids ? static_cast<unsigned long long>(__ldg(ids + pos)) : 0ull;
+          }
+          if (base == 0) {
+            if (lane < nseg)
+              for (int q = my_off; q < my_end; ++q) own[q] = static_cast<uint32_t>(lane) | (static_cast<uint32_t>(my_f) << 22);
+            __syncwarp();
+          }
+#pragma unroll 1
+          for (int u = 0; u < kUnroll; ++u) {
+            if (base + u * 32 >= n_ids) break;           // warp-uniform
+            const int pos = base + u * 32 + lane;
             if (pos < n_ids) {
-              const int o = own[pos];
-              const int c = lookup(s, p, o >> 5, kk[u]);
-              if (c != 0) atomicAdd(&s.warp_cnt[warp][o & 31], c);
+              const uint32_t o = own[pos];
+              const int c = lookup(s, p, static_cast<int>(o >> 22), kk[u]);
+              if (c != 0) atomicAdd(&s.warp_cnt[warp][o & 31u], c);
             }
           }
         }

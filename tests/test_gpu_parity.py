@@ -528,3 +528,35 @@ def test_config_full_size_sampled(name):
                             sub.cand_offsets, cfg.F)
     assert np.array_equal(counts[torch.as_tensor(rows, device=dev)].cpu().numpy(), want)
 
+
+
+@pytest.mark.parametrize("pattern", ["hi_bits", "sequential", "same_fold"])
+def test_hma_structured_ids(pattern):
+    # IDs built to collide under the table hash (low halves zero / consecutive values / equal
+    # lo^hi folds): long probe chains, results must stay exact
+    dev = _cuda()
+    rng = np.random.default_rng(5)
+    F, B, C = 3, 4, 50
+    def ids(n, f):
+        v = rng.integers(0, 96, size=n).astype(np.int64)
+        if pattern == "hi_bits":
+            return (v + 1000 * f) << 32
+        if pattern == "sequential":
+            return v + 1000 * f
+        return ((v + 7 * f) << 32) | (v + 7 * f)        # lo ^ hi = 0 for every ID
+    ulen = rng.integers(0, 65, size=B * F)
+    users = [ids(int(n), k % F) for k, n in enumerate(ulen)]
+    ilen = rng.integers(1, 17, size=B * C * F)
+    items = [ids(int(n), k % F) for k, n in enumerate(ilen)]
+    uo = np.concatenate([[0], np.cumsum([len(x) for x in users])]).astype(np.int64)
+    io = np.concatenate([[0], np.cumsum([len(x) for x in items])]).astype(np.int64)
+    co = np.arange(B + 1, dtype=np.int64) * C
+    ui = np.concatenate(users).astype(np.int64)
+    ii = np.concatenate(items).astype(np.int64)
+    want = oracle.hma_count(ui, uo, ii, io, co, F)
+    c = gb.hma_count(torch.tensor(ui, device=dev), torch.tensor(uo, device=dev),
+                     torch.tensor(ii, device=dev), torch.tensor(io, device=dev),
+                     torch.tensor(co, device=dev), F)
+    torch.cuda.synchronize()
+    assert np.array_equal(c.cpu().numpy(), want)
+    assert want.sum() > 0
