@@ -67,6 +67,9 @@ __device__ unsigned long long g_trace4[64][16][16];  // per unit: epilogue chunk
 
 namespace {
 
+#ifndef GESR_PAIR_L2HINT
+#define GESR_PAIR_L2HINT 1        // 1: Q loads / O stores evict_first; 2: + K/V loads evict_last
+#endif
 #ifndef GESR_PAIR_EPI_SLEEP
 #define GESR_PAIR_EPI_SLEEP 500   // ns per retry of the epilogue's unit-long waits
 #endif
@@ -188,6 +191,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
+#if GESR_PAIR_L2HINT >= 1
+  const uint64_t pol_first = policy_evict_first();   // streamed once: Q in, O out
+#endif
+#if GESR_PAIR_L2HINT >= 2
+  const uint64_t pol_last = policy_evict_last();     // K/V: re-read by the request's other units
+#endif
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&map_q);
@@ -321,16 +330,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const int32_t qrow = static_cast<int32_t>(static_cast<int64_t>(tl.x.h) * p.total_C + tl.x.cbeg) +
                                  static_cast<int32_t>(rank) * 128;
             if (rank == 0) mbar_arrive_expect_tx(q_full, 2 * kQBytes);
+#if GESR_PAIR_L2HINT >= 1
+            tma_load_2d_pair_hint(smem + kQOff, &map_q, q_full, 0, qrow, pol_first);
+            tma_load_2d_pair_hint(smem + kQOff + kQBytes / 2, &map_q, q_full, 64, qrow, pol_first);
+#else
             tma_load_2d_pair(smem + kQOff, &map_q, q_full, 0, qrow);
             tma_load_2d_pair(smem + kQOff + kQBytes / 2, &map_q, q_full, 64, qrow);
+#endif
           }
           const int slot = kst;
           pwait(&kv_empty[slot], kph ^ 1, CTX(2, tl.m, tl.t));
           if (rank == 0) mbar_arrive_expect_tx(&kv_full[slot], 2 * kHalfBytes);
           uint8_t* dst = smem + kRingOff + slot * kHalfBytes;
           const int32_t row = krow_of(tl) + static_cast<int32_t>(rank) * 64;
+#if GESR_PAIR_L2HINT >= 2
+          tma_load_2d_pair_hint(dst, &map_kh, &kv_full[slot], 0, row, pol_last);
+          tma_load_2d_pair_hint(dst + 8192, &map_kh, &kv_full[slot], 64, row, pol_last);
+#else
           tma_load_2d_pair(dst, &map_kh, &kv_full[slot], 0, row);
           tma_load_2d_pair(dst + 8192, &map_kh, &kv_full[slot], 64, row);
+#endif
           if (++kst == kKStages) { kst = 0; kph ^= 1; }
         }
       }
@@ -344,7 +363,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           pwait(&kv_empty[slot], vph ^ 1, CTX(3, tl.m, tl.t));
           if (rank == 0) mbar_arrive_expect_tx(&kv_full[slot], 2 * kHalfBytes);
           uint8_t* dst = smem + kRingOff + slot * kHalfBytes;
+#if GESR_PAIR_L2HINT >= 2
+          tma_load_2d_pair_hint(dst, &map_vh, &kv_full[slot], static_cast<int32_t>(rank) * 64, krow_of(tl), pol_last);
+#else
           tma_load_2d_pair(dst, &map_vh, &kv_full[slot], static_cast<int32_t>(rank) * 64, krow_of(tl));
+#endif
           if (++vst == kVStages) { vst = 0; vph ^= 1; }
         }
       }
@@ -782,7 +805,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if (lane == 0) {
 #pragma unroll
             for (int b = 0; b < 4; ++b)
+#if GESR_PAIR_L2HINT >= 1
+              tma_store_3d_hint(&map_o, stg + b * 2048, b * 32, h, static_cast<int32_t>(x.cbeg + row0), pol_first);
+#else
               tma_store_3d(&map_o, stg + b * 2048, b * 32, h, static_cast<int32_t>(x.cbeg + row0));
+#endif
             bulk_commit_group();
           }
         } else {
