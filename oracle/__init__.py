@@ -19,6 +19,10 @@ blocking/fusion), each citing the passage it follows:
 * :func:`offset_index` / :func:`hma_offset_embed` -- HMA embedding with feature-pair offsets,
   e = E(c + o(M+1)), concatenated over pairs.
   (stride M+1: DESIGN.md reading R14).  Plain numpy.
+* :func:`stu_output` -- the rest of the STU layer's candidate row after the attention (SURVEY
+  s8(f) f1): gating branch, normalisation of attention.value, output projection, residual.
+  SPEC.md:343 (PAPER.md:229 defers the STU internals to HSTU); reading R15.  Plain
+  numpy, fp64.
 
 Parity pins: see tests/test_oracle_*.py.  Every function here is pinned.
 """
@@ -282,3 +286,51 @@ def hma_offset_embed(counts, E, M: int) -> np.ndarray:
             out[t, o * D_h:(o + 1) * D_h] = E[offset_index(int(counts[t, o]), o, M)]
     return out
 
+
+
+def _f64(x) -> np.ndarray:
+    """bf16 / fp32 / fp64 tensor or array -> fp64 numpy array (bf16 widened exactly)."""
+    try:
+        import torch
+        if isinstance(x, torch.Tensor):
+            return x.detach().cpu().to(torch.float64).numpy()
+    except ImportError:  # pragma: no cover
+        pass
+    a = np.asarray(x)
+    if a.dtype == np.uint16:                       # raw bf16 bits
+        return (a.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+    return a.astype(np.float64)
+
+
+def stu_output(T, O, W_g, gamma, beta, W_o, b_g=None, b_o=None, X_res=None, eps=1e-5, act=1):
+    """Candidate rows of one STU layer after the attention, in SPEC.md:343's order (the paper
+    defers STU internals to HSTU; reading R15):
+
+      gating branch     G = act(T W_g^T + b_g)               ("a gating branch by linear
+                                                               projection with sigmoid-linear-
+                                                               unit activation")
+      normalisation     N = (O - mean(O)) / sqrt(var(O) + eps) * gamma + beta, per row over the
+                        D = H*d features of the concatenated heads (population variance)
+      layer output      Y = (N * G) W_o^T + b_o + X_res      ("output-projection(normalize(
+                                                               attention.value) (.) gating-
+                                                               branch) + residual")
+
+    T [C, D_in], O [C, D] (attention.value, heads concatenated), W_g [D, D_in],
+    gamma/beta [D], W_o [D_out, D], b_g [D] / b_o [D_out] / X_res [C, D_out] optional.
+    Returns Y fp64 [C, D_out].  act: 1 = SiLU x/(1+e^-x), 0 = identity.
+    """
+    T, O, W_g, W_o = _f64(T), _f64(O), _f64(W_g), _f64(W_o)
+    gamma, beta = _f64(gamma), _f64(beta)
+    Z = T @ W_g.T
+    if b_g is not None:
+        Z = Z + _f64(b_g)[None, :]
+    G = Z / (1.0 + np.exp(-Z)) if act == 1 else Z
+    mean = O.mean(axis=1, keepdims=True)
+    var = ((O - mean) ** 2).mean(axis=1, keepdims=True)
+    N = (O - mean) / np.sqrt(var + eps) * gamma[None, :] + beta[None, :]
+    Y = (N * G) @ W_o.T
+    if b_o is not None:
+        Y = Y + _f64(b_o)[None, :]
+    if X_res is not None:
+        Y = Y + _f64(X_res)
+    return Y
