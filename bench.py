@@ -193,34 +193,50 @@ def main():
     act = cfg.act
 
     ev = {k: [] for k in ("kv0", "kv1", "t1", "h0", "h1")}
+    # where gesr_hma_count runs: "fork" = first, on a side stream joined by an event;
+    # "kv" = forked after the K/V projection; "serial" = on the main stream after the attention
+    hma_order = os.environ.get("GESR_HMA_ORDER", "fork")
 
     def step(record=False):
         E = (lambda: torch.cuda.Event(enable_timing=True)) if record else None
         if record:
             e_h0, e_h1, e_kv0, e_kv1, e_t1 = E(), E(), E(), E(), E()
-        bufs.ev_fork.record(main_stream)
-        bufs.hma_stream.wait_event(bufs.ev_fork)
-        if record:
-            e_h0.record(bufs.hma_stream)
-        gb.hma_count(batch.user_ids, batch.user_offsets, batch.item_ids, batch.item_offsets,
-                     batch.cand_offsets, cfg.F, 0, counts=bufs.counts, stream=bufs.hma_stream)
-        if record:
-            e_h1.record(bufs.hma_stream)
-        bufs.ev_join.record(bufs.hma_stream)
+        def hma(stream):
+            if record:
+                e_h0.record(stream)
+            gb.hma_count(batch.user_ids, batch.user_offsets, batch.item_ids, batch.item_offsets,
+                         batch.cand_offsets, cfg.F, 0, counts=bufs.counts, stream=stream)
+            if record:
+                e_h1.record(stream)
+
+        def fork():
+            bufs.ev_fork.record(main_stream)
+            bufs.hma_stream.wait_event(bufs.ev_fork)
+            hma(bufs.hma_stream)
+            bufs.ev_join.record(bufs.hma_stream)
+
+        if hma_order == "fork":
+            fork()
         if record:
             e_kv0.record(main_stream)
         gb.kv_project(batch.U, batch.W_k, batch.W_v, cfg.H, cfg.d, act, K_cache=bufs.K,
                       V_cache=bufs.V, stream=main_stream)
         if record:
             e_kv1.record(main_stream)
+        if hma_order == "kv":
+            fork()
         gb.tasa_score(batch.T, batch.cand_offsets, batch.W_q, bufs.K, bufs.V, batch.seq_offsets,
                       cfg.H, cfg.d, act, O=bufs.O, want_lse=False, workspace=bufs.workspace,
                       stream=main_stream)
         if record:
             e_t1.record(main_stream)
+        if hma_order == "serial":
+            hma(main_stream)
+        else:
+            main_stream.wait_event(bufs.ev_join)
+        if record:
             for k, e in (("kv0", e_kv0), ("kv1", e_kv1), ("t1", e_t1), ("h0", e_h0), ("h1", e_h1)):
                 ev[k].append(e)
-        main_stream.wait_event(bufs.ev_join)
 
     launches_per_step = 5  # hma + kv proj + (build_units + q proj + attention)
 

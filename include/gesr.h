@@ -152,6 +152,39 @@ gesr_status gesr_tasa_score_self(const void* T, int64_t total_C, int32_t D_in,
                                  void* workspace, size_t workspace_bytes,
                                  void* stream);
 
+/* gesr_stu_output -- the rest of the STU layer's candidate row after the attention (SURVEY
+ * s8(f) f1; "layer output = output-projection(normalize(attention.value) (.)
+ * gating-branch) + residual", the paper deferring STU internals to HSTU, PAPER.md:229;
+ * DESIGN.md reading R15).  For every candidate row t (D = H*d):
+ *   G[t]  = SiLU(T[t] W_g^T + b_g)                                  gating branch, [D]
+ *   N[t]  = (O[t] - mean(O[t])) / sqrt(var(O[t]) + ln_eps) * ln_gamma + ln_beta
+ *           (mean and population variance over the D features of the concatenated heads)
+ *   Y[t]  = (N[t] (.) G[t]) W_o^T + b_o + X_res[t]
+ *   T          bf16 [total_C, D_in]: the candidate rows the gating branch projects (the same
+ *              normalised rows gesr_tasa_score projects to queries).
+ *   O          [total_C, D] fp32 or bf16 (o_dtype): attention.value from gesr_tasa_score.
+ *   W_g        bf16 [D, D_in] (nn.Linear layout); b_g fp32 [D] or NULL.
+ *   ln_gamma, ln_beta  fp32 [D]; ln_eps >= 0 and finite.
+ *   W_o        bf16 [D_out, D]; b_o fp32 [D_out] or NULL.
+ *   X_res      bf16 [total_C, D_out] residual (the layer input), or NULL (no residual).
+ *   D_out      a multiple of 32 in [32, 16384]; H*d a multiple of 32 and <= 16384.
+ *   Y          bf16 [total_C, D_out] (written).
+ *   workspace  device scratch of >= gesr_stu_workspace_bytes(total_C, H, d) bytes (G, then
+ *              the normalised, gated rows in place); clobbered.
+ * Precision: bf16 operands, fp32 accumulation and normalisation statistics, G and N(.)G rounded
+ * to bf16 (RNE) before the output projection, Y rounded to bf16.  Rows are independent
+ * (bit-identical for any batch composition).  Alignment: every pointer 16-byte aligned.
+ * Errors as the other calls; total_C = 0 is a no-op. */
+size_t gesr_stu_workspace_bytes(int64_t total_C, int32_t H, int32_t d);
+gesr_status gesr_stu_output(const void* T, int64_t total_C, int32_t D_in,
+                            const void* O, int32_t o_dtype,
+                            const void* W_g, const float* b_g,
+                            const float* ln_gamma, const float* ln_beta, float ln_eps,
+                            const void* W_o, const float* b_o, const void* X_res,
+                            int32_t H, int32_t d, int32_t D_out,
+                            void* Y, void* workspace, size_t workspace_bytes,
+                            void* stream);
+
 /* gesr_hma_count -- HMA per-field match counts.
  *   user_ids / user_offsets  int64 CSR: segment b*F+f is request b's user-side ID list of
  *              field f; user_offsets has B*F+1 entries.

@@ -302,7 +302,8 @@ def _f64(x) -> np.ndarray:
     return a.astype(np.float64)
 
 
-def stu_output(T, O, W_g, gamma, beta, W_o, b_g=None, b_o=None, X_res=None, eps=1e-5, act=1):
+def stu_output(T, O, W_g, gamma, beta, W_o, b_g=None, b_o=None, X_res=None, eps=1e-5, act=1,
+               round_bf16=False, parts=False):
     """Candidate rows of one STU layer after the attention, in SPEC.md:343's order (the paper
     defers STU internals to HSTU; reading R15):
 
@@ -318,6 +319,9 @@ def stu_output(T, O, W_g, gamma, beta, W_o, b_g=None, b_o=None, X_res=None, eps=
     T [C, D_in], O [C, D] (attention.value, heads concatenated), W_g [D, D_in],
     gamma/beta [D], W_o [D_out, D], b_g [D] / b_o [D_out] / X_res [C, D_out] optional.
     Returns Y fp64 [C, D_out].  act: 1 = SiLU x/(1+e^-x), 0 = identity.
+    Diagnostic only (not the parity reference): ``round_bf16`` rounds G, N*G and Y to bf16
+    (RNE) where the GPU path stores them, separating kernel bugs from quantisation; ``parts``
+    also returns (N, G).
     """
     T, O, W_g, W_o = _f64(T), _f64(O), _f64(W_g), _f64(W_o)
     gamma, beta = _f64(gamma), _f64(beta)
@@ -325,12 +329,19 @@ def stu_output(T, O, W_g, gamma, beta, W_o, b_g=None, b_o=None, X_res=None, eps=
     if b_g is not None:
         Z = Z + _f64(b_g)[None, :]
     G = Z / (1.0 + np.exp(-Z)) if act == 1 else Z
+    if round_bf16:
+        G = round_to_bf16(G)
     mean = O.mean(axis=1, keepdims=True)
     var = ((O - mean) ** 2).mean(axis=1, keepdims=True)
     N = (O - mean) / np.sqrt(var + eps) * gamma[None, :] + beta[None, :]
-    Y = (N * G) @ W_o.T
+    NG = N * G
+    if round_bf16:
+        NG = round_to_bf16(NG)
+    Y = NG @ W_o.T
     if b_o is not None:
         Y = Y + _f64(b_o)[None, :]
     if X_res is not None:
         Y = Y + _f64(X_res)
-    return Y
+    if round_bf16:
+        Y = round_to_bf16(Y)
+    return (Y, N, G) if parts else Y

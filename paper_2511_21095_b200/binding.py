@@ -73,6 +73,11 @@ def lib():
     L.gesr_hma_count_embed.restype = ctypes.c_int
     L.gesr_hma_count_embed.argtypes = [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _i32, _i32, _vp, _vp,
                                        _i32, _vp, _vp]
+    L.gesr_stu_workspace_bytes.restype = ctypes.c_size_t
+    L.gesr_stu_workspace_bytes.argtypes = [_i64, _i32, _i32]
+    L.gesr_stu_output.restype = ctypes.c_int
+    L.gesr_stu_output.argtypes = [_vp, _i64, _i32, _vp, _i32, _vp, _vp, _vp, _vp, ctypes.c_float,
+                                  _vp, _vp, _vp, _i32, _i32, _i32, _vp, _vp, ctypes.c_size_t, _vp]
     _lib = L
     return L
 
@@ -170,6 +175,30 @@ def tasa_score(T, cand_offsets, W_q, K_cache, V_cache, seq_offsets, H: int, d: i
     return O, lse
 
 
+def stu_workspace_bytes(total_C: int, H: int, d: int) -> int:
+    return int(lib().gesr_stu_workspace_bytes(total_C, H, d))
+
+
+def stu_output(T, O, W_g, ln_gamma, ln_beta, W_o, H: int, d: int, b_g=None, b_o=None,
+               X_res=None, ln_eps: float = 1e-5, Y=None, workspace=None, stream=None):
+    """Y bf16 [total_C, D_out] = (LayerNorm(O) * SiLU(T W_g^T + b_g)) W_o^T + b_o + X_res
+    (gesr_stu_output: the STU layer's candidate row after the attention)."""
+    _dev(T, O, W_g, ln_gamma, ln_beta, W_o, b_g, b_o, X_res, Y, workspace)
+    total_C, D_in = T.shape
+    D_out = W_o.shape[0]
+    if Y is None:
+        Y = torch.empty((total_C, D_out), dtype=torch.bfloat16, device=T.device)
+    o_dtype = GESR_OUT_BF16 if O.dtype == torch.bfloat16 else GESR_OUT_F32
+    if workspace is None:
+        workspace = torch.empty(max(stu_workspace_bytes(total_C, H, d), 256), dtype=torch.uint8,
+                                device=T.device)
+    _check(lib().gesr_stu_output(_ptr(T), total_C, D_in, _ptr(O), o_dtype, _ptr(W_g), _ptr(b_g),
+                                 _ptr(ln_gamma), _ptr(ln_beta), float(ln_eps), _ptr(W_o),
+                                 _ptr(b_o), _ptr(X_res), H, d, D_out, _ptr(Y), _ptr(workspace),
+                                 workspace.numel(), _stream(stream)))
+    return Y
+
+
 def hma_count(user_ids, user_offsets, item_ids, item_offsets, cand_offsets, F: int, cap: int = 0,
               counts=None, stream=None):
     """counts int32 [total_C, F] (gesr_hma_count)."""
@@ -223,19 +252,32 @@ class StepBuffers:
 
 
 def score_step(batch, bufs: StepBuffers, act: int = GESR_ACT_SILU, cap: int = 0,
-               chunk: int = 0, hma: bool = True, stream=None):
+               chunk: int = 0, hma: bool = True, stream=None, hma_order=None):
     """One scoring step: gesr_kv_project -> gesr_tasa_score (optionally in candidate chunks
-    reusing one K/V cache), with gesr_hma_count on a second stream joined by an event."""
+    reusing one K/V cache), with gesr_hma_count on a second stream joined by an event.
+    hma_order (default $GESR_HMA_ORDER or "fork"): "fork" launches HMA first on the side
+    stream, "kv" forks it after the K/V projection is enqueued, "serial" runs it on the main
+    stream after the attention."""
     cfg = batch.cfg
     main = torch.cuda.current_stream() if stream is None else stream
-    if hma:
+    order = hma_order or os.environ.get("GESR_HMA_ORDER", "fork")
+
+    def _hma(s):
+        hma_count(batch.user_ids, batch.user_offsets, batch.item_ids, batch.item_offsets,
+                  batch.cand_offsets, cfg.F, cap, counts=bufs.counts, stream=s)
+
+    def _fork():
         bufs.ev_fork.record(main)
         bufs.hma_stream.wait_event(bufs.ev_fork)
-        hma_count(batch.user_ids, batch.user_offsets, batch.item_ids, batch.item_offsets,
-                  batch.cand_offsets, cfg.F, cap, counts=bufs.counts, stream=bufs.hma_stream)
+        _hma(bufs.hma_stream)
         bufs.ev_join.record(bufs.hma_stream)
+
+    if hma and order == "fork":
+        _fork()
     kv_project(batch.U, batch.W_k, batch.W_v, cfg.H, cfg.d, act, K_cache=bufs.K, V_cache=bufs.V,
                stream=main)
+    if hma and order == "kv":
+        _fork()
     if chunk and batch.B == 1:
         # config 4: the same user's cache reused across candidate chunks (one call per chunk)
         for c0 in range(0, batch.total_C, chunk):
@@ -253,6 +295,8 @@ def score_step(batch, bufs: StepBuffers, act: int = GESR_ACT_SILU, cap: int = 0,
         tasa_score(batch.T, batch.cand_offsets, batch.W_q, bufs.K, bufs.V, batch.seq_offsets,
                    cfg.H, cfg.d, act, O=bufs.O, lse=bufs.lse, want_lse=bufs.lse is not None,
                    workspace=bufs.workspace, stream=main)
-    if hma:
+    if hma and order == "serial":
+        _hma(main)
+    elif hma:
         main.wait_event(bufs.ev_join)
     return bufs.O, bufs.counts

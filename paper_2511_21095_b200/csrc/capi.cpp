@@ -187,6 +187,44 @@ gesr_status run_projection(const void* X, int64_t M, int32_t K, const void* W0, 
   return GESR_OK;
 }
 
+// Row-major projection (STU gating branch and output projection): X [M, K] -> out [M, N]
+// = act(X W^T + b) (+ residual [M, N]), through a {N, M, 1} output map (one "head").
+gesr_status run_projection_rm(const void* X, int64_t M, int32_t K, const void* W, const float* b,
+                              int32_t N, int32_t act, const void* residual, void* out,
+                              cudaStream_t stream) {
+  const int bn = gesr::proj_pick_bn(N);
+  CUtensorMap ma, mb, mo;
+  gesr_status s = make_map_2d(&ma, X, static_cast<uint64_t>(M), static_cast<uint64_t>(K), 128, 64,
+                              CU_TENSOR_MAP_SWIZZLE_128B, "X");
+  if (s != GESR_OK) return s;
+  s = make_map_2d(&mb, W, N, K, bn / 2, 64, CU_TENSOR_MAP_SWIZZLE_128B, "W");
+  if (s != GESR_OK) return s;
+  s = make_out_map(&mo, out, 1, M, N, "out");
+  if (s != GESR_OK) return s;
+  gesr::ProjParams p{};
+  p.M = M;
+  p.K = K;
+  p.n_split = N;
+  p.d = 32;                      // unused: row-major output has no head split
+  p.act = act;
+  p.num_m_blocks = static_cast<int>((M + 255) / 256);
+  p.num_n_blocks = N / bn;
+  p.bias0 = b;
+  p.bias1 = b;
+  p.out0 = static_cast<__nv_bfloat16*>(out);
+  p.out1 = nullptr;
+  p.rowmajor = 1;
+  p.residual = static_cast<const __nv_bfloat16*>(residual);
+  p.res_ld = N;
+  cudaError_t e = gesr::launch_proj(ma, mb, mb, mo, mo, p, bn, num_sms(), stream);
+  if (e != cudaSuccess) return cuda_fail(e, "proj_kernel launch (row-major)");
+  return GESR_OK;
+}
+
+size_t stu_buffer_bytes(int64_t total_C, int64_t D) {
+  return (static_cast<size_t>(total_C) * D * 2 + 1023) & ~static_cast<size_t>(1023);
+}
+
 }  // namespace
 
 extern "C" {
@@ -485,6 +523,56 @@ gesr_status gesr_hma_count_embed(const int64_t* user_ids, const int64_t* user_of
   if (!E) return fail(GESR_ERR_INVALID_ARG, "null embedding table");
   return hma_impl(user_ids, user_offsets, item_ids, item_offsets, cand_offsets, B, total_C, F, M,
                   counts, E, D_h, emb, stream);
+}
+
+size_t gesr_stu_workspace_bytes(int64_t total_C, int32_t H, int32_t d) {
+  if (total_C < 0 || H < 1 || !valid_d(d)) return 0;
+  return stu_buffer_bytes(total_C, static_cast<int64_t>(H) * d);
+}
+
+gesr_status gesr_stu_output(const void* T, int64_t total_C, int32_t D_in, const void* O,
+                            int32_t o_dtype, const void* W_g, const float* b_g,
+                            const float* ln_gamma, const float* ln_beta, float ln_eps,
+                            const void* W_o, const float* b_o, const void* X_res, int32_t H,
+                            int32_t d, int32_t D_out, void* Y, void* workspace,
+                            size_t workspace_bytes, void* stream) {
+  gesr_status s = check_common(D_in, H, d, GESR_ACT_SILU);
+  if (s != GESR_OK) return s;
+  const int64_t D = static_cast<int64_t>(H) * d;
+  if (total_C < 0) return fail(GESR_ERR_INVALID_ARG, "total_C=%lld < 0", (long long)total_C);
+  if (D_out < 32 || D_out > 16384 || (D_out % 32) != 0)
+    return fail(GESR_ERR_INVALID_ARG, "D_out=%d must be a multiple of 32 in [32, 16384]", D_out);
+  if (D % 32 != 0 || D > 16384)
+    return fail(GESR_ERR_INVALID_ARG, "H*d=%lld must be a multiple of 32 and <= 16384", (long long)D);
+  if (o_dtype != GESR_OUT_F32 && o_dtype != GESR_OUT_BF16)
+    return fail(GESR_ERR_INVALID_ARG, "o_dtype=%d is not a gesr_out_dtype", o_dtype);
+  if (!(ln_eps >= 0.0f) || !std::isfinite(ln_eps))
+    return fail(GESR_ERR_INVALID_ARG, "ln_eps must be finite and >= 0");
+  if (total_C >= (int64_t(1) << 31))
+    return fail(GESR_ERR_INVALID_ARG, "total_C exceeds the 2^31 TMA coordinate range");
+  if (total_C == 0) return GESR_OK;
+  if (!T || !O || !W_g || !ln_gamma || !ln_beta || !W_o || !Y)
+    return fail(GESR_ERR_INVALID_ARG, "null required pointer");
+  if (!aligned16(T) || !aligned16(O) || !aligned16(W_g) || !aligned16(b_g) ||
+      !aligned16(ln_gamma) || !aligned16(ln_beta) || !aligned16(W_o) || !aligned16(b_o) ||
+      !aligned16(X_res) || !aligned16(Y) || !aligned16(workspace))
+    return fail(GESR_ERR_INVALID_ARG, "pointers must be 16-byte aligned");
+  const size_t need = stu_buffer_bytes(total_C, D);
+  if (!workspace || workspace_bytes < need)
+    return fail(GESR_ERR_WORKSPACE, "workspace of %zu bytes < %zu needed", workspace_bytes, need);
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // 1. gating branch G = SiLU(T W_g^T + b_g), row-major [total_C, D] bf16 in the workspace
+  s = run_projection_rm(T, total_C, D_in, W_g, b_g, static_cast<int32_t>(D), GESR_ACT_SILU,
+                        nullptr, workspace, st);
+  if (s != GESR_OK) return s;
+  // 2. Z = (LayerNorm(O) gamma + beta) * G, in place over G
+  cudaError_t e = gesr::launch_ln_gate(O, o_dtype == GESR_OUT_BF16 ? 1 : 0,
+                                       static_cast<__nv_bfloat16*>(workspace), ln_gamma, ln_beta,
+                                       ln_eps, total_C, static_cast<int>(D), st);
+  if (e != cudaSuccess) return cuda_fail(e, "ln_gate_kernel launch");
+  // 3. Y = Z W_o^T + b_o + X_res
+  return run_projection_rm(workspace, total_C, static_cast<int32_t>(D), W_o, b_o, D_out,
+                           GESR_ACT_IDENTITY, X_res, Y, st);
 }
 
 }  // extern "C"

@@ -23,6 +23,11 @@ struct ProjParams {
   const float* bias1;
   __nv_bfloat16* out0;   // [H, M, d]
   __nv_bfloat16* out1;   // [H, M, d] or null
+  // row-major output (out0 [M, N] through a {N, M, 1} map): columns are not split into heads
+  int rowmajor;
+  // optional residual added after the activation: out[r][c] += residual[r * res_ld + c]
+  const __nv_bfloat16* residual;
+  int64_t res_ld;
 };
 
 int proj_pick_bn(int n_split);
@@ -74,6 +79,12 @@ cudaError_t launch_attn_self_merge(const AttnParams& p, const void* Q, const voi
 // merges split-L partials: O = sum_s w_s O_s / sum_s w_s, w_s = l_s 2^(m_s - max m)
 cudaError_t launch_attn_combine(const AttnParams& p, int d, cudaStream_t stream);
 cudaError_t launch_attn_empty(const AttnParams& p, int d, cudaStream_t stream);
+
+// ---------------------------------------------------------------- K-STU (stu.cu)
+// Z[t][:] = LayerNorm(O[t][:]) * gamma + beta, times G[t][:] (in place over G), D = H*d
+// features per row (R15).  O fp32 or bf16 [C, D]; G bf16 [C, D].
+cudaError_t launch_ln_gate(const void* O, int o_bf16, __nv_bfloat16* G, const float* gamma,
+                           const float* beta, float eps, int64_t C, int D, cudaStream_t stream);
 
 // ---------------------------------------------------------------- K-HMA (hma.cu)
 struct HmaParams {

@@ -276,6 +276,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int i = 0; i < 32; i += 2) silu2(v[i], v[i + 1]);
         }
+        if (p.residual != nullptr) {
+          // out = act(.) + residual (STU layer output): this lane's row, 32 columns
+          const int64_t rr = static_cast<int64_t>(row0) + lane;
+          if (rr < p.M) {
+            const uint4* src = reinterpret_cast<const uint4*>(p.residual + rr * p.res_ld + within);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const uint4 u = __ldg(src + q);
+              const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                v[8 * q + 2 * e] += __uint_as_float(w[e] << 16);
+                v[8 * q + 2 * e + 1] += __uint_as_float(w[e] & 0xFFFF0000u);
+              }
+            }
+          }
+        }
         uint32_t packed[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) packed[i] = pack_bf16x2(v[2 * i], v[2 * i + 1]);
@@ -295,7 +312,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-          const int h = within >> dshift;
+          const int h = p.rowmajor ? 0 : within >> dshift;
           tma_store_3d(which ? &map_o1 : &map_o0, box, within - (h << dshift), row0, h);
           bulk_commit_group();
         }

@@ -149,3 +149,25 @@ def test_hma_embed_validation(L):
     assert emb(out=None) == gb.GESR_ERR_INVALID_ARG
     assert emb(out=MIS) == gb.GESR_ERR_INVALID_ARG
 
+
+
+def test_stu_output_validation(L):
+    def stu(T=FAKE, C=10, D_in=64, O=FAKE, odt=0, Wg=FAKE, bg=None, g=FAKE, b=FAKE, eps=1e-5,
+            Wo=FAKE, bo=None, X=None, H=2, d=64, D_out=128, Y=FAKE, ws=FAKE, wsb=1 << 30):
+        return L.gesr_stu_output(T, C, D_in, O, odt, Wg, bg, g, b, eps, Wo, bo, X, H, d, D_out,
+                                 Y, ws, wsb, None)
+    assert stu(d=48) == gb.GESR_ERR_INVALID_ARG
+    assert stu(D_out=48) == gb.GESR_ERR_INVALID_ARG
+    assert "D_out=48" in L.gesr_last_error().decode()
+    assert stu(odt=3) == gb.GESR_ERR_INVALID_ARG
+    assert stu(eps=-1.0) == gb.GESR_ERR_INVALID_ARG
+    assert stu(eps=float("nan")) == gb.GESR_ERR_INVALID_ARG
+    assert stu(C=-1) == gb.GESR_ERR_INVALID_ARG
+    assert stu(g=None) == gb.GESR_ERR_INVALID_ARG
+    assert stu(Wo=None) == gb.GESR_ERR_INVALID_ARG
+    assert stu(X=MIS) == gb.GESR_ERR_INVALID_ARG
+    assert stu(wsb=16) == gb.GESR_ERR_WORKSPACE
+    assert stu(C=0, T=None) == gb.GESR_OK                # empty problem: valid no-op
+    # G then the gated rows in place: total_C * H * d bf16, 1 KB granular
+    assert gb.stu_workspace_bytes(1000, 4, 128) == (1000 * 512 * 2 + 1023) // 1024 * 1024
+    assert gb.stu_workspace_bytes(10, 2, 48) == 0

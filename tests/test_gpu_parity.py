@@ -434,6 +434,17 @@ def test_hma_duplicates_and_long_lists():
         assert np.array_equal(_hma_gpu(bt, cfg.F, cap), want)
 
 
+def test_hma_oversized_groups_and_empty_item_lists():
+    # item lists of 0..32 IDs: some 32-segment groups exceed the per-warp staging buffer
+    # (512 IDs) and read their IDs from global memory; empty item lists count 0
+    cfg = configs.get("2").with_(B=6, item_len=(0, 32), vocab=256, F=5)
+    bt = inputs.make_batch(cfg, attention=False, hma_duplicates=True)
+    for cap in (0, 3):
+        want = oracle.hma_count(bt.user_ids, bt.user_offsets, bt.item_ids, bt.item_offsets,
+                                bt.cand_offsets, cfg.F, cap=cap)
+        assert np.array_equal(_hma_gpu(bt, cfg.F, cap), want)
+
+
 def test_hma_edge_ids_and_empty():
     dev = _cuda()
     F = 2

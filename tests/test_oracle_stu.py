@@ -119,3 +119,22 @@ def test_identity_activation_and_bf16_bits_input():
     N = (c["O"] - c["O"].mean(1, keepdims=True)) / np.sqrt(c["O"].var(1, keepdims=True) + 1e-5)
     want = (N * c["gamma"] + c["beta"]) * (T16.double().numpy() @ c["W_g"].T) @ c["W_o"].T
     np.testing.assert_allclose(a, want, rtol=0, atol=1e-12)
+
+
+def test_rounding_aware_mode_within_the_bf16_bound():
+    # diagnostic mode: G, N*G and Y rounded to bf16; differs from fp64 by at most the rounding
+    # bound the GPU tolerance uses, and equals it where nothing rounds (zero gate: Y = X_res
+    # with bf16-exact residual and no output bias)
+    c = _case(C=40, D_in=32, D=64, D_out=48, seed=5)
+    kw = dict(b_g=c["b_g"], b_o=c["b_o"], X_res=c["X_res"])
+    Y, N, G = oracle.stu_output(c["T"], c["O"], c["W_g"], c["gamma"], c["beta"], c["W_o"],
+                                parts=True, **kw)
+    Yr = oracle.stu_output(c["T"], c["O"], c["W_g"], c["gamma"], c["beta"], c["W_o"],
+                           round_bf16=True, **kw)
+    assert not np.array_equal(Y, Yr)
+    bound = 2.0 ** -8 * np.abs(Y) + 2.0 ** -8 * (np.abs(N * G) @ np.abs(c["W_o"]).T)
+    assert (np.abs(Yr - Y) <= bound).all()
+    X16 = torch.tensor(c["X_res"]).to(torch.bfloat16).double().numpy()
+    Yz = oracle.stu_output(c["T"], c["O"], np.zeros_like(c["W_g"]), c["gamma"], c["beta"],
+                           c["W_o"], X_res=X16, round_bf16=True)
+    assert np.array_equal(Yz, X16)
