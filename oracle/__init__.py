@@ -19,6 +19,9 @@ blocking/fusion), each citing the passage it follows:
 * :func:`offset_index` / :func:`hma_offset_embed` -- HMA embedding with feature-pair offsets,
   e = E(c + o(M+1)), concatenated over pairs.
   (stride M+1: DESIGN.md reading R14).  Plain numpy.
+* :func:`nro_cross_attention` -- NRO cross attention: j query slots, each gating the candidate
+  query input elementwise and attending over the request's RO rows with its own projections,
+  concatenated.  PAPER.md:373-380 (s3.4.3); SPEC.md:316-324 (reading R16).  Numpy.
 * :func:`stu_output` -- the rest of the STU layer's candidate row after the attention (SURVEY
   s8(f) f1): gating branch, normalisation of attention.value, output projection, residual.
   SPEC.md:343 (PAPER.md:229 defers the STU internals to HSTU); reading R15.  Plain
@@ -345,3 +348,49 @@ def stu_output(T, O, W_g, gamma, beta, W_o, b_g=None, b_o=None, X_res=None, eps=
     if round_bf16:
         Y = round_to_bf16(Y)
     return (Y, N, G) if parts else Y
+
+
+def nro_cross_attention(T, cand_offsets, W_q, q_gate, U, seq_offsets, W_k, W_v, j, d, act=1,
+                        b_q=None, b_k=None, b_v=None, scale=None):
+    """T_cross = Concat_s Attn_nro(Q_s, RO, RO) (PAPER.md:373-380, s3.4.3; SPEC.md:316-324;
+    DESIGN.md reading R16), in the paper's order, slot by slot:
+
+      gate        x_s = x (.) g_s                   (elementwise query gate, "query-modulation")
+      query       q_s = act(x_s W_{Q,s}^T + b_{Q,s})                 W_q rows [s d, (s+1) d)
+      key/value   K_s = act(U W_{K,s}^T + b_{K,s}),  V_s = act(U W_{V,s}^T + b_{V,s})  (RO rows)
+      attention   O_s = softmax(scale q_s K_s^T) V_s over the candidate's request's history rows
+      concat      T_cross[t] = [O_0[t], ..., O_{j-1}[t]]
+
+    T [total_C, D_in], U [total_L, D_in], W_q/W_k/W_v [j d, D_in], q_gate [j, D_in],
+    offsets int64 [B+1].  Returns fp64 [total_C, j d]; a request with no history rows gives
+    zero rows (reading R6).  scale defaults to 1/sqrt(d).
+    """
+    T, U = _f64(T), _f64(U)
+    Wq, Wk, Wv, g = _f64(W_q), _f64(W_k), _f64(W_v), _f64(q_gate)
+    co, so = _np(cand_offsets, np.int64), _np(seq_offsets, np.int64)
+    sc = (1.0 / np.sqrt(d)) if not scale or scale <= 0 else float(scale)
+
+    def act_(z):
+        return z / (1.0 + np.exp(-z)) if act == 1 else z
+
+    def lin(X, W, b, s):
+        Z = X @ W[s * d:(s + 1) * d].T
+        if b is not None:
+            Z = Z + _f64(b)[s * d:(s + 1) * d][None, :]
+        return act_(Z)
+
+    out = np.zeros((T.shape[0], j * d))
+    for s in range(j):
+        xs = T * g[s][None, :]
+        q = lin(xs, Wq, b_q, s)
+        K = lin(U, Wk, b_k, s)
+        V = lin(U, Wv, b_v, s)
+        for b in range(len(co) - 1):
+            c0, c1, r0, r1 = co[b], co[b + 1], so[b], so[b + 1]
+            if c1 == c0 or r1 == r0:
+                continue
+            S = sc * (q[c0:c1] @ K[r0:r1].T)
+            S = S - S.max(axis=1, keepdims=True)
+            P = np.exp(S)
+            out[c0:c1, s * d:(s + 1) * d] = (P @ V[r0:r1]) / P.sum(axis=1, keepdims=True)
+    return out
