@@ -185,6 +185,40 @@ gesr_status gesr_stu_output(const void* T, int64_t total_C, int32_t D_in,
                             void* Y, void* workspace, size_t workspace_bytes,
                             void* stream);
 
+/* gesr_nro_cross_score -- NRO cross attention (PAPER.md:373-380 s3.4.3 "each
+ * query is paired with an independent attention mechanism, specialized via separate weight
+ * matrices for query-modulation versus key-value relationships ... The resulting individual
+ * outputs are concatenated to form T_cross"; reading R16).  Each of
+ * the j query slots s gates the candidate query input elementwise, projects it with its own
+ * query weight and attends over the request's RO (history) rows with its own key/value
+ * projections:
+ *   q_s = act((x (.) g_s) W_{Q,s}^T + b_{Q,s}),  O[t][s*d + i] = sum_r p_r V_s[r][i],
+ *   p = softmax_r(scale q_s . K_s[r]) over the request's L_b history rows.
+ *   T          bf16 [total_C, D_in]: the query inputs x (candidate embeddings, optionally
+ *              enriched by the caller).
+ *   W_q        bf16 [j*d, D_in]: slot s's query weight is rows [s*d, (s+1)*d).
+ *   q_gate     fp32 [j, D_in]: the slots' elementwise query gates g_s.
+ *   b_q        fp32 [j*d] or NULL.
+ *   K_cache, V_cache  bf16 [j, total_L, d]: gesr_kv_project of the history with the slots' key
+ *              / value weights stacked as heads (H := j).
+ *   O          [total_C, j*d] fp32 or bf16: T_cross, the slots concatenated in slot order.
+ *   workspace  >= gesr_nro_workspace_bytes(B, total_C, j, d, D_in, kv_splits) bytes,
+ *              256-byte aligned.
+ * The gate is folded into the query weight on the device (W'[s*d+i][k] = W_q[s*d+i][k] g_s[k],
+ * rounded to bf16), then the call runs gesr_tasa_score's path with H = j; every other argument,
+ * the tolerance and the error behaviour are gesr_tasa_score's (flags = 0). */
+size_t gesr_nro_workspace_bytes(int64_t B, int64_t total_C, int32_t j, int32_t d, int32_t D_in,
+                                int32_t kv_splits);
+gesr_status gesr_nro_cross_score(const void* T, int64_t total_C, int32_t D_in,
+                                 const int64_t* cand_offsets,
+                                 const void* W_q, const float* q_gate, const float* b_q,
+                                 int32_t act, const void* K_cache, const void* V_cache,
+                                 const int64_t* seq_offsets, int64_t B, int64_t total_L,
+                                 int32_t j, int32_t d, float scale, int32_t kv_splits,
+                                 void* O, int32_t o_dtype, float* lse,
+                                 void* workspace, size_t workspace_bytes,
+                                 void* stream);
+
 /* gesr_hma_count -- HMA per-field match counts.
  *   user_ids / user_offsets  int64 CSR: segment b*F+f is request b's user-side ID list of
  *              field f; user_offsets has B*F+1 entries.

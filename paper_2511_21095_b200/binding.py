@@ -7,6 +7,9 @@ without the built library, raises.
   kv_project(U, W_k, W_v, H, d, ...)      -> (K_cache, V_cache)   gesr_kv_project
   tasa_score(T, cand_offsets, W_q, K, V, seq_offsets, H, d, ...) -> (O, lse)   gesr_tasa_score
   hma_count(user_ids, user_offsets, item_ids, item_offsets, cand_offsets, F, cap) -> counts
+  nro_cross_score(T, cand_offsets, W_q, q_gate, K, V, seq_offsets, j, d) -> T_cross
+                                           gesr_nro_cross_score (NRO cross attention, f3)
+  stu_output(T, O, W_g, ln_gamma, ln_beta, W_o, H, d, ...) -> Y   gesr_stu_output (f1)
   score_step(batch)                        one full scoring step (the three calls; HMA on a
                                            second stream joined by an event)
 """
@@ -73,6 +76,12 @@ def lib():
     L.gesr_hma_count_embed.restype = ctypes.c_int
     L.gesr_hma_count_embed.argtypes = [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _i32, _i32, _vp, _vp,
                                        _i32, _vp, _vp]
+    L.gesr_nro_workspace_bytes.restype = ctypes.c_size_t
+    L.gesr_nro_workspace_bytes.argtypes = [_i64, _i64, _i32, _i32, _i32, _i32]
+    L.gesr_nro_cross_score.restype = ctypes.c_int
+    L.gesr_nro_cross_score.argtypes = [_vp, _i64, _i32, _vp, _vp, _vp, _vp, _i32, _vp, _vp, _vp,
+                                       _i64, _i64, _i32, _i32, ctypes.c_float, _i32, _vp, _i32,
+                                       _vp, _vp, ctypes.c_size_t, _vp]
     L.gesr_stu_workspace_bytes.restype = ctypes.c_size_t
     L.gesr_stu_workspace_bytes.argtypes = [_i64, _i32, _i32]
     L.gesr_stu_output.restype = ctypes.c_int
@@ -173,6 +182,37 @@ def tasa_score(T, cand_offsets, W_q, K_cache, V_cache, seq_offsets, H: int, d: i
                                  o_dtype, _ptr(lse), _ptr(workspace), workspace.numel(),
                                  _stream(stream)))
     return O, lse
+
+
+def nro_workspace_bytes(B: int, total_C: int, j: int, d: int, D_in: int,
+                        kv_splits: int = 0) -> int:
+    return int(lib().gesr_nro_workspace_bytes(B, total_C, j, d, D_in, kv_splits))
+
+
+def nro_cross_score(T, cand_offsets, W_q, q_gate, K_cache, V_cache, seq_offsets, j: int, d: int,
+                    act: int = GESR_ACT_SILU, b_q=None, scale: float = 0.0, kv_splits: int = 0,
+                    out_dtype=torch.float32, want_lse: bool = False, O=None, lse=None,
+                    workspace=None, stream=None):
+    """T_cross [total_C, j*d] (gesr_nro_cross_score: j gated query slots over the history K/V
+    cache [j, total_L, d] from kv_project with the slots' key/value weights as heads)."""
+    _dev(T, cand_offsets, W_q, q_gate, K_cache, V_cache, seq_offsets, b_q, O, lse, workspace)
+    total_C, D_in = T.shape
+    B = cand_offsets.numel() - 1
+    total_L = K_cache.shape[1]
+    if O is None:
+        O = torch.empty((total_C, j * d), dtype=out_dtype, device=T.device)
+    o_dtype = GESR_OUT_BF16 if O.dtype == torch.bfloat16 else GESR_OUT_F32
+    if lse is None and want_lse:
+        lse = torch.empty((total_C, j), dtype=torch.float32, device=T.device)
+    if workspace is None:
+        nbytes = nro_workspace_bytes(B, total_C, j, d, D_in, kv_splits)
+        workspace = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=T.device)
+    _check(lib().gesr_nro_cross_score(_ptr(T), total_C, D_in, _ptr(cand_offsets), _ptr(W_q),
+                                      _ptr(q_gate), _ptr(b_q), act, _ptr(K_cache),
+                                      _ptr(V_cache), _ptr(seq_offsets), B, total_L, j, d,
+                                      float(scale), kv_splits, _ptr(O), o_dtype, _ptr(lse),
+                                      _ptr(workspace), workspace.numel(), _stream(stream)))
+    return O
 
 
 def stu_workspace_bytes(total_C: int, H: int, d: int) -> int:

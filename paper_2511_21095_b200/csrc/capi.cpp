@@ -575,4 +575,47 @@ gesr_status gesr_stu_output(const void* T, int64_t total_C, int32_t D_in, const 
                            GESR_ACT_IDENTITY, X_res, Y, st);
 }
 
+static size_t nro_weight_offset(int64_t B, int64_t total_C, int32_t j, int32_t d,
+                                int32_t kv_splits) {
+  return (gesr_tasa_workspace_bytes(B, total_C, j, d, kv_splits) + 255) & ~static_cast<size_t>(255);
+}
+
+size_t gesr_nro_workspace_bytes(int64_t B, int64_t total_C, int32_t j, int32_t d, int32_t D_in,
+                                int32_t kv_splits) {
+  if (gesr_tasa_workspace_bytes(B, total_C, j, d, kv_splits) == 0 || D_in < 8) return 0;
+  return nro_weight_offset(B, total_C, j, d, kv_splits) +
+         static_cast<size_t>(j) * d * D_in * 2;
+}
+
+gesr_status gesr_nro_cross_score(const void* T, int64_t total_C, int32_t D_in,
+                                 const int64_t* cand_offsets, const void* W_q,
+                                 const float* q_gate, const float* b_q, int32_t act,
+                                 const void* K_cache, const void* V_cache,
+                                 const int64_t* seq_offsets, int64_t B, int64_t total_L,
+                                 int32_t j, int32_t d, float scale, int32_t kv_splits, void* O,
+                                 int32_t o_dtype, float* lse, void* workspace,
+                                 size_t workspace_bytes, void* stream) {
+  gesr_status s = check_common(D_in, j, d, act);
+  if (s != GESR_OK) return s;
+  if (B < 0 || total_C < 0 || total_L < 0)
+    return fail(GESR_ERR_INVALID_ARG, "B, total_C, total_L must be >= 0");
+  if (kv_splits < 0 || kv_splits > kMaxSplits)
+    return fail(GESR_ERR_INVALID_ARG, "kv_splits=%d outside [0, %d]", kv_splits, kMaxSplits);
+  if (total_C == 0 || B == 0) return GESR_OK;
+  if (!W_q || !q_gate || !workspace) return fail(GESR_ERR_INVALID_ARG, "null required pointer");
+  if (!aligned16(W_q) || !aligned16(q_gate) || (reinterpret_cast<uintptr_t>(workspace) & 255u))
+    return fail(GESR_ERR_INVALID_ARG, "misaligned pointer");
+  const size_t need = gesr_nro_workspace_bytes(B, total_C, j, d, D_in, kv_splits);
+  if (workspace_bytes < need)
+    return fail(GESR_ERR_WORKSPACE, "workspace %zu bytes < required %zu", workspace_bytes, need);
+  const size_t off = nro_weight_offset(B, total_C, j, d, kv_splits);
+  void* W_fold = static_cast<uint8_t*>(workspace) + off;
+  cudaError_t e = gesr::launch_fold_gate(W_q, q_gate, W_fold, j, d, D_in,
+                                         static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "fold_gate launch");
+  return tasa_impl(T, total_C, D_in, cand_offsets, W_fold, b_q, act, K_cache, V_cache,
+                   seq_offsets, B, total_L, j, d, scale, kv_splits, 0, nullptr, nullptr, O,
+                   o_dtype, lse, workspace, off, stream);
+}
+
 }  // extern "C"

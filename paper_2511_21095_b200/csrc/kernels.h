@@ -86,6 +86,12 @@ cudaError_t launch_attn_empty(const AttnParams& p, int d, cudaStream_t stream);
 cudaError_t launch_ln_gate(const void* O, int o_bf16, __nv_bfloat16* G, const float* gamma,
                            const float* beta, float eps, int64_t C, int D, cudaStream_t stream);
 
+// ---------------------------------------------------------------- NRO query gate (nro.cu)
+// out[s*d + i][k] = bf16(W_q[s*d + i][k] * gate[s][k]): the elementwise query gate of NRO
+// cross-attention slot s folded into its query weight (R16).
+cudaError_t launch_fold_gate(const void* W_q, const float* gate, void* out, int j, int d, int D_in,
+                             cudaStream_t stream);
+
 // ---------------------------------------------------------------- K-HMA (hma.cu)
 struct HmaParams {
   const int64_t* user_ids;

@@ -171,3 +171,19 @@ def test_stu_output_validation(L):
     # G then the gated rows in place: total_C * H * d bf16, 1 KB granular
     assert gb.stu_workspace_bytes(1000, 4, 128) == (1000 * 512 * 2 + 1023) // 1024 * 1024
     assert gb.stu_workspace_bytes(10, 2, 48) == 0
+
+
+def test_nro_cross_validation(L):
+    def nro(Wq=FAKE, g=FAKE, j=2, d=64, splits=0, ws=FAKE, wsb=1 << 30, C=10, B=2):
+        return L.gesr_nro_cross_score(FAKE, C, 64, FAKE, Wq, g, None, 1, FAKE, FAKE, FAKE, B, 10,
+                                      j, d, 0.0, splits, FAKE, 0, None, ws, wsb, None)
+    assert nro(g=None) == gb.GESR_ERR_INVALID_ARG
+    assert nro(g=MIS) == gb.GESR_ERR_INVALID_ARG
+    assert nro(j=0) == gb.GESR_ERR_INVALID_ARG
+    assert nro(d=96) == gb.GESR_ERR_INVALID_ARG
+    assert nro(splits=65) == gb.GESR_ERR_INVALID_ARG
+    assert nro(wsb=64) == gb.GESR_ERR_WORKSPACE
+    assert nro(C=0) == gb.GESR_OK
+    # the tasa workspace (256-aligned) followed by the folded query weight [j*d, D_in] bf16
+    t = (gb.tasa_workspace_bytes(2, 10, 2, 64) + 255) // 256 * 256
+    assert gb.nro_workspace_bytes(2, 10, 2, 64, 64) == t + 2 * 64 * 64 * 2
