@@ -22,6 +22,9 @@ blocking/fusion), each citing the passage it follows:
 * :func:`nro_cross_attention` -- NRO cross attention: j query slots, each gating the candidate
   query input elementwise and attending over the request's RO rows with its own projections,
   concatenated.  PAPER.md:373-380 (s3.4.3); SPEC.md:316-324 (reading R16).  Numpy.
+* :func:`history_attention` -- causal self-attention of each user's history over itself (the U
+  rows of one [U, T] layer: mask rule (1); SPEC.md:277 user block lower-
+  triangular; reading R17).  Numpy.
 * :func:`stu_output` -- the rest of the STU layer's candidate row after the attention (SURVEY
   s8(f) f1): gating branch, normalisation of attention.value, output projection, residual.
   SPEC.md:343 (PAPER.md:229 defers the STU internals to HSTU); reading R15.  Plain
@@ -394,3 +397,48 @@ def nro_cross_attention(T, cand_offsets, W_q, q_gate, U, seq_offsets, W_k, W_v, 
             P = np.exp(S)
             out[c0:c1, s * d:(s + 1) * d] = (P @ V[r0:r1]) / P.sum(axis=1, keepdims=True)
     return out
+
+
+def history_attention(U, seq_offsets, W_q, W_k, W_v, H, d, act=1, b_q=None, b_k=None, b_v=None,
+                      scale=None):
+    """U rows of one target-aware layer (PAPER.md:341 mask rule (1): "user embeddings in U will
+    not attend to future positions"; the user block of the mask is lower-
+    triangular, diagonal included; reading R17).  Per request b, head h and history
+    position p (row r = seq_offsets[b] + p):
+
+      q, k, v = act(U W^T + b) split into heads            (as kv_project)
+      s_i = scale q_p . k_i for i <= p;  w_i = exp(s_i - max_i s_i)
+      O[r][h d:(h+1) d] = sum_i w_i v_i / sum_i w_i;  lse[r][h] = max + log sum_i w_i
+
+    U [total_L, D_in], W_* [H d, D_in].  Returns (O fp64 [total_L, H d], lse [total_L, H]).
+    """
+    U = _f64(U)
+    Wq, Wk, Wv = _f64(W_q), _f64(W_k), _f64(W_v)
+    so = _np(seq_offsets, np.int64)
+    sc = (1.0 / np.sqrt(d)) if not scale or scale <= 0 else float(scale)
+
+    def proj(W, b):
+        Z = U @ W.T
+        if b is not None:
+            Z = Z + _f64(b)[None, :]
+        return Z / (1.0 + np.exp(-Z)) if act == 1 else Z
+
+    Q, K, V = proj(Wq, b_q), proj(Wk, b_k), proj(Wv, b_v)
+    O = np.zeros((U.shape[0], H * d))
+    lse = np.zeros((U.shape[0], H))
+    for b in range(len(so) - 1):
+        r0, r1 = so[b], so[b + 1]
+        n = r1 - r0
+        if n == 0:
+            continue
+        allowed = np.tril(np.ones((n, n), bool))           # key i <= query p
+        for h in range(H):
+            cs = slice(h * d, (h + 1) * d)
+            S = sc * (Q[r0:r1, cs] @ K[r0:r1, cs].T)
+            S = np.where(allowed, S, -np.inf)
+            m = S.max(axis=1, keepdims=True)
+            w = np.exp(S - m)
+            l = w.sum(axis=1, keepdims=True)
+            O[r0:r1, cs] = (w @ V[r0:r1, cs]) / l
+            lse[r0:r1, h] = (m + np.log(l))[:, 0]
+    return O, lse
