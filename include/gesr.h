@@ -219,6 +219,30 @@ gesr_status gesr_nro_cross_score(const void* T, int64_t total_C, int32_t D_in,
                                  void* workspace, size_t workspace_bytes,
                                  void* stream);
 
+/* gesr_history_attention -- causal self-attention of every user's history over itself (SURVEY
+ * s8(f) f4: the U rows of one [U, T] layer, PAPER.md:341 mask rule (1) "user embeddings in U
+ * will not attend to future positions"; "user block lower-triangular", diagonal
+ * included; reading R17).  For history row r = seq_offsets[b] + p of request b and head
+ * h:
+ *   q = act(U[r] W_q^T + b_q)[h*d:(h+1)*d],
+ *   O[r][h*d + j] = sum_{i <= p} w_i V[h][seq_offsets[b] + i][j] / sum_{i <= p} w_i,
+ *   w_i = exp(scale q . K[h][seq_offsets[b] + i] - max).
+ *   U          bf16 [total_L, D_in]: the layer's (normalised) history rows.
+ *   K_cache, V_cache  bf16 [H, total_L, d]: gesr_kv_project of the same U -- the cache the
+ *              layer's candidates then attend to with gesr_tasa_score.
+ *   O          [total_L, H*d] fp32 or bf16; lse fp32 [total_L, H] or NULL.
+ *   workspace  >= gesr_tasa_workspace_bytes(B, total_L, H, d, 1) bytes, 256-byte aligned.
+ * Arguments, tolerance and errors as gesr_tasa_score with T := U, cand_offsets := seq_offsets,
+ * one key split (batch-invariant). */
+gesr_status gesr_history_attention(const void* U, int64_t total_L, int32_t D_in,
+                                   const int64_t* seq_offsets, int64_t B,
+                                   const void* W_q, const float* b_q, int32_t act,
+                                   const void* K_cache, const void* V_cache,
+                                   int32_t H, int32_t d, float scale,
+                                   void* O, int32_t o_dtype, float* lse,
+                                   void* workspace, size_t workspace_bytes,
+                                   void* stream);
+
 /* gesr_hma_count -- HMA per-field match counts.
  *   user_ids / user_offsets  int64 CSR: segment b*F+f is request b's user-side ID list of
  *              field f; user_offsets has B*F+1 entries.

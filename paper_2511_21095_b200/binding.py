@@ -10,6 +10,7 @@ without the built library, raises.
   nro_cross_score(T, cand_offsets, W_q, q_gate, K, V, seq_offsets, j, d) -> T_cross
                                            gesr_nro_cross_score (NRO cross attention, f3)
   stu_output(T, O, W_g, ln_gamma, ln_beta, W_o, H, d, ...) -> Y   gesr_stu_output (f1)
+  history_attention(U, seq_offsets, W_q, K, V, H, d) -> (O, lse)  gesr_history_attention (f4)
   score_step(batch)                        one full scoring step (the three calls; HMA on a
                                            second stream joined by an event)
 """
@@ -76,17 +77,19 @@ def lib():
     L.gesr_hma_count_embed.restype = ctypes.c_int
     L.gesr_hma_count_embed.argtypes = [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _i32, _i32, _vp, _vp,
                                        _i32, _vp, _vp]
-    L.gesr_nro_workspace_bytes.restype = ctypes.c_size_t
-    L.gesr_nro_workspace_bytes.argtypes = [_i64, _i64, _i32, _i32, _i32, _i32]
-    L.gesr_nro_cross_score.restype = ctypes.c_int
-    L.gesr_nro_cross_score.argtypes = [_vp, _i64, _i32, _vp, _vp, _vp, _vp, _i32, _vp, _vp, _vp,
-                                       _i64, _i64, _i32, _i32, ctypes.c_float, _i32, _vp, _i32,
-                                       _vp, _vp, ctypes.c_size_t, _vp]
-    L.gesr_stu_workspace_bytes.restype = ctypes.c_size_t
-    L.gesr_stu_workspace_bytes.argtypes = [_i64, _i32, _i32]
-    L.gesr_stu_output.restype = ctypes.c_int
-    L.gesr_stu_output.argtypes = [_vp, _i64, _i32, _vp, _i32, _vp, _vp, _vp, _vp, ctypes.c_float,
-                                  _vp, _vp, _vp, _i32, _i32, _i32, _vp, _vp, ctypes.c_size_t, _vp]
+    # entry points added after the first ABI: a GESR_LIB override (A/B of an older build) may
+    # lack them; the in-tree library must export every one (tests/test_boundary.py)
+    for name, res, args in (
+            ("gesr_nro_workspace_bytes", ctypes.c_size_t, [_i64, _i64, _i32, _i32, _i32, _i32]),
+            ("gesr_nro_cross_score", ctypes.c_int, [_vp, _i64, _i32, _vp, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _i64, _i64, _i32, _i32, ctypes.c_float, _i32, _vp, _i32, _vp, _vp, ctypes.c_size_t, _vp]),
+            ("gesr_history_attention", ctypes.c_int, [_vp, _i64, _i32, _vp, _i64, _vp, _vp, _i32, _vp, _vp, _i32, _i32, ctypes.c_float, _vp, _i32, _vp, _vp, ctypes.c_size_t, _vp]),
+            ("gesr_stu_workspace_bytes", ctypes.c_size_t, [_i64, _i32, _i32]),
+            ("gesr_stu_output", ctypes.c_int, [_vp, _i64, _i32, _vp, _i32, _vp, _vp, _vp, _vp, ctypes.c_float, _vp, _vp, _vp, _i32, _i32, _i32, _vp, _vp, ctypes.c_size_t, _vp]),
+    ):
+        if not hasattr(L, name) and os.environ.get("GESR_LIB"):
+            continue
+        getattr(L, name).restype = res
+        getattr(L, name).argtypes = args
     _lib = L
     return L
 
@@ -181,6 +184,30 @@ def tasa_score(T, cand_offsets, W_q, K_cache, V_cache, seq_offsets, H: int, d: i
                                  B, total_L, H, d, float(scale), kv_splits, flags, _ptr(O),
                                  o_dtype, _ptr(lse), _ptr(workspace), workspace.numel(),
                                  _stream(stream)))
+    return O, lse
+
+
+def history_attention(U, seq_offsets, W_q, K_cache, V_cache, H: int, d: int,
+                      act: int = GESR_ACT_SILU, b_q=None, scale: float = 0.0,
+                      out_dtype=torch.float32, want_lse: bool = False, O=None, lse=None,
+                      workspace=None, stream=None):
+    """O [total_L, H*d]: causal self-attention of every history over itself
+    (gesr_history_attention; K/V cache [H, total_L, d] from kv_project of the same U)."""
+    _dev(U, seq_offsets, W_q, K_cache, V_cache, b_q, O, lse, workspace)
+    total_L, D_in = U.shape
+    B = seq_offsets.numel() - 1
+    if O is None:
+        O = torch.empty((total_L, H * d), dtype=out_dtype, device=U.device)
+    o_dtype = GESR_OUT_BF16 if O.dtype == torch.bfloat16 else GESR_OUT_F32
+    if lse is None and want_lse:
+        lse = torch.empty((total_L, H), dtype=torch.float32, device=U.device)
+    if workspace is None:
+        nbytes = tasa_workspace_bytes(B, total_L, H, d, 1)
+        workspace = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=U.device)
+    _check(lib().gesr_history_attention(_ptr(U), total_L, D_in, _ptr(seq_offsets), B, _ptr(W_q),
+                                        _ptr(b_q), act, _ptr(K_cache), _ptr(V_cache), H, d,
+                                        float(scale), _ptr(O), o_dtype, _ptr(lse),
+                                        _ptr(workspace), workspace.numel(), _stream(stream)))
     return O, lse
 
 

@@ -121,7 +121,7 @@ __device__ __forceinline__ void exp2_poly2(float& y0, float& y1, float x0, float
   y1 = __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23));
 }
 
-template <int D>
+template <int D, bool kCausal>
 __global__ void __launch_bounds__(AttnCfg<D>::kThreads, 1)
     attn_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
                 const __grid_constant__ CUtensorMap map_v, const __grid_constant__ CUtensorMap map_o,
@@ -353,7 +353,10 @@ __global__ void __launch_bounds__(AttnCfg<D>::kThreads, 1)
       const Work x = decode(w, nx);              // descriptor fetched one unit ahead
       if (w + static_cast<int>(gridDim.x) < W) nx = fetch(w + gridDim.x);
       if (i >= x.nq) continue;
-      const int L = x.L, nkv = x.nkv, rows_valid = x.rows_valid, h = x.h;
+      // causal: this row sees keys [0, L - rows_valid + row] only
+      int L = x.L;
+      if constexpr (kCausal) L = min(x.L, x.L - x.rows_valid + row_in_unit + 1);
+      const int nkv = x.nkv, rows_valid = x.rows_valid, h = x.h;
       const int64_t cbeg = x.cbeg;
       float m_run = -INFINITY;
       float l = 0.f;
@@ -569,7 +572,8 @@ __global__ void __launch_bounds__(AttnCfg<D>::kThreads, 1)
 // valid rows}, so the attention kernel decodes a unit with a single 16-byte load.
 __global__ void build_units_kernel(const int64_t* __restrict__ seq_offsets,
                                    const int64_t* __restrict__ cand_offsets, int64_t B,
-                                   int4* __restrict__ units, int* __restrict__ count) {
+                                   int4* __restrict__ units, int* __restrict__ count,
+                                   int causal) {
   __shared__ int warp_sums[32];
   __shared__ int running;
   const int lane = threadIdx.x & 31;
@@ -609,6 +613,8 @@ __global__ void build_units_kernel(const int64_t* __restrict__ seq_offsets,
     const int excl = running + (x - n) + (w > 0 ? warp_sums[w - 1] : 0);
     for (int k = 0; k < n; ++k) {
       const int64_t rem = c - static_cast<int64_t>(k) * kUnitRows;
+      // causal: queries [256 k, 256 k + rows) of the history see keys up to the last of them
+      if (causal) L = static_cast<int64_t>(k) * kUnitRows + (rem < kUnitRows ? rem : kUnitRows);
       units[excl + k] = make_int4(static_cast<int>(s0), static_cast<int>(L),
                                   static_cast<int>(cb0 + static_cast<int64_t>(k) * kUnitRows),
                                   static_cast<int>(rem < kUnitRows ? rem : kUnitRows));
@@ -680,8 +686,11 @@ cudaError_t launch_d(const CUtensorMap& mq, const CUtensorMap& mk, const CUtenso
   using C = AttnCfg<D>;
   static bool attr_done = false;
   if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(attn_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         C::kSmemBytes);
+    cudaError_t e = cudaFuncSetAttribute(attn_kernel<D, false>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(attn_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             C::kSmemBytes);
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
@@ -690,7 +699,10 @@ cudaError_t launch_d(const CUtensorMap& mq, const CUtensorMap& mk, const CUtenso
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t work = max_units * p.H;
   const unsigned grid = static_cast<unsigned>(work < sms ? work : sms);
-  attn_kernel<D><<<grid, C::kThreads, C::kSmemBytes, stream>>>(mq, mk, mv, mo, p);
+  if (p.causal)
+    attn_kernel<D, true><<<grid, C::kThreads, C::kSmemBytes, stream>>>(mq, mk, mv, mo, p);
+  else
+    attn_kernel<D, false><<<grid, C::kThreads, C::kSmemBytes, stream>>>(mq, mk, mv, mo, p);
   return cudaGetLastError();
 }
 
@@ -703,8 +715,8 @@ extern "C" int gesr_debug_trace_copy(void* host) {
 #endif
 
 cudaError_t launch_build_units(const int64_t* seq_offsets, const int64_t* cand_offsets, int64_t B,
-                               int4* units, int* count, cudaStream_t stream) {
-  build_units_kernel<<<1, 1024, 0, stream>>>(seq_offsets, cand_offsets, B, units, count);
+                               int4* units, int* count, int causal, cudaStream_t stream) {
+  build_units_kernel<<<1, 1024, 0, stream>>>(seq_offsets, cand_offsets, B, units, count, causal);
   return cudaGetLastError();
 }
 

@@ -152,6 +152,9 @@ struct Work {
   int64_t s0, cbeg;
 };
 
+// kCausal: history self-attention (gesr_history_attention); a separate instantiation keeps the
+// target-aware kernel's code unchanged
+template <bool kCausal>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     attn_pair_kernel(const __grid_constant__ CUtensorMap map_q,
                      const __grid_constant__ CUtensorMap map_kh,
@@ -493,7 +496,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const Work x = decode(w, nx);
       if (w + npairs < W) nx = fetch(w + npairs);
       const int nkv = x.nkv;
-      const int L = x.L - kKeys * x.t0;                // keys from this work item's first tile
+      // keys from this work item's first tile; causal (t0 = 0): row 128 rank + rloc of the
+      // unit sees keys [0, L - rows + row] only
+      int L = x.L - kKeys * x.t0;
+      if constexpr (kCausal) L = min(x.L, x.L - x.rows_valid + 128 * static_cast<int>(rank) + rloc + 1);
       if (nkv == 0) continue;                          // the epilogue warps write O = 0
       const uint32_t tO = tmem + lane_addr + kTO + (m & 1) * kD;   // this unit's O
       float m_loc = -INFINITY;
@@ -903,8 +909,11 @@ cudaError_t launch_attn_pair(const CUtensorMap& mq, const CUtensorMap& mkh, cons
                              cudaStream_t stream) {
   static int max_pairs = 0;
   if (max_pairs == 0) {
-    cudaError_t e = cudaFuncSetAttribute(attn_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         kSmemBytes);
+    cudaError_t e = cudaFuncSetAttribute(attn_pair_kernel<false>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(attn_pair_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kSmemBytes);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr;
@@ -918,7 +927,7 @@ cudaError_t launch_attn_pair(const CUtensorMap& mq, const CUtensorMap& mkh, cons
     cfg.attrs = &attr;
     cfg.numAttrs = 1;
     int clusters = 0;
-    e = cudaOccupancyMaxActiveClusters(&clusters, attn_pair_kernel, &cfg);
+    e = cudaOccupancyMaxActiveClusters(&clusters, attn_pair_kernel<false>, &cfg);
     if (e != cudaSuccess || clusters <= 0) {
       int dev = 0, sms = 148;
       cudaGetDevice(&dev);
@@ -930,7 +939,10 @@ cudaError_t launch_attn_pair(const CUtensorMap& mq, const CUtensorMap& mkh, cons
   }
   const int64_t work = max_units * p.H * p.splits;
   const unsigned pairs = static_cast<unsigned>(work < max_pairs ? work : max_pairs);
-  attn_pair_kernel<<<2 * pairs, kThreads, kSmemBytes, stream>>>(mq, mkh, mvh, mo, p);
+  if (p.causal)
+    attn_pair_kernel<true><<<2 * pairs, kThreads, kSmemBytes, stream>>>(mq, mkh, mvh, mo, p);
+  else
+    attn_pair_kernel<false><<<2 * pairs, kThreads, kSmemBytes, stream>>>(mq, mkh, mvh, mo, p);
   return cudaGetLastError();
 }
 

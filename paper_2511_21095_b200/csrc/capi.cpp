@@ -316,7 +316,8 @@ static gesr_status tasa_impl(const void* T, int64_t total_C, int32_t D_in, const
                       const void* V_cache, const int64_t* seq_offsets, int64_t B, int64_t total_L,
                       int32_t H, int32_t d, float scale, int32_t kv_splits, uint32_t flags,
                       const void* K_self, const void* V_self, void* O, int32_t o_dtype,
-                      float* lse, void* workspace, size_t workspace_bytes, void* stream) {
+                      float* lse, void* workspace, size_t workspace_bytes, void* stream,
+                      int causal = 0) {
   const bool self = K_self != nullptr || V_self != nullptr;
   gesr_status s = check_common(D_in, H, d, act);
   if (s != GESR_OK) return s;
@@ -329,6 +330,8 @@ static gesr_status tasa_impl(const void* T, int64_t total_C, int32_t D_in, const
     return fail(GESR_ERR_INVALID_ARG, "o_dtype=%d is not a gesr_out_dtype", o_dtype);
   if (kv_splits < 0 || kv_splits > kMaxSplits)
     return fail(GESR_ERR_INVALID_ARG, "kv_splits=%d outside [0, %d]", kv_splits, kMaxSplits);
+  if (causal && kv_splits > 1)
+    return fail(GESR_ERR_UNSUPPORTED, "kv_splits > 1 is not supported for causal attention");
   if (kv_splits > 1 && (d != 128 || !pair_attention_enabled()))
     return fail(GESR_ERR_UNSUPPORTED, "kv_splits > 1 needs d = 128 (CTA-pair attention kernel)");
   if ((flags & GESR_TASA_SELF_KEY) && !self)
@@ -394,13 +397,14 @@ static gesr_status tasa_impl(const void* T, int64_t total_C, int32_t D_in, const
 
   p.units = units;
   p.unit_count = count;
-  p.splits = pick_splits(B, total_C, total_L, H, d, kv_splits);
+  p.splits = causal ? 1 : pick_splits(B, total_C, total_L, H, d, kv_splits);
+  p.causal = causal;
 
   if (p.splits > 1) {
     p.part_ml = reinterpret_cast<float2*>(part);
     p.part_o = reinterpret_cast<float*>(part + split_ml_bytes(total_C, H, p.splits));
   }
-  cudaError_t e = gesr::launch_build_units(seq_offsets, cand_offsets, B, units, count, st);
+  cudaError_t e = gesr::launch_build_units(seq_offsets, cand_offsets, B, units, count, causal, st);
   if (e != cudaSuccess) return cuda_fail(e, "build_units launch");
   s = run_projection(T, total_C, D_in, W_q, nullptr, b_q, nullptr, H, d, act, Q, nullptr, st);
   if (s != GESR_OK) return s;
@@ -616,6 +620,18 @@ gesr_status gesr_nro_cross_score(const void* T, int64_t total_C, int32_t D_in,
   return tasa_impl(T, total_C, D_in, cand_offsets, W_fold, b_q, act, K_cache, V_cache,
                    seq_offsets, B, total_L, j, d, scale, kv_splits, 0, nullptr, nullptr, O,
                    o_dtype, lse, workspace, off, stream);
+}
+
+gesr_status gesr_history_attention(const void* U, int64_t total_L, int32_t D_in,
+                                   const int64_t* seq_offsets, int64_t B, const void* W_q,
+                                   const float* b_q, int32_t act, const void* K_cache,
+                                   const void* V_cache, int32_t H, int32_t d, float scale,
+                                   void* O, int32_t o_dtype, float* lse, void* workspace,
+                                   size_t workspace_bytes, void* stream) {
+  // the history rows are the queries: candidate offsets := sequence offsets, one split
+  return tasa_impl(U, total_L, D_in, seq_offsets, W_q, b_q, act, K_cache, V_cache, seq_offsets,
+                   B, total_L, H, d, scale, 1, 0, nullptr, nullptr, O, o_dtype, lse, workspace,
+                   workspace_bytes, stream, 1);
 }
 
 }  // extern "C"

@@ -56,12 +56,18 @@ struct AttnParams {
   int splits;
   float* part_o;           // [splits, total_C, H, d]
   float2* part_ml;         // [splits, total_C, H]
+  // causal self-attention over the history (gesr_history_attention): the queries are
+  // the history rows themselves; a unit {s0, L, first row, rows} covers query rows
+  // [L - rows, L) of its request and row r (0-based in the unit) sees keys [0, L - rows + r]
+  int causal;
 };
 
 constexpr int kUnitRows = 256;   // candidates per work unit (two 128-row Q tiles)
 
+// causal = 1: queries are the history rows (cand_offsets == seq_offsets), unit k of request b
+// is {s0, 256 k + rows, s0 + 256 k, rows} (keys up to the unit's last query row)
 cudaError_t launch_build_units(const int64_t* seq_offsets, const int64_t* cand_offsets, int64_t B,
-                               int4* units, int* count,
+                               int4* units, int* count, int causal,
                                cudaStream_t stream);
 // map_o: bf16 O as [total_C, H, d] (box {32, 1, 32}, 64B swizzle), used when p.o_tma
 cudaError_t launch_attn(int d, const CUtensorMap& map_q, const CUtensorMap& map_k,
