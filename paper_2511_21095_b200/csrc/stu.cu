@@ -10,7 +10,8 @@
 // B200 design: one warp per row, 16-byte vector loads (8 bf16 / 2x4 fp32 per chunk, chunk q of
 // a row at lane q mod 32: every warp instruction reads 512 contiguous bytes), two-pass mean and
 // variance in fp32 from the row held in registers (D <= 1024) or re-read through L1 (larger D),
-// Z written in place over G as bf16 (RNE).
+// the gate chunks loaded together with O (one DRAM round trip per row), Z written in place over
+// G as bf16 (RNE).
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -21,7 +22,6 @@ namespace gesr {
 namespace {
 
 constexpr int kWarpsPerCta = 8;
-constexpr int kRegChunks = 4;     // rows with D <= 32 * 8 * kRegChunks = 1024 stay in registers
 
 __device__ __forceinline__ void load8(const void* O, int o_bf16, int64_t idx, float* x) {
   if (o_bf16) {
@@ -46,11 +46,12 @@ __device__ __forceinline__ float warp_sum(float v) {
   return v;
 }
 
-// z = (x - mean) * rstd * gamma + beta, times the gate; 8 features at column c
+// z = (x - mean) * rstd * gamma + beta, times the gate gu (8 bf16, loaded by the caller);
+// 8 features at column c, written over the gate
 __device__ __forceinline__ void emit8(const float* x, float mean, float rstd, const float* gamma,
-                                      const float* beta, __nv_bfloat16* G, int64_t gidx, int c) {
+                                      const float* beta, __nv_bfloat16* G, int64_t gidx, int c,
+                                      const uint4 gu) {
   uint4* gp = reinterpret_cast<uint4*>(G + gidx);
-  const uint4 gu = *gp;
   const uint32_t gw[4] = {gu.x, gu.y, gu.z, gu.w};
   const float4 g0 = __ldg(reinterpret_cast<const float4*>(gamma + c));
   const float4 g1 = __ldg(reinterpret_cast<const float4*>(gamma + c) + 1);
@@ -71,7 +72,10 @@ __device__ __forceinline__ void emit8(const float* x, float mean, float rstd, co
   *gp = make_uint4(out[0], out[1], out[2], out[3]);
 }
 
-__global__ void __launch_bounds__(kWarpsPerCta * 32)
+// kRegChunks: 8-feature chunks per lane held in registers (rows with D <= 256 kRegChunks);
+// longer rows take the three-pass path
+template <int kRegChunks>
+__global__ void __launch_bounds__(kWarpsPerCta * 32, kRegChunks <= 2 ? 5 : 3)
     ln_gate_kernel(const void* __restrict__ O, int o_bf16, __nv_bfloat16* __restrict__ G,
                    const float* __restrict__ gamma, const float* __restrict__ beta, float eps,
                    int64_t C, int D) {
@@ -83,12 +87,21 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
   const float inv_d = 1.0f / static_cast<float>(D);
   if (nch <= 32 * kRegChunks) {
     float x[kRegChunks][8];
+    uint4 gq[kRegChunks];
     float s = 0.f;
+    // the row's gate chunks are loaded together with O, so the row costs one DRAM round trip
 #pragma unroll
     for (int k = 0; k < kRegChunks; ++k) {
       const int q = lane + 32 * k;
       if (q < nch) {
         load8(O, o_bf16, base + 8 * q, x[k]);
+        gq[k] = *reinterpret_cast<const uint4*>(G + base + 8 * q);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kRegChunks; ++k) {
+      const int q = lane + 32 * k;
+      if (q < nch) {
 #pragma unroll
         for (int e = 0; e < 8; ++e) s += x[k][e];
       }
@@ -107,7 +120,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
 #pragma unroll
     for (int k = 0; k < kRegChunks; ++k) {
       const int q = lane + 32 * k;
-      if (q < nch) emit8(x[k], mean, rstd, gamma, beta, G, base + 8 * q, 8 * q);
+      if (q < nch) emit8(x[k], mean, rstd, gamma, beta, G, base + 8 * q, 8 * q, gq[k]);
     }
     return;
   }
@@ -128,7 +141,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
   const float rstd = rsqrtf(warp_sum(v) * inv_d + eps);
   for (int q = lane; q < nch; q += 32) {
     load8(O, o_bf16, base + 8 * q, x);
-    emit8(x, mean, rstd, gamma, beta, G, base + 8 * q, 8 * q);
+    emit8(x, mean, rstd, gamma, beta, G, base + 8 * q, 8 * q,
+          *reinterpret_cast<const uint4*>(G + base + 8 * q));
   }
 }
 
@@ -138,8 +152,12 @@ cudaError_t launch_ln_gate(const void* O, int o_bf16, __nv_bfloat16* G, const fl
                            const float* beta, float eps, int64_t C, int D, cudaStream_t stream) {
   if (C <= 0) return cudaSuccess;
   const int64_t blocks = (C + kWarpsPerCta - 1) / kWarpsPerCta;
-  ln_gate_kernel<<<static_cast<unsigned>(blocks), kWarpsPerCta * 32, 0, stream>>>(
-      O, o_bf16, G, gamma, beta, eps, C, D);
+  if (D <= 512)
+    ln_gate_kernel<2><<<static_cast<unsigned>(blocks), kWarpsPerCta * 32, 0, stream>>>(
+        O, o_bf16, G, gamma, beta, eps, C, D);
+  else
+    ln_gate_kernel<4><<<static_cast<unsigned>(blocks), kWarpsPerCta * 32, 0, stream>>>(
+        O, o_bf16, G, gamma, beta, eps, C, D);
   return cudaGetLastError();
 }
 

@@ -9,3 +9,10 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"attn_pair|proj_kernel|hma_kernel" -s 4 -c 4 -o gpurun_out/prof_$TAG python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_full_$TAG.log 2>&1
 fi
 echo all_done
+if [ "${NCU_EXTRA:-0}" = "1" ]; then
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_stu_$TAG.csv python scripts/stu_bench.py --iters 2 > gpurun_out/ncu_stu_$TAG.log 2>&1
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_hist_$TAG.csv python scripts/history_bench.py --iters 2 > gpurun_out/ncu_hist_$TAG.log 2>&1
+timeout 120 python scripts/stu_bench.py > gpurun_out/stu_$TAG.json 2>&1
+timeout 120 python scripts/history_bench.py > gpurun_out/hist_$TAG.json 2>&1
+fi
+echo extra_done
