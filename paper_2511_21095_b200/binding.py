@@ -367,3 +367,111 @@ def score_step(batch, bufs: StepBuffers, act: int = GESR_ACT_SILU, cap: int = 0,
     elif hma:
         main.wait_event(bufs.ev_join)
     return bufs.O, bufs.counts
+
+
+class PipelinedHostScorer:
+    """End-to-end scoring of a HOST-resident batch (pinned CPU tensors) through the C ABI, with
+    the requests cut into chunks pipelined over three CUDA streams: while the kernels of chunk i
+    run, chunk i+1's inputs are copied host->device and chunk i-1's outputs device->host (the
+    copy engines of both directions and the SMs all busy).  Two device buffer sets alternate
+    between chunks.  Per chunk: gesr_kv_project -> gesr_tasa_score -> gesr_hma_count on the
+    compute stream.  Results land in the caller's pinned host O / counts.
+
+        sc = PipelinedHostScorer(host_batch, n_chunks=8, out_dtype=torch.bfloat16)
+        sc.run(h_O, h_counts)      # enqueues everything; torch.cuda.synchronize() to wait
+    """
+
+    def __init__(self, hb, n_chunks: int = 8, out_dtype=torch.bfloat16, act: int = GESR_ACT_SILU,
+                 cap: int = 0, device=None):
+        cfg = hb.cfg
+        self.cfg, self.act, self.cap, self.out_dtype = cfg, act, cap, out_dtype
+        dev = torch.device("cuda") if device is None else torch.device(device)
+        F, B = cfg.F, hb.B
+        so, co = hb.seq_offsets.tolist(), hb.cand_offsets.tolist()
+        uo, io = hb.user_offsets, hb.item_offsets
+        n_chunks = max(1, min(n_chunks, B))
+        edges = [B * k // n_chunks for k in range(n_chunks + 1)]
+        self.chunks = []
+        for b0, b1 in zip(edges[:-1], edges[1:]):
+            r0, r1, c0, c1 = so[b0], so[b1], co[b0], co[b1]
+            u0, u1 = int(uo[b0 * F]), int(uo[b1 * F])
+            i0, i1 = int(io[c0 * F]), int(io[c1 * F])
+            pin = lambda t: t.contiguous().pin_memory()   # noqa: E731
+            self.chunks.append(dict(
+                B=b1 - b0, rows=(r0, r1), cands=(c0, c1),
+                h_so=pin(hb.seq_offsets[b0:b1 + 1] - r0), h_co=pin(hb.cand_offsets[b0:b1 + 1] - c0),
+                h_uo=pin(uo[b0 * F:b1 * F + 1] - u0), h_io=pin(io[c0 * F:c1 * F + 1] - i0),
+                h_U=hb.U[r0:r1], h_T=hb.T[c0:c1], h_ui=hb.user_ids[u0:u1],
+                h_ii=hb.item_ids[i0:i1]))
+        mx = lambda k: max(c[k].shape[0] for c in self.chunks)   # noqa: E731
+        H, d = cfg.H, cfg.d
+        mB, mL, mC = max(c["B"] for c in self.chunks), mx("h_U"), mx("h_T")
+        ws = max(tasa_workspace_bytes(c["B"], c["h_T"].shape[0], H, d, 0) for c in self.chunks)
+        self.sets = []
+        for _ in range(2):
+            self.sets.append(dict(
+                so=torch.empty(mB + 1, dtype=torch.int64, device=dev),
+                co=torch.empty(mB + 1, dtype=torch.int64, device=dev),
+                uo=torch.empty(mB * F + 1, dtype=torch.int64, device=dev),
+                io=torch.empty(mC * F + 1, dtype=torch.int64, device=dev),
+                U=torch.empty(mL, cfg.D_in, dtype=torch.bfloat16, device=dev),
+                T=torch.empty(mC, cfg.D_in, dtype=torch.bfloat16, device=dev),
+                ui=torch.empty(mx("h_ui"), dtype=torch.int64, device=dev),
+                ii=torch.empty(mx("h_ii"), dtype=torch.int64, device=dev),
+                K=torch.empty(H * mL * d, dtype=torch.bfloat16, device=dev),   # [H, nL, d] views
+                V=torch.empty(H * mL * d, dtype=torch.bfloat16, device=dev),
+                O=torch.empty(mC, H * d, dtype=out_dtype, device=dev),
+                counts=torch.empty(mC, F, dtype=torch.int32, device=dev),
+                ws=torch.empty(max(ws, 256), dtype=torch.uint8, device=dev),
+                h2d=torch.cuda.Event(), done=torch.cuda.Event(), free=torch.cuda.Event()))
+        self.W = (hb.W_q.to(dev), hb.W_k.to(dev), hb.W_v.to(dev))
+        self.s_in = torch.cuda.Stream(device=dev)
+        self.s_out = torch.cuda.Stream(device=dev)
+        self.h2d_bytes = sum(c[k].numel() * c[k].element_size() for c in self.chunks
+                             for k in ("h_so", "h_co", "h_uo", "h_io", "h_U", "h_T", "h_ui", "h_ii"))
+
+    def run(self, h_O, h_counts, stream=None):
+        """Enqueue one end-to-end pass; h_O [total_C, H*d] and h_counts [total_C, F] pinned."""
+        cfg, (W_q, W_k, W_v) = self.cfg, self.W
+        main = torch.cuda.current_stream() if stream is None else stream
+        start = torch.cuda.Event()
+        start.record(main)
+        self.s_in.wait_event(start)
+        self.s_out.wait_event(start)
+        for i, c in enumerate(self.chunks):
+            s = self.sets[i % 2]
+            nL, nC = c["h_U"].shape[0], c["h_T"].shape[0]
+            nu, ni = c["h_ui"].shape[0], c["h_ii"].shape[0]
+            with torch.cuda.stream(self.s_in):
+                if i >= 2:
+                    self.s_in.wait_event(s["free"])
+                for dst, src, n in (("so", "h_so", c["B"] + 1), ("co", "h_co", c["B"] + 1),
+                                    ("uo", "h_uo", c["B"] * cfg.F + 1),
+                                    ("io", "h_io", nC * cfg.F + 1), ("U", "h_U", nL),
+                                    ("T", "h_T", nC), ("ui", "h_ui", nu), ("ii", "h_ii", ni)):
+                    s[dst][:n].copy_(c[src], non_blocking=True)
+                s["h2d"].record(self.s_in)
+            main.wait_event(s["h2d"])
+            U, T = s["U"][:nL], s["T"][:nC]
+            K = s["K"][:cfg.H * nL * cfg.d].view(cfg.H, nL, cfg.d)
+            V = s["V"][:cfg.H * nL * cfg.d].view(cfg.H, nL, cfg.d)
+            if nL > 0:
+                kv_project(U, W_k, W_v, cfg.H, cfg.d, self.act, K_cache=K, V_cache=V,
+                           stream=main)
+            O, cnt = s["O"][:nC], s["counts"][:nC]
+            tasa_score(T, s["co"][:c["B"] + 1], W_q, K, V,
+                       s["so"][:c["B"] + 1], cfg.H, cfg.d, self.act, O=O, want_lse=False,
+                       workspace=s["ws"], stream=main)
+            hma_count(s["ui"][:max(nu, 1)], s["uo"][:c["B"] * cfg.F + 1], s["ii"][:max(ni, 1)],
+                      s["io"][:nC * cfg.F + 1], s["co"][:c["B"] + 1], cfg.F, self.cap,
+                      counts=cnt, stream=main)
+            s["done"].record(main)
+            with torch.cuda.stream(self.s_out):
+                self.s_out.wait_event(s["done"])
+                c0, c1 = c["cands"]
+                h_O[c0:c1].copy_(O, non_blocking=True)
+                h_counts[c0:c1].copy_(cnt, non_blocking=True)
+                s["free"].record(self.s_out)
+        end = torch.cuda.Event()
+        end.record(self.s_out)
+        main.wait_event(end)

@@ -571,3 +571,28 @@ def test_hma_structured_ids(pattern):
     torch.cuda.synchronize()
     assert np.array_equal(c.cpu().numpy(), want)
     assert want.sum() > 0
+
+
+def test_pipelined_host_scorer_matches_score_step_exactly():
+    """End-to-end path (host-resident pinned inputs, request chunks pipelined over H2D / kernel /
+    D2H streams) gives the same O and counts as score_step on device-resident inputs: rows are
+    independent of batch composition (reading R9; no split-L at these sizes)."""
+    dev = _cuda()
+    cfg = configs.get("2")
+    bt = inputs.make_batch(cfg)
+    g = bt.to(dev)
+    bufs = gb.StepBuffers(g, out_dtype=torch.bfloat16)
+    O, counts = gb.score_step(g, bufs)
+    pin = lambda t: t.contiguous().pin_memory()   # noqa: E731
+    hb = inputs.Batch(cfg, bt.requests, pin(bt.seq_offsets), pin(bt.cand_offsets), pin(bt.U),
+                      pin(bt.T), bt.W_q, bt.W_k, bt.W_v, pin(bt.user_ids), pin(bt.user_offsets),
+                      pin(bt.item_ids), pin(bt.item_offsets))
+    for chunks in (1, 3, 5):
+        sc = gb.PipelinedHostScorer(hb, n_chunks=chunks, out_dtype=torch.bfloat16, device=dev)
+        h_O = torch.zeros(O.shape, dtype=O.dtype).pin_memory()
+        h_c = torch.zeros(counts.shape, dtype=torch.int32).pin_memory()
+        sc.run(h_O, h_c)
+        sc.run(h_O, h_c)           # twice: buffer sets reused across passes
+        torch.cuda.synchronize()
+        assert torch.equal(h_O, O.cpu()), chunks
+        assert torch.equal(h_c, counts.cpu()), chunks
