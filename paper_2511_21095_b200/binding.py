@@ -369,6 +369,29 @@ def score_step(batch, bufs: StepBuffers, act: int = GESR_ACT_SILU, cap: int = 0,
     return bufs.O, bufs.counts
 
 
+def plan_chunks(hb, n_chunks: int, pin: bool = False) -> list:
+    """Cut a host batch into n_chunks contiguous request ranges (host logic of
+    PipelinedHostScorer): per chunk the row / candidate ranges, the sliced inputs and the
+    offsets rebased to the chunk (seq, cand, user [b*F], item [t*F] offsets start at 0)."""
+    F, B = hb.cfg.F, hb.B
+    so, co = hb.seq_offsets.tolist(), hb.cand_offsets.tolist()
+    uo, io = hb.user_offsets, hb.item_offsets
+    n_chunks = max(1, min(n_chunks, B))
+    edges = [B * k // n_chunks for k in range(n_chunks + 1)]
+    fix = (lambda t: t.contiguous().pin_memory()) if pin else (lambda t: t.contiguous())
+    chunks = []
+    for b0, b1 in zip(edges[:-1], edges[1:]):
+        r0, r1, c0, c1 = so[b0], so[b1], co[b0], co[b1]
+        u0, u1 = int(uo[b0 * F]), int(uo[b1 * F])
+        i0, i1 = int(io[c0 * F]), int(io[c1 * F])
+        chunks.append(dict(
+            B=b1 - b0, reqs=(b0, b1), rows=(r0, r1), cands=(c0, c1),
+            h_so=fix(hb.seq_offsets[b0:b1 + 1] - r0), h_co=fix(hb.cand_offsets[b0:b1 + 1] - c0),
+            h_uo=fix(uo[b0 * F:b1 * F + 1] - u0), h_io=fix(io[c0 * F:c1 * F + 1] - i0),
+            h_U=hb.U[r0:r1], h_T=hb.T[c0:c1], h_ui=hb.user_ids[u0:u1], h_ii=hb.item_ids[i0:i1]))
+    return chunks
+
+
 class PipelinedHostScorer:
     """End-to-end scoring of a HOST-resident batch (pinned CPU tensors) through the C ABI, with
     the requests cut into chunks pipelined over three CUDA streams: while the kernels of chunk i
@@ -386,23 +409,8 @@ class PipelinedHostScorer:
         cfg = hb.cfg
         self.cfg, self.act, self.cap, self.out_dtype = cfg, act, cap, out_dtype
         dev = torch.device("cuda") if device is None else torch.device(device)
-        F, B = cfg.F, hb.B
-        so, co = hb.seq_offsets.tolist(), hb.cand_offsets.tolist()
-        uo, io = hb.user_offsets, hb.item_offsets
-        n_chunks = max(1, min(n_chunks, B))
-        edges = [B * k // n_chunks for k in range(n_chunks + 1)]
-        self.chunks = []
-        for b0, b1 in zip(edges[:-1], edges[1:]):
-            r0, r1, c0, c1 = so[b0], so[b1], co[b0], co[b1]
-            u0, u1 = int(uo[b0 * F]), int(uo[b1 * F])
-            i0, i1 = int(io[c0 * F]), int(io[c1 * F])
-            pin = lambda t: t.contiguous().pin_memory()   # noqa: E731
-            self.chunks.append(dict(
-                B=b1 - b0, rows=(r0, r1), cands=(c0, c1),
-                h_so=pin(hb.seq_offsets[b0:b1 + 1] - r0), h_co=pin(hb.cand_offsets[b0:b1 + 1] - c0),
-                h_uo=pin(uo[b0 * F:b1 * F + 1] - u0), h_io=pin(io[c0 * F:c1 * F + 1] - i0),
-                h_U=hb.U[r0:r1], h_T=hb.T[c0:c1], h_ui=hb.user_ids[u0:u1],
-                h_ii=hb.item_ids[i0:i1]))
+        F = cfg.F
+        self.chunks = plan_chunks(hb, n_chunks, pin=True)
         mx = lambda k: max(c[k].shape[0] for c in self.chunks)   # noqa: E731
         H, d = cfg.H, cfg.d
         mB, mL, mC = max(c["B"] for c in self.chunks), mx("h_U"), mx("h_T")
