@@ -10,12 +10,15 @@
 // B200 design (HBM-bound on the item-ID stream, ~8.5 int64 IDs per (candidate, field)):
 //   grid (B, Y): CTA (b, y) owns request b and candidate chunks y, y+Y, ... of `chunk` rows.
 //   1. The request's F user lists go into per-field open-addressing tables in shared memory:
-//      64-bit keys (INT64_MIN marks an empty slot; that one ID value is counted on the side)
-//      with their multiplicities in a parallel array.  Insertion is parallel (64-bit atomicCAS,
-//      linear probing); the home slot is the even slot of a multiplicative hash of the key's
-//      two 32-bit halves, and at load factor <= 1/4 a lookup almost always ends within that
-//      slot pair: ONE 16-byte shared load and two 64-bit compares, no fingerprint indirection.
-//      Fields whose tables do not fit the pool fall back to a direct scan of global memory.
+//      64-bit keys only (INT64_MIN marks an empty slot; that one ID value is counted on the side),
+//      every OCCURRENCE of a user ID in its own slot (parallel 64-bit atomicCAS, linear probing
+//      from the even slot of a multiplicative hash of the key's two 32-bit halves), >= 8 slots
+//      per ID when the 8192-slot pool allows (load factor <= 1/8), else >= 4.  All copies of a
+//      key lie between its home slot and the first empty slot after it, so a lookup COUNTS the
+//      matches in the 4-slot window of its home pair and the next (two 16-byte reads, no
+//      multiplicity array) and walks on only when the whole window is occupied -- rare enough at
+//      1/8 that the warp seldom executes the walk.  Fields whose tables do not fit the pool fall
+//      back to a direct scan of global memory.
 //   2. Each warp takes 32 consecutive (candidate, field) segments of the CSR item stream.
 //      Lane k writes its segment id into a per-warp owner map (one uint16 per ID position),
 //      then the warp reads the group's IDs COALESCED (lane l reads ID start + l + 32 i), looks
@@ -34,21 +37,20 @@ constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
 constexpr int kChunkMin = 256;            // candidates per CTA chunk (runtime: 256 or 1024)
 constexpr int kChunkMax = 1024;
-constexpr int kPoolSlots = 4096;          // table slots per CTA (32 KB keys + 16 KB counts)
+constexpr int kPoolSlots = 8192;          // table slots per CTA (64 KB of keys)
 constexpr int kMaxFields = 256;
 constexpr int kOwnerCap = 512;            // IDs per 32-segment group handled with the owner map
 constexpr unsigned long long kSentinel = 0x8000000000000000ull;   // INT64_MIN: empty slot
 constexpr uint32_t kMul = 0x9E3779B1u;
 
 struct HmaSmem {
-  unsigned long long key[kPoolSlots];             // kSentinel = empty
-  int cnt[kPoolSlots];
+  unsigned long long key[kPoolSlots];             // kSentinel = empty; one slot per occurrence
   int2 tab[kMaxFields];                           // {first slot, hash shift}; first < 0: global
   int sent_cnt[kMaxFields];                       // multiplicity of INT64_MIN
   long long uoff[kMaxFields + 1];                 // this request's user_offsets (F+1)
   int warp_cnt[kWarps][32];
   // owner word of each ID position of a warp's 32-segment group: segment lane (bits 0-4), the
-  // field's hash shift (5-9), its first table slot (10-21), the field (22-29)
+  // field's hash shift (5-9), its first table slot (10-22), the field (23-30)
   uint32_t owner[kWarps][kOwnerCap];
   int any_global;                                 // some field scans global memory instead
 };
@@ -60,22 +62,42 @@ __device__ __forceinline__ uint32_t home_pair(unsigned long long key, int shift)
   return h >> shift;
 }
 
+// Copies of `key` in a field's table (first slot `base`, 2^(32 - shift) slot pairs).  Every
+// occurrence of a user ID has its own slot, filled by linear probing from the even slot of its
+// home pair, so all copies lie between the home slot and the first empty slot after it: count
+// matches over the 4-slot window of the home pair and the next one (two 16-byte reads) and walk
+// on only if the whole window is occupied (rare at load factor <= 1/8).
+__device__ __forceinline__ int window_count(const unsigned long long* tb, uint32_t pr,
+                                            uint32_t pmask, unsigned long long key, bool& open) {
+  const ulonglong2 a = *reinterpret_cast<const ulonglong2*>(tb + 2 * pr);
+  const ulonglong2 b = *reinterpret_cast<const ulonglong2*>(tb + 2 * ((pr + 1) & pmask));
+  open = a.x != kSentinel && a.y != kSentinel && b.x != kSentinel && b.y != kSentinel;
+  return (a.x == key ? 1 : 0) + (a.y == key ? 1 : 0) + (b.x == key ? 1 : 0) + (b.y == key ? 1 : 0);
+}
+// the rest of the walk after a full window starting at pair pr
+__device__ __forceinline__ int walk_on(const unsigned long long* tb, uint32_t pr, uint32_t pmask,
+                                    unsigned long long key) {
+  int c = 0;
+  pr = (pr + 2) & pmask;
+  while (true) {
+    const ulonglong2 a = *reinterpret_cast<const ulonglong2*>(tb + 2 * pr);
+    c += (a.x == key ? 1 : 0) + (a.y == key ? 1 : 0);
+    if (a.x == kSentinel || a.y == kSentinel) return c;
+    pr = (pr + 1) & pmask;
+  }
+}
+
 __device__ __forceinline__ int lookup(const HmaSmem& s, const HmaParams& p, int f,
                                       unsigned long long key) {
   if (key == kSentinel) return s.sent_cnt[f];
   const int2 t = s.tab[f];
   if (t.x >= 0) {
     const uint32_t pmask = 0xFFFFFFFFu >> t.y;
-    uint32_t pr = home_pair(key, t.y);
-    while (true) {
-      const int sl = t.x + 2 * static_cast<int>(pr);
-      const ulonglong2 kk = *reinterpret_cast<const ulonglong2*>(&s.key[sl]);
-      if (kk.x == key) return s.cnt[sl];
-      if (kk.x == kSentinel) return 0;               // slots fill in probe order
-      if (kk.y == key) return s.cnt[sl + 1];
-      if (kk.y == kSentinel) return 0;
-      pr = (pr + 1) & pmask;
-    }
+    const uint32_t pr = home_pair(key, t.y);
+    bool open;
+    int c = window_count(s.key + t.x, pr, pmask, key, open);
+    if (open) c += walk_on(s.key + t.x, pr, pmask, key);
+    return c;
   }
   // global fallback: direct scan of the user list
   int c = 0;
@@ -106,8 +128,10 @@ __global__ void __launch_bounds__(kThreads, 2)
     s.any_global = 0;
     for (int f = 0; f < F; ++f) {
       const long long n = s.uoff[f + 1] - s.uoff[f];
-      int ns = 4, shift = 31;                         // >= 4n slots: load factor <= 1/4
-      while (ns < 4 * n && ns < kPoolSlots) { ns <<= 1; --shift; }
+      // >= 8n slots (load factor <= 1/8) when the pool allows, else >= 4n
+      int ns = 4, shift = 31;
+      while (ns < 8 * n && ns < kPoolSlots) { ns <<= 1; --shift; }
+      if (used + ns > kPoolSlots && ns >= 8 && 4 * n <= ns / 2) { ns >>= 1; ++shift; }
       if (4 * n <= ns && used + ns <= kPoolSlots) {
         s.tab[f] = make_int2(used, shift);           // ns / 2 = 2^(32 - shift) slot pairs
         used += ns;
@@ -118,10 +142,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       s.sent_cnt[f] = 0;
     }
   }
-  for (int i = tid; i < kPoolSlots; i += kThreads) {
-    s.key[i] = kSentinel;
-    s.cnt[i] = 0;
-  }
+  for (int i = tid; i < kPoolSlots; i += kThreads) s.key[i] = kSentinel;
   for (int i = tid; i < kWarps * 32; i += kThreads) (&s.warp_cnt[0][0])[i] = 0;
   __syncthreads();
   {
@@ -144,24 +165,18 @@ __global__ void __launch_bounds__(kThreads, 2)
       }
       const uint32_t smask = (0xFFFFFFFFu >> t.y) * 2 + 1;   // slots - 1
       uint32_t slot = home_pair(key, t.y) * 2;
-      while (true) {
-        const unsigned long long prev = atomicCAS(&s.key[t.x + slot], kSentinel, key);
-        if (prev == kSentinel || prev == key) {
-          atomicAdd(&s.cnt[t.x + slot], 1);
-          break;
-        }
-        slot = (slot + 1) & smask;
-      }
+      // every occurrence takes its own slot (a duplicate probes past its earlier copies)
+      while (atomicCAS(&s.key[t.x + slot], kSentinel, key) != kSentinel) slot = (slot + 1) & smask;
     }
   }
   __syncthreads();
 
   // ---- 2. coalesced scan of the item-ID stream, 32 segments per warp step.  The next group's
   //         offsets are fetched while the current group is processed, and all of a group's IDs
-  //         (kUnroll per lane) are loaded before the first lookup, so each warp keeps ~2 KB of
+  //         (kUnroll per lane) are loaded before the first lookup, so each warp keeps ~1 KB of
   //         loads in flight.
-  constexpr int kUnroll = 8;
-  constexpr int kBatch = 4;
+  constexpr int kUnroll = 4;
+  constexpr int kBatch = 2;
   uint32_t* own = s.owner[warp];
   for (int64_t c0 = first; c0 < ce; c0 += static_cast<int64_t>(gridDim.y) * chunk) {
     const int64_t c1 = (c0 + chunk < ce) ? c0 + chunk : ce;
@@ -193,7 +208,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         // owner words of this group's ID positions (one table-info read per segment)
         const int2 t = s.tab[my_f];
         const uint32_t ow = static_cast<uint32_t>(lane) | (static_cast<uint32_t>(t.y) << 5) |
-                            (static_cast<uint32_t>(t.x) << 10) | (static_cast<uint32_t>(my_f) << 22);
+                            (static_cast<uint32_t>(t.x) << 10) | (static_cast<uint32_t>(my_f) << 23);
         for (int base = 0; base < n_ids; base += kUnroll * 32) {
           unsigned long long kk[kUnroll];
 #pragma unroll
@@ -207,14 +222,14 @@ __global__ void __launch_bounds__(kThreads, 2)
             __syncwarp();
           }
           // batches of kBatch positions in straight-line code, so their shared-memory reads
-          // overlap: owner word -> home slot pair -> one 16-byte key read -> compare; a
-          // position not settled by its home pair (rare at load factor 1/4) probes on after
-          // the batch
+          // overlap: owner word -> home slot pair -> the 4-slot window (two 16-byte reads) ->
+          // count the key's copies; a position whose window is full (rare at load factor
+          // <= 1/8) walks on after the batch
 #pragma unroll
           for (int u0 = 0; u0 < kUnroll; u0 += kBatch) {
             if (base + u0 * 32 >= n_ids) break;          // warp-uniform
-            uint32_t o[kBatch];
-            int sl[kBatch], c[kBatch];
+            uint32_t o[kBatch], pr[kBatch];
+            int c[kBatch];
             bool open[kBatch];
 #pragma unroll
             for (int v = 0; v < kBatch; ++v) {
@@ -226,13 +241,11 @@ __global__ void __launch_bounds__(kThreads, 2)
               const unsigned long long key = kk[u0 + v];
               const int pos = base + (u0 + v) * 32 + lane;
               const int shift = static_cast<int>((o[v] >> 5) & 31u);
-              sl[v] = static_cast<int>((o[v] >> 10) & 4095u) + 2 * static_cast<int>(home_pair(key, shift));
-              const ulonglong2 kv = *reinterpret_cast<const ulonglong2*>(&s.key[sl[v]]);
-              const bool m0 = kv.x == key, m1 = kv.y == key;
-              c[v] = (m0 || m1) ? s.cnt[sl[v] + (m0 ? 0 : 1)] : 0;
-              open[v] = !(m0 || m1 || kv.x == kSentinel || kv.y == kSentinel);
+              pr[v] = home_pair(key, shift);
+              c[v] = window_count(s.key + ((o[v] >> 10) & 8191u), pr[v], 0xFFFFFFFFu >> shift,
+                                  key, open[v]);
               if (key == kSentinel) {                        // the empty marker's own ID value
-                c[v] = s.sent_cnt[o[v] >> 22];
+                c[v] = s.sent_cnt[o[v] >> 23];
                 open[v] = false;
               }
               if (pos >= n_ids) { c[v] = 0; open[v] = false; }
@@ -242,19 +255,10 @@ __global__ void __launch_bounds__(kThreads, 2)
             for (int v = 0; v < kBatch; ++v) any_open |= open[v];
             if (__any_sync(0xffffffffu, any_open)) {
 #pragma unroll
-              for (int v = 0; v < kBatch; ++v) {
-                if (open[v]) {
-                  const uint32_t smask = (0xFFFFFFFFu >> ((o[v] >> 5) & 31u)) * 2 + 1;
-                  const int off = static_cast<int>((o[v] >> 10) & 4095u);
-                  int q = (sl[v] - off + 2) & static_cast<int>(smask);
-                  while (true) {
-                    const unsigned long long kq = s.key[off + q];
-                    if (kq == kk[u0 + v]) { c[v] = s.cnt[off + q]; break; }
-                    if (kq == kSentinel) break;
-                    q = (q + 1) & static_cast<int>(smask);
-                  }
-                }
-              }
+              for (int v = 0; v < kBatch; ++v)
+                if (open[v])
+                  c[v] += walk_on(s.key + ((o[v] >> 10) & 8191u), pr[v],
+                                  0xFFFFFFFFu >> ((o[v] >> 5) & 31u), kk[u0 + v]);
             }
 #pragma unroll
             for (int v = 0; v < kBatch; ++v)
@@ -271,7 +275,7 @@ __global__ void __launch_bounds__(kThreads, 2)
           }
           if (base == 0) {
             if (lane < nseg)
-              for (int q = my_off; q < my_end; ++q) own[q] = static_cast<uint32_t>(lane) | (static_cast<uint32_t>(my_f) << 22);
+              for (int q = my_off; q < my_end; ++q) own[q] = static_cast<uint32_t>(lane) | (static_cast<uint32_t>(my_f) << 23);
             __syncwarp();
           }
 #pragma unroll 1
@@ -280,7 +284,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             const int pos = base + u * 32 + lane;
             if (pos < n_ids) {
               const uint32_t o = own[pos];
-              const int c = lookup(s, p, static_cast<int>(o >> 22), kk[u]);
+              const int c = lookup(s, p, static_cast<int>(o >> 23), kk[u]);
               if (c != 0) atomicAdd(&s.warp_cnt[warp][o & 31u], c);
             }
           }
