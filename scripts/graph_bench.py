@@ -1,4 +1,4 @@
-"""Configs 1 and 4 eager vs CUDA-graph capture, and config 4's K/V-cache reuse speedup.
+"""Configs 1, 2 and 4 eager vs CUDA-graph capture, and config 4's K/V-cache reuse speedup.
 
     python scripts/graph_bench.py [--iters 50]
 
@@ -40,7 +40,7 @@ def main():
     args = ap.parse_args()
     dev = torch.device("cuda:0")
     out = []
-    for name in ("1", "4"):
+    for name in ("1", "2", "4"):
         cfg = configs.get(name)
         bt = inputs.make_batch(cfg, device=dev)
         bufs = gb.StepBuffers(bt, out_dtype=torch.bfloat16)
