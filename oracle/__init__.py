@@ -25,6 +25,9 @@ blocking/fusion), each citing the passage it follows:
 * :func:`history_attention` -- causal self-attention of each user's history over itself (the U
   rows of one [U, T] layer: mask rule (1); SPEC.md:277 user block lower-
   triangular; reading R17).  Numpy.
+* :func:`stu_stack_forward` -- a stack of full target-aware STU layers over [U, T] per request
+  (SPEC.md:298 self_attention_forward, SPEC.md:343 layer internals, mask SPEC.md:277 with the
+  candidate diagonal; reading R18), brute force over the (N+n)^2 mask.  Numpy.
 * :func:`stu_output` -- the rest of the STU layer's candidate row after the attention (SURVEY
   s8(f) f1): gating branch, normalisation of attention.value, output projection, residual.
   SPEC.md:343 (PAPER.md:229 defers the STU internals to HSTU); reading R15.  Plain
@@ -442,3 +445,49 @@ def history_attention(U, seq_offsets, W_q, W_k, W_v, H, d, act=1, b_q=None, b_k=
             O[r0:r1, cs] = (w @ V[r0:r1, cs]) / l
             lse[r0:r1, h] = (m + np.log(l))[:, 0]
     return O, lse
+
+
+def stu_stack_forward(U, T, seq_offsets, cand_offsets, layers, H, d, eps=1e-5):
+    """[U_self, T_self] after len(layers) STU layers over [U, T], per request (SPEC.md:298
+    self_attention_forward; reading R18), brute force, in SPEC.md:343's order per layer:
+
+      Xn = LN_in(X)                                     "normalize input"
+      Q, K, V, G = SiLU(Xn W_q^T), SiLU(Xn W_k^T), SiLU(Xn W_v^T), SiLU(Xn W_g^T)
+      A = masked row-softmax(Q K^T / sqrt(d)) V per head, mask = build_mask(N, n, self_key=True)
+          (user block lower-triangular, candidates see all users and themselves)
+      X <- (LN_out(A) (.) G) W_o^T + X                  "output-projection(normalize(attention.
+                                                          value) (.) gating-branch) + residual"
+
+    layers: list of dicts with W_q, W_k, W_v, W_g, W_o [D, D] and ln_in / ln_out (gamma, beta)
+    [D]; D = H d.  Returns (U_out fp64 [total_L, D], T_out fp64 [total_C, D]).
+    """
+    U, T = _f64(U), _f64(T)
+    so, co = _np(seq_offsets, np.int64), _np(cand_offsets, np.int64)
+    D = H * d
+    Uo, To = np.zeros_like(U), np.zeros_like(T)
+
+    def ln(X, g, b):
+        mu = X.mean(axis=1, keepdims=True)
+        var = ((X - mu) ** 2).mean(axis=1, keepdims=True)
+        return (X - mu) / np.sqrt(var + eps) * _f64(g)[None, :] + _f64(b)[None, :]
+
+    def silu(Z):
+        return Z / (1.0 + np.exp(-Z))
+
+    for b in range(len(so) - 1):
+        N, n = int(so[b + 1] - so[b]), int(co[b + 1] - co[b])
+        X = np.concatenate([U[so[b]:so[b + 1]], T[co[b]:co[b + 1]]], axis=0)
+        allowed = build_mask(N, n, self_key=True).astype(bool)
+        for lay in layers:
+            Xn = ln(X, *lay["ln_in"])
+            Q, K = silu(Xn @ _f64(lay["W_q"]).T), silu(Xn @ _f64(lay["W_k"]).T)
+            V, G = silu(Xn @ _f64(lay["W_v"]).T), silu(Xn @ _f64(lay["W_g"]).T)
+            A = np.zeros_like(X)
+            for h in range(H):
+                cs = slice(h * d, (h + 1) * d)
+                S = np.where(allowed, (Q[:, cs] @ K[:, cs].T) / np.sqrt(d), -np.inf)
+                w = np.exp(S - S.max(axis=1, keepdims=True))
+                A[:, cs] = (w @ V[:, cs]) / w.sum(axis=1, keepdims=True)
+            X = (ln(A, *lay["ln_out"]) * G) @ _f64(lay["W_o"]).T + X
+        Uo[so[b]:so[b + 1]], To[co[b]:co[b + 1]] = X[:N], X[N:]
+    return Uo, To
