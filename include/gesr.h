@@ -243,6 +243,17 @@ gesr_status gesr_history_attention(const void* U, int64_t total_L, int32_t D_in,
                                    void* workspace, size_t workspace_bytes,
                                    void* stream);
 
+/* gesr_layer_norm -- the STU layer's input normalisation ("per layer -- normalize
+ * input"; reading R18): for every row r of X,
+ *   Y[r] = (X[r] - mean(X[r])) / sqrt(var(X[r]) + eps) * gamma + beta
+ * (population variance over the D features, fp32 statistics).
+ *   X, Y       bf16 [rows, D] (Y may alias X); D a multiple of 8 in [8, 16384].
+ *   gamma, beta  fp32 [D]; eps >= 0 and finite.  16-byte aligned pointers.
+ * With gesr_kv_project, gesr_history_attention, gesr_tasa_score_self and gesr_stu_output it
+ * composes one full target-aware STU layer over [U, T] (binding.stu_layer). */
+gesr_status gesr_layer_norm(const void* X, int64_t rows, int32_t D, const float* gamma,
+                            const float* beta, float eps, void* Y, void* stream);
+
 /* gesr_hma_count -- HMA per-field match counts.
  *   user_ids / user_offsets  int64 CSR: segment b*F+f is request b's user-side ID list of
  *              field f; user_offsets has B*F+1 entries.

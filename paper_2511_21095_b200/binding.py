@@ -11,6 +11,8 @@ without the built library, raises.
                                            gesr_nro_cross_score (NRO cross attention, f3)
   stu_output(T, O, W_g, ln_gamma, ln_beta, W_o, H, d, ...) -> Y   gesr_stu_output (f1)
   history_attention(U, seq_offsets, W_q, K, V, H, d) -> (O, lse)  gesr_history_attention (f4)
+  layer_norm(X, gamma, beta) -> Y                                gesr_layer_norm
+  stu_layer / stu_stack(U, T, ..., layers, H, d) -> (U', T')     full STU layers (composition)
   score_step(batch)                        one full scoring step (the three calls; HMA on a
                                            second stream joined by an event)
 """
@@ -84,6 +86,7 @@ def lib():
             ("gesr_nro_cross_score", ctypes.c_int, [_vp, _i64, _i32, _vp, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _i64, _i64, _i32, _i32, ctypes.c_float, _i32, _vp, _i32, _vp, _vp, ctypes.c_size_t, _vp]),
             ("gesr_history_attention", ctypes.c_int, [_vp, _i64, _i32, _vp, _i64, _vp, _vp, _i32, _vp, _vp, _i32, _i32, ctypes.c_float, _vp, _i32, _vp, _vp, ctypes.c_size_t, _vp]),
             ("gesr_stu_workspace_bytes", ctypes.c_size_t, [_i64, _i32, _i32]),
+            ("gesr_layer_norm", ctypes.c_int, [_vp, _i64, _i32, _vp, _vp, ctypes.c_float, _vp, _vp]),
             ("gesr_stu_output", ctypes.c_int, [_vp, _i64, _i32, _vp, _i32, _vp, _vp, _vp, _vp, ctypes.c_float, _vp, _vp, _vp, _i32, _i32, _i32, _vp, _vp, ctypes.c_size_t, _vp]),
     ):
         if not hasattr(L, name) and os.environ.get("GESR_LIB"):
@@ -264,6 +267,51 @@ def stu_output(T, O, W_g, ln_gamma, ln_beta, W_o, H: int, d: int, b_g=None, b_o=
                                  _ptr(b_o), _ptr(X_res), H, d, D_out, _ptr(Y), _ptr(workspace),
                                  workspace.numel(), _stream(stream)))
     return Y
+
+
+def layer_norm(X, gamma, beta, eps: float = 1e-5, Y=None, stream=None):
+    """Y bf16 [rows, D] = LayerNorm(X) * gamma + beta (gesr_layer_norm; Y may be X)."""
+    _dev(X, gamma, beta, Y)
+    rows, D = X.shape
+    if Y is None:
+        Y = torch.empty_like(X)
+    _check(lib().gesr_layer_norm(_ptr(X), rows, D, _ptr(gamma), _ptr(beta), float(eps), _ptr(Y),
+                                 _stream(stream)))
+    return Y
+
+
+def stu_layer(U, T, seq_offsets, cand_offsets, layer: dict, H: int, d: int, eps: float = 1e-5,
+              stream=None):
+    """One full target-aware STU layer over [U, T] (mask SPEC.md:277 with the
+    candidate diagonal; reading R18) as a sequence of C-ABI calls:
+      Un, Tn = layer_norm(U), layer_norm(T)                            input normalisation
+      K, V   = kv_project(Un)  (the cache), K_T, V_T = kv_project(Tn)  (candidate self keys)
+      O_U    = history_attention(Un, K, V)                             causal, rule (1)
+      O_T    = tasa_score_self(Tn, K, V, K_T, V_T)                     history + own key
+      U', T' = stu_output(Un, O_U, ..., X_res=U), stu_output(Tn, O_T, ..., X_res=T)
+    layer: W_q, W_k, W_v, W_g, W_o bf16 [D, D]; ln_in, ln_out (gamma, beta) fp32 [D].
+    Returns (U', T') bf16."""
+    act = GESR_ACT_SILU
+    Un = layer_norm(U, *layer["ln_in"], eps=eps, stream=stream)
+    Tn = layer_norm(T, *layer["ln_in"], eps=eps, stream=stream)
+    K, V = kv_project(Un, layer["W_k"], layer["W_v"], H, d, act, stream=stream)
+    K_T, V_T = kv_project(Tn, layer["W_k"], layer["W_v"], H, d, act, stream=stream)
+    O_U, _ = history_attention(Un, seq_offsets, layer["W_q"], K, V, H, d, act, stream=stream)
+    O_T, _ = tasa_score(Tn, cand_offsets, layer["W_q"], K, V, seq_offsets, H, d, act,
+                        want_lse=False, stream=stream, K_self=K_T, V_self=V_T)
+    U2 = stu_output(Un, O_U, layer["W_g"], *layer["ln_out"], layer["W_o"], H, d, X_res=U,
+                    ln_eps=eps, stream=stream)
+    T2 = stu_output(Tn, O_T, layer["W_g"], *layer["ln_out"], layer["W_o"], H, d, X_res=T,
+                    ln_eps=eps, stream=stream)
+    return U2, T2
+
+
+def stu_stack(U, T, seq_offsets, cand_offsets, layers, H: int, d: int, eps: float = 1e-5,
+              stream=None):
+    """[U_self, T_self] after len(layers) STU layers (SPEC.md:298 self_attention_forward)."""
+    for layer in layers:
+        U, T = stu_layer(U, T, seq_offsets, cand_offsets, layer, H, d, eps, stream)
+    return U, T
 
 
 def hma_count(user_ids, user_offsets, item_ids, item_offsets, cand_offsets, F: int, cap: int = 0,

@@ -634,4 +634,20 @@ gesr_status gesr_history_attention(const void* U, int64_t total_L, int32_t D_in,
                    workspace_bytes, stream, 1);
 }
 
+gesr_status gesr_layer_norm(const void* X, int64_t rows, int32_t D, const float* gamma,
+                            const float* beta, float eps, void* Y, void* stream) {
+  if (rows < 0) return fail(GESR_ERR_INVALID_ARG, "rows=%lld < 0", (long long)rows);
+  if (D < 8 || D > 16384 || (D % 8) != 0)
+    return fail(GESR_ERR_INVALID_ARG, "D=%d must be a multiple of 8 in [8, 16384]", D);
+  if (!(eps >= 0.0f) || !std::isfinite(eps))
+    return fail(GESR_ERR_INVALID_ARG, "eps must be finite and >= 0");
+  if (rows == 0) return GESR_OK;
+  if (!X || !gamma || !beta || !Y) return fail(GESR_ERR_INVALID_ARG, "null required pointer");
+  if (!aligned16(X) || !aligned16(gamma) || !aligned16(beta) || !aligned16(Y))
+    return fail(GESR_ERR_INVALID_ARG, "pointers must be 16-byte aligned");
+  cudaError_t e = gesr::launch_layer_norm(X, Y, gamma, beta, eps, rows, D,
+                                          static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? GESR_OK : cuda_fail(e, "layer_norm_kernel launch");
+}
+
 }  // extern "C"

@@ -92,6 +92,10 @@ cudaError_t launch_attn_empty(const AttnParams& p, int d, cudaStream_t stream);
 cudaError_t launch_ln_gate(const void* O, int o_bf16, __nv_bfloat16* G, const float* gamma,
                            const float* beta, float eps, int64_t C, int D, cudaStream_t stream);
 
+// Y[r] = LayerNorm(X[r]) * gamma + beta over D features, bf16 in / out (stu.cu; R18).
+cudaError_t launch_layer_norm(const void* X, void* Y, const float* gamma, const float* beta,
+                              float eps, int64_t rows, int D, cudaStream_t stream);
+
 // ---------------------------------------------------------------- NRO query gate (nro.cu)
 // out[s*d + i][k] = bf16(W_q[s*d + i][k] * gate[s][k]): the elementwise query gate of NRO
 // cross-attention slot s folded into its query weight (R16).

@@ -146,6 +146,74 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, kRegChunks <= 2 ? 5 : 3)
   }
 }
 
+// Plain row LayerNorm of bf16 rows (the STU layer's input normalisation, "normalize
+// input"; R18): Y[r] = (X[r] - mean) / sqrt(var + eps) * gamma + beta, bf16 out.
+// One warp per row, 16-byte loads, fp32 two-pass statistics from registers (D <= 1024) or
+// through L1 (larger D).
+template <int kRegChunks>
+__global__ void __launch_bounds__(kWarpsPerCta * 32)
+    layer_norm_kernel(const __nv_bfloat16* __restrict__ X, __nv_bfloat16* __restrict__ Y,
+                      const float* __restrict__ gamma, const float* __restrict__ beta, float eps,
+                      int64_t rows, int D) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * kWarpsPerCta + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const int nch = D >> 3;
+  const int64_t base = row * D;
+  const float inv_d = 1.0f / static_cast<float>(D);
+  const uint4 ones = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);  // bf16 1.0
+  auto emit = [&](const float* x, float mean, float rstd, int q) {
+    // emit8 multiplies by a gate: a gate of ones (exact) leaves (x - mean) rstd gamma + beta
+    emit8(x, mean, rstd, gamma, beta, Y, base + 8 * q, 8 * q, ones);
+  };
+  if (nch <= 32 * kRegChunks) {
+    float x[kRegChunks][8];
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < kRegChunks; ++k) {
+      const int q = lane + 32 * k;
+      if (q < nch) load8(X, 1, base + 8 * q, x[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < kRegChunks; ++k)
+      if (lane + 32 * k < nch) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) s += x[k][e];
+      }
+    const float mean = warp_sum(s) * inv_d;
+    float v = 0.f;
+#pragma unroll
+    for (int k = 0; k < kRegChunks; ++k)
+      if (lane + 32 * k < nch) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) { const float t = x[k][e] - mean; v += t * t; }
+      }
+    const float rstd = rsqrtf(warp_sum(v) * inv_d + eps);
+#pragma unroll
+    for (int k = 0; k < kRegChunks; ++k)
+      if (lane + 32 * k < nch) emit(x[k], mean, rstd, lane + 32 * k);
+    return;
+  }
+  float s = 0.f, x[8];
+  for (int q = lane; q < nch; q += 32) {
+    load8(X, 1, base + 8 * q, x);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) s += x[e];
+  }
+  const float mean = warp_sum(s) * inv_d;
+  float v = 0.f;
+  for (int q = lane; q < nch; q += 32) {
+    load8(X, 1, base + 8 * q, x);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) { const float t = x[e] - mean; v += t * t; }
+  }
+  const float rstd = rsqrtf(warp_sum(v) * inv_d + eps);
+  for (int q = lane; q < nch; q += 32) {
+    load8(X, 1, base + 8 * q, x);
+    emit(x, mean, rstd, q);
+  }
+}
+
 }  // namespace
 
 cudaError_t launch_ln_gate(const void* O, int o_bf16, __nv_bfloat16* G, const float* gamma,
@@ -158,6 +226,21 @@ cudaError_t launch_ln_gate(const void* O, int o_bf16, __nv_bfloat16* G, const fl
   else
     ln_gate_kernel<4><<<static_cast<unsigned>(blocks), kWarpsPerCta * 32, 0, stream>>>(
         O, o_bf16, G, gamma, beta, eps, C, D);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_layer_norm(const void* X, void* Y, const float* gamma, const float* beta,
+                              float eps, int64_t rows, int D, cudaStream_t stream) {
+  if (rows <= 0) return cudaSuccess;
+  const int64_t blocks = (rows + kWarpsPerCta - 1) / kWarpsPerCta;
+  const auto* x = static_cast<const __nv_bfloat16*>(X);
+  auto* y = static_cast<__nv_bfloat16*>(Y);
+  if (D <= 512)
+    layer_norm_kernel<2><<<static_cast<unsigned>(blocks), kWarpsPerCta * 32, 0, stream>>>(
+        x, y, gamma, beta, eps, rows, D);
+  else
+    layer_norm_kernel<4><<<static_cast<unsigned>(blocks), kWarpsPerCta * 32, 0, stream>>>(
+        x, y, gamma, beta, eps, rows, D);
   return cudaGetLastError();
 }
 
