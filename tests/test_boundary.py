@@ -187,3 +187,14 @@ def test_nro_cross_validation(L):
     # the tasa workspace (256-aligned) followed by the folded query weight [j*d, D_in] bf16
     t = (gb.tasa_workspace_bytes(2, 10, 2, 64) + 255) // 256 * 256
     assert gb.nro_workspace_bytes(2, 10, 2, 64, 64) == t + 2 * 64 * 64 * 2
+
+
+def test_layer_norm_validation(L):
+    def ln(X=FAKE, rows=10, D=64, g=FAKE, b=FAKE, eps=1e-5, Y=FAKE):
+        return L.gesr_layer_norm(X, rows, D, g, b, eps, Y, None)
+    assert ln(D=12) == gb.GESR_ERR_INVALID_ARG
+    assert ln(rows=-1) == gb.GESR_ERR_INVALID_ARG
+    assert ln(eps=-1.0) == gb.GESR_ERR_INVALID_ARG
+    assert ln(g=None) == gb.GESR_ERR_INVALID_ARG
+    assert ln(Y=MIS) == gb.GESR_ERR_INVALID_ARG
+    assert ln(rows=0, X=None) == gb.GESR_OK
