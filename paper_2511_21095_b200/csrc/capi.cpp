@@ -569,6 +569,32 @@ gesr_status gesr_stu_output(const void* T, int64_t total_C, int32_t D_in, const 
   s = run_projection_rm(T, total_C, D_in, W_g, b_g, static_cast<int32_t>(D), GESR_ACT_SILU,
                         nullptr, workspace, st);
   if (s != GESR_OK) return s;
+  // 2+3 fused (opt-in GESR_STU_FUSED=1; D = 512, D_out % 256 == 0): the normalised, gated rows
+  // are produced into shared memory as the output GEMM's A operand (stu_fused.cu: slower than
+  // the two kernels below at the headline, kept for the record)
+  static const char* fused_env = getenv("GESR_STU_FUSED");
+  const bool fused = gesr::stu_fused_supported(static_cast<int>(D), D_out) &&
+                     fused_env != nullptr && fused_env[0] == '1';
+  if (fused) {
+    CUtensorMap mw, my;
+    s = make_map_2d(&mw, W_o, D_out, D, 128, 64, CU_TENSOR_MAP_SWIZZLE_128B, "W_o");
+    if (s != GESR_OK) return s;
+    s = make_out_map(&my, Y, 1, total_C, D_out, "Y");
+    if (s != GESR_OK) return s;
+    gesr::StuFusedParams fp{};
+    fp.M = total_C;
+    fp.N = D_out;
+    fp.o_bf16 = o_dtype == GESR_OUT_BF16 ? 1 : 0;
+    fp.O = O;
+    fp.G = static_cast<const __nv_bfloat16*>(workspace);
+    fp.gamma = ln_gamma;
+    fp.beta = ln_beta;
+    fp.eps = ln_eps;
+    fp.b_o = b_o;
+    fp.X_res = static_cast<const __nv_bfloat16*>(X_res);
+    cudaError_t ef = gesr::launch_stu_fused(mw, my, fp, num_sms(), st);
+    return ef == cudaSuccess ? GESR_OK : cuda_fail(ef, "stu_fused_kernel launch");
+  }
   // 2. Z = (LayerNorm(O) gamma + beta) * G, in place over G
   cudaError_t e = gesr::launch_ln_gate(O, o_dtype == GESR_OUT_BF16 ? 1 : 0,
                                        static_cast<__nv_bfloat16*>(workspace), ln_gamma, ln_beta,

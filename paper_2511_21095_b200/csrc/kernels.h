@@ -92,6 +92,25 @@ cudaError_t launch_attn_empty(const AttnParams& p, int d, cudaStream_t stream);
 cudaError_t launch_ln_gate(const void* O, int o_bf16, __nv_bfloat16* G, const float* gamma,
                            const float* beta, float eps, int64_t C, int D, cudaStream_t stream);
 
+// Fused LayerNorm(O) * gamma + beta, times G, then W_o (+ b_o + X_res) (stu_fused.cu): one
+// kernel for D = 512 and D_out a multiple of 256 (stu_fused_supported); map_w: W_o [D_out, 512]
+// box {64, 128} SW128; map_y: Y as {D_out, M, 1} box {32, 32, 1} SW64.
+struct StuFusedParams {
+  int64_t M;               // rows
+  int N;                   // D_out
+  int o_bf16;
+  const void* O;           // [M, 512] fp32 or bf16
+  const __nv_bfloat16* G;  // [M, 512]
+  const float* gamma;
+  const float* beta;
+  float eps;
+  const float* b_o;        // [N] or null
+  const __nv_bfloat16* X_res;   // [M, N] or null
+};
+bool stu_fused_supported(int D, int D_out);
+cudaError_t launch_stu_fused(const CUtensorMap& map_w, const CUtensorMap& map_y,
+                             const StuFusedParams& p, int num_sms, cudaStream_t stream);
+
 // Y[r] = LayerNorm(X[r]) * gamma + beta over D features, bf16 in / out (stu.cu; R18).
 cudaError_t launch_layer_norm(const void* X, void* Y, const float* gamma, const float* beta,
                               float eps, int64_t rows, int D, cudaStream_t stream);
