@@ -25,6 +25,9 @@ blocking/fusion), each citing the passage it follows:
 * :func:`history_attention` -- causal self-attention of each user's history over itself (the U
   rows of one [U, T] layer: mask rule (1); SPEC.md:277 user block lower-
   triangular; reading R17).  Numpy.
+* :func:`ro_cross_attention` -- RO cross attention: i learnable seeds (optionally plus per-request
+  context tokens) attend over the request's history with per-seed projections, concatenated.
+  PAPER.md:362-370 (s3.4.3); SPEC.md:309-315 (reading R19).  Numpy.
 * :func:`stu_stack_forward` -- a stack of full target-aware STU layers over [U, T] per request
   (SPEC.md:298 self_attention_forward, SPEC.md:343 layer internals, mask SPEC.md:277 with the
   candidate diagonal; reading R18), brute force over the (N+n)^2 mask.  Numpy.
@@ -491,3 +494,41 @@ def stu_stack_forward(U, T, seq_offsets, cand_offsets, layers, H, d, eps=1e-5):
             X = (ln(A, *lay["ln_out"]) * G) @ _f64(lay["W_o"]).T + X
         Uo[so[b]:so[b + 1]], To[co[b]:co[b + 1]] = X[:N], X[N:]
     return Uo, To
+
+
+def ro_cross_attention(seeds, W_q, U, seq_offsets, W_k, W_v, i, d, ctx=None, act=1, scale=None):
+    """U_cross = Concat_s Attn_ro(Q_s, RO, RO) per request (PAPER.md:362-370; SPEC.md:309-315;
+    DESIGN.md reading R19), seed by seed:
+
+      query       q_s = act((seed_s + ctx[b][s]) W_{Q,s}^T)           W_q rows [s d, (s+1) d)
+      key/value   K_s = act(U_b W_{K,s}^T),  V_s = act(U_b W_{V,s}^T)   (the request's RO rows)
+      attention   O_s = softmax(scale q_s K_s^T) V_s
+      concat      U_cross[b] = [O_0, ..., O_{i-1}]
+
+    seeds [i, D_in], ctx [B, i, D_in] or None, U [total_L, D_in], W_* [i d, D_in].
+    Returns fp64 [B, i d]; a request without history rows gives zeros (reading R6).
+    """
+    S, U = _f64(seeds), _f64(U)
+    Wq, Wk, Wv = _f64(W_q), _f64(W_k), _f64(W_v)
+    so = _np(seq_offsets, np.int64)
+    B = len(so) - 1
+    C = None if ctx is None else _f64(ctx)
+    sc = (1.0 / np.sqrt(d)) if not scale or scale <= 0 else float(scale)
+
+    def act_(z):
+        return z / (1.0 + np.exp(-z)) if act == 1 else z
+
+    out = np.zeros((B, i * d))
+    for b in range(B):
+        r0, r1 = so[b], so[b + 1]
+        if r1 == r0:
+            continue
+        for s in range(i):
+            cs = slice(s * d, (s + 1) * d)
+            x = S[s] + (C[b, s] if C is not None else 0.0)
+            q = act_(x @ Wq[cs].T)
+            K, V = act_(U[r0:r1] @ Wk[cs].T), act_(U[r0:r1] @ Wv[cs].T)
+            z = sc * (K @ q)
+            w = np.exp(z - z.max())
+            out[b, cs] = (w @ V) / w.sum()
+    return out
