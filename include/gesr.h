@@ -254,6 +254,29 @@ gesr_status gesr_history_attention(const void* U, int64_t total_L, int32_t D_in,
 gesr_status gesr_layer_norm(const void* X, int64_t rows, int32_t D, const float* gamma,
                             const float* beta, float eps, void* Y, void* stream);
 
+/* gesr_ro_cross_score -- RO cross attention (PAPER.md:362-370 s3.4.3 "its query is a set of
+ * learnable seeds, optionally enriched with customised RO tokens ... Each query attends
+ * independently to user signals, and the results are concatenated to yield U_cross"; SPEC.md
+ * 309-315; reading R19).  Per request b and seed s of the i seeds:
+ *   q_s = act((seeds[s] + ctx[b][s]) W_{Q,s}^T + b_{Q,s}),
+ *   U_cross[b][s*d + j] = sum_r p_r V_s[r][j],  p = softmax_r(scale q_s . K_s[r])
+ * over the request's history rows (keys and values RO only, the prose reading of SPEC.md:358).
+ *   seeds      bf16 [i, D_in]; ctx bf16 [B, i, D_in] context tokens or NULL.
+ *   W_q        bf16 [i*d, D_in]: seed s's query weight is rows [s*d, (s+1)*d); b_q fp32 or NULL.
+ *   K_cache, V_cache  bf16 [i, total_L, d]: gesr_kv_project of the history with the seeds' key
+ *              / value weights stacked as heads (H := i).
+ *   U_cross    [B, i*d] fp32 or bf16 (o_dtype); a request without history gives zeros.
+ *   workspace  >= gesr_ro_workspace_bytes(B, i, d, D_in) bytes, 256-byte aligned.
+ * U_cross is per request (RO): a caller expands it to the request's candidates by indexing
+ * (SPEC.md:325 expand_ro).  Same tolerance and errors as gesr_tasa_score. */
+size_t gesr_ro_workspace_bytes(int64_t B, int32_t i, int32_t d, int32_t D_in);
+gesr_status gesr_ro_cross_score(const void* seeds, const void* ctx, int32_t i, int32_t D_in,
+                                const void* W_q, const float* b_q, int32_t act,
+                                const void* K_cache, const void* V_cache,
+                                const int64_t* seq_offsets, int64_t B, int64_t total_L,
+                                int32_t d, float scale, void* U_cross, int32_t o_dtype,
+                                void* workspace, size_t workspace_bytes, void* stream);
+
 /* gesr_hma_count -- HMA per-field match counts.
  *   user_ids / user_offsets  int64 CSR: segment b*F+f is request b's user-side ID list of
  *              field f; user_offsets has B*F+1 entries.

@@ -12,6 +12,7 @@ without the built library, raises.
   stu_output(T, O, W_g, ln_gamma, ln_beta, W_o, H, d, ...) -> Y   gesr_stu_output (f1)
   history_attention(U, seq_offsets, W_q, K, V, H, d) -> (O, lse)  gesr_history_attention (f4)
   layer_norm(X, gamma, beta) -> Y                                gesr_layer_norm
+  ro_cross_score(seeds, W_q, K, V, seq_offsets, i, d, ctx) -> U_cross  gesr_ro_cross_score
   stu_layer / stu_stack(U, T, ..., layers, H, d) -> (U', T')     full STU layers (composition)
   score_step(batch)                        one full scoring step (the three calls; HMA on a
                                            second stream joined by an event)
@@ -86,6 +87,10 @@ def lib():
             ("gesr_nro_cross_score", ctypes.c_int, [_vp, _i64, _i32, _vp, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _i64, _i64, _i32, _i32, ctypes.c_float, _i32, _vp, _i32, _vp, _vp, ctypes.c_size_t, _vp]),
             ("gesr_history_attention", ctypes.c_int, [_vp, _i64, _i32, _vp, _i64, _vp, _vp, _i32, _vp, _vp, _i32, _i32, ctypes.c_float, _vp, _i32, _vp, _vp, ctypes.c_size_t, _vp]),
             ("gesr_stu_workspace_bytes", ctypes.c_size_t, [_i64, _i32, _i32]),
+            ("gesr_ro_workspace_bytes", ctypes.c_size_t, [_i64, _i32, _i32, _i32]),
+            ("gesr_ro_cross_score", ctypes.c_int, [_vp, _vp, _i32, _i32, _vp, _vp, _i32, _vp, _vp,
+                                                   _vp, _i64, _i64, _i32, ctypes.c_float, _vp,
+                                                   _i32, _vp, ctypes.c_size_t, _vp]),
             ("gesr_layer_norm", ctypes.c_int, [_vp, _i64, _i32, _vp, _vp, ctypes.c_float, _vp, _vp]),
             ("gesr_stu_output", ctypes.c_int, [_vp, _i64, _i32, _vp, _i32, _vp, _vp, _vp, _vp, ctypes.c_float, _vp, _vp, _vp, _i32, _i32, _i32, _vp, _vp, ctypes.c_size_t, _vp]),
     ):
@@ -267,6 +272,29 @@ def stu_output(T, O, W_g, ln_gamma, ln_beta, W_o, H: int, d: int, b_g=None, b_o=
                                  _ptr(b_o), _ptr(X_res), H, d, D_out, _ptr(Y), _ptr(workspace),
                                  workspace.numel(), _stream(stream)))
     return Y
+
+
+def ro_cross_score(seeds, W_q, K_cache, V_cache, seq_offsets, i: int, d: int, ctx=None,
+                   act: int = GESR_ACT_SILU, b_q=None, scale: float = 0.0,
+                   out_dtype=torch.float32, U_cross=None, workspace=None, stream=None):
+    """U_cross [B, i*d] (gesr_ro_cross_score: i seeds, plus optional per-request context tokens
+    ctx [B, i, D_in], over the history K/V cache [i, total_L, d] from kv_project with the seeds'
+    key/value weights as heads)."""
+    _dev(seeds, W_q, K_cache, V_cache, seq_offsets, ctx, b_q, U_cross, workspace)
+    D_in = seeds.shape[1]
+    B = seq_offsets.numel() - 1
+    total_L = K_cache.shape[1]
+    if U_cross is None:
+        U_cross = torch.empty((B, i * d), dtype=out_dtype, device=seeds.device)
+    o_dtype = GESR_OUT_BF16 if U_cross.dtype == torch.bfloat16 else GESR_OUT_F32
+    if workspace is None:
+        nbytes = int(lib().gesr_ro_workspace_bytes(B, i, d, D_in))
+        workspace = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=seeds.device)
+    _check(lib().gesr_ro_cross_score(_ptr(seeds), _ptr(ctx), i, D_in, _ptr(W_q), _ptr(b_q), act,
+                                     _ptr(K_cache), _ptr(V_cache), _ptr(seq_offsets), B, total_L,
+                                     d, float(scale), _ptr(U_cross), o_dtype, _ptr(workspace),
+                                     workspace.numel(), _stream(stream)))
+    return U_cross
 
 
 def layer_norm(X, gamma, beta, eps: float = 1e-5, Y=None, stream=None):

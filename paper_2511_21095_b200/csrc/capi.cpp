@@ -676,4 +676,60 @@ gesr_status gesr_layer_norm(const void* X, int64_t rows, int32_t D, const float*
   return e == cudaSuccess ? GESR_OK : cuda_fail(e, "layer_norm_kernel launch");
 }
 
+// RO cross attention workspace: [query rows X bf16 | offsets int64 | O_full fp32 | tasa ws]
+static size_t ro_layout(int64_t B, int32_t i, int32_t d, int32_t D_in, size_t* off_offs,
+                        size_t* off_o, size_t* off_ws) {
+  auto up = [](size_t x) { return (x + 255) & ~static_cast<size_t>(255); };
+  const size_t x_bytes = up(static_cast<size_t>(B) * i * D_in * 2);
+  const size_t offs_bytes = up(static_cast<size_t>(B + 1) * 8);
+  const size_t o_bytes = up(static_cast<size_t>(B) * i * i * d * 4);
+  *off_offs = x_bytes;
+  *off_o = x_bytes + offs_bytes;
+  *off_ws = *off_o + o_bytes;
+  return *off_ws + gesr_tasa_workspace_bytes(B, B * i, i, d, 1);
+}
+
+size_t gesr_ro_workspace_bytes(int64_t B, int32_t i, int32_t d, int32_t D_in) {
+  if (B < 0 || i < 1 || !valid_d(d) || D_in < 8) return 0;
+  size_t a, b, c;
+  return ro_layout(B, i, d, D_in, &a, &b, &c);
+}
+
+gesr_status gesr_ro_cross_score(const void* seeds, const void* ctx, int32_t i, int32_t D_in,
+                                const void* W_q, const float* b_q, int32_t act,
+                                const void* K_cache, const void* V_cache,
+                                const int64_t* seq_offsets, int64_t B, int64_t total_L,
+                                int32_t d, float scale, void* U_cross, int32_t o_dtype,
+                                void* workspace, size_t workspace_bytes, void* stream) {
+  gesr_status s = check_common(D_in, i, d, act);
+  if (s != GESR_OK) return s;
+  if (B < 0 || total_L < 0) return fail(GESR_ERR_INVALID_ARG, "B, total_L must be >= 0");
+  if (o_dtype != GESR_OUT_F32 && o_dtype != GESR_OUT_BF16)
+    return fail(GESR_ERR_INVALID_ARG, "o_dtype=%d is not a gesr_out_dtype", o_dtype);
+  if (B == 0) return GESR_OK;
+  if (!seeds || !W_q || !seq_offsets || !U_cross || !workspace)
+    return fail(GESR_ERR_INVALID_ARG, "null required pointer");
+  if (!aligned16(seeds) || !aligned16(ctx) || !aligned16(W_q) || !aligned16(U_cross) ||
+      (reinterpret_cast<uintptr_t>(workspace) & 255u))
+    return fail(GESR_ERR_INVALID_ARG, "misaligned pointer");
+  size_t off_offs, off_o, off_ws;
+  const size_t need = ro_layout(B, i, d, D_in, &off_offs, &off_o, &off_ws);
+  if (workspace_bytes < need)
+    return fail(GESR_ERR_WORKSPACE, "workspace %zu bytes < required %zu", workspace_bytes, need);
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int64_t* offs = reinterpret_cast<int64_t*>(ws + off_offs);
+  float* O_full = reinterpret_cast<float*>(ws + off_o);
+  cudaError_t e = gesr::launch_ro_queries(seeds, ctx, ws, offs, B, i, D_in, st);
+  if (e != cudaSuccess) return cuda_fail(e, "ro_queries launch");
+  // the i query rows of every request through the target-aware path with the slots as heads
+  // (all slots for every row: the i x i products are tiny next to the history), one split
+  s = tasa_impl(ws, B * i, D_in, offs, W_q, b_q, act, K_cache, V_cache, seq_offsets, B, total_L,
+                i, d, scale, 1, 0, nullptr, nullptr, O_full, GESR_OUT_F32, nullptr, ws + off_ws,
+                need - off_ws, stream);
+  if (s != GESR_OK) return s;
+  e = gesr::launch_ro_gather(O_full, U_cross, o_dtype == GESR_OUT_BF16 ? 1 : 0, B, i, d, st);
+  return e == cudaSuccess ? GESR_OK : cuda_fail(e, "ro_gather launch");
+}
+
 }  // extern "C"

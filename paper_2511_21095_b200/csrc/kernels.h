@@ -121,6 +121,13 @@ cudaError_t launch_layer_norm(const void* X, void* Y, const float* gamma, const 
 cudaError_t launch_fold_gate(const void* W_q, const float* gate, void* out, int j, int d, int D_in,
                              cudaStream_t stream);
 
+// RO cross attention (nro.cu): query rows X[b*i + s] = seeds[s] (+ ctx[b][s]) and offsets i*b;
+// then the diagonal gather U_cross[b][s*d + j] = O_full[b*i + s][s*d + j]
+cudaError_t launch_ro_queries(const void* seeds, const void* ctx, void* X, int64_t* offs,
+                              int64_t B, int i, int D_in, cudaStream_t stream);
+cudaError_t launch_ro_gather(const float* O_full, void* out, int o_bf16, int64_t B, int i, int d,
+                             cudaStream_t stream);
+
 // ---------------------------------------------------------------- K-HMA (hma.cu)
 struct HmaParams {
   const int64_t* user_ids;

@@ -32,7 +32,57 @@ __global__ void fold_gate_kernel(const __nv_bfloat16* __restrict__ W, const floa
   }
 }
 
+// RO cross attention queries: row b*i + s = seed s (+ the request's context
+// token ctx[b][s]) in bf16, and the candidate offsets of the i query rows per request.
+__global__ void ro_queries_kernel(const __nv_bfloat16* __restrict__ seeds,
+                                  const __nv_bfloat16* __restrict__ ctx,
+                                  __nv_bfloat16* __restrict__ X, int64_t* __restrict__ offs,
+                                  int64_t B, int i, int D_in) {
+  const int64_t n = B * i * D_in;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t row = e / D_in;
+    const int k = static_cast<int>(e - row * D_in);
+    const int s = static_cast<int>(row % i);
+    float v = __bfloat162float(seeds[static_cast<int64_t>(s) * D_in + k]);
+    if (ctx != nullptr) v += __bfloat162float(ctx[e]);
+    X[e] = __float2bfloat16_rn(v);
+  }
+  for (int64_t b = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; b <= B;
+       b += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    offs[b] = b * i;
+}
+
+// U_cross[b][s*d + j] = O_full[b*i + s][s*d + j]: query row s of request b keeps slot s's output
+__global__ void ro_gather_kernel(const float* __restrict__ O_full, void* __restrict__ out,
+                                 int o_bf16, int64_t B, int i, int d) {
+  const int64_t n = B * i * d;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t b = e / (static_cast<int64_t>(i) * d);
+    const int sj = static_cast<int>(e - b * i * d);          // s * d + j
+    const int s = sj / d;
+    const float v = O_full[(b * i + s) * static_cast<int64_t>(i) * d + sj];
+    if (o_bf16) static_cast<__nv_bfloat16*>(out)[e] = __float2bfloat16_rn(v);
+    else static_cast<float*>(out)[e] = v;
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_ro_queries(const void* seeds, const void* ctx, void* X, int64_t* offs,
+                              int64_t B, int i, int D_in, cudaStream_t stream) {
+  ro_queries_kernel<<<148 * 4, 256, 0, stream>>>(static_cast<const __nv_bfloat16*>(seeds),
+                                                 static_cast<const __nv_bfloat16*>(ctx),
+                                                 static_cast<__nv_bfloat16*>(X), offs, B, i, D_in);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ro_gather(const float* O_full, void* out, int o_bf16, int64_t B, int i, int d,
+                             cudaStream_t stream) {
+  ro_gather_kernel<<<148 * 4, 256, 0, stream>>>(O_full, out, o_bf16, B, i, d);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_fold_gate(const void* W_q, const float* gate, void* out, int j, int d, int D_in,
                              cudaStream_t stream) {

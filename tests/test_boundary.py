@@ -198,3 +198,15 @@ def test_layer_norm_validation(L):
     assert ln(g=None) == gb.GESR_ERR_INVALID_ARG
     assert ln(Y=MIS) == gb.GESR_ERR_INVALID_ARG
     assert ln(rows=0, X=None) == gb.GESR_OK
+
+
+def test_ro_cross_validation(L):
+    def ro(seeds=FAKE, i=2, d=64, odt=0, ws=FAKE, wsb=1 << 30, B=2):
+        return L.gesr_ro_cross_score(seeds, None, i, 64, FAKE, None, 1, FAKE, FAKE, FAKE, B, 10, d,
+                                     0.0, FAKE, odt, ws, wsb, None)
+    assert ro(seeds=None) == gb.GESR_ERR_INVALID_ARG
+    assert ro(i=0) == gb.GESR_ERR_INVALID_ARG
+    assert ro(d=96) == gb.GESR_ERR_INVALID_ARG
+    assert ro(odt=4) == gb.GESR_ERR_INVALID_ARG
+    assert ro(wsb=64) == gb.GESR_ERR_WORKSPACE
+    assert ro(B=0) == gb.GESR_OK
