@@ -28,6 +28,8 @@ blocking/fusion), each citing the passage it follows:
 * :func:`ro_cross_attention` -- RO cross attention: i learnable seeds (optionally plus per-request
   context tokens) attend over the request's history with per-seed projections, concatenated.
   PAPER.md:362-370 (s3.4.3); SPEC.md:309-315 (reading R19).  Numpy.
+* :func:`tasa_score_hstu` -- target-aware attention with HSTU's pointwise normalisation
+  SiLU(scale q.k)/N instead of the softmax (A1's alternative reading, R20).  Numpy.
 * :func:`stu_stack_forward` -- a stack of full target-aware STU layers over [U, T] per request
   (SPEC.md:298 self_attention_forward, SPEC.md:343 layer internals, mask SPEC.md:277 with the
   candidate diagonal; reading R18), brute force over the (N+n)^2 mask.  Numpy.
@@ -531,4 +533,30 @@ def ro_cross_attention(seeds, W_q, U, seq_offsets, W_k, W_v, i, d, ctx=None, act
             z = sc * (K @ q)
             w = np.exp(z - z.max())
             out[b, cs] = (w @ V) / w.sum()
+    return out
+
+
+def tasa_score_hstu(T, cand_offsets, W_q, K, V, seq_offsets, H, d, act=1, scale=None):
+    """Candidate rows of the target-aware attention with HSTU's pointwise normalisation
+    (the paper defers the STU internals to HSTU; reading R20):
+      q = act(T[t] W_q^T)[h d:(h+1) d];  O[t][h] = sum_i SiLU(scale q . K[h][r_i]) V[h][r_i] / L_b
+    over the request's L_b history rows (L_b = 0 -> zeros).  K, V fp64 [H, total_L, d] (as
+    returned by kv_project).  Returns fp64 [total_C, H d]."""
+    T = _f64(T)
+    Wq = _f64(W_q)
+    K, V = np.asarray(K, np.float64), np.asarray(V, np.float64)
+    co, so = _np(cand_offsets, np.int64), _np(seq_offsets, np.int64)
+    sc = (1.0 / np.sqrt(d)) if not scale or scale <= 0 else float(scale)
+    Z = T @ Wq.T
+    Q = Z / (1.0 + np.exp(-Z)) if act == 1 else Z
+    out = np.zeros((T.shape[0], H * d))
+    for b in range(len(co) - 1):
+        c0, c1, r0, r1 = co[b], co[b + 1], so[b], so[b + 1]
+        if c1 == c0 or r1 == r0:
+            continue
+        for h in range(H):
+            cs = slice(h * d, (h + 1) * d)
+            s_ = sc * (Q[c0:c1, cs] @ K[h, r0:r1].T)
+            w = s_ / (1.0 + np.exp(-s_))
+            out[c0:c1, cs] = (w @ V[h, r0:r1]) / (r1 - r0)
     return out
