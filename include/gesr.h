@@ -59,6 +59,11 @@ typedef enum { GESR_OUT_F32 = 0, GESR_OUT_BF16 = 1 } gesr_out_dtype;
 /* gesr_tasa_score flag, reserved: the candidate also attends to its own key (SPEC.md:277's
  * diagonal, reading R2).  Returns GESR_ERR_UNSUPPORTED in this version. */
 #define GESR_TASA_SELF_KEY 0x1u
+/* HSTU pointwise normalisation instead of the softmax (reading R20: the paper defers
+ * to HSTU, whose attention is SiLU(scale q.k)/N, N = the number of keys):
+ *   O[t][h] = sum_i SiLU(scale q_h . K[h][r_i]) V[h][r_i] / L_b   (L_b = 0 -> zeros)
+ * gesr_tasa_score only; lse must be NULL; one key split (kv_splits 0 or 1). */
+#define GESR_TASA_HSTU_SILU 0x2u
 
 /* Library version (major*10000 + minor*100 + patch). */
 int gesr_version(void);
@@ -109,7 +114,8 @@ size_t gesr_tasa_workspace_bytes(int64_t B, int64_t total_C, int32_t H, int32_t 
  *              runs unsplit.  For a fixed kv_splits >= 1 each output row depends only on its
  *              own candidate and its user's K/V: results are bit-identical across chunking,
  *              batch composition and GPU count (reading R9).  kv_splits > 64 is invalid.
- *   flags      0.  GESR_TASA_SELF_KEY needs the candidates' own keys / values: it returns
+ *   flags      0 or GESR_TASA_HSTU_SILU (above).  GESR_TASA_SELF_KEY needs the candidates'
+ *              own keys / values: it returns
  *              GESR_ERR_UNSUPPORTED here; use gesr_tasa_score_self.
  *   O          [total_C, H*d] fp32 or bf16 (o_dtype): O[t][h*d+j] = sum_i p_i V[h][r_i][j] with
  *              p = softmax_i(scale * q_h . K[h][r_i]) over the request's L_b history rows.

@@ -35,6 +35,7 @@ GESR_OK, GESR_ERR_INVALID_ARG, GESR_ERR_UNSUPPORTED, GESR_ERR_CUDA, GESR_ERR_WOR
 GESR_ACT_IDENTITY, GESR_ACT_SILU = 0, 1
 GESR_OUT_F32, GESR_OUT_BF16 = 0, 1
 GESR_TASA_SELF_KEY = 0x1
+GESR_TASA_HSTU_SILU = 0x2   # HSTU pointwise SiLU(s)/N normalisation (R20)
 
 
 class GesrError(RuntimeError):

@@ -121,7 +121,10 @@ __device__ __forceinline__ void exp2_poly2(float& y0, float& y1, float x0, float
   y1 = __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23));
 }
 
-template <int D, bool kCausal>
+// kCausal: history self-attention; kHstu: HSTU pointwise normalisation SiLU(s)/L_b instead of
+// the softmax (GESR_TASA_HSTU_SILU; reading R20).  Separate instantiations keep the
+// default kernel's code unchanged.
+template <int D, bool kCausal, bool kHstu>
 __global__ void __launch_bounds__(AttnCfg<D>::kThreads, 1)
     attn_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
                 const __grid_constant__ CUtensorMap map_v, const __grid_constant__ CUtensorMap map_o,
@@ -370,6 +373,29 @@ __global__ void __launch_bounds__(AttnCfg<D>::kThreads, 1)
 #pragma unroll
         for (int c = 0; c < kCols / 32; ++c) tmem_ld32(tS + c * 32, r + c * 32);
         tmem_ld_wait();
+        if constexpr (kHstu) {
+          // p = SiLU(scale s) (masked keys: SiLU(0) = 0), no running max; l counts the keys
+          const int hv = L - kBlockKeys * j - half * kCols;
+          const float sc = sl2 * 0.69314718055994530942f;
+#pragma unroll
+          for (int k = 0; k < kCols / 2; ++k) {
+            const float x0 = 2 * k < hv ? __uint_as_float(r[2 * k]) * sc : 0.f;
+            const float x1 = 2 * k + 1 < hv ? __uint_as_float(r[2 * k + 1]) * sc : 0.f;
+            float y0, y1;
+            asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y0) : "f"(1.0f + ex2(-1.4426950408889634f * x0)));
+            asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y1) : "f"(1.0f + ex2(-1.4426950408889634f * x1)));
+            r[k] = pack_bf16x2(x0 * y0, x1 * y1);
+          }
+          l += static_cast<float>(hv < 0 ? 0 : (hv > kCols ? kCols : hv));
+#pragma unroll
+          for (int c = 0; c < kCols / 64; ++c) tmem_st32(tP + c * 32, r + c * 32);
+          if constexpr (kCols / 2 % 32 != 0) tmem_st16(tP, r);
+          tmem_st_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&p_full[i]);
+          continue;
+        }
         const int valid = L - kBlockKeys * j - half * kCols;   // valid keys in my columns
         const bool full = valid >= kCols;
         if (!full) {
@@ -686,11 +712,14 @@ cudaError_t launch_d(const CUtensorMap& mq, const CUtensorMap& mk, const CUtenso
   using C = AttnCfg<D>;
   static bool attr_done = false;
   if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(attn_kernel<D, false>,
+    cudaError_t e = cudaFuncSetAttribute(attn_kernel<D, false, false>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(attn_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             C::kSmemBytes);
+    e = cudaFuncSetAttribute(attn_kernel<D, true, false>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(attn_kernel<D, false, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
@@ -699,10 +728,12 @@ cudaError_t launch_d(const CUtensorMap& mq, const CUtensorMap& mk, const CUtenso
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t work = max_units * p.H;
   const unsigned grid = static_cast<unsigned>(work < sms ? work : sms);
-  if (p.causal)
-    attn_kernel<D, true><<<grid, C::kThreads, C::kSmemBytes, stream>>>(mq, mk, mv, mo, p);
+  if (p.hstu)
+    attn_kernel<D, false, true><<<grid, C::kThreads, C::kSmemBytes, stream>>>(mq, mk, mv, mo, p);
+  else if (p.causal)
+    attn_kernel<D, true, false><<<grid, C::kThreads, C::kSmemBytes, stream>>>(mq, mk, mv, mo, p);
   else
-    attn_kernel<D, false><<<grid, C::kThreads, C::kSmemBytes, stream>>>(mq, mk, mv, mo, p);
+    attn_kernel<D, false, false><<<grid, C::kThreads, C::kSmemBytes, stream>>>(mq, mk, mv, mo, p);
   return cudaGetLastError();
 }
 

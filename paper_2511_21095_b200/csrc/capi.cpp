@@ -337,7 +337,16 @@ static gesr_status tasa_impl(const void* T, int64_t total_C, int32_t D_in, const
   if ((flags & GESR_TASA_SELF_KEY) && !self)
     return fail(GESR_ERR_UNSUPPORTED,
                 "GESR_TASA_SELF_KEY needs the candidates' own K/V: use gesr_tasa_score_self");
-  if (flags & ~GESR_TASA_SELF_KEY) return fail(GESR_ERR_INVALID_ARG, "unknown flags 0x%x", flags);
+  if (flags & ~(GESR_TASA_SELF_KEY | GESR_TASA_HSTU_SILU))
+    return fail(GESR_ERR_INVALID_ARG, "unknown flags 0x%x", flags);
+  const bool hstu = (flags & GESR_TASA_HSTU_SILU) != 0;
+  if (hstu && (self || causal))
+    return fail(GESR_ERR_UNSUPPORTED, "GESR_TASA_HSTU_SILU is not combined with a self key or "
+                "causal attention");
+  if (hstu && kv_splits > 1)
+    return fail(GESR_ERR_UNSUPPORTED, "GESR_TASA_HSTU_SILU runs one key split");
+  if (hstu && lse != nullptr)
+    return fail(GESR_ERR_INVALID_ARG, "lse is undefined for GESR_TASA_HSTU_SILU (pass NULL)");
   if (total_C == 0 || B == 0) return GESR_OK;
   if (!T || !cand_offsets || !W_q || !seq_offsets || !O || !workspace)
     return fail(GESR_ERR_INVALID_ARG, "null required pointer");
@@ -397,8 +406,9 @@ static gesr_status tasa_impl(const void* T, int64_t total_C, int32_t D_in, const
 
   p.units = units;
   p.unit_count = count;
-  p.splits = causal ? 1 : pick_splits(B, total_C, total_L, H, d, kv_splits);
+  p.splits = (causal || hstu) ? 1 : pick_splits(B, total_C, total_L, H, d, kv_splits);
   p.causal = causal;
+  p.hstu = hstu ? 1 : 0;
 
   if (p.splits > 1) {
     p.part_ml = reinterpret_cast<float2*>(part);
@@ -425,7 +435,7 @@ static gesr_status tasa_impl(const void* T, int64_t total_C, int32_t D_in, const
     if (s != GESR_OK) return s;
     p.o_tma = 1;
   }
-  if (d == 128 && pair_attention_enabled()) {
+  if (d == 128 && pair_attention_enabled() && !hstu) {
     CUtensorMap mkh;
     s = make_map_2d(&mkh, K_cache, static_cast<uint64_t>(H) * total_L, d, 64, 64, swz, "K half");
     if (s != GESR_OK) return s;

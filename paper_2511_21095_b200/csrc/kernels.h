@@ -60,6 +60,9 @@ struct AttnParams {
   // the history rows themselves; a unit {s0, L, first row, rows} covers query rows
   // [L - rows, L) of its request and row r (0-based in the unit) sees keys [0, L - rows + r]
   int causal;
+  // HSTU pointwise normalisation (GESR_TASA_HSTU_SILU): O = sum_i SiLU(scale s_i) v_i / L_b
+  // (1-CTA kernel only; no lse, one split)
+  int hstu;
 };
 
 constexpr int kUnitRows = 256;   // candidates per work unit (two 128-row Q tiles)
