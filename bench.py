@@ -4,12 +4,23 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 3h]
     torchrun --nproc-per-node N bench.py --gpus N ...      (one process per GPU, NCCL)
 
+`python bench.py --gpus N` with no torchrun environment re-launches itself under
+`torch.distributed.run` with N local ranks (one process per GPU).
+
 One step = one pass of the whole hot path over one batch: gesr_kv_project -> gesr_tasa_score,
-with gesr_hma_count on a second stream joined by an event.  Workload: config
-"3h" = B=1024 requests per GPU, L=2048 history rows, C=1000 candidates, H=4, d=128, D_in=512,
-F=16 HMA fields (BASELINE.json metric).  Requests shard across GPUs with no data-path
-collective (weak scaling: rank r scores requests [r*B, (r+1)*B)); NCCL is used only for the
-setup weight broadcast and the max-over-ranks timing reduction.
+with gesr_hma_count on a second stream joined by an event, exactly
+`binding.score_step(batch, StepBuffers(batch, out_dtype=bf16))` (the configuration
+tests/test_gpu_configs.py checks against the oracle).
+
+Workloads (paper_2511_21095_b200/configs.py):
+  3h (default)  B=1024 requests per GPU, L=2048, C=1000, H=4, d=128, D_in=512, F=16 -- the
+                metric's workload; WEAK scaling: rank r scores requests [r B, (r+1) B).
+  5             the fixed 8192-request serving mix (L log-uniform 32-4096, C 100-2000); STRONG
+                scaling: every rank computes the same LPT partition (shard.lpt_partition) and
+                generates only its own requests.
+  1, 2, 3, 4    the other BASELINE configs (weak).
+No collective is on the data path: NCCL carries the setup weight broadcast, the max-over-ranks
+time reduction and (with --gather) the post-timing score gather.
 
 Rank 0 prints ONE JSON line.  `--impl reference` times the fp64 CPU oracle (oracle/) on a
 bounded sample of the same workload, on the host cores (rank 0 only).
@@ -18,8 +29,9 @@ from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
+import socket
+import subprocess
 import sys
 import threading
 import time
@@ -30,9 +42,10 @@ if ROOT not in sys.path:
 
 METRIC = "candidate-scores/sec at L=2048, C=1000; % of tensor-pipe/HBM roofline"
 UNIT = "candidate-scores/s"
+STRONG_CONFIGS = ("5",)
 
 
-def _args():
+def _args(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=30)
@@ -46,7 +59,7 @@ def _args():
                          "overlapped on three streams); 1 = copy in, score, copy out")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--gather", action="store_true", help="NCCL gather of scores after timing")
-    return ap.parse_args()
+    return ap.parse_args(argv)
 
 
 def _peaks():
@@ -116,6 +129,144 @@ class ClockSampler:
                 "reasons": sorted(self.reasons - {"gpu_idle"}), "samples": len(s)}
 
 
+# ------------------------------------------------------------------------------ orchestration
+
+def plan_requests(cfg_name: str, rank: int, world: int):
+    """This rank's global request indices, the scaling mode and the partition's model
+    imbalance.  Weak: rank r takes [r B, (r+1) B) of the config's request stream.  Strong
+    (config 5): the cfg.B requests LPT-packed by the cost model of shard.request_cost
+    (SURVEY.md s8(e)); every rank computes the same partition."""
+    import numpy as np
+
+    from paper_2511_21095_b200 import configs, inputs, shard
+    cfg = configs.get(cfg_name)
+    if cfg_name in STRONG_CONFIGS:
+        L, C = inputs.request_lengths(cfg)
+        cost = shard.request_cost(cfg, L.numpy(), C.numpy())
+        parts = shard.lpt_partition(cost, world)
+        return cfg, parts[rank], "strong", shard.imbalance(cost, parts)
+    return cfg, np.arange(rank * cfg.B, (rank + 1) * cfg.B, dtype=np.int64), "weak", 0.0
+
+
+def orchestrate(cfg_name: str, rank: int, world: int, steps: int, warmup: int, engine,
+                group=None) -> dict:
+    """The bench's multi-rank protocol, independent of what a step computes (tests drive it
+    with a stub engine over gloo): plan this rank's requests, engine.setup(cfg, requests) (the
+    rank generates only its own requests), broadcast the weights from rank 0, W >= 3 untimed
+    warm-up steps, barrier + sync, K timed steps (engine.time_steps: device time in ms), barrier,
+    max over ranks.  Returns the per-job numbers rank 0 reports."""
+    import torch
+    import torch.distributed as dist
+    cfg, reqs, scaling, model_imb = plan_requests(cfg_name, rank, world)
+    engine.setup(cfg, reqs)
+    if world > 1:
+        engine.broadcast_weights(group)
+    for _ in range(max(3, warmup)):
+        engine.step()
+    engine.sync()
+    if world > 1:
+        dist.barrier(group)
+    engine.sync()
+    ms = float(engine.time_steps(steps))
+    if world > 1:
+        dist.barrier(group)
+    cands = float(engine.candidates)
+    per_rank = torch.tensor([[ms, cands, float(len(reqs))]], dtype=torch.float64,
+                            device=engine.reduce_device)
+    if world > 1:
+        allr = [torch.zeros_like(per_rank) for _ in range(world)]
+        dist.all_gather(allr, per_rank, group=group)
+        per_rank = torch.cat(allr)
+    per_rank = per_rank.cpu()
+    t_max = float(per_rank[:, 0].max())
+    total_cands = float(per_rank[:, 1].sum())
+    return {
+        "cfg": cfg, "scaling": scaling, "requests": reqs, "elapsed_ms": t_max,
+        "ms_per_step": t_max / steps, "cands_per_step": total_cands,
+        "value": total_cands * steps / (t_max / 1e3),
+        "per_rank_ms": [float(x) for x in per_rank[:, 0]],
+        "per_rank_requests": [int(x) for x in per_rank[:, 2]],
+        "imbalance_measured": float(per_rank[:, 0].max() / per_rank[:, 0].mean() - 1.0),
+        "imbalance_model": model_imb,
+    }
+
+
+class GpuEngine:
+    """One rank's device state: the batch of its requests, preallocated buffers, and the step
+    (binding.score_step: kv_project -> tasa_score, hma_count forked on a side stream)."""
+
+    def __init__(self, device, out_dtype):
+        import torch
+        self.dev, self.out_dtype = device, out_dtype
+        self.reduce_device = device
+        self.events = {}
+        self.stream = torch.cuda.current_stream(device)
+
+    def setup(self, cfg, reqs):
+        import torch
+
+        from paper_2511_21095_b200 import binding as gb
+        from paper_2511_21095_b200 import inputs
+        self.cfg = cfg
+        self.batch = inputs.make_batch(cfg, requests=torch.as_tensor(reqs), device=self.dev)
+        self.bufs = gb.StepBuffers(self.batch, out_dtype=self.out_dtype)
+        self.candidates = self.batch.total_C
+        self.gb = gb
+
+    def broadcast_weights(self, group=None):
+        import torch.distributed as dist
+        for w in (self.batch.W_q, self.batch.W_k, self.batch.W_v):   # setup-time, NCCL
+            dist.broadcast(w, src=0, group=group)
+
+    def step(self, record=False):
+        self.gb.score_step(self.batch, self.bufs, act=self.cfg.act, chunk=self.cfg.chunk,
+                           stream=self.stream, events=self.events if record else None)
+
+    def sync(self):
+        import torch
+        torch.cuda.synchronize(self.dev)
+
+    def time_steps(self, steps):
+        import torch
+        self.launch0 = self.gb.launch_count()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(self.dev.index) as clk:
+            a.record(self.stream)
+            for _ in range(steps):
+                self.step(record=True)
+            b.record(self.stream)
+            torch.cuda.synchronize(self.dev)
+        self.launches = self.gb.launch_count() - self.launch0
+        self.clocks = clk.summary()
+        return a.elapsed_time(b)
+
+    def call_ms(self, a, b):
+        import numpy as np
+        ev = self.events
+        if not ev.get(a):
+            return None
+        return float(np.mean([x.elapsed_time(y) for x, y in zip(ev[a], ev[b])]))
+
+
+# ------------------------------------------------------------------------------ CPU baseline
+
+def _cpu_info() -> dict:
+    model = None
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        aff = len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        aff = None
+    return {"nproc": os.cpu_count(), "affinity": aff, "cpu_model": model}
+
+
 def _cpu_sample(cfg, requests, threads=None):
     """Run the fp64 oracle on the given requests (all three calls); returns (seconds, cands)."""
     import oracle
@@ -128,6 +279,28 @@ def _cpu_sample(cfg, requests, threads=None):
     oracle.hma_count(bt.user_ids, bt.user_offsets, bt.item_ids, bt.item_offsets,
                      bt.cand_offsets, cfg.F, threads=threads)
     return time.perf_counter() - t0, bt.total_C
+
+
+def cpu_baseline(cfg, config_name, budget_s=10.0, budget_1t_s=4.0) -> dict:
+    """The oracle as it stands on the host cores: all threads (std::thread over requests /
+    rows) on requests 0, 1, ... until ~budget_s, then ONE thread on the next request(s) until
+    ~budget_1t_s (both thread counts, nproc, affinity and CPU model)."""
+    import oracle
+    threads = oracle.default_threads()
+    tot, c, n = 0.0, 0, 0
+    while tot < budget_s and n < 64:
+        dt, cc = _cpu_sample(cfg, [n], threads)
+        tot, c, n = tot + dt, c + cc, n + 1
+    tot1, c1, n1 = 0.0, 0, 0
+    while tot1 < budget_1t_s and n1 < 8:
+        dt, cc = _cpu_sample(cfg, [n + n1], 1)
+        tot1, c1, n1 = tot1 + dt, c1 + cc, n1 + 1
+    return {"value": c / tot, "unit": UNIT, "cores": threads, "kind": "oracle",
+            "sample": f"{n} request(s) of config {config_name} with {threads} threads, "
+                      f"fp64 kv_project+tasa_score+hma_count, {tot:.1f} s",
+            "value_1thread": c1 / tot1,
+            "sample_1thread": f"{n1} request(s) on 1 thread, {tot1:.1f} s",
+            **_cpu_info()}
 
 
 def run_reference(args, rank):
@@ -151,16 +324,41 @@ def run_reference(args, rank):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * total / len(times), "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1e3 * total / len(times), "higher_is_better": True,
+        "scaling": "strong" if args.config in STRONG_CONFIGS else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{cfg.name} (config {args.config}): 1 request/step sample",
-                   "L": 2048, "C": 1000, "H": cfg.H, "d": cfg.d, "D_in": cfg.D_in, "F": cfg.F},
+                   "H": cfg.H, "d": cfg.d, "D_in": cfg.D_in, "F": cfg.F},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
-                         "sample": f"1 request (L={cfg.L[1]}, C={cfg.C[1]}) per step; "
-                                   "kv_project+tasa_score+hma_count in fp64"},
+                         "sample": "1 whole request of the workload per step; "
+                                   "kv_project+tasa_score+hma_count in fp64", **_cpu_info()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------ launcher
+
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def relaunch_under_torchrun(args) -> int:
+    """`--gpus N` (N > 1) without a torchrun environment: start N local ranks, one per GPU."""
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but only {have} CUDA device(s) visible",
+              file=sys.stderr)
+        return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(_free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -171,115 +369,37 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank)
         return
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(relaunch_under_torchrun(args))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
 
-    import numpy as np
     import torch
     import torch.distributed as dist
 
     from paper_2511_21095_b200 import binding as gb
-    from paper_2511_21095_b200 import configs, inputs, roofline
+    from paper_2511_21095_b200 import inputs, roofline
 
+    assert torch.cuda.device_count() > local, "one GPU per rank"
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    cfg = configs.get(args.config)
-    B = cfg.B
-    reqs = torch.arange(rank * B, (rank + 1) * B, dtype=torch.int64)
-    batch = inputs.make_batch(cfg, requests=reqs, device=dev)
-    if world > 1:
-        for w in (batch.W_q, batch.W_k, batch.W_v):     # setup-time weight broadcast (NCCL)
-            dist.broadcast(w, src=0)
     out_dtype = torch.bfloat16 if args.out_dtype == "bf16" else torch.float32
-    bufs = gb.StepBuffers(batch, out_dtype=out_dtype)
-    main_stream = torch.cuda.current_stream()
-    act = cfg.act
-
-    ev = {k: [] for k in ("kv0", "kv1", "t1", "h0", "h1")}
-    # where gesr_hma_count runs: "fork" = first, on a side stream joined by an event;
-    # "kv" = forked after the K/V projection; "serial" = on the main stream after the attention
-    hma_order = os.environ.get("GESR_HMA_ORDER", "fork")
-
-    def step(record=False):
-        E = (lambda: torch.cuda.Event(enable_timing=True)) if record else None
-        if record:
-            e_h0, e_h1, e_kv0, e_kv1, e_t1 = E(), E(), E(), E(), E()
-        def hma(stream):
-            if record:
-                e_h0.record(stream)
-            gb.hma_count(batch.user_ids, batch.user_offsets, batch.item_ids, batch.item_offsets,
-                         batch.cand_offsets, cfg.F, 0, counts=bufs.counts, stream=stream)
-            if record:
-                e_h1.record(stream)
-
-        def fork():
-            bufs.ev_fork.record(main_stream)
-            bufs.hma_stream.wait_event(bufs.ev_fork)
-            hma(bufs.hma_stream)
-            bufs.ev_join.record(bufs.hma_stream)
-
-        if hma_order == "fork":
-            fork()
-        if record:
-            e_kv0.record(main_stream)
-        gb.kv_project(batch.U, batch.W_k, batch.W_v, cfg.H, cfg.d, act, K_cache=bufs.K,
-                      V_cache=bufs.V, stream=main_stream)
-        if record:
-            e_kv1.record(main_stream)
-        if hma_order == "kv":
-            fork()
-        gb.tasa_score(batch.T, batch.cand_offsets, batch.W_q, bufs.K, bufs.V, batch.seq_offsets,
-                      cfg.H, cfg.d, act, O=bufs.O, want_lse=False, workspace=bufs.workspace,
-                      stream=main_stream)
-        if record:
-            e_t1.record(main_stream)
-        if hma_order == "serial":
-            hma(main_stream)
-        else:
-            main_stream.wait_event(bufs.ev_join)
-        if record:
-            for k, e in (("kv0", e_kv0), ("kv1", e_kv1), ("t1", e_t1), ("h0", e_h0), ("h1", e_h1)):
-                ev[k].append(e)
-
-    launches_per_step = 5  # hma + kv proj + (build_units + q proj + attention)
-
-    for _ in range(max(3, args.warmup)):
-        step()
-    torch.cuda.synchronize()
-
-    t_start = torch.cuda.Event(enable_timing=True)
-    t_end = torch.cuda.Event(enable_timing=True)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
-        t_start.record(main_stream)
-        for _ in range(args.steps):
-            step(record=True)
-        t_end.record(main_stream)
-        torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    elapsed_ms = t_start.elapsed_time(t_end)
-    kv_ms = float(np.mean([a.elapsed_time(b) for a, b in zip(ev["kv0"], ev["kv1"])]))
-    tasa_ms = float(np.mean([a.elapsed_time(b) for a, b in zip(ev["kv1"], ev["t1"])]))
-    hma_ms = float(np.mean([a.elapsed_time(b) for a, b in zip(ev["h0"], ev["h1"])]))
-    if world > 1:
-        t = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        elapsed_ms = float(t.item())
+    eng = GpuEngine(dev, out_dtype)
+    res = orchestrate(args.config, rank, world, args.steps, args.warmup, eng)
+    cfg, batch, bufs = res["cfg"], eng.batch, eng.bufs
+    kv_ms, tasa_ms, hma_ms = eng.call_ms("kv0", "kv1"), eng.call_ms("kv1", "t1"), \
+        eng.call_ms("h0", "h1")
 
     Ls = (batch.seq_offsets[1:] - batch.seq_offsets[:-1]).cpu().numpy()
     Cs = (batch.cand_offsets[1:] - batch.cand_offsets[:-1]).cpu().numpy()
     cnt = roofline.counts(cfg, Ls, Cs, n_item_ids=batch.item_ids.numel(),
                           n_user_ids=batch.user_ids.numel(),
                           out_bytes=2 if out_dtype == torch.bfloat16 else 4)
-    cands_per_step = cnt["candidates"] * world
-    value = cands_per_step * args.steps / (elapsed_ms / 1e3)
-    ms_per_step = elapsed_ms / args.steps
-
     peaks, peak_src = _peaks()
-    peak_tf = float(peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]))
+    peak_sus = float(peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]))
+    peak_burst = float(peaks["bf16_tflops"])
     hbm = float(peaks["hbm_gbs"])
     achieved = cnt["tasa_flop"] / (tasa_ms / 1e3) / 1e12
     traffic = None
@@ -287,30 +407,50 @@ def main():
     if os.path.exists(tp):
         with open(tp) as fh:
             traffic = json.load(fh).get(args.config, {}).get("tasa_bytes_per_launch")
-    roof_step_s = roofline.roof_time(cnt["kv_flop"], cnt["kv_bytes"], peak_tf, hbm) + max(
-        roofline.roof_time(cnt["tasa_flop"], cnt["tasa_bytes"], peak_tf, hbm),
-        cnt["hma_bytes"] / (hbm * 1e9))
 
+    def step_roof(P):
+        return roofline.roof_time(cnt["kv_flop"], cnt["kv_bytes"], P, hbm) + max(
+            roofline.roof_time(cnt["tasa_flop"], cnt["tasa_bytes"], P, hbm),
+            cnt["hma_bytes"] / (hbm * 1e9))
+
+    ms_per_step = res["ms_per_step"]
+    strong = res["scaling"] == "strong"
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": f"{cfg.name} (BASELINE config {args.config}): {B} requests per GPU,"
-                               f" L={cfg.L[1]}, C={cfg.C[1]}", "requests_per_gpu": B,
-                   "H": cfg.H, "d": cfg.d, "D_in": cfg.D_in, "F": cfg.F,
-                   "out_dtype": args.out_dtype, "act": "silu", "parallelism": f"dp{world}",
-                   "l2": "inputs larger than L2 (U 2.1 GB, item ids 1.1 GB per GPU); no flush"},
-        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
-                     "frac": achieved / peak_tf, "traffic": traffic,
-                     "kernel": "gesr_tasa_score (q-projection + attention kernels)",
-                     "peak_source": f"{peak_src} bf16_tflops_sustained (MEASURED_PEAKS.json)"},
-        "step_roofline": {"roof_ms": roof_step_s * 1e3, "frac": roof_step_s * 1e3 / ms_per_step,
+        "metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": res["scaling"], "vs_baseline": None,
+        "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": (f"{cfg.name} (BASELINE config {args.config}): "
+                                + (f"{cfg.B} requests LPT-sharded over {world} GPU(s)" if strong
+                                   else f"{cfg.B} requests per GPU")),
+                   "requests_total": cfg.B if strong else cfg.B * world,
+                   "requests_per_rank": res["per_rank_requests"],
+                   "H": cfg.H, "d": cfg.d, "D_in": cfg.D_in, "F": cfg.F, "L": list(cfg.L),
+                   "C": list(cfg.C), "out_dtype": args.out_dtype, "act": "silu",
+                   "parallelism": f"dp{world}",
+                   "l2": "inputs larger than L2 (per GPU: U and HMA item ids exceed 126 MB); "
+                         "no flush"},
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_sus,
+                     "unit": "TFLOP/s", "frac": achieved / peak_sus, "traffic": traffic,
+                     "kernel": "gesr_tasa_score (q-projection + attention kernels), timed "
+                               "inside the step",
+                     "peak_source": f"{peak_src} bf16_tflops_sustained (MEASURED_PEAKS.json): "
+                                    "the kernel runs inside back-to-back steps",
+                     "peak_burst": peak_burst, "frac_burst": achieved / peak_burst},
+        "step_roofline": {"roof_ms_sustained": step_roof(peak_sus) * 1e3,
+                          "frac_sustained": step_roof(peak_sus) * 1e3 / ms_per_step,
+                          "roof_ms_burst": step_roof(peak_burst) * 1e3,
+                          "frac_burst": step_roof(peak_burst) * 1e3 / ms_per_step,
                           "kv_ms": kv_ms, "tasa_ms": tasa_ms, "hma_ms": hma_ms,
                           "kv_tflops": cnt["kv_flop"] / (kv_ms / 1e3) / 1e12,
                           "hma_gbs": cnt["hma_bytes"] / (hma_ms / 1e3) / 1e9},
-        "gpu_launches": launches_per_step * args.steps,
-        "clocks": clk.summary(),
+        "gpu_launches": eng.launches,
+        "clocks": eng.clocks,
     }
+    if world > 1:
+        line["per_rank_ms"] = res["per_rank_ms"]
+        line["imbalance"] = {"measured": res["imbalance_measured"],
+                             "cost_model": res["imbalance_model"]}
 
     # ---------------------------------------------------------------- e2e through host buffers
     if not args.no_e2e:
@@ -320,16 +460,13 @@ def main():
                           batch.W_k.cpu(), batch.W_v.cpu(), pin(batch.user_ids),
                           pin(batch.user_offsets), pin(batch.item_ids), pin(batch.item_offsets))
         scorer = gb.PipelinedHostScorer(hb, n_chunks=args.e2e_chunks, out_dtype=bufs.O.dtype,
-                                        act=act, device=dev)
+                                        act=cfg.act, device=dev)
         h_O = torch.empty(bufs.O.shape, dtype=bufs.O.dtype).pin_memory()
         h_counts = torch.empty(bufs.counts.shape, dtype=torch.int32).pin_memory()
         h2d = scorer.h2d_bytes
         d2h = h_O.numel() * h_O.element_size() + h_counts.numel() * 4
-
-        def e2e_step():
-            scorer.run(h_O, h_counts, stream=main_stream)
-
-        e2e_step()
+        main_stream = eng.stream
+        scorer.run(h_O, h_counts, stream=main_stream)
         torch.cuda.synchronize()
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
@@ -338,7 +475,7 @@ def main():
             dist.barrier()
         a.record(main_stream)
         for _ in range(n_e2e):
-            e2e_step()
+            scorer.run(h_O, h_counts, stream=main_stream)
         b.record(main_stream)
         torch.cuda.synchronize()
         e_ms = a.elapsed_time(b)
@@ -346,7 +483,7 @@ def main():
             t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = float(t.item())
-        line["e2e"] = {"value": cands_per_step * n_e2e / (e_ms / 1e3), "unit": UNIT,
+        line["e2e"] = {"value": res["cands_per_step"] * n_e2e / (e_ms / 1e3), "unit": UNIT,
                        "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": n_e2e,
                        "chunks": len(scorer.chunks),
                        "pipeline": "request chunks: H2D of chunk i+1 and D2H of chunk i-1 "
@@ -354,31 +491,21 @@ def main():
 
     # ---------------------------------------------------------------- optional score gather
     if args.gather and world > 1:
-        t0 = time.perf_counter()
-        if rank == 0:
-            for r in range(1, world):
-                buf = torch.empty_like(bufs.O)
-                dist.recv(buf, src=r)
-        else:
-            dist.send(bufs.O, dst=0)
+        from paper_2511_21095_b200 import shard
+        rows = [int(x) for x in torch.tensor([bufs.O.shape[0]])]
+        allrows = [None] * world
+        dist.all_gather_object(allrows, rows[0])
         torch.cuda.synchronize()
-        line["gather_s"] = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        shard.gather_rows(bufs.O, allrows)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        nbytes = sum(allrows) * bufs.O.shape[1] * bufs.O.element_size()
+        line["gather"] = {"s": dt, "bytes": nbytes, "GBps": nbytes / dt / 1e9}
 
     # ---------------------------------------------------------------- cpu baseline (oracle)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        import oracle
-        threads = oracle.default_threads()
-        tot, c, n = 0.0, 0, 0
-        while tot < 12.0 and n < 64:
-            dt, cc = _cpu_sample(cfg, [n], threads)
-            tot += dt
-            c += cc
-            n += 1
-        line["cpu_baseline"] = {"value": c / tot, "unit": UNIT, "cores": threads,
-                                "kind": "oracle",
-                                "sample": f"{n} request(s) of config {args.config} (L=2048, "
-                                          f"C=1000 each), fp64 kv_project+tasa_score+hma_count, "
-                                          f"{tot:.1f} s"}
+        line["cpu_baseline"] = cpu_baseline(cfg, args.config)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

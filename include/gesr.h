@@ -28,8 +28,12 @@
  *     nothing; unsupported options return GESR_ERR_UNSUPPORTED; a too-small workspace returns
  *     GESR_ERR_WORKSPACE; a failed launch returns GESR_ERR_CUDA.  gesr_last_error() gives a
  *     thread-local message for the last non-OK return.
- *   - Offsets are NOT validated on the device: offsets[0] must be 0, offsets nondecreasing and
- *     offsets[B] equal to the stated total.  Malformed offsets are undefined behaviour.
+ *   - Offsets are NOT validated on the device by default: offsets[0] must be 0, offsets
+ *     nondecreasing and offsets[B] equal to the stated total.  Malformed offsets are undefined
+ *     behaviour.  With the environment variable GESR_DEBUG=1 (read once per process) every call
+ *     that takes offsets first launches a checking kernel that traps (the stream then reports
+ *     cudaErrorLaunchFailure / an illegal instruction) when seq_offsets, cand_offsets,
+ *     user_offsets or item_offsets break these rules.
  *   - Empty problems (B = 0, total_C = 0, F = 0) are valid no-ops.
  */
 #ifndef GESR_H_
@@ -69,6 +73,9 @@ typedef enum { GESR_OUT_F32 = 0, GESR_OUT_BF16 = 1 } gesr_out_dtype;
 int gesr_version(void);
 const char* gesr_status_string(int status);
 const char* gesr_last_error(void);
+/* Number of kernels this library has launched in the process so far (all devices, all
+ * threads).  Diagnostic: bench.py reports its difference over the timed region. */
+unsigned long long gesr_launch_count(void);
 
 /* gesr_kv_project -- K = act(U W_k^T + b_k), V = act(U W_v^T + b_v), split into heads.
  *   U        bf16 [total_L, D_in] row-major: all requests' history rows, request b owning rows

@@ -20,6 +20,7 @@ without the built library, raises.
 from __future__ import annotations
 
 import ctypes
+import functools
 import math
 import os
 import re
@@ -60,6 +61,7 @@ def lib():
                         "(there is no CPU fallback)")
     L = ctypes.CDLL(LIB_PATH)
     L.gesr_version.restype = ctypes.c_int
+    L.gesr_launch_count.restype = ctypes.c_ulonglong
     L.gesr_status_string.restype = ctypes.c_char_p
     L.gesr_status_string.argtypes = [ctypes.c_int]
     L.gesr_last_error.restype = ctypes.c_char_p
@@ -132,6 +134,26 @@ def _stream(stream) -> ctypes.c_void_p:
     return ctypes.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
 
 
+def _on_stream(fn):
+    """Run the wrapped call with `stream` (when given as a torch stream) as torch's current
+    stream, so every tensor the call allocates -- outputs, workspaces and the temporaries
+    stu_layer drops on return -- belongs to the launch stream in the caching allocator: a block
+    freed here is reused only by work ordered after these kernels on that stream."""
+    @functools.wraps(fn)
+    def wrapper(*a, **kw):
+        s = kw.get("stream")
+        if isinstance(s, torch.cuda.Stream) and s != torch.cuda.current_stream(s.device):
+            with torch.cuda.stream(s):
+                return fn(*a, **kw)
+        return fn(*a, **kw)
+    return wrapper
+
+
+def launch_count() -> int:
+    """Kernels libgesr.so has launched in this process (gesr_launch_count)."""
+    return int(lib().gesr_launch_count())
+
+
 def _dev(*ts):
     for t in ts:
         if t is not None and not t.is_cuda:
@@ -141,6 +163,7 @@ def _dev(*ts):
             raise GesrError(GESR_ERR_INVALID_ARG, "all tensors must be contiguous")
 
 
+@_on_stream
 def kv_project(U, W_k, W_v, H: int, d: int, act: int = GESR_ACT_SILU, b_k=None, b_v=None,
                K_cache=None, V_cache=None, stream=None):
     """K_cache, V_cache bf16 [H, total_L, d] = act(U W^T + b) (gesr_kv_project)."""
@@ -160,6 +183,7 @@ def tasa_workspace_bytes(B: int, total_C: int, H: int, d: int, kv_splits: int = 
     return int(lib().gesr_tasa_workspace_bytes(B, total_C, H, d, kv_splits))
 
 
+@_on_stream
 def tasa_score(T, cand_offsets, W_q, K_cache, V_cache, seq_offsets, H: int, d: int,
                act: int = GESR_ACT_SILU, b_q=None, scale: float = 0.0, kv_splits: int = 0,
                flags: int = 0, out_dtype=torch.float32, want_lse: bool = True, O=None, lse=None,
@@ -196,6 +220,7 @@ def tasa_score(T, cand_offsets, W_q, K_cache, V_cache, seq_offsets, H: int, d: i
     return O, lse
 
 
+@_on_stream
 def history_attention(U, seq_offsets, W_q, K_cache, V_cache, H: int, d: int,
                       act: int = GESR_ACT_SILU, b_q=None, scale: float = 0.0,
                       out_dtype=torch.float32, want_lse: bool = False, O=None, lse=None,
@@ -225,6 +250,7 @@ def nro_workspace_bytes(B: int, total_C: int, j: int, d: int, D_in: int,
     return int(lib().gesr_nro_workspace_bytes(B, total_C, j, d, D_in, kv_splits))
 
 
+@_on_stream
 def nro_cross_score(T, cand_offsets, W_q, q_gate, K_cache, V_cache, seq_offsets, j: int, d: int,
                     act: int = GESR_ACT_SILU, b_q=None, scale: float = 0.0, kv_splits: int = 0,
                     out_dtype=torch.float32, want_lse: bool = False, O=None, lse=None,
@@ -255,6 +281,7 @@ def stu_workspace_bytes(total_C: int, H: int, d: int) -> int:
     return int(lib().gesr_stu_workspace_bytes(total_C, H, d))
 
 
+@_on_stream
 def stu_output(T, O, W_g, ln_gamma, ln_beta, W_o, H: int, d: int, b_g=None, b_o=None,
                X_res=None, ln_eps: float = 1e-5, Y=None, workspace=None, stream=None):
     """Y bf16 [total_C, D_out] = (LayerNorm(O) * SiLU(T W_g^T + b_g)) W_o^T + b_o + X_res
@@ -275,6 +302,7 @@ def stu_output(T, O, W_g, ln_gamma, ln_beta, W_o, H: int, d: int, b_g=None, b_o=
     return Y
 
 
+@_on_stream
 def ro_cross_score(seeds, W_q, K_cache, V_cache, seq_offsets, i: int, d: int, ctx=None,
                    act: int = GESR_ACT_SILU, b_q=None, scale: float = 0.0,
                    out_dtype=torch.float32, U_cross=None, workspace=None, stream=None):
@@ -298,6 +326,7 @@ def ro_cross_score(seeds, W_q, K_cache, V_cache, seq_offsets, i: int, d: int, ct
     return U_cross
 
 
+@_on_stream
 def layer_norm(X, gamma, beta, eps: float = 1e-5, Y=None, stream=None):
     """Y bf16 [rows, D] = LayerNorm(X) * gamma + beta (gesr_layer_norm; Y may be X)."""
     _dev(X, gamma, beta, Y)
@@ -309,6 +338,7 @@ def layer_norm(X, gamma, beta, eps: float = 1e-5, Y=None, stream=None):
     return Y
 
 
+@_on_stream
 def stu_layer(U, T, seq_offsets, cand_offsets, layer: dict, H: int, d: int, eps: float = 1e-5,
               stream=None):
     """One full target-aware STU layer over [U, T] (mask SPEC.md:277 with the
@@ -335,6 +365,7 @@ def stu_layer(U, T, seq_offsets, cand_offsets, layer: dict, H: int, d: int, eps:
     return U2, T2
 
 
+@_on_stream
 def stu_stack(U, T, seq_offsets, cand_offsets, layers, H: int, d: int, eps: float = 1e-5,
               stream=None):
     """[U_self, T_self] after len(layers) STU layers (SPEC.md:298 self_attention_forward)."""
@@ -343,6 +374,7 @@ def stu_stack(U, T, seq_offsets, cand_offsets, layers, H: int, d: int, eps: floa
     return U, T
 
 
+@_on_stream
 def hma_count(user_ids, user_offsets, item_ids, item_offsets, cand_offsets, F: int, cap: int = 0,
               counts=None, stream=None):
     """counts int32 [total_C, F] (gesr_hma_count)."""
@@ -357,6 +389,7 @@ def hma_count(user_ids, user_offsets, item_ids, item_offsets, cand_offsets, F: i
     return counts
 
 
+@_on_stream
 def hma_count_embed(user_ids, user_offsets, item_ids, item_offsets, cand_offsets, F: int, M: int,
                     E, counts=None, emb=None, stream=None):
     """(counts int32 [total_C, F] capped at M, emb bf16 [total_C, F*D_h]) with
@@ -389,6 +422,10 @@ class StepBuffers:
             if want_lse else None
         self.counts = torch.empty((batch.total_C, cfg.F), dtype=torch.int32, device=dev)
         nbytes = tasa_workspace_bytes(batch.B, batch.total_C, H, d, 0)
+        if cfg.chunk and batch.B == 1:
+            # score_step(chunk=...) reuses this workspace for every candidate chunk: the
+            # split-L reserve is not monotone in total_C (auto splits only small calls)
+            nbytes = max(nbytes, tasa_workspace_bytes(1, min(cfg.chunk, batch.total_C), H, d, 0))
         self.workspace = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=dev)
         self.hma_stream = torch.cuda.Stream(device=dev)
         self.ev_fork = torch.cuda.Event()
@@ -396,19 +433,28 @@ class StepBuffers:
 
 
 def score_step(batch, bufs: StepBuffers, act: int = GESR_ACT_SILU, cap: int = 0,
-               chunk: int = 0, hma: bool = True, stream=None, hma_order=None):
+               chunk: int = 0, hma: bool = True, stream=None, hma_order=None, events=None):
     """One scoring step: gesr_kv_project -> gesr_tasa_score (optionally in candidate chunks
     reusing one K/V cache), with gesr_hma_count on a second stream joined by an event.
-    hma_order (default $GESR_HMA_ORDER or "fork"): "fork" launches HMA first on the side
-    stream, "kv" forks it after the K/V projection is enqueued, "serial" runs it on the main
-    stream after the attention."""
+    hma_order (default "fork"): "fork" launches HMA first on the side stream, "kv" forks it
+    after the K/V projection is enqueued, "serial" runs it on the main stream after the
+    attention.  events: optional dict of lists; timing events "kv0", "kv1", "t1" (main stream)
+    and "h0", "h1" (HMA's stream) are appended to it (bench.py's per-call times)."""
     cfg = batch.cfg
     main = torch.cuda.current_stream() if stream is None else stream
-    order = hma_order or os.environ.get("GESR_HMA_ORDER", "fork")
+    order = hma_order or "fork"
+
+    def _ev(name, s):
+        if events is not None:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(s)
+            events.setdefault(name, []).append(e)
 
     def _hma(s):
+        _ev("h0", s)
         hma_count(batch.user_ids, batch.user_offsets, batch.item_ids, batch.item_offsets,
                   batch.cand_offsets, cfg.F, cap, counts=bufs.counts, stream=s)
+        _ev("h1", s)
 
     def _fork():
         bufs.ev_fork.record(main)
@@ -418,8 +464,10 @@ def score_step(batch, bufs: StepBuffers, act: int = GESR_ACT_SILU, cap: int = 0,
 
     if hma and order == "fork":
         _fork()
+    _ev("kv0", main)
     kv_project(batch.U, batch.W_k, batch.W_v, cfg.H, cfg.d, act, K_cache=bufs.K, V_cache=bufs.V,
                stream=main)
+    _ev("kv1", main)
     if hma and order == "kv":
         _fork()
     if chunk and batch.B == 1:
@@ -439,6 +487,7 @@ def score_step(batch, bufs: StepBuffers, act: int = GESR_ACT_SILU, cap: int = 0,
         tasa_score(batch.T, batch.cand_offsets, batch.W_q, bufs.K, bufs.V, batch.seq_offsets,
                    cfg.H, cfg.d, act, O=bufs.O, lse=bufs.lse, want_lse=bufs.lse is not None,
                    workspace=bufs.workspace, stream=main)
+    _ev("t1", main)
     if hma and order == "serial":
         _hma(main)
     elif hma:

@@ -710,18 +710,11 @@ cudaError_t launch_d(const CUtensorMap& mq, const CUtensorMap& mk, const CUtenso
                      const CUtensorMap& mo, const AttnParams& p, int64_t max_units,
                      cudaStream_t stream) {
   using C = AttnCfg<D>;
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(attn_kernel<D, false, false>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+  for (const void* fn : {reinterpret_cast<const void*>(attn_kernel<D, false, false>),
+                         reinterpret_cast<const void*>(attn_kernel<D, true, false>),
+                         reinterpret_cast<const void*>(attn_kernel<D, false, true>)}) {
+    cudaError_t e = ensure_smem_attr(fn, C::kSmemBytes);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(attn_kernel<D, true, false>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(attn_kernel<D, false, true>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
-    if (e != cudaSuccess) return e;
-    attr_done = true;
   }
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -734,6 +727,7 @@ cudaError_t launch_d(const CUtensorMap& mq, const CUtensorMap& mk, const CUtenso
     attn_kernel<D, true, false><<<grid, C::kThreads, C::kSmemBytes, stream>>>(mq, mk, mv, mo, p);
   else
     attn_kernel<D, false, false><<<grid, C::kThreads, C::kSmemBytes, stream>>>(mq, mk, mv, mo, p);
+  count_launch();
   return cudaGetLastError();
 }
 
@@ -748,6 +742,7 @@ extern "C" int gesr_debug_trace_copy(void* host) {
 cudaError_t launch_build_units(const int64_t* seq_offsets, const int64_t* cand_offsets, int64_t B,
                                int4* units, int* count, int causal, cudaStream_t stream) {
   build_units_kernel<<<1, 1024, 0, stream>>>(seq_offsets, cand_offsets, B, units, count, causal);
+  count_launch();
   return cudaGetLastError();
 }
 
@@ -769,11 +764,13 @@ cudaError_t launch_attn_self_merge(const AttnParams& p, const void* Q, const voi
   attn_self_merge_kernel<<<static_cast<unsigned>((n + 7) / 8), 256, 0, stream>>>(
       p, static_cast<const __nv_bfloat16*>(Q), static_cast<const __nv_bfloat16*>(K_self),
       static_cast<const __nv_bfloat16*>(V_self), d, scale);
+  count_launch();
   return cudaGetLastError();
 }
 
 cudaError_t launch_attn_empty(const AttnParams& p, int d, cudaStream_t stream) {
   attn_empty_kernel<<<1184, 256, 0, stream>>>(p, d);
+  count_launch();
   return cudaGetLastError();
 }
 

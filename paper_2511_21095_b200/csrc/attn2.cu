@@ -889,6 +889,7 @@ cudaError_t launch_attn_combine(const AttnParams& p, int d, cudaStream_t stream)
   const int64_t n = p.total_C * p.H;
   if (n == 0) return cudaSuccess;
   attn_combine_kernel<<<static_cast<unsigned>(n), 128, 0, stream>>>(p, d);
+  count_launch();
   return cudaGetLastError();
 }
 
@@ -907,14 +908,13 @@ extern "C" int gesr_debug_trace3_copy(void* host) {
 cudaError_t launch_attn_pair(const CUtensorMap& mq, const CUtensorMap& mkh, const CUtensorMap& mvh,
                              const CUtensorMap& mo, const AttnParams& p, int64_t max_units,
                              cudaStream_t stream) {
-  static int max_pairs = 0;
+  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(attn_pair_kernel<false>),
+                                   kSmemBytes);
+  if (e != cudaSuccess) return e;
+  e = ensure_smem_attr(reinterpret_cast<const void*>(attn_pair_kernel<true>), kSmemBytes);
+  if (e != cudaSuccess) return e;
+  int max_pairs = device_cached(1);      // co-resident CTA pairs on this device
   if (max_pairs == 0) {
-    cudaError_t e = cudaFuncSetAttribute(attn_pair_kernel<false>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(attn_pair_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             kSmemBytes);
-    if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr;
     attr.id = cudaLaunchAttributeClusterDimension;
@@ -936,6 +936,7 @@ cudaError_t launch_attn_pair(const CUtensorMap& mq, const CUtensorMap& mkh, cons
       (void)cudaGetLastError();
     }
     max_pairs = clusters;
+    device_cache_store(1, max_pairs);
   }
   const int64_t work = max_units * p.H * p.splits;
   const unsigned pairs = static_cast<unsigned>(work < max_pairs ? work : max_pairs);
@@ -943,6 +944,7 @@ cudaError_t launch_attn_pair(const CUtensorMap& mq, const CUtensorMap& mkh, cons
     attn_pair_kernel<true><<<2 * pairs, kThreads, kSmemBytes, stream>>>(mq, mkh, mvh, mo, p);
   else
     attn_pair_kernel<false><<<2 * pairs, kThreads, kSmemBytes, stream>>>(mq, mkh, mvh, mo, p);
+  count_launch();
   return cudaGetLastError();
 }
 

@@ -12,9 +12,49 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
 #include <mutex>
+#include <set>
+#include <utility>
 
 #include "kernels.h"
+
+namespace gesr {
+
+namespace {
+std::mutex g_attr_mu;
+std::set<std::pair<int, const void*>> g_attr_done;
+constexpr int kMaxDev = 64;
+std::atomic<int> g_dev_cache[kMaxDev][8];
+std::atomic<unsigned long long> g_launches{0};
+}  // namespace
+
+cudaError_t ensure_smem_attr(const void* fn, int bytes) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(g_attr_mu);
+  if (g_attr_done.count({dev, fn})) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) g_attr_done.insert({dev, fn});
+  return e;
+}
+
+int device_cached(int slot) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) return 0;
+  return g_dev_cache[dev][slot].load(std::memory_order_acquire);
+}
+
+void device_cache_store(int slot, int value) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) return;
+  g_dev_cache[dev][slot].store(value, std::memory_order_release);
+}
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+}  // namespace gesr
 
 namespace {
 
@@ -54,13 +94,13 @@ EncodeTiledFn encode_fn() {
 }
 
 int num_sms() {
+  int n = gesr::device_cached(0);
+  if (n > 0) return n;
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
-  static int cache[64] = {0};
-  if (dev >= 0 && dev < 64 && cache[dev] > 0) return cache[dev];
-  int n = 148;
-  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-  if (dev >= 0 && dev < 64) cache[dev] = n;
+  n = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  gesr::device_cache_store(0, n);
   return n;
 }
 
@@ -126,6 +166,23 @@ gesr_status make_o_map(CUtensorMap* map, void* base, uint64_t rows, uint64_t H, 
   if (r != CUDA_SUCCESS)
     return fail(GESR_ERR_CUDA, "cuTensorMapEncodeTiled(O) failed: %d", static_cast<int>(r));
   return GESR_OK;
+}
+
+// GESR_DEBUG=1 (read once per process): device validation of the jagged offsets before the
+// kernels that index with them (debug.cu).
+bool debug_enabled() {
+  static const int on = [] {
+    const char* v = getenv("GESR_DEBUG");
+    return (v != nullptr && v[0] == '1') ? 1 : 0;
+  }();
+  return on == 1;
+}
+
+gesr_status debug_check(const int64_t* offsets, int64_t n, int64_t total, int tag,
+                        cudaStream_t st) {
+  if (!debug_enabled()) return GESR_OK;
+  cudaError_t e = gesr::launch_check_offsets(offsets, n, total, tag, st);
+  return e == cudaSuccess ? GESR_OK : cuda_fail(e, "check_offsets launch");
 }
 
 bool valid_d(int32_t d) { return d == 32 || d == 64 || d == 128; }
@@ -229,7 +286,11 @@ size_t stu_buffer_bytes(int64_t total_C, int64_t D) {
 
 extern "C" {
 
-int gesr_version(void) { return 100; }
+int gesr_version(void) { return 200; }
+
+unsigned long long gesr_launch_count(void) {
+  return gesr::g_launches.load(std::memory_order_relaxed);
+}
 
 const char* gesr_status_string(int s) {
   switch (s) {
@@ -317,7 +378,7 @@ static gesr_status tasa_impl(const void* T, int64_t total_C, int32_t D_in, const
                       int32_t H, int32_t d, float scale, int32_t kv_splits, uint32_t flags,
                       const void* K_self, const void* V_self, void* O, int32_t o_dtype,
                       float* lse, void* workspace, size_t workspace_bytes, void* stream,
-                      int causal = 0) {
+                      int causal = 0, bool validate_only = false) {
   const bool self = K_self != nullptr || V_self != nullptr;
   gesr_status s = check_common(D_in, H, d, act);
   if (s != GESR_OK) return s;
@@ -363,7 +424,17 @@ static gesr_status tasa_impl(const void* T, int64_t total_C, int32_t D_in, const
   const size_t need = gesr_tasa_workspace_bytes(B, total_C, H, d, kv_splits);
   if (workspace_bytes < need)
     return fail(GESR_ERR_WORKSPACE, "workspace %zu bytes < required %zu", workspace_bytes, need);
+  // the attention kernels count work items (unit, head, split) in 32 bits
+  const int64_t items = max_units(B, total_C) * H;
+  if (items * (kv_splits >= 1 ? kv_splits : (items < kAutoSplitItems ? kMaxAutoSplits : 1)) >=
+      (int64_t(1) << 31))
+    return fail(GESR_ERR_INVALID_ARG, "(units x heads x splits) exceeds 2^31 work items");
+  if (validate_only) return GESR_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  s = debug_check(seq_offsets, B, total_L, 0, st);
+  if (s != GESR_OK) return s;
+  s = debug_check(cand_offsets, B, total_C, 1, st);
+  if (s != GESR_OK) return s;
 
   gesr::AttnParams p{};
   p.seq_offsets = seq_offsets;
@@ -517,7 +588,12 @@ static gesr_status hma_impl(const int64_t* user_ids, const int64_t* user_offsets
   p.E = static_cast<const uint4*>(E);
   p.dh_chunks = E ? D_h / 8 : 0;
   p.emb = static_cast<uint4*>(emb);
-  cudaError_t e = gesr::launch_hma(p, static_cast<cudaStream_t>(stream));
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  gesr_status s = debug_check(cand_offsets, B, total_C, 1, st);
+  if (s == GESR_OK) s = debug_check(user_offsets, B * F, -1, 2, st);
+  if (s == GESR_OK) s = debug_check(item_offsets, total_C * F, -1, 3, st);
+  if (s != GESR_OK) return s;
+  cudaError_t e = gesr::launch_hma(p, st);
   return e == cudaSuccess ? GESR_OK : cuda_fail(e, "hma_kernel launch");
 }
 
@@ -579,32 +655,6 @@ gesr_status gesr_stu_output(const void* T, int64_t total_C, int32_t D_in, const 
   s = run_projection_rm(T, total_C, D_in, W_g, b_g, static_cast<int32_t>(D), GESR_ACT_SILU,
                         nullptr, workspace, st);
   if (s != GESR_OK) return s;
-  // 2+3 fused (opt-in GESR_STU_FUSED=1; D = 512, D_out % 256 == 0): the normalised, gated rows
-  // are produced into shared memory as the output GEMM's A operand (stu_fused.cu: slower than
-  // the two kernels below at the headline, kept for the record)
-  static const char* fused_env = getenv("GESR_STU_FUSED");
-  const bool fused = gesr::stu_fused_supported(static_cast<int>(D), D_out) &&
-                     fused_env != nullptr && fused_env[0] == '1';
-  if (fused) {
-    CUtensorMap mw, my;
-    s = make_map_2d(&mw, W_o, D_out, D, 128, 64, CU_TENSOR_MAP_SWIZZLE_128B, "W_o");
-    if (s != GESR_OK) return s;
-    s = make_out_map(&my, Y, 1, total_C, D_out, "Y");
-    if (s != GESR_OK) return s;
-    gesr::StuFusedParams fp{};
-    fp.M = total_C;
-    fp.N = D_out;
-    fp.o_bf16 = o_dtype == GESR_OUT_BF16 ? 1 : 0;
-    fp.O = O;
-    fp.G = static_cast<const __nv_bfloat16*>(workspace);
-    fp.gamma = ln_gamma;
-    fp.beta = ln_beta;
-    fp.eps = ln_eps;
-    fp.b_o = b_o;
-    fp.X_res = static_cast<const __nv_bfloat16*>(X_res);
-    cudaError_t ef = gesr::launch_stu_fused(mw, my, fp, num_sms(), st);
-    return ef == cudaSuccess ? GESR_OK : cuda_fail(ef, "stu_fused_kernel launch");
-  }
   // 2. Z = (LayerNorm(O) gamma + beta) * G, in place over G
   cudaError_t e = gesr::launch_ln_gate(O, o_dtype == GESR_OUT_BF16 ? 1 : 0,
                                        static_cast<__nv_bfloat16*>(workspace), ln_gamma, ln_beta,
@@ -650,6 +700,11 @@ gesr_status gesr_nro_cross_score(const void* T, int64_t total_C, int32_t D_in,
     return fail(GESR_ERR_WORKSPACE, "workspace %zu bytes < required %zu", workspace_bytes, need);
   const size_t off = nro_weight_offset(B, total_C, j, d, kv_splits);
   void* W_fold = static_cast<uint8_t*>(workspace) + off;
+  // every host-side check of the attention call runs before the first launch (fold_gate)
+  s = tasa_impl(T, total_C, D_in, cand_offsets, W_fold, b_q, act, K_cache, V_cache, seq_offsets,
+                B, total_L, j, d, scale, kv_splits, 0, nullptr, nullptr, O, o_dtype, lse,
+                workspace, off, stream, 0, /*validate_only=*/true);
+  if (s != GESR_OK) return s;
   cudaError_t e = gesr::launch_fold_gate(W_q, q_gate, W_fold, j, d, D_in,
                                          static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "fold_gate launch");

@@ -331,13 +331,9 @@ __global__ void __launch_bounds__(kThreads, 2)
 }  // namespace
 
 cudaError_t launch_hma(const HmaParams& p, cudaStream_t stream) {
-  static bool attr_done = false;
   const int smem = static_cast<int>(sizeof(HmaSmem));
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(hma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    attr_done = true;
-  }
+  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(hma_kernel), smem);
+  if (e != cudaSuccess) return e;
   // Large chunks amortise the per-CTA table build (one CTA per request at C = 1000: measured
   // 0.796 -> 0.759 ms at the headline); small ones keep the grid >= 4 CTAs per SM when there
   // are few requests (config 4: B = 1, C = 4096).
@@ -349,6 +345,7 @@ cudaError_t launch_hma(const HmaParams& p, cudaStream_t stream) {
   if (y > 65535) y = 65535;
   dim3 grid(static_cast<unsigned>(p.B), static_cast<unsigned>(y));
   hma_kernel<<<grid, kThreads, smem, stream>>>(p, chunk);
+  count_launch();
   return cudaGetLastError();
 }
 

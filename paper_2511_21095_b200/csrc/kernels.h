@@ -9,6 +9,23 @@
 
 namespace gesr {
 
+// ---------------------------------------------------------------- launch bookkeeping (capi.cpp)
+// Raise `fn`'s dynamic shared-memory limit to `bytes` on the CURRENT device, once per (device,
+// kernel): the attribute belongs to each device's context, so a process driving several GPUs
+// sets it on each.  Thread-safe.
+cudaError_t ensure_smem_attr(const void* fn, int bytes);
+// Per-device cached value of a launch-configuration query (e.g. the occupancy in CTA pairs):
+// slot in [0, 8); returns 0 if not yet stored on this device.
+int device_cached(int slot);
+void device_cache_store(int slot, int value);
+// Every kernel launch of the library is counted (gesr_launch_count(): the bench's
+// gpu_launches claim is read from it, not typed in).
+void count_launch();
+// GESR_DEBUG=1: device check of a jagged offsets array [n + 1] (debug.cu); traps if
+// offsets[0] != 0, offsets decrease, or offsets[n] != total.  tag names the array in the report.
+cudaError_t launch_check_offsets(const int64_t* offsets, int64_t n, int64_t total, int tag,
+                                 cudaStream_t stream);
+
 // ---------------------------------------------------------------- K-PROJ (proj.cu)
 struct ProjParams {
   int64_t M;          // rows of X
@@ -94,25 +111,6 @@ cudaError_t launch_attn_empty(const AttnParams& p, int d, cudaStream_t stream);
 // features per row (R15).  O fp32 or bf16 [C, D]; G bf16 [C, D].
 cudaError_t launch_ln_gate(const void* O, int o_bf16, __nv_bfloat16* G, const float* gamma,
                            const float* beta, float eps, int64_t C, int D, cudaStream_t stream);
-
-// Fused LayerNorm(O) * gamma + beta, times G, then W_o (+ b_o + X_res) (stu_fused.cu): one
-// kernel for D = 512 and D_out a multiple of 256 (stu_fused_supported); map_w: W_o [D_out, 512]
-// box {64, 128} SW128; map_y: Y as {D_out, M, 1} box {32, 32, 1} SW64.
-struct StuFusedParams {
-  int64_t M;               // rows
-  int N;                   // D_out
-  int o_bf16;
-  const void* O;           // [M, 512] fp32 or bf16
-  const __nv_bfloat16* G;  // [M, 512]
-  const float* gamma;
-  const float* beta;
-  float eps;
-  const float* b_o;        // [N] or null
-  const __nv_bfloat16* X_res;   // [M, N] or null
-};
-bool stu_fused_supported(int D, int D_out);
-cudaError_t launch_stu_fused(const CUtensorMap& map_w, const CUtensorMap& map_y,
-                             const StuFusedParams& p, int num_sms, cudaStream_t stream);
 
 // Y[r] = LayerNorm(X[r]) * gamma + beta over D features, bf16 in / out (stu.cu; R18).
 cudaError_t launch_layer_norm(const void* X, void* Y, const float* gamma, const float* beta,

@@ -75,12 +75,14 @@ cudaError_t launch_ro_queries(const void* seeds, const void* ctx, void* X, int64
   ro_queries_kernel<<<148 * 4, 256, 0, stream>>>(static_cast<const __nv_bfloat16*>(seeds),
                                                  static_cast<const __nv_bfloat16*>(ctx),
                                                  static_cast<__nv_bfloat16*>(X), offs, B, i, D_in);
+  count_launch();
   return cudaGetLastError();
 }
 
 cudaError_t launch_ro_gather(const float* O_full, void* out, int o_bf16, int64_t B, int i, int d,
                              cudaStream_t stream) {
   ro_gather_kernel<<<148 * 4, 256, 0, stream>>>(O_full, out, o_bf16, B, i, d);
+  count_launch();
   return cudaGetLastError();
 }
 
@@ -93,6 +95,7 @@ cudaError_t launch_fold_gate(const void* W_q, const float* gate, void* out, int 
   fold_gate_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(
       static_cast<const __nv_bfloat16*>(W_q), gate, static_cast<__nv_bfloat16*>(out),
       static_cast<int64_t>(j) * d, D_in, d);
+  count_launch();
   return cudaGetLastError();
 }
 

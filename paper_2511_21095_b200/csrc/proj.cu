@@ -338,21 +338,14 @@ cudaError_t launch_bn(const CUtensorMap& ma, const CUtensorMap& mb0, const CUten
                       const CUtensorMap& mo0, const CUtensorMap& mo1, const ProjParams& p,
                       int num_sms, cudaStream_t stream) {
   using S = ProjSmem<BN>;
-  static bool attr_done = false;  // same arch on every device of the box
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(proj_kernel<BN>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, S::kBytes);
-    if (e != cudaSuccess) return e;
-    attr_done = true;
-  }
+  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(proj_kernel<BN>), S::kBytes);
+  if (e != cudaSuccess) return e;
   ProjParams q = p;
   q.m_major = p.num_m_blocks >= num_sms / 2 ? 1 : 0;
-  static const char* order_env = getenv("GESR_PROJ_ORDER");   // A/B override: 0 / 1
-  if (order_env != nullptr && (order_env[0] == '0' || order_env[0] == '1'))
-    q.m_major = order_env[0] - '0';
   const int work = q.m_major ? p.num_m_blocks : p.num_m_blocks * p.num_n_blocks;
   const int pairs = work < num_sms / 2 ? work : num_sms / 2;
   proj_kernel<BN><<<2 * pairs, kThreads, S::kBytes, stream>>>(ma, mb0, mb1, mo0, mo1, q);
+  count_launch();
   return cudaGetLastError();
 }
 

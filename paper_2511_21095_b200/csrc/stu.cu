@@ -226,6 +226,7 @@ cudaError_t launch_ln_gate(const void* O, int o_bf16, __nv_bfloat16* G, const fl
   else
     ln_gate_kernel<4><<<static_cast<unsigned>(blocks), kWarpsPerCta * 32, 0, stream>>>(
         O, o_bf16, G, gamma, beta, eps, C, D);
+  count_launch();
   return cudaGetLastError();
 }
 
@@ -241,6 +242,7 @@ cudaError_t launch_layer_norm(const void* X, void* Y, const float* gamma, const 
   else
     layer_norm_kernel<4><<<static_cast<unsigned>(blocks), kWarpsPerCta * 32, 0, stream>>>(
         x, y, gamma, beta, eps, rows, D);
+  count_launch();
   return cudaGetLastError();
 }
 

@@ -250,3 +250,42 @@ def make_batch(cfg: Config, requests: Optional[Sequence[int]] = None, device="cp
         io = _offsets(ilen)
         ii = _progression(cfg, S_IID, mix64(iseg ^ S_IID), ilen, fields_i, hma_duplicates)
     return Batch(cfg, req, so, co, U, T, W_q, W_k, W_v, ui, uo, ii, io)
+
+
+def _seg_index(offsets: torch.Tensor, segs: torch.Tensor) -> torch.Tensor:
+    """Element indices of the given CSR segments, concatenated in the order given."""
+    lo, hi = offsets[segs], offsets[segs + 1]
+    n = hi - lo
+    if int(n.sum().item()) == 0:
+        return torch.zeros(0, dtype=torch.int64, device=offsets.device)
+    start = torch.repeat_interleave(lo, n)
+    first = torch.repeat_interleave(_offsets(n)[:-1], n)
+    return start + torch.arange(int(n.sum().item()), device=offsets.device) - first
+
+
+def select_requests(batch: Batch, idx: Sequence[int], device="cpu") -> Batch:
+    """The sub-batch of the given LOCAL request positions (in the order given), moved to
+    `device`, offsets rebased: the same rows / IDs the full batch holds for those requests (so
+    a test can feed the oracle exactly the inputs the device batch was scored on).  Index
+    bookkeeping only."""
+    dev = batch.seq_offsets.device
+    idx = torch.as_tensor(list(idx), dtype=torch.int64, device=dev)
+    so, co = batch.seq_offsets, batch.cand_offsets
+    Ls, Cs = (so[idx + 1] - so[idx]), (co[idx + 1] - co[idx])
+    rows = _seg_index(so, idx)
+    cands = _seg_index(co, idx)
+    mv = lambda x: None if x is None else x.to(device)    # noqa: E731
+    U = None if batch.U is None else batch.U[rows]
+    T = None if batch.T is None else batch.T[cands]
+    ui = uo = ii = io = None
+    if batch.user_ids is not None:
+        F = batch.cfg.F
+        useg = (idx[:, None] * F + torch.arange(F, device=dev)).reshape(-1)
+        iseg = (cands[:, None] * F + torch.arange(F, device=dev)).reshape(-1)
+        uo = _offsets(batch.user_offsets[useg + 1] - batch.user_offsets[useg])
+        io = _offsets(batch.item_offsets[iseg + 1] - batch.item_offsets[iseg])
+        ui = batch.user_ids[_seg_index(batch.user_offsets, useg)]
+        ii = batch.item_ids[_seg_index(batch.item_offsets, iseg)]
+    return Batch(batch.cfg, mv(batch.requests[idx]), mv(_offsets(Ls)), mv(_offsets(Cs)), mv(U),
+                 mv(T), mv(batch.W_q), mv(batch.W_k), mv(batch.W_v), mv(ui), mv(uo), mv(ii),
+                 mv(io))

@@ -1,0 +1,147 @@
+"""GPU parity on the five BASELINE configs at full size, in bench.py's exact launch configuration
+(VERDICT r1 missing 2, weak 2-3), plus the ABI arguments the headline never exercises.
+
+bench.py times `binding.score_step(batch, StepBuffers(batch, out_dtype=bf16))`: HMA forked
+first on a side stream, kv_splits = 0 (auto), bf16 O through the TMA-store epilogue.  Here the
+same two calls run on the whole config batch, then:
+
+  * HMA counts are compared with the fp64/int64 oracle for EVERY candidate of configs 3, 3h and 5
+    (bit-exact; the oracle runs over request chunks of the same device-generated inputs);
+  * attention rows are compared element by element (max-abs 2e-2, mean-abs 2e-3 vs fp64) on the
+    SURVEY.md s8(c) seeded subset of >= 64 requests: the 8 longest-L, 8 shortest-L, 8 largest-C,
+    8 smallest-C and 32 random requests (seed 2511), topped up with random ones if these overlap.
+
+The oracle is fed `inputs.select_requests(...)` of the device batch: exactly the rows and IDs
+the kernels scored (generator output, never a kernel output).
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2511_21095_b200 import binding as gb
+from paper_2511_21095_b200 import configs, inputs
+from subsets import survey_subset
+
+pytestmark = pytest.mark.gpu
+
+MAX_ABS, MEAN_ABS = 2e-2, 2e-3
+
+
+def _cuda():
+    assert torch.cuda.is_available(), "GPU tests need a B200 (run through gpurun)"
+    return torch.device("cuda:0")
+
+
+def _attn_check(O_gpu, O_or, what):
+    O_gpu = O_gpu.astype(np.float64)
+    assert np.isfinite(O_gpu).all(), f"{what}: non-finite output"
+    diff = np.abs(O_gpu - O_or)
+    mx, mn = float(diff.max()), float(diff.mean())
+    assert mx <= MAX_ABS and mn <= MEAN_ABS, f"{what}: max-abs {mx:.3e} mean-abs {mn:.3e}"
+    return mx, mn
+
+
+def _rows_of(co: np.ndarray, reqs):
+    return np.concatenate([np.arange(co[b], co[b + 1]) for b in reqs])
+
+
+@pytest.mark.parametrize("name", ["3", "3h", "5"])
+def test_config_bench_launch_parity(name):
+    dev = _cuda()
+    cfg = configs.get(name)
+    bt = inputs.make_batch(cfg, device=dev)
+    bufs = gb.StepBuffers(bt, out_dtype=torch.bfloat16)      # bench.py's buffers
+    gb.score_step(bt, bufs)                                    # bench.py's step
+    torch.cuda.synchronize()
+    co = bt.cand_offsets.cpu().numpy()
+    so = bt.seq_offsets.cpu().numpy()
+
+    # HMA: every candidate, bit-exact, oracle over request chunks
+    chunk = 512
+    checked = 0
+    for b0 in range(0, cfg.B, chunk):
+        reqs = list(range(b0, min(cfg.B, b0 + chunk)))
+        sub = inputs.select_requests(bt, reqs)
+        want = oracle.hma_count(sub.user_ids, sub.user_offsets, sub.item_ids, sub.item_offsets,
+                                sub.cand_offsets, cfg.F)
+        got = bufs.counts[co[b0]:co[reqs[-1] + 1]].cpu().numpy()
+        assert np.array_equal(got, want), f"config {name}: HMA mismatch in requests {b0}.."
+        checked += got.shape[0]
+    assert checked == bt.total_C
+
+    # attention: the s8(c) subset, elementwise
+    Ls, Cs = np.diff(so), np.diff(co)
+    reqs = survey_subset(Ls, Cs)
+    assert len(reqs) >= min(64, cfg.B)
+    sub = inputs.select_requests(bt, reqs)
+    K, V = oracle.kv_project(sub.U, sub.W_k, sub.W_v, cfg.H, cfg.d, act=cfg.act)
+    O_or, _ = oracle.tasa_score(sub.T, sub.cand_offsets, sub.W_q, K, V, sub.seq_offsets, cfg.H,
+                                cfg.d, act=cfg.act)
+    rows = torch.as_tensor(_rows_of(co, reqs), device=dev)
+    O = bufs.O[rows].float().cpu().numpy()
+    mx, mn = _attn_check(O, O_or, f"config {name} subset of {len(reqs)} requests")
+    print(f"config {name}: HMA {checked} candidates exact; attention {len(reqs)} requests "
+          f"({rows.numel()} rows) max-abs {mx:.2e} mean-abs {mn:.2e}")
+
+
+# ----------------------------------------------------------------------------- ABI arguments
+
+def _ragged(d, H, D_in, cfg_id):
+    cfg = configs.Config("args", cfg_id, B=7, L=("uniform", 0, 300), C=("uniform", 0, 280), H=H,
+                         d=d, D_in=D_in, F=2)
+    return cfg, inputs.make_batch(cfg, hma=False)
+
+
+@pytest.mark.parametrize("d,H,D_in", [(32, 2, 64), (64, 2, 128), (128, 2, 256)])
+@pytest.mark.parametrize("act", [0, 1])
+@pytest.mark.parametrize("scale", [0.05, 0.0, 0.5])
+def test_tasa_bias_scale_act(d, H, D_in, act, scale):
+    """gesr_tasa_score with b_q != NULL, a non-default scale (0 -> 1/sqrt(d)) and act =
+    identity / SiLU at d = 32 / 64 / 128 (1-CTA and pair kernels), fp32 O and lse."""
+    dev = _cuda()
+    cfg, bt = _ragged(d, H, D_in, 300 + d + act)
+    HD = H * d
+    b_q = torch.linspace(-0.8, 0.6, HD, dtype=torch.float32)
+    b_k = torch.linspace(0.5, -0.5, HD, dtype=torch.float32)
+    b_v = torch.linspace(-0.3, 0.9, HD, dtype=torch.float32)
+    K_or, V_or = oracle.kv_project(bt.U, bt.W_k, bt.W_v, H, d, act=act, b_k=b_k.double(),
+                                   b_v=b_v.double())
+    O_or, lse_or = oracle.tasa_score(bt.T, bt.cand_offsets, bt.W_q, K_or, V_or, bt.seq_offsets,
+                                     H, d, act=act, b_q=b_q.double(),
+                                     scale=None if scale == 0.0 else scale)
+    g = bt.to(dev)
+    K, V = gb.kv_project(g.U, g.W_k, g.W_v, H, d, act, b_k=b_k.to(dev), b_v=b_v.to(dev))
+    O, lse = gb.tasa_score(g.T, g.cand_offsets, g.W_q, K, V, g.seq_offsets, H, d, act,
+                           b_q=b_q.to(dev), scale=scale)
+    torch.cuda.synchronize()
+    _attn_check(O.cpu().numpy(), O_or, f"d={d} act={act} scale={scale}")
+    lse = lse.cpu().numpy()
+    fin = np.isfinite(lse_or)
+    assert np.array_equal(fin, np.isfinite(lse))
+    assert np.abs(lse[fin] - lse_or[fin]).max() < 3e-2
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_tasa_identity_bf16_out_forced_splits(d):
+    """act = identity with bf16 O and forced kv_splits: every split count gives the oracle's
+    rows within tolerance; splits = 1 is bit-identical run to run."""
+    dev = _cuda()
+    cfg, bt = _ragged(d, 2, 128, 400 + d)
+    K_or, V_or = oracle.kv_project(bt.U, bt.W_k, bt.W_v, 2, d, act=0)
+    O_or, _ = oracle.tasa_score(bt.T, bt.cand_offsets, bt.W_q, K_or, V_or, bt.seq_offsets, 2, d,
+                                act=0)
+    g = bt.to(dev)
+    K, V = gb.kv_project(g.U, g.W_k, g.W_v, 2, d, 0)
+    outs = {}
+    for s in (1, 2, 3):
+        O, _ = gb.tasa_score(g.T, g.cand_offsets, g.W_q, K, V, g.seq_offsets, 2, d, 0,
+                             kv_splits=s, out_dtype=torch.bfloat16, want_lse=False)
+        outs[s] = O.clone()
+        _attn_check(O.float().cpu().numpy(), O_or, f"identity d={d} splits={s}")
+    O1b, _ = gb.tasa_score(g.T, g.cand_offsets, g.W_q, K, V, g.seq_offsets, 2, d, 0,
+                           kv_splits=1, out_dtype=torch.bfloat16, want_lse=False)
+    torch.cuda.synchronize()
+    assert torch.equal(O1b, outs[1])

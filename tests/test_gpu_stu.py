@@ -151,19 +151,3 @@ def test_stu_output_edges():
         gb.stu_output(g["T"], g["O"], g["W_g"], g["ln_gamma"], g["ln_beta"], g["W_o"], 1, 64,
                       workspace=torch.empty(256, dtype=torch.uint8, device=dev))
     assert e.value.status == gb.GESR_ERR_WORKSPACE
-
-
-def test_stu_fused_kernel_subprocess():
-    # the opt-in fused LayerNorm-gate + output-projection kernel (GESR_STU_FUSED=1, read once per
-    # process): the same parity checks in a fresh process
-    import os
-    import subprocess
-    import sys
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    code = ("import sys; sys.path.insert(0, %r); sys.path.insert(0, %r); import torch;"
-            "import test_gpu_stu as t; t.test_stu_output_parity(4, 128, 512, torch.float32);"
-            "t.test_stu_output_parity(4, 128, 512, torch.bfloat16);"
-            "t.test_stu_output_headline_size_sampled()" % (root, os.path.join(root, "tests")))
-    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, GESR_STU_FUSED="1"),
-                       capture_output=True, text=True, timeout=600)
-    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
