@@ -7,24 +7,27 @@
 // multiplicity lookup: each item ID contributes the number of times it occurs in the user's
 // list of the same field.  Exact integer arithmetic; bit-identical to the definition.
 //
-// B200 design (HBM-bound on the item-ID stream, ~8.5 int64 IDs per (candidate, field)):
+// B200 design.  The kernel is bound by the item-ID stream (~8.5 int64 IDs per (candidate,
+// field) segment, read once); round 1's version spent ~114 instructions per ID (owner-map
+// writes, 64-bit window probes with continuation tests) and ran at 0.31 of HBM.  This one is
+// built around a per-ID instruction budget of ~40:
 //   grid (B, Y): CTA (b, y) owns request b and candidate chunks y, y+Y, ... of `chunk` rows.
-//   1. The request's F user lists go into per-field open-addressing tables in shared memory:
-//      64-bit keys only (INT64_MIN marks an empty slot; that one ID value is counted on the side),
-//      every OCCURRENCE of a user ID in its own slot (parallel 64-bit atomicCAS, linear probing
-//      from the even slot of a multiplicative hash of the key's two 32-bit halves), >= 8 slots
-//      per ID when the 8192-slot pool allows (load factor <= 1/8), else >= 4.  All copies of a
-//      key lie between its home slot and the first empty slot after it, so a lookup COUNTS the
-//      matches in the 4-slot window of its home pair and the next (two 16-byte reads, no
-//      multiplicity array) and walks on only when the whole window is occupied -- rare enough at
-//      1/8 that the warp seldom executes the walk.  Fields whose tables do not fit the pool fall
-//      back to a direct scan of global memory.
-//   2. Each warp takes 32 consecutive (candidate, field) segments of the CSR item stream.
-//      Lane k writes its segment id into a per-warp owner map (one uint16 per ID position),
-//      then the warp reads the group's IDs COALESCED (lane l reads ID start + l + 32 i), looks
-//      each up in its field's table, and adds hits into a per-warp shared counter.  Lane k then
-//      stores segment k's count: one coalesced 128-byte int32 store per 32 segments.
-//      Groups with more than kOwnerCap IDs use a shuffle binary search instead of the map.
+//   1. Table build: the request's F user lists go into per-field BUCKETED hash tables in shared
+//      memory -- 2^k buckets of 4 64-bit slots (32 bytes, two 16-byte reads), one slot per
+//      OCCURRENCE of a user ID (so a lookup counts matching slots; no count array), >= 2 buckets
+//      per ID (mean bucket load <= 1/2).  A bucket that overflows spills into a small per-CTA
+//      stash; a field whose list does not fit the pool is looked up in global memory.  The ID
+//      value INT64_MIN marks an empty slot and is counted on the side.
+//   2. Scan: each warp takes 32 consecutive (candidate, field) segments (their IDs are one
+//      contiguous range of the CSR stream) and walks the range in 32-ID windows, one coalesced
+//      8-byte load per lane, 4 windows in flight.  The segment of each ID position comes from
+//      the segment starts that fall in the window: lane k contributes bit (off_k - base), one
+//      redux.sync.or forms the window's start mask, and position l's segment is the running
+//      start count plus popc(mask & lanemask_le) - 1 (no owner map in shared memory; groups
+//      with an empty segment take a binary-search path).  The segment's table word comes by
+//      shuffle from its lane; the lookup is hash -> bucket -> two 16-byte reads -> four 64-bit
+//      compares; hits go to a per-warp shared counter (predicated shared atomics), and lane k
+//      stores segment k's count (one coalesced 128-byte store per group).
 #include <cuda_runtime.h>
 
 #include "kernels.h"
@@ -35,75 +38,81 @@ namespace {
 
 constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
-constexpr int kChunkMin = 256;            // candidates per CTA chunk (runtime: 256 or 1024)
+constexpr int kChunkMin = 256;             // candidates per CTA chunk (runtime: 256 or 1024)
 constexpr int kChunkMax = 1024;
-constexpr int kPoolSlots = 8192;          // table slots per CTA (64 KB of keys)
+constexpr int kPoolBuckets = 2048;         // 4 slots each: 64 KB of keys per CTA
+constexpr int kStash = 256;                // overflowing user IDs (key, field)
 constexpr int kMaxFields = 256;
-constexpr int kOwnerCap = 512;            // IDs per 32-segment group handled with the owner map
+constexpr int kWinUnroll = 4;              // 32-ID windows in flight per warp
+constexpr int kFastMaxIds = 32 * 64;       // groups up to this many IDs take the fast path
 constexpr unsigned long long kSentinel = 0x8000000000000000ull;   // INT64_MIN: empty slot
-constexpr uint32_t kMul = 0x9E3779B1u;
+constexpr uint32_t kMulLo = 0x9E3779B1u;
+constexpr uint32_t kMulHi = 0x85EBCA77u;
+
+// table word of a field: first bucket (bits 0-11), hash shift (12-17), flags
+constexpr uint32_t kFlagStash = 1u << 18;    // some of the field's IDs are in the stash
+constexpr uint32_t kFlagGlobal = 1u << 19;   // the field's list is scanned in global memory
 
 struct HmaSmem {
-  unsigned long long key[kPoolSlots];             // kSentinel = empty; one slot per occurrence
-  int2 tab[kMaxFields];                           // {first slot, hash shift}; first < 0: global
-  int sent_cnt[kMaxFields];                       // multiplicity of INT64_MIN
-  long long uoff[kMaxFields + 1];                 // this request's user_offsets (F+1)
+  ulonglong2 bkt[kPoolBuckets][2];           // kSentinel = empty slot
+  unsigned long long stash_key[kStash];
+  int stash_field[kStash];
+  uint32_t tab[kMaxFields];
+  int sent_cnt[kMaxFields];                  // multiplicity of INT64_MIN per field
+  long long uoff[kMaxFields + 1];            // this request's user_offsets (F+1)
   int warp_cnt[kWarps][32];
-  // owner word of each ID position of a warp's 32-segment group: segment lane (bits 0-4), the
-  // field's hash shift (5-9), its first table slot (10-22), the field (23-30)
-  uint32_t owner[kWarps][kOwnerCap];
-  int any_global;                                 // some field scans global memory instead
+  int stash_n;
+  int slow_any;                              // some field has stash entries or goes global
 };
 
-// Home slot pair of a key in a table of 2^(32 - shift) slot pairs (top bits of a
-// multiplicative hash of the folded key).
-__device__ __forceinline__ uint32_t home_pair(unsigned long long key, int shift) {
-  const uint32_t h = (static_cast<uint32_t>(key) ^ static_cast<uint32_t>(key >> 32)) * kMul;
-  return h >> shift;
+__device__ __forceinline__ uint32_t key_hash(unsigned long long key) {
+  return (static_cast<uint32_t>(key) * kMulLo) ^ (static_cast<uint32_t>(key >> 32) * kMulHi);
+}
+// PTX shifts clamp the shift amount (>= 32 gives 0), unlike C++ shifts
+__device__ __forceinline__ uint32_t shr_clamp(uint32_t a, uint32_t n) {
+  uint32_t r;
+  asm("shr.b32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(n));
+  return r;
+}
+__device__ __forceinline__ uint32_t shl_clamp(uint32_t a, uint32_t n) {
+  uint32_t r;
+  asm("shl.b32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(n));
+  return r;
+}
+__device__ __forceinline__ uint32_t bucket_of(uint32_t tab, unsigned long long key) {
+  return (tab & 4095u) + shr_clamp(key_hash(key), (tab >> 12) & 63u);
 }
 
-// Copies of `key` in a field's table (first slot `base`, 2^(32 - shift) slot pairs).  Every
-// occurrence of a user ID has its own slot, filled by linear probing from the even slot of its
-// home pair, so all copies lie between the home slot and the first empty slot after it: count
-// matches over the 4-slot window of the home pair and the next one (two 16-byte reads) and walk
-// on only if the whole window is occupied (rare at load factor <= 1/8).
-__device__ __forceinline__ int window_count(const unsigned long long* tb, uint32_t pr,
-                                            uint32_t pmask, unsigned long long key, bool& open) {
-  const ulonglong2 a = *reinterpret_cast<const ulonglong2*>(tb + 2 * pr);
-  const ulonglong2 b = *reinterpret_cast<const ulonglong2*>(tb + 2 * ((pr + 1) & pmask));
-  open = a.x != kSentinel && a.y != kSentinel && b.x != kSentinel && b.y != kSentinel;
-  return (a.x == key ? 1 : 0) + (a.y == key ? 1 : 0) + (b.x == key ? 1 : 0) + (b.y == key ? 1 : 0);
-}
-// the rest of the walk after a full window starting at pair pr
-__device__ __forceinline__ int walk_on(const unsigned long long* tb, uint32_t pr, uint32_t pmask,
-                                    unsigned long long key) {
-  int c = 0;
-  pr = (pr + 2) & pmask;
-  while (true) {
-    const ulonglong2 a = *reinterpret_cast<const ulonglong2*>(tb + 2 * pr);
-    c += (a.x == key ? 1 : 0) + (a.y == key ? 1 : 0);
-    if (a.x == kSentinel || a.y == kSentinel) return c;
-    pr = (pr + 1) & pmask;
-  }
+__device__ __forceinline__ int bucket_count(const HmaSmem& s, uint32_t tab,
+                                            unsigned long long key) {
+  const uint32_t b = bucket_of(tab, key);
+  const ulonglong2 a = s.bkt[b][0];
+  const ulonglong2 c = s.bkt[b][1];
+  return (a.x == key) + (a.y == key) + (c.x == key) + (c.y == key);
 }
 
-__device__ __forceinline__ int lookup(const HmaSmem& s, const HmaParams& p, int f,
-                                      unsigned long long key) {
-  if (key == kSentinel) return s.sent_cnt[f];
-  const int2 t = s.tab[f];
-  if (t.x >= 0) {
-    const uint32_t pmask = 0xFFFFFFFFu >> t.y;
-    const uint32_t pr = home_pair(key, t.y);
-    bool open;
-    int c = window_count(s.key + t.x, pr, pmask, key, open);
-    if (open) c += walk_on(s.key + t.x, pr, pmask, key);
+// Everything the bucket lookup does not cover: INT64_MIN, stash entries, global-memory fields.
+__device__ __noinline__ int slow_count(const HmaSmem& s, const HmaParams& p, int f, uint32_t tab,
+                                       unsigned long long key) {
+  if (tab & kFlagGlobal) {     // (INT64_MIN included: the scan compares raw values)
+    int c = 0;
+    for (long long i = s.uoff[f]; i < s.uoff[f + 1]; ++i)
+      c += (static_cast<unsigned long long>(__ldg(p.user_ids + i)) == key) ? 1 : 0;
     return c;
   }
-  // global fallback: direct scan of the user list
-  int c = 0;
-  for (long long i = s.uoff[f]; i < s.uoff[f + 1]; ++i)
-    c += (static_cast<unsigned long long>(__ldg(p.user_ids + i)) == key) ? 1 : 0;
+  if (key == kSentinel) return s.sent_cnt[f];
+  int c = bucket_count(s, tab, key);
+  if (tab & kFlagStash) {
+    const int n = s.stash_n < kStash ? s.stash_n : kStash;
+    for (int i = 0; i < n; ++i) c += (s.stash_field[i] == f && s.stash_key[i] == key) ? 1 : 0;
+  }
   return c;
+}
+
+__device__ __forceinline__ int lookup_any(const HmaSmem& s, const HmaParams& p, int f,
+                                          uint32_t tab, unsigned long long key) {
+  if (key == kSentinel || (tab & (kFlagStash | kFlagGlobal))) return slow_count(s, p, f, tab, key);
+  return bucket_count(s, tab, key);
 }
 
 __global__ void __launch_bounds__(kThreads, 2)
@@ -120,30 +129,35 @@ __global__ void __launch_bounds__(kThreads, 2)
   const int lane = tid & 31;
   const int warp = tid >> 5;
 
-  // ---- 1. per-field hash tables of the request's user lists
+  // ---- 1. per-field bucketed tables of the request's user lists
   for (int f = tid; f <= F; f += kThreads) s.uoff[f] = p.user_offsets[static_cast<int64_t>(b) * F + f];
   __syncthreads();
   if (tid == 0) {
     int used = 0;
-    s.any_global = 0;
+    s.slow_any = 0;
+    s.stash_n = 0;
     for (int f = 0; f < F; ++f) {
       const long long n = s.uoff[f + 1] - s.uoff[f];
-      // >= 8n slots (load factor <= 1/8) when the pool allows, else >= 4n
-      int ns = 4, shift = 31;
-      while (ns < 8 * n && ns < kPoolSlots) { ns <<= 1; --shift; }
-      if (used + ns > kPoolSlots && ns >= 8 && 4 * n <= ns / 2) { ns >>= 1; ++shift; }
-      if (4 * n <= ns && used + ns <= kPoolSlots) {
-        s.tab[f] = make_int2(used, shift);           // ns / 2 = 2^(32 - shift) slot pairs
-        used += ns;
+      // 2^k buckets, >= 2 per ID (mean load <= 2 of 4 slots) when the pool allows, else >= 1
+      int nb = 1, shift = 32;
+      while (nb < 2 * n && nb < kPoolBuckets) { nb <<= 1; --shift; }
+      if (used + nb > kPoolBuckets && nb > n && nb >= 2) { nb >>= 1; ++shift; }
+      if (nb >= n && used + nb <= kPoolBuckets) {
+        s.tab[f] = static_cast<uint32_t>(used) | (static_cast<uint32_t>(shift & 63) << 12);
+        used += nb;
       } else {
-        s.tab[f] = make_int2(-1, 0);
-        s.any_global = 1;
+        s.tab[f] = kFlagGlobal;
+        s.slow_any = 1;
       }
       s.sent_cnt[f] = 0;
     }
   }
-  for (int i = tid; i < kPoolSlots; i += kThreads) s.key[i] = kSentinel;
-  for (int i = tid; i < kWarps * 32; i += kThreads) (&s.warp_cnt[0][0])[i] = 0;
+  {
+    const ulonglong2 e = make_ulonglong2(kSentinel, kSentinel);
+    ulonglong2* flat = &s.bkt[0][0];
+    for (int i = tid; i < 2 * kPoolBuckets; i += kThreads) flat[i] = e;
+    for (int i = tid; i < kWarps * 32; i += kThreads) (&s.warp_cnt[0][0])[i] = 0;
+  }
   __syncthreads();
   {
     const long long u0 = s.uoff[0];
@@ -156,28 +170,35 @@ __global__ void __launch_bounds__(kThreads, 2)
         if (s.uoff[mid] <= pos) lo = mid; else hi = mid - 1;
       }
       const int f = lo;
-      const int2 t = s.tab[f];
-      if (t.x < 0) continue;
+      const uint32_t t = s.tab[f];
+      if (t & kFlagGlobal) continue;
       const unsigned long long key = static_cast<unsigned long long>(__ldg(p.user_ids + pos));
       if (key == kSentinel) {
         atomicAdd(&s.sent_cnt[f], 1);
         continue;
       }
-      const uint32_t smask = (0xFFFFFFFFu >> t.y) * 2 + 1;   // slots - 1
-      uint32_t slot = home_pair(key, t.y) * 2;
-      // every occurrence takes its own slot (a duplicate probes past its earlier copies)
-      while (atomicCAS(&s.key[t.x + slot], kSentinel, key) != kSentinel) slot = (slot + 1) & smask;
+      const uint32_t bk = bucket_of(t, key);
+      unsigned long long* slots = reinterpret_cast<unsigned long long*>(&s.bkt[bk][0]);
+      bool placed = false;
+      for (int q = 0; q < 4 && !placed; ++q)
+        placed = atomicCAS(slots + q, kSentinel, key) == kSentinel;
+      if (!placed) {
+        const int at = atomicAdd(&s.stash_n, 1);
+        if (at < kStash) {
+          s.stash_key[at] = key;
+          s.stash_field[at] = f;
+          atomicOr(&s.tab[f], kFlagStash);
+        } else {
+          atomicOr(&s.tab[f], kFlagGlobal);    // stash full: this field scans global memory
+        }
+        s.slow_any = 1;
+      }
     }
   }
   __syncthreads();
+  const bool slow_any = s.slow_any != 0;
 
-  // ---- 2. coalesced scan of the item-ID stream, 32 segments per warp step.  The next group's
-  //         offsets are fetched while the current group is processed, and all of a group's IDs
-  //         (kUnroll per lane) are loaded before the first lookup, so each warp keeps ~1 KB of
-  //         loads in flight.
-  constexpr int kUnroll = 4;
-  constexpr int kBatch = 2;
-  uint32_t* own = s.owner[warp];
+  // ---- 2. the item-ID stream, 32 segments per warp step
   for (int64_t c0 = first; c0 < ce; c0 += static_cast<int64_t>(gridDim.y) * chunk) {
     const int64_t c1 = (c0 + chunk < ce) ? c0 + chunk : ce;
     const int64_t seg_begin = c0 * F, seg_end = c1 * F;
@@ -191,105 +212,58 @@ __global__ void __launch_bounds__(kThreads, 2)
       }
     };
     fetch_offsets(g, off_cur, end_cur);
+    int my_f = static_cast<int>((g - seg_begin + lane) % F);   // seg_begin % F == 0
+    const int f_step = (kWarps * 32) % F;
     for (; g < seg_end; g += static_cast<int64_t>(kWarps) * 32) {
       const int nseg = (seg_end - g) < 32 ? static_cast<int>(seg_end - g) : 32;
       // lane k holds the start offset of segment g+k; lanes nseg..31 hold the end offset
-      const int64_t my_off64 = off_cur;
+      const int64_t my_off = off_cur;
       const int64_t end = end_cur;
       fetch_offsets(g + static_cast<int64_t>(kWarps) * 32, off_cur, end_cur);   // prefetch next
-      const int64_t start = __shfl_sync(0xffffffffu, my_off64, 0);
-      const int my_off = static_cast<int>(my_off64 - start);
-      const int nxt = __shfl_down_sync(0xffffffffu, my_off, 1);
+      const int64_t start = __shfl_sync(0xffffffffu, my_off, 0);
+      const int64_t nxt = __shfl_down_sync(0xffffffffu, my_off, 1);
+      const int64_t my_end = lane + 1 < nseg ? nxt : end;
       const int n_ids = static_cast<int>(end - start);
-      const int my_end = lane + 1 < nseg ? nxt : n_ids;
-      const int my_f = static_cast<int>(g - seg_begin + lane) % F;   // seg_begin % F == 0
+      const uint32_t my_tab = s.tab[my_f];
       const int64_t* ids = p.item_ids + start;
-      if (n_ids <= kOwnerCap && !s.any_global) {
-        // owner words of this group's ID positions (one table-info read per segment)
-        const int2 t = s.tab[my_f];
-        const uint32_t ow = static_cast<uint32_t>(lane) | (static_cast<uint32_t>(t.y) << 5) |
-                            (static_cast<uint32_t>(t.x) << 10) | (static_cast<uint32_t>(my_f) << 23);
-        for (int base = 0; base < n_ids; base += kUnroll * 32) {
-          unsigned long long kk[kUnroll];
+      const bool empty_seg = lane < nseg && my_end == my_off;
+      if (!__any_sync(0xffffffffu, empty_seg) && n_ids <= kFastMaxIds) {
+        // fast path: every segment of the group non-empty, so segment starts are distinct
+        const uint32_t rel = static_cast<uint32_t>(my_off - start);   // lanes >= nseg: n_ids
+        const uint32_t le_mask = 0xffffffffu >> (31 - lane);         // lanemask_le
+        int cum = 0;
+        for (int base = 0; base < n_ids; base += kWinUnroll * 32) {
+          unsigned long long kk[kWinUnroll];
 #pragma unroll
-          for (int u = 0; u < kUnroll; ++u) {
+          for (int u = 0; u < kWinUnroll; ++u) {
             const int pos = base + u * 32 + lane;
             kk[u] = pos < n_ids ? static_cast<unsigned long long>(__ldg(ids + pos)) : 0ull;
           }
-          if (base == 0) {
-            if (lane < nseg)
-              for (int q = my_off; q < my_end; ++q) own[q] = ow;
-            __syncwarp();
-          }
-          // batches of kBatch positions in straight-line code, so their shared-memory reads
-          // overlap: owner word -> home slot pair -> the 4-slot window (two 16-byte reads) ->
-          // count the key's copies; a position whose window is full (rare at load factor
-          // <= 1/8) walks on after the batch
 #pragma unroll
-          for (int u0 = 0; u0 < kUnroll; u0 += kBatch) {
-            if (base + u0 * 32 >= n_ids) break;          // warp-uniform
-            uint32_t o[kBatch], pr[kBatch];
-            int c[kBatch];
-            bool open[kBatch];
-#pragma unroll
-            for (int v = 0; v < kBatch; ++v) {
-              const int pos = base + (u0 + v) * 32 + lane;
-              o[v] = pos < n_ids ? own[pos] : 0u;
+          for (int u = 0; u < kWinUnroll; ++u) {
+            const int wbase = base + u * 32;
+            if (wbase >= n_ids) break;                                  // warp-uniform
+            // shl by >= 32 gives 0: only starts inside the window set a bit
+            const uint32_t bit = lane < nseg ? shl_clamp(1u, rel - static_cast<uint32_t>(wbase)) : 0u;
+            const uint32_t starts = __reduce_or_sync(0xffffffffu, bit);
+            const int seg = cum + __popc(starts & le_mask) - 1;
+            cum += __popc(starts);
+            const unsigned long long key = kk[u];
+            const bool valid = wbase + lane < n_ids;
+            const uint32_t t = __shfl_sync(0xffffffffu, my_tab, seg & 31);
+            int c;
+            if (!slow_any && !__any_sync(0xffffffffu, key == kSentinel)) {
+              c = bucket_count(s, t, key);
+            } else {
+              const int f = __shfl_sync(0xffffffffu, my_f, seg & 31);
+              c = valid ? lookup_any(s, p, f, t, key) : 0;
             }
-#pragma unroll
-            for (int v = 0; v < kBatch; ++v) {
-              const unsigned long long key = kk[u0 + v];
-              const int pos = base + (u0 + v) * 32 + lane;
-              const int shift = static_cast<int>((o[v] >> 5) & 31u);
-              pr[v] = home_pair(key, shift);
-              c[v] = window_count(s.key + ((o[v] >> 10) & 8191u), pr[v], 0xFFFFFFFFu >> shift,
-                                  key, open[v]);
-              if (key == kSentinel) {                        // the empty marker's own ID value
-                c[v] = s.sent_cnt[o[v] >> 23];
-                open[v] = false;
-              }
-              if (pos >= n_ids) { c[v] = 0; open[v] = false; }
-            }
-            bool any_open = false;
-#pragma unroll
-            for (int v = 0; v < kBatch; ++v) any_open |= open[v];
-            if (__any_sync(0xffffffffu, any_open)) {
-#pragma unroll
-              for (int v = 0; v < kBatch; ++v)
-                if (open[v])
-                  c[v] += walk_on(s.key + ((o[v] >> 10) & 8191u), pr[v],
-                                  0xFFFFFFFFu >> ((o[v] >> 5) & 31u), kk[u0 + v]);
-            }
-#pragma unroll
-            for (int v = 0; v < kBatch; ++v)
-              if (c[v] != 0) atomicAdd(&s.warp_cnt[warp][o[v] & 31u], c[v]);
-          }
-        }
-      } else if (n_ids <= kOwnerCap) {
-        for (int base = 0; base < n_ids; base += kUnroll * 32) {
-          unsigned long long kk[kUnroll];
-#pragma unroll
-          for (int u = 0; u < kUnroll; ++u) {
-            const int pos = base + u * 32 + lane;
-            kk[u] = pos < n_ids ? static_cast<unsigned long long>(__ldg(ids + pos)) : 0ull;
-          }
-          if (base == 0) {
-            if (lane < nseg)
-              for (int q = my_off; q < my_end; ++q) own[q] = static_cast<uint32_t>(lane) | (static_cast<uint32_t>(my_f) << 23);
-            __syncwarp();
-          }
-#pragma unroll 1
-          for (int u = 0; u < kUnroll; ++u) {
-            if (base + u * 32 >= n_ids) break;           // warp-uniform
-            const int pos = base + u * 32 + lane;
-            if (pos < n_ids) {
-              const uint32_t o = own[pos];
-              const int c = lookup(s, p, static_cast<int>(o >> 23), kk[u]);
-              if (c != 0) atomicAdd(&s.warp_cnt[warp][o & 31u], c);
-            }
+            if (valid && c != 0) atomicAdd(&s.warp_cnt[warp][seg], c);
           }
         }
       } else {
+        // a group with empty segments (or very long lists): owning segment by binary search
+        const int rel = static_cast<int>(my_off - start);
         for (int base = 0; base < n_ids; base += 32) {
           const int pos = base + lane;
           const bool ok = pos < n_ids;
@@ -297,12 +271,13 @@ __global__ void __launch_bounds__(kThreads, 2)
           int k = 0;     // owning segment: largest k with off[k] <= pos
 #pragma unroll
           for (int step = 16; step >= 1; step >>= 1) {
-            const int o = __shfl_sync(0xffffffffu, my_off, k + step);
+            const int o = __shfl_sync(0xffffffffu, rel, k + step);
             if (o <= pos) k += step;
           }
           const int f = __shfl_sync(0xffffffffu, my_f, k);
+          const uint32_t t = __shfl_sync(0xffffffffu, my_tab, k);
           if (ok) {
-            const int c = lookup(s, p, f, key);
+            const int c = lookup_any(s, p, f, t, key);
             if (c != 0) atomicAdd(&s.warp_cnt[warp][k], c);
           }
         }
@@ -315,8 +290,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         if (p.E != nullptr) {
           // offset embedding (stride cap + 1: DESIGN.md R14): segment
           // g + lane = (candidate t, field f) owns out[t][f D_h, (f + 1) D_h) -- contiguous
-          const int f = static_cast<int>(g - seg_begin + lane) % F;
-          const int64_t rowE = static_cast<int64_t>(c) + static_cast<int64_t>(f) * (p.cap + 1);
+          const int64_t rowE = static_cast<int64_t>(c) + static_cast<int64_t>(my_f) * (p.cap + 1);
           const uint4* src = p.E + rowE * p.dh_chunks;
           uint4* dst = p.emb + (g + lane) * p.dh_chunks;
           for (int q = 0; q < p.dh_chunks; ++q) dst[q] = __ldg(src + q);
@@ -324,6 +298,8 @@ __global__ void __launch_bounds__(kThreads, 2)
       }
       s.warp_cnt[warp][lane] = 0;
       __syncwarp();
+      my_f += f_step;
+      if (my_f >= F) my_f -= F;
     }
   }
 }
@@ -334,9 +310,8 @@ cudaError_t launch_hma(const HmaParams& p, cudaStream_t stream) {
   const int smem = static_cast<int>(sizeof(HmaSmem));
   cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(hma_kernel), smem);
   if (e != cudaSuccess) return e;
-  // Large chunks amortise the per-CTA table build (one CTA per request at C = 1000: measured
-  // 0.796 -> 0.759 ms at the headline); small ones keep the grid >= 4 CTAs per SM when there
-  // are few requests (config 4: B = 1, C = 4096).
+  // Large chunks amortise the per-CTA table build; small ones keep the grid >= 4 CTAs per SM
+  // when there are few requests (config 4: B = 1, C = 4096).
   int64_t per = p.B > 0 ? (p.total_C + p.B - 1) / p.B : 1;
   int chunk = kChunkMax;
   if (p.B * ((per + kChunkMax - 1) / kChunkMax) < 4 * 148) chunk = kChunkMin;

@@ -16,4 +16,5 @@ if [ "${NCU:-1}" = "1" ]; then
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"attn|proj_kernel|hma_kernel|build_units" --csv --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_launch_$TAG.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"attn_pair|proj_kernel|hma_kernel" -s 4 -c 4 -o gpurun_out/prof_$TAG python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_full_$TAG.log 2>&1
 fi
+if [ -n "${POST:-}" ]; then bash -c "$POST" > gpurun_out/post_$TAG.log 2>&1; fi
 echo all_done
