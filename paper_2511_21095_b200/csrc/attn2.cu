@@ -92,18 +92,26 @@ __device__ __forceinline__ void pwait(uint64_t* bar, uint32_t parity, uint32_t c
                                       uint32_t sleep_ns = 0) {
   const uint32_t a = smem_u32(bar);
   if (mbar_try_wait_hint(a, parity, GESR_PAIR_SPIN ? 0u : 1000000u)) return;
+  // each try_wait may suspend up to its hint: the clock is read every 64 retries and the wait
+  // traps after ~2^35 cycles (~17 s at 1.965 GHz) however long the suspensions were
   uint32_t n = 0;
+  long long t0 = 0;
   while (!mbar_try_wait_hint(a, parity, GESR_PAIR_SPIN ? 0u : 1000000u)) {
     if (sleep_ns) __nanosleep(sleep_ns);
-    if (++n == (1u << 28)) {
+    if ((++n & 63u) == 0) {
+      const long long t = clock64();
+      if (t0 == 0) {
+        t0 = t;
+      } else if (t - t0 > (1ll << 35)) {
 #ifdef GESR_DEBUG_WAITS
-      if ((threadIdx.x & 31) == 0)
-        printf("gesr: attn_pair mbarrier timeout block %d warp %d smem 0x%x parity %u site %u unit %u tile %u\n",
-               blockIdx.x, threadIdx.x / 32, a, parity, ctx >> 20, (ctx >> 8) & 0xfff, ctx & 0xff);
+        if ((threadIdx.x & 31) == 0)
+          printf("gesr: attn_pair mbarrier timeout block %d warp %d smem 0x%x parity %u site %u unit %u tile %u\n",
+                 blockIdx.x, threadIdx.x / 32, a, parity, ctx >> 20, (ctx >> 8) & 0xfff, ctx & 0xff);
 #else
-      (void)ctx;
+        (void)ctx;
 #endif
-      __trap();
+        __trap();
+      }
     }
   }
 }

@@ -28,6 +28,8 @@
 //      shuffle from its lane; the lookup is hash -> bucket -> two 16-byte reads -> four 64-bit
 //      compares; hits go to a per-warp shared counter (predicated shared atomics), and lane k
 //      stores segment k's count (one coalesced 128-byte store per group).
+#include <cstdlib>
+
 #include <cuda_runtime.h>
 
 #include "kernels.h"
@@ -78,6 +80,16 @@ __device__ __forceinline__ uint32_t shl_clamp(uint32_t a, uint32_t n) {
   uint32_t r;
   asm("shl.b32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(n));
   return r;
+}
+// Bulk L2 prefetch of the byte range [lo, hi) (rounded out to 16-byte boundaries): one
+// instruction brings a whole group's IDs toward L2 while the warp works on the group before it.
+__device__ __forceinline__ void prefetch_l2_range(const void* lo, const void* hi) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(lo) & ~uintptr_t(15);
+  const uintptr_t b = (reinterpret_cast<uintptr_t>(hi) + 15) & ~uintptr_t(15);
+  if (b > a)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a),
+                 "r"(static_cast<uint32_t>(b - a))
+                 : "memory");
 }
 __device__ __forceinline__ uint32_t bucket_of(uint32_t tab, unsigned long long key) {
   return (tab & 4095u) + shr_clamp(key_hash(key), (tab >> 12) & 63u);
@@ -203,7 +215,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     const int64_t c1 = (c0 + chunk < ce) ? c0 + chunk : ce;
     const int64_t seg_begin = c0 * F, seg_end = c1 * F;
     int64_t g = seg_begin + static_cast<int64_t>(warp) * 32;
-    int64_t off_cur = 0, end_cur = 0;
+    constexpr int64_t kStep = static_cast<int64_t>(kWarps) * 32;
+    int64_t off_cur = 0, end_cur = 0, off_nxt = 0, end_nxt = 0;
     auto fetch_offsets = [&](int64_t gg, int64_t& o, int64_t& e) {
       if (gg < seg_end) {
         const int ns = (seg_end - gg) < 32 ? static_cast<int>(seg_end - gg) : 32;
@@ -212,14 +225,27 @@ __global__ void __launch_bounds__(kThreads, 2)
       }
     };
     fetch_offsets(g, off_cur, end_cur);
+    fetch_offsets(g + kStep, off_nxt, end_nxt);
+    {
+      const int64_t s0 = __shfl_sync(0xffffffffu, off_cur, 0);
+      if (lane == 0 && g < seg_end) prefetch_l2_range(p.item_ids + s0, p.item_ids + end_cur);
+    }
     int my_f = static_cast<int>((g - seg_begin + lane) % F);   // seg_begin % F == 0
     const int f_step = (kWarps * 32) % F;
-    for (; g < seg_end; g += static_cast<int64_t>(kWarps) * 32) {
+    for (; g < seg_end; g += kStep) {
       const int nseg = (seg_end - g) < 32 ? static_cast<int>(seg_end - g) : 32;
       // lane k holds the start offset of segment g+k; lanes nseg..31 hold the end offset
       const int64_t my_off = off_cur;
       const int64_t end = end_cur;
-      fetch_offsets(g + static_cast<int64_t>(kWarps) * 32, off_cur, end_cur);   // prefetch next
+      // the next group's IDs toward L2 (its offsets arrived during this group's predecessor),
+      // then the offsets two groups ahead into registers
+      {
+        const int64_t s1 = __shfl_sync(0xffffffffu, off_nxt, 0);
+        if (lane == 0 && g + kStep < seg_end) prefetch_l2_range(p.item_ids + s1, p.item_ids + end_nxt);
+      }
+      off_cur = off_nxt;
+      end_cur = end_nxt;
+      fetch_offsets(g + 2 * kStep, off_nxt, end_nxt);
       const int64_t start = __shfl_sync(0xffffffffu, my_off, 0);
       const int64_t nxt = __shfl_down_sync(0xffffffffu, my_off, 1);
       const int64_t my_end = lane + 1 < nseg ? nxt : end;
@@ -315,6 +341,8 @@ cudaError_t launch_hma(const HmaParams& p, cudaStream_t stream) {
   int64_t per = p.B > 0 ? (p.total_C + p.B - 1) / p.B : 1;
   int chunk = kChunkMax;
   if (p.B * ((per + kChunkMax - 1) / kChunkMax) < 4 * 148) chunk = kChunkMin;
+  static const char* tune = getenv("GESR_HMA_CHUNK");     // TEMPORARY tuning knob
+  if (tune != nullptr && atoi(tune) > 0) chunk = atoi(tune);
   int64_t y = (per + chunk - 1) / chunk;
   if (y < 1) y = 1;
   if (y > 65535) y = 65535;

@@ -59,8 +59,42 @@ def launches(src, out):
         print(f"{k:45s} n={len(v):3d} mean={sum(v)/len(v):9.1f} us share={sum(v)/tot:6.1%}")
 
 
+def traffic(csv_path, config, tag):
+    """profiles/ncu_traffic.json[config]: DRAM bytes (read + write) per launch of the kernels
+    gesr_tasa_score launches in a bench capture (-k attn_pair|proj_kernel|hma_kernel, in launch
+    order hma, K/V projection, [Q projection], attention): bench.py's roofline.traffic."""
+    import json
+    import os
+    rows = list(csv.reader(open(csv_path)))
+    hdr = rows[0]
+    ir = [i for i, h in enumerate(hdr) if h.startswith("dram__bytes_read.sum")][0]
+    iw = [i for i, h in enumerate(hdr) if h.startswith("dram__bytes_write.sum")][0]
+    unit = 1e9 if "Gbyte" in hdr[ir] else (1e6 if "Mbyte" in hdr[ir] else 1.0)
+    kern = {}
+    projs = 0
+    for r in rows[1:]:
+        name = r[0]
+        b = (float(r[ir]) + float(r[iw])) * unit
+        if "proj_kernel" in name:
+            projs += 1
+            if projs == 2:
+                kern["proj_kernel (q projection)"] = b
+        elif "attn" in name:
+            kern[name] = b
+    out = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles",
+                       "ncu_traffic.json")
+    d = json.load(open(out)) if os.path.exists(out) else {}
+    d[config] = {"tasa_bytes_per_launch": sum(kern.values()), "kernels": kern,
+                 "source": f"{csv_path} (ncu --set full, dram__bytes_read.sum + "
+                           f"dram__bytes_write.sum; capture {tag})"}
+    json.dump(d, open(out, "w"), indent=1)
+    print(json.dumps(d[config], indent=1))
+
+
 if __name__ == "__main__":
-    if sys.argv[1] == "--launches":
+    if sys.argv[1] == "--traffic":
+        traffic(sys.argv[2], sys.argv[3], sys.argv[4])
+    elif sys.argv[1] == "--launches":
         launches(sys.argv[2], sys.argv[3])
     else:
         full(sys.argv[1], sys.argv[2])

@@ -140,8 +140,9 @@ def test_tasa_bias_scale_act(d, H, D_in, act, scale):
 
 @pytest.mark.parametrize("d", [64, 128])
 def test_tasa_identity_bf16_out_forced_splits(d):
-    """act = identity with bf16 O and forced kv_splits: every split count gives the oracle's
-    rows within tolerance; splits = 1 is bit-identical run to run."""
+    """act = identity with bf16 O and forced kv_splits (split-L runs on the d = 128 pair kernel
+    only): every split count gives the oracle's rows within tolerance; splits = 1 is
+    bit-identical run to run."""
     dev = _cuda()
     cfg, bt = _ragged(d, 2, 128, 400 + d)
     K_or, V_or = oracle.kv_project(bt.U, bt.W_k, bt.W_v, 2, d, act=0)
@@ -150,7 +151,7 @@ def test_tasa_identity_bf16_out_forced_splits(d):
     g = bt.to(dev)
     K, V = gb.kv_project(g.U, g.W_k, g.W_v, 2, d, 0)
     outs = {}
-    for s in (1, 2, 3):
+    for s in ((1, 2, 3) if d == 128 else (1,)):
         O, _ = gb.tasa_score(g.T, g.cand_offsets, g.W_q, K, V, g.seq_offsets, 2, d, 0,
                              kv_splits=s, out_dtype=torch.bfloat16, want_lse=False)
         outs[s] = O.clone()
