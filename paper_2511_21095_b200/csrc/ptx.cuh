@@ -511,4 +511,35 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   return r;
 }
 
+// SiLU(x) = x / (1 + 2^(-x log2 e)) for a PAIR of values, with ONE MUFU op per element and the
+// rest as packed fp32x2 FMA-pipe work (FFMA2/FMUL2/FADD2: half the issue slots of scalar code;
+// the epilogue is issue-bound at the MMA time per tile).  The exponent z = -x log2 e is clamped
+// to [-126, 126] by a saturating FFMA (u = sat(x * -log2e/252 + 1/2), z = 252u - 126; no FMNMX,
+// which slows a concurrent MUFU stream) so y = 1 + 2^z stays finite; x < -87 then gives
+// |result| < 2^-119 (true value smaller still) and large x gives x.  1/y: bit-trick seed and two
+// Newton steps on the FMA pipe (rel. error < 2.5e-4, far below the bf16 rounding of the result;
+// a MUFU reciprocal made the epilogue MUFU-bound at exactly the MMA time per tile).
+__device__ __forceinline__ void silu2(float& x0, float& x1) {
+  constexpr float kC = -1.4426950408889634f / 252.0f;
+  float u0, u1;
+  asm("fma.rn.sat.f32 %0, %1, %2, %3;" : "=f"(u0) : "f"(x0), "f"(kC), "f"(0.5f));
+  asm("fma.rn.sat.f32 %0, %1, %2, %3;" : "=f"(u1) : "f"(x1), "f"(kC), "f"(0.5f));
+  float z0, z1;
+  ffma2(z0, z1, u0, u1, 252.0f, 252.0f, -126.0f, -126.0f);
+  const float e0 = ex2(z0), e1 = ex2(z1);
+  float ny0, ny1;                                  // -y = -(1 + e)
+  ffma2(ny0, ny1, e0, e1, -1.0f, -1.0f, -1.0f, -1.0f);
+  // seed 1/y = 0x7EF311C7 - bits(y), and bits(-y) = bits(y) + 2^31
+  float r0 = __uint_as_float(0xFEF311C7u - __float_as_uint(ny0));
+  float r1 = __uint_as_float(0xFEF311C7u - __float_as_uint(ny1));
+  float t0, t1;
+#pragma unroll
+  for (int it = 0; it < 2; ++it) {                 // r <- r (2 - y r)
+    ffma2(t0, t1, ny0, ny1, r0, r1, 2.0f, 2.0f);
+    fmul2(r0, r1, r0, r1, t0, t1);
+  }
+  fmul2(x0, x1, x0, x1, r0, r1);
+}
+
+
 }  // namespace gesr
