@@ -373,7 +373,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     return false;
   };
   const int nkb = p.d_in / 64;                    // fused Q: 64-wide K blocks of the projection
-  auto qp_point = [&](const Tile& tl) { return tl.t == min(2, tl.x.nkv - 1); };
+  const int nqc = (nkb + 1) / 2;                  // projection chunks (two K blocks each)
+  // unit m+1's projection chunk c follows K tile qp_point(c) of unit m: spread over the unit's
+  // last tiles (one chunk every other tile, done ~2 tiles before the unit ends), so the
+  // projection MMAs never hold back an S MMA by more than one chunk (8 MMAs)
+  auto qp_point = [&](const Tile& tl, int c) { return max(0, tl.x.nkv - 1 - 2 * (nqc - c)); };
 
   if (warp < 4) {
     setmaxnreg_dec<kCtrlRegs>();
@@ -399,37 +403,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if (++kst == kKStages) { kst = 0; kph ^= 1; }
           return slot;
         };
-        // fused Q: the projection operands of one unit, per pair of 64-wide K blocks: the two
+        // fused Q: the projection operands of one unit, chunk c = K blocks 2c, 2c+1: the two
         // W_q halves [64 rows of head h][64] (8 KB each, one slot), then the two T row blocks
-        // [128 rows][64] (16 KB each, one slot each)
-        auto emit_qp = [&](const Work& x) {
+        // [128 rows][64] (16 KB each, one slot each).  T is re-read by the unit's other heads
+        // (adjacent pairs): no evict-first hint.
+        auto emit_chunk = [&](const Work& x, int c) {
           const int32_t trow = static_cast<int32_t>(x.cbeg) + static_cast<int32_t>(rank) * 128;
           const int32_t wrow = x.h * kD + static_cast<int32_t>(rank) * 64;
-          for (int kb = 0; kb < nkb; kb += 2) {
-            const int nb = (kb + 1 < nkb) ? 2 : 1;
-            int slot = next_slot();
-            if (rank == 0) mbar_arrive_expect_tx(&kv_full[slot], 2 * nb * (kHalfBytes / 2));
-            uint8_t* dst = smem + Lay::kRingOff + slot * kHalfBytes;
-            for (int i = 0; i < nb; ++i)
-              tma_load_2d_pair(dst + i * (kHalfBytes / 2), &map_w, &kv_full[slot], (kb + i) * 64, wrow);
-            for (int i = 0; i < nb; ++i) {
-              slot = next_slot();
-              if (rank == 0) mbar_arrive_expect_tx(&kv_full[slot], 2 * kHalfBytes);
-#if GESR_PAIR_L2HINT >= 1
-              tma_load_2d_pair_hint(smem + Lay::kRingOff + slot * kHalfBytes, &map_q,
-                                    &kv_full[slot], (kb + i) * 64, trow, pol_first);
-#else
-              tma_load_2d_pair(smem + Lay::kRingOff + slot * kHalfBytes, &map_q, &kv_full[slot],
-                               (kb + i) * 64, trow);
-#endif
-            }
+          const int kb = 2 * c;
+          const int nb = (kb + 1 < nkb) ? 2 : 1;
+          int slot = next_slot();
+          if (rank == 0) mbar_arrive_expect_tx(&kv_full[slot], 2 * nb * (kHalfBytes / 2));
+          uint8_t* dst = smem + Lay::kRingOff + slot * kHalfBytes;
+          for (int i = 0; i < nb; ++i)
+            tma_load_2d_pair(dst + i * (kHalfBytes / 2), &map_w, &kv_full[slot], (kb + i) * 64, wrow);
+          for (int i = 0; i < nb; ++i) {
+            slot = next_slot();
+            if (rank == 0) mbar_arrive_expect_tx(&kv_full[slot], 2 * kHalfBytes);
+            tma_load_2d_pair(smem + Lay::kRingOff + slot * kHalfBytes, &map_q, &kv_full[slot],
+                             (kb + i) * 64, trow);
           }
         };
         ItemCursor qc;
         Work qx;
+        bool qhave = false;
         if (kFusedQ) {
           item_init(qc);
-          if (item_next(qc, qx)) emit_qp(qx);
+          qhave = item_next(qc, qx);
+          if (qhave)
+            for (int c = 0; c < nqc; ++c) emit_chunk(qx, c);
         }
         while (stream_next(st, tl)) {
           if (!kFusedQ && tl.t == 0) {
@@ -458,7 +460,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           tma_load_2d_pair(dst, &map_kh, &kv_full[slot], 0, row);
           tma_load_2d_pair(dst + 8192, &map_kh, &kv_full[slot], 64, row);
 #endif
-          if (kFusedQ && qp_point(tl) && item_next(qc, qx)) emit_qp(qx);
+          if (kFusedQ) {
+            for (int c = 0; c < nqc; ++c) {
+              if (qp_point(tl, c) != tl.t) continue;
+              if (c == 0) qhave = item_next(qc, qx);
+              if (qhave) emit_chunk(qx, c);
+            }
+          }
         }
       }
     } else if (warp == 2) {
@@ -491,38 +499,42 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (++kst == kKStages) { kst = 0; kph ^= 1; }
         return slot;
       };
-      // fused Q: unit mm's projection into its O accumulator (free once unit mm-2's epilogue
-      // has read it), operands from the K ring in emit_qp's order
-      auto issue_qp = [&](int mm) {
+      // fused Q: chunk c of unit mm's projection into its O accumulator (free once unit mm-2's
+      // epilogue has read it), operands from the K ring in emit_chunk's order
+      auto issue_chunk = [&](int mm, int c) {
         const int ob = mm & 1;
-        if (mm >= 2) pwait(&o_free[ob], ((mm >> 1) - 1) & 1, CTX(16, mm, 0));
-        for (int kb = 0; kb < nkb; kb += 2) {
-          const int nb = (kb + 1 < nkb) ? 2 : 1;
-          const int wslot = take_slot();
-          for (int i = 0; i < nb; ++i) {
-            const int aslot = take_slot();
-            tc_fence_after();
-            if (elect_one()) {
-              const uint32_t ab = sRing + aslot * kHalfBytes;
-              const uint32_t wb = sRing + wslot * kHalfBytes + i * (kHalfBytes / 2);
+        if (c == 0 && mm >= 2) pwait(&o_free[ob], ((mm >> 1) - 1) & 1, CTX(16, mm, 0));
+        const int kb = 2 * c;
+        const int nb = (kb + 1 < nkb) ? 2 : 1;
+        const int wslot = take_slot();
+        for (int i = 0; i < nb; ++i) {
+          const int aslot = take_slot();
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t ab = sRing + aslot * kHalfBytes;
+            const uint32_t wb = sRing + wslot * kHalfBytes + i * (kHalfBytes / 2);
 #pragma unroll
-              for (int ks = 0; ks < 4; ++ks)
-                mma_ss_pair(tmem + kTO + ob * kD, kdesc(ab, 0, ks), kdesc(wb, 0, ks), idesc_s,
-                            (kb + i > 0 || ks > 0) ? 1u : 0u);
-              mma_commit_pair_mc(&kv_empty[aslot], 0x3);
-              if (i == nb - 1) mma_commit_pair_mc(&kv_empty[wslot], 0x3);
-              if (kb + i == nkb - 1) mma_commit_pair_mc(&qp_done[ob], 0x3);
-            }
-            __syncwarp();
+            for (int ks = 0; ks < 4; ++ks)
+              mma_ss_pair(tmem + kTO + ob * kD, kdesc(ab, 0, ks), kdesc(wb, 0, ks), idesc_s,
+                          (kb + i > 0 || ks > 0) ? 1u : 0u);
+            mma_commit_pair_mc(&kv_empty[aslot], 0x3);
+            if (i == nb - 1) mma_commit_pair_mc(&kv_empty[wslot], 0x3);
+            if (kb + i == nkb - 1) mma_commit_pair_mc(&qp_done[ob], 0x3);
           }
+          __syncwarp();
         }
       };
       ItemCursor qc;
       Work qx;
-      int qm = 0;                                  // projections issued so far
+      bool qhave = false;
+      int qm = 0;                                  // projections started so far
       if (kFusedQ) {
         item_init(qc);
-        if (item_next(qc, qx)) issue_qp(qm++);
+        qhave = item_next(qc, qx);
+        if (qhave) {
+          for (int c = 0; c < nqc; ++c) issue_chunk(0, c);
+          qm = 1;
+        }
       }
       while (stream_next(st, tl)) {
         const int buf = tl.t & 1;
@@ -551,7 +563,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if (tl.t == tl.x.nkv - 1) mma_commit_pair_mc(&q_empty[qb], 0x3);
         }
         __syncwarp();
-        if (kFusedQ && qp_point(tl) && item_next(qc, qx)) issue_qp(qm++);
+        if (kFusedQ) {
+          for (int c = 0; c < nqc; ++c) {
+            if (qp_point(tl, c) != tl.t) continue;
+            if (c == 0) {
+              qhave = item_next(qc, qx);
+              if (qhave) ++qm;
+            }
+            if (qhave) issue_chunk(qm - 1, c);
+          }
+        }
       }
     } else if (warp == 3 && rank == 0) {
       // ---------------------------------------------------------- PV MMA issuer (leader only)

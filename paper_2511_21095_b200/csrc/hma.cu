@@ -57,6 +57,10 @@ constexpr uint32_t kFlagGlobal = 1u << 19;   // the field's list is scanned in g
 
 struct HmaSmem {
   ulonglong2 bkt[kPoolBuckets][2];           // kSentinel = empty slot
+  // prefilter: 16 bits per bucket (a field's bits follow its buckets' order), bit h >> (shift-4)
+  // set for every user ID of the field; a lookup reads one 32-bit word (few bank conflicts) and
+  // touches its bucket only if the bit is set -- ~28% of IDs (matches + ~3% false positives)
+  uint32_t bits[kPoolBuckets / 2];
   unsigned long long stash_key[kStash];
   int stash_field[kStash];
   uint32_t tab[kMaxFields];
@@ -95,6 +99,9 @@ __device__ __forceinline__ uint32_t bucket_of(uint32_t tab, unsigned long long k
   return (tab & 4095u) + shr_clamp(key_hash(key), (tab >> 12) & 63u);
 }
 
+__device__ __forceinline__ uint32_t filter_bit(uint32_t tab, uint32_t h) {
+  return (tab & 4095u) * 16u + shr_clamp(h, ((tab >> 12) & 63u) - 4u);
+}
 __device__ __forceinline__ int bucket_count(const HmaSmem& s, uint32_t tab,
                                             unsigned long long key) {
   const uint32_t b = bucket_of(tab, key);
@@ -168,6 +175,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     const ulonglong2 e = make_ulonglong2(kSentinel, kSentinel);
     ulonglong2* flat = &s.bkt[0][0];
     for (int i = tid; i < 2 * kPoolBuckets; i += kThreads) flat[i] = e;
+    for (int i = tid; i < kPoolBuckets / 2; i += kThreads) s.bits[i] = 0u;
     for (int i = tid; i < kWarps * 32; i += kThreads) (&s.warp_cnt[0][0])[i] = 0;
   }
   __syncthreads();
@@ -189,6 +197,8 @@ __global__ void __launch_bounds__(kThreads, 2)
         atomicAdd(&s.sent_cnt[f], 1);
         continue;
       }
+      const uint32_t fb = filter_bit(t, key_hash(key));
+      atomicOr(&s.bits[fb >> 5], 1u << (fb & 31u));
       const uint32_t bk = bucket_of(t, key);
       unsigned long long* slots = reinterpret_cast<unsigned long long*>(&s.bkt[bk][0]);
       bool placed = false;
@@ -279,7 +289,9 @@ __global__ void __launch_bounds__(kThreads, 2)
             const uint32_t t = __shfl_sync(0xffffffffu, my_tab, seg & 31);
             int c;
             if (!slow_any && !__any_sync(0xffffffffu, key == kSentinel)) {
-              c = bucket_count(s, t, key);
+              const uint32_t fb = filter_bit(t, key_hash(key));
+              const bool maybe = (s.bits[fb >> 5] >> (fb & 31u)) & 1u;
+              c = maybe ? bucket_count(s, t, key) : 0;
             } else {
               const int f = __shfl_sync(0xffffffffu, my_f, seg & 31);
               c = valid ? lookup_any(s, p, f, t, key) : 0;
