@@ -124,11 +124,23 @@ constexpr uint32_t kHalfBytes = 16384;           // K half [2][64 keys][64] or V
 // Shared-memory layout per variant.  kFusedQ (the Q projection inside the kernel): two Q
 // buffers (unit m+1's Q is produced while unit m's S MMAs read unit m's), the K ring also
 // carries the projection's operands (T row blocks and W_q halves), V ring 3 stages.
+#ifndef GESR_FQ_KSTAGES
+#define GESR_FQ_KSTAGES 4
+#endif
+#ifndef GESR_FQ_VSTAGES
+#define GESR_FQ_VSTAGES 3
+#endif
+#ifndef GESR_FQ_ORDER
+#define GESR_FQ_ORDER 0          // fused Q work order: 0 head-fastest, 1 unit-fastest
+#endif
+#ifndef GESR_FQ_EARLY
+#define GESR_FQ_EARLY 0          // 1: the next unit's projection right after S(0)
+#endif
 template <bool kFusedQ>
 struct PairLayout {
   static constexpr int kQBufs = kFusedQ ? 2 : 1;
-  static constexpr int kKStages = 4;             // K-half ring
-  static constexpr int kVStages = kFusedQ ? 3 : 5;   // V-half ring
+  static constexpr int kKStages = kFusedQ ? GESR_FQ_KSTAGES : 4;     // K-half ring
+  static constexpr int kVStages = kFusedQ ? GESR_FQ_VSTAGES : 5;     // V-half ring
   static constexpr int kStages = kKStages + kVStages;
   static constexpr uint32_t kQOff = 0;
   static constexpr uint32_t kRingOff = kQBufs * kQBytes;
@@ -284,13 +296,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   // to back, read 11% MORE from HBM).  Fused Q: head w % H, split (w / H) % S, unit w / (H S):
   // the H pairs projecting one unit's candidate rows T run side by side, so T is read from HBM
   // once and from L2 by the other heads (the units of a request still run on adjacent pairs).
-  auto unit_of = [&](int w) { return kFusedQ ? w / (p.H * S) : w % U; };
+  constexpr bool kHeadFast = kFusedQ && GESR_FQ_ORDER == 0;
+  auto unit_of = [&](int w) { return kHeadFast ? w / (p.H * S) : w % U; };
   // the unit descriptor of work item w is one 16-byte load, fetched one item ahead
   auto fetch = [&](int w) { return __ldg(p.units + unit_of(w)); };
   auto decode = [&](int w, int4 d) {
     Work x;
     int split, h;
-    if (kFusedQ) {
+    if (kHeadFast) {
       h = w % p.H;
       split = (w / p.H) % S;
     } else {
@@ -377,7 +390,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   // unit m+1's projection chunk c follows K tile qp_point(c) of unit m: spread over the unit's
   // last tiles (one chunk every other tile, done ~2 tiles before the unit ends), so the
   // projection MMAs never hold back an S MMA by more than one chunk (8 MMAs)
-  auto qp_point = [&](const Tile& tl, int c) { return max(0, tl.x.nkv - 1 - 2 * (nqc - c)); };
+  auto qp_point = [&](const Tile& tl, int c) {
+    return GESR_FQ_EARLY ? 0 : max(0, tl.x.nkv - 1 - 2 * (nqc - c));
+  };
 
   if (warp < 4) {
     setmaxnreg_dec<kCtrlRegs>();

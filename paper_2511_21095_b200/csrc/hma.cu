@@ -16,8 +16,12 @@
 //      memory -- 2^k buckets of 4 64-bit slots (32 bytes, two 16-byte reads), one slot per
 //      OCCURRENCE of a user ID (so a lookup counts matching slots; no count array), >= 2 buckets
 //      per ID (mean bucket load <= 1/2).  A bucket that overflows spills into a small per-CTA
-//      stash; a field whose list does not fit the pool is looked up in global memory.  The ID
-//      value INT64_MIN marks an empty slot and is counted on the side.
+//      stash; a field whose list does not fit the pool is looked up in global memory.  An empty
+//      slot holds a FILLER key that hashes into the other half of the table (bucket index top
+//      bit flipped), so no key that hashes to this bucket can equal it: every int64 value,
+//      INT64_MIN included, is an ordinary ID and a lookup needs no emptiness test.  A 16-bit-
+//      per-bucket bitmap of the user IDs' hashes is read first (one 32-bit shared load); the
+//      bucket (two 16-byte loads, predicated) only for the ~28% of IDs whose bit is set.
 //   2. Scan: each warp takes 32 consecutive (candidate, field) segments (their IDs are one
 //      contiguous range of the CSR stream) and walks the range in 32-ID windows, one coalesced
 //      8-byte load per lane, 4 windows in flight.  The segment of each ID position comes from
@@ -33,6 +37,7 @@
 #include <cuda_runtime.h>
 
 #include "kernels.h"
+#include "ptx.cuh"
 
 namespace gesr {
 
@@ -47,16 +52,22 @@ constexpr int kStash = 256;                // overflowing user IDs (key, field)
 constexpr int kMaxFields = 256;
 constexpr int kWinUnroll = 4;              // 32-ID windows in flight per warp
 constexpr int kFastMaxIds = 32 * 64;       // groups up to this many IDs take the fast path
-constexpr unsigned long long kSentinel = 0x8000000000000000ull;   // INT64_MIN: empty slot
 constexpr uint32_t kMulLo = 0x9E3779B1u;
 constexpr uint32_t kMulHi = 0x85EBCA77u;
+__host__ __device__ constexpr uint32_t key_hash_c(unsigned long long key) {
+  return (static_cast<uint32_t>(key) * kMulLo) ^ (static_cast<uint32_t>(key >> 32) * kMulHi);
+}
+// empty-slot fillers: kFill[0] fills buckets whose index has top bit 0 (its own hash has top bit
+// 1), kFill[1] the others; tables have >= 2 buckets, so the top hash bit is the bucket's
+constexpr unsigned long long kFill0 = 1ull, kFill1 = 2ull;
+static_assert((key_hash_c(kFill0) >> 31) == 1u && (key_hash_c(kFill1) >> 31) == 0u, "fillers");
 
 // table word of a field: first bucket (bits 0-11), hash shift (12-17), flags
 constexpr uint32_t kFlagStash = 1u << 18;    // some of the field's IDs are in the stash
 constexpr uint32_t kFlagGlobal = 1u << 19;   // the field's list is scanned in global memory
 
 struct HmaSmem {
-  ulonglong2 bkt[kPoolBuckets][2];           // kSentinel = empty slot
+  ulonglong2 bkt[kPoolBuckets][2];           // empty slots hold the bucket half's filler
   // prefilter: 16 bits per bucket (a field's bits follow its buckets' order), bit h >> (shift-4)
   // set for every user ID of the field; a lookup reads one 32-bit word (few bank conflicts) and
   // touches its bucket only if the bit is set -- ~28% of IDs (matches + ~3% false positives)
@@ -64,16 +75,13 @@ struct HmaSmem {
   unsigned long long stash_key[kStash];
   int stash_field[kStash];
   uint32_t tab[kMaxFields];
-  int sent_cnt[kMaxFields];                  // multiplicity of INT64_MIN per field
   long long uoff[kMaxFields + 1];            // this request's user_offsets (F+1)
   int warp_cnt[kWarps][32];
   int stash_n;
   int slow_any;                              // some field has stash entries or goes global
 };
 
-__device__ __forceinline__ uint32_t key_hash(unsigned long long key) {
-  return (static_cast<uint32_t>(key) * kMulLo) ^ (static_cast<uint32_t>(key >> 32) * kMulHi);
-}
+__device__ __forceinline__ uint32_t key_hash(unsigned long long key) { return key_hash_c(key); }
 // PTX shifts clamp the shift amount (>= 32 gives 0), unlike C++ shifts
 __device__ __forceinline__ uint32_t shr_clamp(uint32_t a, uint32_t n) {
   uint32_t r;
@@ -110,7 +118,29 @@ __device__ __forceinline__ int bucket_count(const HmaSmem& s, uint32_t tab,
   return (a.x == key) + (a.y == key) + (c.x == key) + (c.y == key);
 }
 
-// Everything the bucket lookup does not cover: INT64_MIN, stash entries, global-memory fields.
+// The fast path's lookup with raw shared addresses (no generic-to-shared conversion per access)
+// and the bucket read predicated on the filter bit: lanes whose bit is clear issue no bucket
+// traffic and keep ~key in the compare registers (never equal to key).
+__device__ __forceinline__ int fast_count(uint32_t s_bkt, uint32_t s_bits, uint32_t tab,
+                                          unsigned long long key) {
+  const uint32_t h = key_hash(key);
+  const uint32_t base = tab & 4095u, sh = (tab >> 12) & 63u;
+  const uint32_t fb = base * 16u + shr_clamp(h, sh - 4u);
+  uint32_t word;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(word) : "r"(s_bits + ((fb >> 5) << 2)));
+  const uint32_t maybe = (word >> (fb & 31u)) & 1u;
+  const uint32_t addr = s_bkt + ((base + shr_clamp(h, sh)) << 5);
+  unsigned long long k0 = ~key, k1 = ~key, k2 = ~key, k3 = ~key;
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.u32 p, %4, 0;\n"
+      " @p ld.shared.v2.u64 {%0, %1}, [%5];\n"
+      " @p ld.shared.v2.u64 {%2, %3}, [%5+16];\n}\n"
+      : "+l"(k0), "+l"(k1), "+l"(k2), "+l"(k3)
+      : "r"(maybe), "r"(addr));
+  return (k0 == key) + (k1 == key) + (k2 == key) + (k3 == key);
+}
+
+// Everything the bucket lookup does not cover: stash entries, global-memory fields.
 __device__ __noinline__ int slow_count(const HmaSmem& s, const HmaParams& p, int f, uint32_t tab,
                                        unsigned long long key) {
   if (tab & kFlagGlobal) {     // (INT64_MIN included: the scan compares raw values)
@@ -119,8 +149,8 @@ __device__ __noinline__ int slow_count(const HmaSmem& s, const HmaParams& p, int
       c += (static_cast<unsigned long long>(__ldg(p.user_ids + i)) == key) ? 1 : 0;
     return c;
   }
-  if (key == kSentinel) return s.sent_cnt[f];
-  int c = bucket_count(s, tab, key);
+  const uint32_t fb = filter_bit(tab, key_hash(key));
+  int c = ((s.bits[fb >> 5] >> (fb & 31u)) & 1u) ? bucket_count(s, tab, key) : 0;
   if (tab & kFlagStash) {
     const int n = s.stash_n < kStash ? s.stash_n : kStash;
     for (int i = 0; i < n; ++i) c += (s.stash_field[i] == f && s.stash_key[i] == key) ? 1 : 0;
@@ -130,8 +160,9 @@ __device__ __noinline__ int slow_count(const HmaSmem& s, const HmaParams& p, int
 
 __device__ __forceinline__ int lookup_any(const HmaSmem& s, const HmaParams& p, int f,
                                           uint32_t tab, unsigned long long key) {
-  if (key == kSentinel || (tab & (kFlagStash | kFlagGlobal))) return slow_count(s, p, f, tab, key);
-  return bucket_count(s, tab, key);
+  if (tab & (kFlagStash | kFlagGlobal)) return slow_count(s, p, f, tab, key);
+  const uint32_t fb = filter_bit(tab, key_hash(key));
+  return ((s.bits[fb >> 5] >> (fb & 31u)) & 1u) ? bucket_count(s, tab, key) : 0;
 }
 
 __global__ void __launch_bounds__(kThreads, 2)
@@ -157,10 +188,11 @@ __global__ void __launch_bounds__(kThreads, 2)
     s.stash_n = 0;
     for (int f = 0; f < F; ++f) {
       const long long n = s.uoff[f + 1] - s.uoff[f];
-      // 2^k buckets, >= 2 per ID (mean load <= 2 of 4 slots) when the pool allows, else >= 1
-      int nb = 1, shift = 32;
+      // 2^k >= 2 buckets, >= 2 per ID (mean load <= 2 of 4 slots) when the pool allows, else
+      // >= 1 per ID
+      int nb = 2, shift = 31;
       while (nb < 2 * n && nb < kPoolBuckets) { nb <<= 1; --shift; }
-      if (used + nb > kPoolBuckets && nb > n && nb >= 2) { nb >>= 1; ++shift; }
+      if (used + nb > kPoolBuckets && nb > n && nb > 2) { nb >>= 1; ++shift; }
       if (nb >= n && used + nb <= kPoolBuckets) {
         s.tab[f] = static_cast<uint32_t>(used) | (static_cast<uint32_t>(shift & 63) << 12);
         used += nb;
@@ -168,15 +200,22 @@ __global__ void __launch_bounds__(kThreads, 2)
         s.tab[f] = kFlagGlobal;
         s.slow_any = 1;
       }
-      s.sent_cnt[f] = 0;
     }
   }
-  {
-    const ulonglong2 e = make_ulonglong2(kSentinel, kSentinel);
-    ulonglong2* flat = &s.bkt[0][0];
-    for (int i = tid; i < 2 * kPoolBuckets; i += kThreads) flat[i] = e;
-    for (int i = tid; i < kPoolBuckets / 2; i += kThreads) s.bits[i] = 0u;
-    for (int i = tid; i < kWarps * 32; i += kThreads) (&s.warp_cnt[0][0])[i] = 0;
+  for (int i = tid; i < kPoolBuckets / 2; i += kThreads) s.bits[i] = 0u;
+  for (int i = tid; i < kWarps * 32; i += kThreads) (&s.warp_cnt[0][0])[i] = 0;
+  __syncthreads();
+  // empty slots: each field's lower half of buckets gets kFill0, the upper half kFill1
+  for (int f = 0; f < F; ++f) {
+    const uint32_t t = s.tab[f];
+    if (t & kFlagGlobal) continue;
+    const int base = static_cast<int>(t & 4095u);
+    const int nb = 1 << (32 - static_cast<int>((t >> 12) & 63u));
+    for (int i = tid; i < nb; i += kThreads) {
+      const unsigned long long e = (i < nb / 2) ? kFill0 : kFill1;
+      s.bkt[base + i][0] = make_ulonglong2(e, e);
+      s.bkt[base + i][1] = make_ulonglong2(e, e);
+    }
   }
   __syncthreads();
   {
@@ -193,17 +232,14 @@ __global__ void __launch_bounds__(kThreads, 2)
       const uint32_t t = s.tab[f];
       if (t & kFlagGlobal) continue;
       const unsigned long long key = static_cast<unsigned long long>(__ldg(p.user_ids + pos));
-      if (key == kSentinel) {
-        atomicAdd(&s.sent_cnt[f], 1);
-        continue;
-      }
       const uint32_t fb = filter_bit(t, key_hash(key));
       atomicOr(&s.bits[fb >> 5], 1u << (fb & 31u));
       const uint32_t bk = bucket_of(t, key);
       unsigned long long* slots = reinterpret_cast<unsigned long long*>(&s.bkt[bk][0]);
+      const unsigned long long fill = (bk - (t & 4095u)) < (1u << (31 - ((t >> 12) & 63u))) ? kFill0 : kFill1;
       bool placed = false;
       for (int q = 0; q < 4 && !placed; ++q)
-        placed = atomicCAS(slots + q, kSentinel, key) == kSentinel;
+        placed = atomicCAS(slots + q, fill, key) == fill;
       if (!placed) {
         const int at = atomicAdd(&s.stash_n, 1);
         if (at < kStash) {
@@ -219,6 +255,8 @@ __global__ void __launch_bounds__(kThreads, 2)
   }
   __syncthreads();
   const bool slow_any = s.slow_any != 0;
+  const uint32_t s_bkt = smem_u32(&s.bkt[0][0]);
+  const uint32_t s_bits = smem_u32(&s.bits[0]);
 
   // ---- 2. the item-ID stream, 32 segments per warp step
   for (int64_t c0 = first; c0 < ce; c0 += static_cast<int64_t>(gridDim.y) * chunk) {
@@ -288,10 +326,8 @@ __global__ void __launch_bounds__(kThreads, 2)
             const bool valid = wbase + lane < n_ids;
             const uint32_t t = __shfl_sync(0xffffffffu, my_tab, seg & 31);
             int c;
-            if (!slow_any && !__any_sync(0xffffffffu, key == kSentinel)) {
-              const uint32_t fb = filter_bit(t, key_hash(key));
-              const bool maybe = (s.bits[fb >> 5] >> (fb & 31u)) & 1u;
-              c = maybe ? bucket_count(s, t, key) : 0;
+            if (!slow_any) {
+              c = fast_count(s_bkt, s_bits, t, key);
             } else {
               const int f = __shfl_sync(0xffffffffu, my_f, seg & 31);
               c = valid ? lookup_any(s, p, f, t, key) : 0;
