@@ -121,36 +121,17 @@ constexpr int kKeys = 128;                       // keys per tile (S columns)
 constexpr int kThreads = 512;
 constexpr uint32_t kQBytes = 128 * kD * 2;       // 32 KB: Q tile, [2 col blocks][128 rows][64]
 constexpr uint32_t kHalfBytes = 16384;           // K half [2][64 keys][64] or V half [128][64]
-// Shared-memory layout per variant.  kFusedQ (the Q projection inside the kernel): two Q
-// buffers (unit m+1's Q is produced while unit m's S MMAs read unit m's), the K ring also
-// carries the projection's operands (T row blocks and W_q halves), V ring 3 stages.
-#ifndef GESR_FQ_KSTAGES
-#define GESR_FQ_KSTAGES 4
-#endif
-#ifndef GESR_FQ_VSTAGES
-#define GESR_FQ_VSTAGES 3
-#endif
-#ifndef GESR_FQ_ORDER
-#define GESR_FQ_ORDER 0          // fused Q work order: 0 head-fastest, 1 unit-fastest
-#endif
-#ifndef GESR_FQ_EARLY
-#define GESR_FQ_EARLY 0          // 1: the next unit's projection right after S(0)
-#endif
-template <bool kFusedQ>
-struct PairLayout {
-  static constexpr int kQBufs = kFusedQ ? 2 : 1;
-  static constexpr int kKStages = kFusedQ ? GESR_FQ_KSTAGES : 4;     // K-half ring
-  static constexpr int kVStages = kFusedQ ? GESR_FQ_VSTAGES : 5;     // V-half ring
-  static constexpr int kStages = kKStages + kVStages;
-  static constexpr uint32_t kQOff = 0;
-  static constexpr uint32_t kRingOff = kQBufs * kQBytes;
-  static constexpr uint32_t kStgOff = kRingOff + kStages * kHalfBytes;   // 4 x 2 KB boxes per epilogue warp
-  static constexpr uint32_t kBarOff = kStgOff + 4 * 8192;
-  static constexpr uint32_t kXchOff = kBarOff + 512;                      // [unit % 4][WG][m, l][row]
-  static constexpr uint32_t kMshOff = kXchOff + 4 * 2 * 2 * 128 * 4;      // [row] {running max, tile}
-  static constexpr uint32_t kSmemBytes = kMshOff + 128 * 8 + 1024;
-  static_assert(kSmemBytes <= 232448, "shared memory budget");
-};
+constexpr int kKStages = 4;                     // K-half ring
+constexpr int kVStages = 5;                     // V-half ring
+constexpr int kStages = kKStages + kVStages;
+constexpr uint32_t kQOff = 0;
+constexpr uint32_t kRingOff = kQBytes;
+constexpr uint32_t kStgOff = kRingOff + kStages * kHalfBytes;        // 4 x 2 KB boxes per epilogue warp
+constexpr uint32_t kBarOff = kStgOff + 4 * 8192;
+constexpr uint32_t kXchOff = kBarOff + 512;                          // [unit % 4][WG][m, l][row]
+constexpr uint32_t kMshOff = kXchOff + 4 * 2 * 2 * 128 * 4;          // [row] {running max, tile}
+constexpr uint32_t kSmemBytes = kMshOff + 128 * 8 + 1024;
+static_assert(kSmemBytes <= 232448, "shared memory budget");
 // register split (setmaxnreg per warpgroup; launch registers 128 x 512 threads): control 56,
 // softmax 184, epilogue 88
 constexpr int kCtrlRegs = 56;
@@ -181,24 +162,12 @@ struct Work {
 
 // kCausal: history self-attention (gesr_history_attention); a separate instantiation keeps the
 // target-aware kernel's code unchanged
-// kCausal: history self-attention (gesr_history_attention); a separate instantiation keeps the
-// target-aware kernel's code unchanged.  kFusedQ: the Q projection Q = act(T W_q[h]^T + b_q) is
-// computed inside the kernel (DESIGN.md s6 K-ATTN "fused Q"): map_q is then the candidate rows
-// T [total_C, D_in] (box 128 x 64) and map_w the query weight W_q [H d, D_in] (box 64 x 64);
-// the leader's S issuer runs the projection's M=256 N=128 MMAs into the unit's O accumulator
-// before the unit's first PV, the epilogue warps convert it (bias, activation, bf16) into the
-// unit's Q buffer in shared memory, and no Q tensor ever reaches HBM.
-template <bool kCausal, bool kFusedQ>
+template <bool kCausal>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     attn_pair_kernel(const __grid_constant__ CUtensorMap map_q,
                      const __grid_constant__ CUtensorMap map_kh,
                      const __grid_constant__ CUtensorMap map_vh,
-                     const __grid_constant__ CUtensorMap map_o,
-                     const __grid_constant__ CUtensorMap map_w, const AttnParams p) {
-  using Lay = PairLayout<kFusedQ>;
-  constexpr int kKStages = Lay::kKStages;
-  constexpr int kVStages = Lay::kVStages;
-  constexpr int kStages = Lay::kStages;
+                     const __grid_constant__ CUtensorMap map_o, const AttnParams p) {
   const int U = __ldg(p.unit_count);
   const int S = p.splits;
   const int W = U * p.H * S;
@@ -210,10 +179,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  uint64_t* q_full = reinterpret_cast<uint64_t*>(smem + Lay::kBarOff);   // [2] leader's used
-  uint64_t* q_empty = q_full + 2;                 // [2] each CTA
-  uint64_t* qp_done = q_empty + 2;                // [2] each CTA (fused Q: projection landed)
-  uint64_t* kv_full = qp_done + 2;                // [kStages]  K ring, then V ring (leader's used)
+  uint64_t* q_full = reinterpret_cast<uint64_t*>(smem + kBarOff);   // leader's used
+  uint64_t* q_empty = q_full + 1;                 // each CTA
+  uint64_t* kv_full = q_empty + 1;                // [kStages]  K ring, then V ring (leader's used)
   uint64_t* kv_empty = kv_full + kStages;         // [kStages]  (each CTA)
   uint64_t* s_full = kv_empty + kStages;          // [2]        (each CTA)
   uint64_t* s_free = s_full + 2;                  //            (leader; 4 warps x 2 CTAs per S)
@@ -230,8 +198,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t* ml_empty = ml_full + 4;               // [4]        (each CTA; its 4 epilogue warps)
   uint64_t* pv_done = ml_empty + 4;               //            (each CTA; one phase per PV)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 1);
-  static_assert((6 + 2 * kStages + 2 * 6 + 8 + 1) * 8 + 4 <= Lay::kXchOff - Lay::kBarOff,
-                "barrier area");
+  static_assert((2 + 2 * kStages + 2 * 6 + 8 + 1) * 8 + 4 <= kXchOff - kBarOff, "barrier area");
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -247,13 +214,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     tma_prefetch_desc(&map_kh);
     tma_prefetch_desc(&map_vh);
     if (p.o_tma) tma_prefetch_desc(&map_o);
-    if (kFusedQ) tma_prefetch_desc(&map_w);
-    for (int i = 0; i < 2; ++i) {
-      // fused Q: the leader's q_full takes one arrival per converting warp of the pair
-      mbar_init(&q_full[i], kFusedQ ? 8 : 1);
-      mbar_init(&q_empty[i], 1);
-      mbar_init(&qp_done[i], 1);
-    }
+    mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&kv_full[s], 1);
       mbar_init(&kv_empty[s], 1);
@@ -280,49 +242,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     tmem_relinquish_pair();
   }
   if (threadIdx.x < 128) {        // running-max words: no tile decided yet
-    const uint32_t w = smem_u32(smem + Lay::kMshOff) + threadIdx.x * 8;
+    const uint32_t w = smem_u32(smem + kMshOff) + threadIdx.x * 8;
     asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(w), "r"(0u), "r"(0xFFFFFFFFu) : "memory");
   }
   tc_fence_before();
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t sQ = smem_u32(smem + Lay::kQOff);
-  const uint32_t sRing = smem_u32(smem + Lay::kRingOff);
+  const uint32_t sQ = smem_u32(smem + kQOff);
+  const uint32_t sRing = smem_u32(smem + kRingOff);
 
-  // w -> (unit, split, head).  Unfused: unit w % U, split (w / U) % S, head w / (U S):
-  // neighbouring pairs share a head and run the units of one request at the same time (K/V
-  // shared in L2; measured: a pair taking a contiguous block of items, units of a request back
-  // to back, read 11% MORE from HBM).  Fused Q: head w % H, split (w / H) % S, unit w / (H S):
-  // the H pairs projecting one unit's candidate rows T run side by side, so T is read from HBM
-  // once and from L2 by the other heads (the units of a request still run on adjacent pairs).
-  constexpr bool kHeadFast = kFusedQ && GESR_FQ_ORDER == 0;
-  auto unit_of = [&](int w) { return kHeadFast ? w / (p.H * S) : w % U; };
   // the unit descriptor of work item w is one 16-byte load, fetched one item ahead
-  auto fetch = [&](int w) { return __ldg(p.units + unit_of(w)); };
+  auto fetch = [&](int w) { return __ldg(p.units + (w % U)); };
+  // w -> (unit w % U, split (w / U) % S, head w / (U S)): neighbouring pairs share a head and
+  // run the units of one request at the same time (K/V shared in L2; measured: a pair taking
+  // a contiguous block of items, units of a request back to back, read 11% MORE from HBM)
   auto decode = [&](int w, int4 d) {
     Work x;
-    int split, h;
-    if (kHeadFast) {
-      h = w % p.H;
-      split = (w / p.H) % S;
-    } else {
-      const int rest = w / U;
-      split = rest % S;
-      h = rest / S;
-    }
+    const int rest = w / U;
     x.s0 = d.x;
     x.L = d.y;
     x.cbeg = d.z;
     x.rows_valid = d.w;
-    x.h = h;
     const int n = (x.L + kKeys - 1) / kKeys;
     if (S == 1) {
       x.split = 0;
+      x.h = rest;
       x.t0 = 0;
       x.nkv = n;
     } else {
-      x.split = split;
+      x.split = rest % S;
+      x.h = rest / S;
       x.t0 = x.split * n / S;              // n <= 2^24, S <= 64: no int32 overflow
       x.nkv = (x.split + 1) * n / S - x.t0;
     }
@@ -364,35 +314,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     out.m = st.m;
     return true;
   };
-  // Fused Q: a second cursor over the work items WITH keys (the units that need a Q), kept one
-  // unit ahead of the tile stream: the projection of unit m+1 is emitted into the K ring right
-  // after K tile min(2, nkv - 1) of unit m (unit 0's before everything), by the producer and
-  // the S issuer alike, so both walk the same slot sequence.
-  struct ItemCursor {
-    int w;
-    int4 nx;
-  };
-  auto item_init = [&](ItemCursor& c) {
-    c.w = pair;
-    c.nx = pair < W ? fetch(pair) : make_int4(0, 0, 0, 0);
-  };
-  auto item_next = [&](ItemCursor& c, Work& x) -> bool {
-    while (c.w < W) {
-      x = decode(c.w, c.nx);
-      c.w += npairs;
-      if (c.w < W) c.nx = fetch(c.w);
-      if (x.nkv > 0) return true;
-    }
-    return false;
-  };
-  const int nkb = p.d_in / 64;                    // fused Q: 64-wide K blocks of the projection
-  const int nqc = (nkb + 1) / 2;                  // projection chunks (two K blocks each)
-  // unit m+1's projection chunk c follows K tile qp_point(c) of unit m: spread over the unit's
-  // last tiles (one chunk every other tile, done ~2 tiles before the unit ends), so the
-  // projection MMAs never hold back an S MMA by more than one chunk (8 MMAs)
-  auto qp_point = [&](const Tile& tl, int c) {
-    return GESR_FQ_EARLY ? 0 : max(0, tl.x.nkv - 1 - 2 * (nqc - c));
-  };
 
   if (warp < 4) {
     setmaxnreg_dec<kCtrlRegs>();
@@ -412,44 +333,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       if (elect_one()) {
         int kst = 0;
         uint32_t kph = 0;
-        auto next_slot = [&]() {
-          const int slot = kst;
-          pwait(&kv_empty[slot], kph ^ 1, CTX(2, 0, 0));
-          if (++kst == kKStages) { kst = 0; kph ^= 1; }
-          return slot;
-        };
-        // fused Q: the projection operands of one unit, chunk c = K blocks 2c, 2c+1: the two
-        // W_q halves [64 rows of head h][64] (8 KB each, one slot), then the two T row blocks
-        // [128 rows][64] (16 KB each, one slot each).  T is re-read by the unit's other heads
-        // (adjacent pairs): no evict-first hint.
-        auto emit_chunk = [&](const Work& x, int c) {
-          const int32_t trow = static_cast<int32_t>(x.cbeg) + static_cast<int32_t>(rank) * 128;
-          const int32_t wrow = x.h * kD + static_cast<int32_t>(rank) * 64;
-          const int kb = 2 * c;
-          const int nb = (kb + 1 < nkb) ? 2 : 1;
-          int slot = next_slot();
-          if (rank == 0) mbar_arrive_expect_tx(&kv_full[slot], 2 * nb * (kHalfBytes / 2));
-          uint8_t* dst = smem + Lay::kRingOff + slot * kHalfBytes;
-          for (int i = 0; i < nb; ++i)
-            tma_load_2d_pair(dst + i * (kHalfBytes / 2), &map_w, &kv_full[slot], (kb + i) * 64, wrow);
-          for (int i = 0; i < nb; ++i) {
-            slot = next_slot();
-            if (rank == 0) mbar_arrive_expect_tx(&kv_full[slot], 2 * kHalfBytes);
-            tma_load_2d_pair(smem + Lay::kRingOff + slot * kHalfBytes, &map_q, &kv_full[slot],
-                             (kb + i) * 64, trow);
-          }
-        };
-        ItemCursor qc;
-        Work qx;
-        bool qhave = false;
-        if (kFusedQ) {
-          item_init(qc);
-          qhave = item_next(qc, qx);
-          if (qhave)
-            for (int c = 0; c < nqc; ++c) emit_chunk(qx, c);
-        }
         while (stream_next(st, tl)) {
-          if (!kFusedQ && tl.t == 0) {
+          if (tl.t == 0) {
             // the unit's Q: the previous unit's S MMAs must be done with the single Q buffer
             if (tl.m > 0) pwait(q_empty, (tl.m - 1) & 1, CTX(1, tl.m, tl.t));
             GESR_T3(3, tl.m);
@@ -457,16 +342,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                                  static_cast<int32_t>(rank) * 128;
             if (rank == 0) mbar_arrive_expect_tx(q_full, 2 * kQBytes);
 #if GESR_PAIR_L2HINT >= 1
-            tma_load_2d_pair_hint(smem + Lay::kQOff, &map_q, q_full, 0, qrow, pol_first);
-            tma_load_2d_pair_hint(smem + Lay::kQOff + kQBytes / 2, &map_q, q_full, 64, qrow, pol_first);
+            tma_load_2d_pair_hint(smem + kQOff, &map_q, q_full, 0, qrow, pol_first);
+            tma_load_2d_pair_hint(smem + kQOff + kQBytes / 2, &map_q, q_full, 64, qrow, pol_first);
 #else
-            tma_load_2d_pair(smem + Lay::kQOff, &map_q, q_full, 0, qrow);
-            tma_load_2d_pair(smem + Lay::kQOff + kQBytes / 2, &map_q, q_full, 64, qrow);
+            tma_load_2d_pair(smem + kQOff, &map_q, q_full, 0, qrow);
+            tma_load_2d_pair(smem + kQOff + kQBytes / 2, &map_q, q_full, 64, qrow);
 #endif
           }
-          const int slot = next_slot();
+          const int slot = kst;
+          pwait(&kv_empty[slot], kph ^ 1, CTX(2, tl.m, tl.t));
           if (rank == 0) mbar_arrive_expect_tx(&kv_full[slot], 2 * kHalfBytes);
-          uint8_t* dst = smem + Lay::kRingOff + slot * kHalfBytes;
+          uint8_t* dst = smem + kRingOff + slot * kHalfBytes;
           const int32_t row = krow_of(tl) + static_cast<int32_t>(rank) * 64;
 #if GESR_PAIR_L2HINT >= 2
           tma_load_2d_pair_hint(dst, &map_kh, &kv_full[slot], 0, row, pol_last);
@@ -475,13 +361,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           tma_load_2d_pair(dst, &map_kh, &kv_full[slot], 0, row);
           tma_load_2d_pair(dst + 8192, &map_kh, &kv_full[slot], 64, row);
 #endif
-          if (kFusedQ) {
-            for (int c = 0; c < nqc; ++c) {
-              if (qp_point(tl, c) != tl.t) continue;
-              if (c == 0) qhave = item_next(qc, qx);
-              if (qhave) emit_chunk(qx, c);
-            }
-          }
+          if (++kst == kKStages) { kst = 0; kph ^= 1; }
         }
       }
     } else if (warp == 2) {
@@ -493,7 +373,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const int slot = kKStages + vst;
           pwait(&kv_empty[slot], vph ^ 1, CTX(3, tl.m, tl.t));
           if (rank == 0) mbar_arrive_expect_tx(&kv_full[slot], 2 * kHalfBytes);
-          uint8_t* dst = smem + Lay::kRingOff + slot * kHalfBytes;
+          uint8_t* dst = smem + kRingOff + slot * kHalfBytes;
 #if GESR_PAIR_L2HINT >= 2
           tma_load_2d_pair_hint(dst, &map_vh, &kv_full[slot], static_cast<int32_t>(rank) * 64, krow_of(tl), pol_last);
 #else
@@ -504,90 +384,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
     } else if (warp == 1 && rank == 0) {
       // ---------------------------------------------------------- S MMA issuer (leader only)
-      const uint32_t idesc_s = make_idesc_bf16(256, kKeys, 0, 0);   // also the projection's
+      const uint32_t idesc_s = make_idesc_bf16(256, kKeys, 0, 0);
       int kst = 0;
       uint32_t kph = 0;
       uint32_t sn0 = 0;                            // S issued so far
-      auto take_slot = [&]() {
-        const int slot = kst;
-        pwait(&kv_full[slot], kph, CTX(6, 0, 0));
-        if (++kst == kKStages) { kst = 0; kph ^= 1; }
-        return slot;
-      };
-      // fused Q: chunk c of unit mm's projection into its O accumulator (free once unit mm-2's
-      // epilogue has read it), operands from the K ring in emit_chunk's order
-      auto issue_chunk = [&](int mm, int c) {
-        const int ob = mm & 1;
-        if (c == 0 && mm >= 2) pwait(&o_free[ob], ((mm >> 1) - 1) & 1, CTX(16, mm, 0));
-        const int kb = 2 * c;
-        const int nb = (kb + 1 < nkb) ? 2 : 1;
-        const int wslot = take_slot();
-        for (int i = 0; i < nb; ++i) {
-          const int aslot = take_slot();
-          tc_fence_after();
-          if (elect_one()) {
-            const uint32_t ab = sRing + aslot * kHalfBytes;
-            const uint32_t wb = sRing + wslot * kHalfBytes + i * (kHalfBytes / 2);
-#pragma unroll
-            for (int ks = 0; ks < 4; ++ks)
-              mma_ss_pair(tmem + kTO + ob * kD, kdesc(ab, 0, ks), kdesc(wb, 0, ks), idesc_s,
-                          (kb + i > 0 || ks > 0) ? 1u : 0u);
-            mma_commit_pair_mc(&kv_empty[aslot], 0x3);
-            if (i == nb - 1) mma_commit_pair_mc(&kv_empty[wslot], 0x3);
-            if (kb + i == nkb - 1) mma_commit_pair_mc(&qp_done[ob], 0x3);
-          }
-          __syncwarp();
-        }
-      };
-      ItemCursor qc;
-      Work qx;
-      bool qhave = false;
-      int qm = 0;                                  // projections started so far
-      if (kFusedQ) {
-        item_init(qc);
-        qhave = item_next(qc, qx);
-        if (qhave) {
-          for (int c = 0; c < nqc; ++c) issue_chunk(0, c);
-          qm = 1;
-        }
-      }
       while (stream_next(st, tl)) {
         const int buf = tl.t & 1;
-        const int qb = kFusedQ ? (tl.m & 1) : 0;
         if (tl.t == 0) {
-          // the unit's Q tile (both CTAs)
-          pwait(&q_full[qb], kFusedQ ? ((tl.m >> 1) & 1) : (tl.m & 1), CTX(4, tl.m, tl.t));
+          pwait(q_full, tl.m & 1, CTX(4, tl.m, tl.t));   // the unit's Q tile (both CTAs)
           if (lane == 0) GESR_T3(0, tl.m);
         }
         // the single S buffer's previous S must have been loaded into registers (both CTAs)
         if (sn0 > 0) pwait(s_free, (sn0 - 1) & 1, CTX(5, tl.m, tl.t));
         ++sn0;
-        const int slot = take_slot();
+        const int slot = kst;
+        pwait(&kv_full[slot], kph, CTX(6, tl.m, tl.t));
+        if (++kst == kKStages) { kst = 0; kph ^= 1; }
         if (lane == 0) GESR_T2(7, tl.m * 16 + tl.t);
         const uint32_t kb = sRing + slot * kHalfBytes;
-        const uint32_t sQb = sQ + qb * kQBytes;
         tc_fence_after();
         if (elect_one()) {
 #pragma unroll
           for (int ks = 0; ks < kD / 16; ++ks)
-            mma_ss_pair(tmem + kTS, kdesc(sQb, kQBytes / 2, ks), kdesc(kb, 8192, ks), idesc_s,
+            mma_ss_pair(tmem + kTS, kdesc(sQ, kQBytes / 2, ks), kdesc(kb, 8192, ks), idesc_s,
                         ks > 0 ? 1u : 0u);
           mma_commit_pair_mc(&s_full[buf], 0x3);
           mma_commit_pair_mc(&kv_empty[slot], 0x3);
           // the unit's last S: its Q buffer may be reloaded
-          if (tl.t == tl.x.nkv - 1) mma_commit_pair_mc(&q_empty[qb], 0x3);
+          if (tl.t == tl.x.nkv - 1) mma_commit_pair_mc(q_empty, 0x3);
         }
         __syncwarp();
-        if (kFusedQ) {
-          for (int c = 0; c < nqc; ++c) {
-            if (qp_point(tl, c) != tl.t) continue;
-            if (c == 0) {
-              qhave = item_next(qc, qx);
-              if (qhave) ++qm;
-            }
-            if (qhave) issue_chunk(qm - 1, c);
-          }
-        }
       }
     } else if (warp == 3 && rank == 0) {
       // ---------------------------------------------------------- PV MMA issuer (leader only)
@@ -601,10 +427,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         pwait(&kv_full[vslot], vph, CTX(7, tl.m, tl.t));
         if (++vst == kVStages) { vst = 0; vph ^= 1; }
         const int ob = tl.m & 1;                     // O buffer of this unit
-        if (!kFusedQ && tl.t == 0 && tl.m >= 2) {
+        if (tl.t == 0 && tl.m >= 2) {
           // the unit's first PV overwrites its O buffer: unit m-2's epilogue must have read it
-          // (fused Q: the projection waited for that already, and the Q conversion read the
-          // projection before S(0) -- and so PV(0) -- could start)
           pwait(&o_free[ob], ((tl.m >> 1) - 1) & 1, CTX(8, tl.m, tl.t));
           if (lane == 0) GESR_T3(1, tl.m);
         }
@@ -649,8 +473,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const uint32_t tP = tmem + lane_addr + kTP + g * (kKeys / 2);
     const uint32_t s_free_leader = mapa_shared(smem_u32(s_free), 0);
     const uint32_t p_full_leader = mapa_shared(smem_u32(&p_full[g]), 0);
-    const uint32_t xch = smem_u32(smem + Lay::kXchOff);
-    const uint32_t msh = smem_u32(smem + Lay::kMshOff) + rloc * 8;
+    const uint32_t xch = smem_u32(smem + kXchOff);
+    const uint32_t msh = smem_u32(smem + kMshOff) + rloc * 8;
     // {m, tile} of this row: the running max as decided by CTA-wide key tile `tile` (tiles
     // decide in order; one 8-byte store / load, so the pair is always consistent)
     auto publish_m = [&](float mv, int tile) {
@@ -886,67 +710,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const uint32_t tO0 = tmem + ((sub * 32) << 16) + kTO;   // O buffer 0; buffer 1 at + kD
     const uint32_t o_free_leader0 = mapa_shared(smem_u32(&o_free[0]), 0);
     const uint32_t o_free_leader1 = mapa_shared(smem_u32(&o_free[1]), 0);
-    const uint32_t xch = smem_u32(smem + Lay::kXchOff);
-    uint8_t* stg = smem + Lay::kStgOff + sub * 8192;
+    const uint32_t xch = smem_u32(smem + kXchOff);
+    uint8_t* stg = smem + kStgOff + sub * 8192;
     const uint32_t stg_s = smem_u32(stg);
     const int64_t HD = static_cast<int64_t>(p.H) * kD;
-    // fused Q: unit mm's projection (fp32, in its O accumulator) -> + b_q, act, bf16 -> the
-    // unit's Q buffer in the 128B-swizzled K-major layout the S MMA reads (row rloc: 16-byte
-    // chunk c of column block k at k 16 KB + rloc 128 B + (c ^ (rloc & 7)) 16 B, as TMA writes
-    // it); then one release arrival per warp on the leader's q_full.  Runs a unit ahead of the
-    // epilogue: unit m+1's conversion is done during unit m.
-    const uint32_t q_full_leader0 = mapa_shared(smem_u32(&q_full[0]), 0);
-    const uint32_t q_full_leader1 = mapa_shared(smem_u32(&q_full[1]), 0);
-    auto convert_q = [&](const Work& qx, int mm) {
-      const int ob = mm & 1;
-      pwait(&qp_done[ob], (mm >> 1) & 1, CTX(17, mm, 0), GESR_PAIR_EPI_SLEEP);
-      if (mm >= 2) pwait(&q_empty[ob], ((mm >> 1) - 1) & 1, CTX(18, mm, 0));
-      tc_fence_after();
-      const uint32_t tQ = tO0 + ob * kD;
-      const uint32_t dst = sQ + ob * kQBytes + rloc * 128;
-      const float* bq = p.bq != nullptr ? p.bq + qx.h * kD : nullptr;
-#pragma unroll 1
-      for (int c = 0; c < kD / 32; ++c) {
-        uint32_t o[32];
-        tmem_ld32(tQ + c * 32, o);
-        tmem_ld_wait();
-        uint32_t pk[16];
-#pragma unroll
-        for (int e = 0; e < 32; e += 2) {
-          float v0 = __uint_as_float(o[e]), v1 = __uint_as_float(o[e + 1]);
-          if (bq != nullptr) {
-            v0 += __ldg(bq + c * 32 + e);
-            v1 += __ldg(bq + c * 32 + e + 1);
-          }
-          if (p.act == 1) silu2(v0, v1);
-          pk[e / 2] = pack_bf16x2(v0, v1);
-        }
-#pragma unroll
-        for (int qq = 0; qq < 4; ++qq) {
-          const int cc = c * 4 + qq;                      // 16-byte chunk of the 256-byte row
-          st_shared_v4(dst + (cc >> 3) * (kQBytes / 2) + (((cc & 7) ^ (rloc & 7)) << 4),
-                       pk[4 * qq], pk[4 * qq + 1], pk[4 * qq + 2], pk[4 * qq + 3]);
-        }
-      }
-      fence_proxy_async_smem();        // the S MMA (async proxy, issued by the leader) reads it
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(ob ? q_full_leader1 : q_full_leader0);
-    };
-    ItemCursor cc;
-    Work cx;
-    if (kFusedQ) {
-      item_init(cc);
-      if (item_next(cc, cx)) convert_q(cx, 0);
-    }
     int m = 0;
     int4 nx = fetch(pair);
     for (int w = pair; w < W; w += npairs) {
       const Work x = decode(w, nx);
       if (w + npairs < W) nx = fetch(w + npairs);
       const int nkv = x.nkv, h = x.h;
-      // fused Q: the next unit's Q first (it is due before this unit ends)
-      if (kFusedQ && nkv > 0 && item_next(cc, cx)) convert_q(cx, m + 1);
       const bool row_ok = row_in_unit < x.rows_valid;
       const int64_t row = x.cbeg + row_in_unit;
       const bool split_out = S > 1;                     // write split-L partials, not O
@@ -1141,16 +914,12 @@ extern "C" int gesr_debug_trace3_copy(void* host) {
 #endif
 
 cudaError_t launch_attn_pair(const CUtensorMap& mq, const CUtensorMap& mkh, const CUtensorMap& mvh,
-                             const CUtensorMap& mo, const CUtensorMap& mw, const AttnParams& p,
-                             int64_t max_units, cudaStream_t stream) {
-  constexpr uint32_t kBytesU = PairLayout<false>::kSmemBytes;
-  constexpr uint32_t kBytesF = PairLayout<true>::kSmemBytes;
-  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(attn_pair_kernel<false, false>),
-                                   kBytesU);
+                             const CUtensorMap& mo, const AttnParams& p, int64_t max_units,
+                             cudaStream_t stream) {
+  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(attn_pair_kernel<false>),
+                                   kSmemBytes);
   if (e != cudaSuccess) return e;
-  e = ensure_smem_attr(reinterpret_cast<const void*>(attn_pair_kernel<true, false>), kBytesU);
-  if (e != cudaSuccess) return e;
-  e = ensure_smem_attr(reinterpret_cast<const void*>(attn_pair_kernel<false, true>), kBytesF);
+  e = ensure_smem_attr(reinterpret_cast<const void*>(attn_pair_kernel<true>), kSmemBytes);
   if (e != cudaSuccess) return e;
   int max_pairs = device_cached(1);      // co-resident CTA pairs on this device
   if (max_pairs == 0) {
@@ -1162,11 +931,11 @@ cudaError_t launch_attn_pair(const CUtensorMap& mq, const CUtensorMap& mkh, cons
     attr.val.clusterDim.z = 1;
     cfg.gridDim = dim3(2, 1, 1);
     cfg.blockDim = dim3(kThreads, 1, 1);
-    cfg.dynamicSmemBytes = kBytesU > kBytesF ? kBytesU : kBytesF;
+    cfg.dynamicSmemBytes = kSmemBytes;
     cfg.attrs = &attr;
     cfg.numAttrs = 1;
     int clusters = 0;
-    e = cudaOccupancyMaxActiveClusters(&clusters, attn_pair_kernel<false, false>, &cfg);
+    e = cudaOccupancyMaxActiveClusters(&clusters, attn_pair_kernel<false>, &cfg);
     if (e != cudaSuccess || clusters <= 0) {
       int dev = 0, sms = 148;
       cudaGetDevice(&dev);
@@ -1180,11 +949,9 @@ cudaError_t launch_attn_pair(const CUtensorMap& mq, const CUtensorMap& mkh, cons
   const int64_t work = max_units * p.H * p.splits;
   const unsigned pairs = static_cast<unsigned>(work < max_pairs ? work : max_pairs);
   if (p.causal)
-    attn_pair_kernel<true, false><<<2 * pairs, kThreads, kBytesU, stream>>>(mq, mkh, mvh, mo, mw, p);
-  else if (p.fused_q)
-    attn_pair_kernel<false, true><<<2 * pairs, kThreads, kBytesF, stream>>>(mq, mkh, mvh, mo, mw, p);
+    attn_pair_kernel<true><<<2 * pairs, kThreads, kSmemBytes, stream>>>(mq, mkh, mvh, mo, p);
   else
-    attn_pair_kernel<false, false><<<2 * pairs, kThreads, kBytesU, stream>>>(mq, mkh, mvh, mo, mw, p);
+    attn_pair_kernel<false><<<2 * pairs, kThreads, kSmemBytes, stream>>>(mq, mkh, mvh, mo, p);
   count_launch();
   return cudaGetLastError();
 }

@@ -185,15 +185,6 @@ gesr_status debug_check(const int64_t* offsets, int64_t n, int64_t total, int ta
   return e == cudaSuccess ? GESR_OK : cuda_fail(e, "check_offsets launch");
 }
 
-// TEMPORARY A/B knob while the fused Q projection is evaluated: GESR_FUSED_Q=0 disables it
-bool fused_q_enabled() {
-  static const int on = [] {
-    const char* v = getenv("GESR_FUSED_Q");
-    return (v != nullptr && v[0] == '0') ? 0 : 1;
-  }();
-  return on == 1;
-}
-
 bool valid_d(int32_t d) { return d == 32 || d == 64 || d == 128; }
 
 gesr_status check_common(int32_t D_in, int32_t H, int32_t d, int32_t act) {
@@ -494,37 +485,17 @@ static gesr_status tasa_impl(const void* T, int64_t total_C, int32_t D_in, const
     p.part_ml = reinterpret_cast<float2*>(part);
     p.part_o = reinterpret_cast<float*>(part + split_ml_bytes(total_C, H, p.splits));
   }
-  // d = 128 on the pair kernel: the Q projection runs inside the attention kernel (no Q
-  // workspace round trip); the self-key merge reads Q from the workspace, so it keeps the
-  // separate projection
   const bool pair = d == 128 && pair_attention_enabled() && !hstu;
-  const bool fused = pair && !causal && !self && (D_in % 64) == 0 && fused_q_enabled();
   cudaError_t e = gesr::launch_build_units(seq_offsets, cand_offsets, B, units, count, causal, st);
   if (e != cudaSuccess) return cuda_fail(e, "build_units launch");
-  if (!fused) {
-    s = run_projection(T, total_C, D_in, W_q, nullptr, b_q, nullptr, H, d, act, Q, nullptr, st);
-    if (s != GESR_OK) return s;
-  }
+  s = run_projection(T, total_C, D_in, W_q, nullptr, b_q, nullptr, H, d, act, Q, nullptr, st);
+  if (s != GESR_OK) return s;
 
-  CUtensorMap mq, mk, mv, mw;
+  CUtensorMap mq, mk, mv;
   const uint32_t box_cols = d >= 64 ? 64 : 32;
   const CUtensorMapSwizzle swz = d >= 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
-  if (fused) {
-    s = make_map_2d(&mq, T, static_cast<uint64_t>(total_C), D_in, 128, 64,
-                    CU_TENSOR_MAP_SWIZZLE_128B, "T");
-    if (s != GESR_OK) return s;
-    s = make_map_2d(&mw, W_q, static_cast<uint64_t>(H) * d, D_in, 64, 64,
-                    CU_TENSOR_MAP_SWIZZLE_128B, "W_q");
-    if (s != GESR_OK) return s;
-    p.fused_q = 1;
-    p.bq = b_q;
-    p.act = act;
-    p.d_in = D_in;
-  } else {
-    s = make_map_2d(&mq, Q, static_cast<uint64_t>(H) * total_C, d, 128, box_cols, swz, "Q");
-    if (s != GESR_OK) return s;
-    mw = mq;
-  }
+  s = make_map_2d(&mq, Q, static_cast<uint64_t>(H) * total_C, d, 128, box_cols, swz, "Q");
+  if (s != GESR_OK) return s;
   s = make_map_2d(&mk, K_cache, static_cast<uint64_t>(H) * total_L, d, 128, box_cols, swz, "K");
   if (s != GESR_OK) return s;
   s = make_map_2d(&mv, V_cache, static_cast<uint64_t>(H) * total_L, d, 128, box_cols, swz, "V");
@@ -540,7 +511,7 @@ static gesr_status tasa_impl(const void* T, int64_t total_C, int32_t D_in, const
     CUtensorMap mkh;
     s = make_map_2d(&mkh, K_cache, static_cast<uint64_t>(H) * total_L, d, 64, 64, swz, "K half");
     if (s != GESR_OK) return s;
-    e = gesr::launch_attn_pair(mq, mkh, mv, mo, mw, p, max_units(B, total_C), st);
+    e = gesr::launch_attn_pair(mq, mkh, mv, mo, p, max_units(B, total_C), st);
     if (e != cudaSuccess) return cuda_fail(e, "attn_pair_kernel launch");
     if (p.splits > 1) {
       e = gesr::launch_attn_combine(p, d, st);

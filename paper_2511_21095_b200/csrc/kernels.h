@@ -80,12 +80,6 @@ struct AttnParams {
   // HSTU pointwise normalisation (GESR_TASA_HSTU_SILU): O = sum_i SiLU(scale s_i) v_i / L_b
   // (1-CTA kernel only; no lse, one split)
   int hstu;
-  // fused Q projection (pair kernel, d = 128, D_in % 64 == 0): Q = act(T W_q^T + b_q) is
-  // computed inside the attention kernel (map_q = T, map_w = W_q); no Q workspace
-  int fused_q;
-  const float* bq;         // fp32 [H*d] or null
-  int act;                 // gesr_act
-  int d_in;                // D_in
 };
 
 constexpr int kUnitRows = 256;   // candidates per work unit (two 128-row Q tiles)
@@ -100,12 +94,10 @@ cudaError_t launch_attn(int d, const CUtensorMap& map_q, const CUtensorMap& map_
                         const CUtensorMap& map_v, const CUtensorMap& map_o, const AttnParams& p,
                         int64_t max_units,
                         cudaStream_t stream);
-// d = 128: CTA-pair kernel (attn2.cu); K map box {64, 64}, Q / V maps box {64, 128}.  With
-// p.fused_q: map_q = T [total_C, D_in] (box {64, 128}), map_w = W_q [H d, D_in] (box {64, 64}).
+// d = 128: CTA-pair kernel (attn2.cu); K map box {64, 64}, Q / V maps box {64, 128}
 cudaError_t launch_attn_pair(const CUtensorMap& map_q, const CUtensorMap& map_kh,
                              const CUtensorMap& map_vh, const CUtensorMap& map_o,
-                             const CUtensorMap& map_w, const AttnParams& p, int64_t max_units,
-                             cudaStream_t stream);
+                             const AttnParams& p, int64_t max_units, cudaStream_t stream);
 // candidate self key (GESR_TASA_SELF_KEY): merges each row's own key / value into O and lse
 // (p.lse must be set): s = scale q.k_self, O' = (O e^lse + v_self e^s) / (e^lse + e^s)
 cudaError_t launch_attn_self_merge(const AttnParams& p, const void* Q, const void* K_self,
