@@ -32,8 +32,6 @@
 //      shuffle from its lane; the lookup is hash -> bucket -> two 16-byte reads -> four 64-bit
 //      compares; hits go to a per-warp shared counter (predicated shared atomics), and lane k
 //      stores segment k's count (one coalesced 128-byte store per group).
-#include <cstdlib>
-
 #include <cuda_runtime.h>
 
 #include "kernels.h"
@@ -389,8 +387,6 @@ cudaError_t launch_hma(const HmaParams& p, cudaStream_t stream) {
   int64_t per = p.B > 0 ? (p.total_C + p.B - 1) / p.B : 1;
   int chunk = kChunkMax;
   if (p.B * ((per + kChunkMax - 1) / kChunkMax) < 4 * 148) chunk = kChunkMin;
-  static const char* tune = getenv("GESR_HMA_CHUNK");     // TEMPORARY tuning knob
-  if (tune != nullptr && atoi(tune) > 0) chunk = atoi(tune);
   int64_t y = (per + chunk - 1) / chunk;
   if (y < 1) y = 1;
   if (y > 65535) y = 65535;

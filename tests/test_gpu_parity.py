@@ -596,3 +596,59 @@ def test_pipelined_host_scorer_matches_score_step_exactly():
         torch.cuda.synchronize()
         assert torch.equal(h_O, O.cpu()), chunks
         assert torch.equal(h_c, counts.cpu()), chunks
+
+
+def test_hma_int64_min_in_long_and_short_lists():
+    """INT64_MIN inside a user list too long for the shared-memory tables (the
+    global-memory path) and inside short lists (the bucket path: an ordinary key there), plus
+    the two empty-slot filler values (1 and 2) as user and item IDs."""
+    dev = _cuda()
+    rng = np.random.default_rng(17)
+    imin = -(1 << 63)
+    F = 3
+    # request 0: field 0 has a 3000-long list with INT64_MIN twice; request 1: short lists
+    long_list = rng.integers(-(1 << 62), 1 << 62, size=3000).astype(np.int64)
+    long_list[[7, 2999]] = imin
+    users = [long_list, np.array([imin, 1, 2], np.int64), np.array([2, 2, 5], np.int64),
+             np.array([imin], np.int64), np.array([1, imin, 9], np.int64), np.array([], np.int64)]
+    C = [40, 30]
+    co = np.array([0, C[0], C[0] + C[1]], np.int64)
+    items = []
+    for b in range(2):
+        for t in range(C[b]):
+            for f in range(F):
+                u = users[b * F + f]
+                pick = rng.choice(np.concatenate([u, [imin, 1, 2, 3]]).astype(np.int64),
+                                  size=int(rng.integers(1, 9)))
+                items.append(pick.astype(np.int64))
+    uo = np.concatenate([[0], np.cumsum([len(x) for x in users])]).astype(np.int64)
+    io = np.concatenate([[0], np.cumsum([len(x) for x in items])]).astype(np.int64)
+    ui = np.concatenate(users).astype(np.int64)
+    ii = np.concatenate(items).astype(np.int64)
+    want = oracle.hma_count(ui, uo, ii, io, co, F)
+    c = gb.hma_count(torch.tensor(ui, device=dev), torch.tensor(uo, device=dev),
+                     torch.tensor(ii, device=dev), torch.tensor(io, device=dev),
+                     torch.tensor(co, device=dev), F)
+    torch.cuda.synchronize()
+    assert np.array_equal(c.cpu().numpy(), want)
+    assert want[:, 0].max() >= 2          # INT64_MIN matched twice in the long list
+
+
+def test_chunked_score_step_workspace_large_chunked_request():
+    """score_step(chunk=...) on one request with C >= 4608 (the split-L reserve of a
+    512-row chunk exceeds the full batch's): StepBuffers sizes the workspace for both."""
+    dev = _cuda()
+    cfg = configs.get("4").with_(C=("fixed", 5120), L=("fixed", 1024))
+    bt = inputs.make_batch(cfg, device=dev)
+    bufs = gb.StepBuffers(bt, out_dtype=torch.bfloat16)
+    O, counts = gb.score_step(bt, bufs, chunk=cfg.chunk)
+    torch.cuda.synchronize()
+    sub = inputs.select_requests(bt, [0])
+    reqs = [0]
+    K, V = oracle.kv_project(sub.U, sub.W_k, sub.W_v, cfg.H, cfg.d, act=cfg.act)
+    rows = np.arange(0, 5120, 7)           # a strided sample of the 5120 rows
+    T = sub.T[torch.as_tensor(rows)]
+    co = torch.tensor([0, len(rows)], dtype=torch.int64)
+    O_or, _ = oracle.tasa_score(T, co, sub.W_q, K, V, sub.seq_offsets, cfg.H, cfg.d, act=cfg.act)
+    _attn_tol(O[torch.as_tensor(rows, device=dev)].float().cpu().numpy(), O_or, "chunked C=5120")
+    assert reqs == [0]
