@@ -142,6 +142,10 @@ static_assert(128 * kCtrlRegs + 256 * kSoftRegs + 128 * kEpiRegs <= 128 * kThrea
 constexpr uint32_t kTS = 0;          // S: one buffer, alternately A's and B's tiles
 constexpr uint32_t kTP = 128;        // P_A at 128, P_B at 192 (bf16 pairs, 64 columns each)
 constexpr uint32_t kTO = 256;        // O of even units at 256, of odd units at 384
+// unit m's m / l hand-off from the softmax to the epilogue warps: named barrier 1 + m % 4 (ids
+// 5-12 are the MUFU tokens), 8 softmax + 4 epilogue warps
+constexpr uint32_t kMlBarBase = 1;
+constexpr uint32_t kMlBarThreads = 12 * 32;
 
 // K-major descriptor (SW128) for a [rows][128] bf16 tile stored as 2 column blocks of
 // `block_bytes` each, at K step ks (16 elements).
@@ -192,7 +196,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   // per unit % 4: the softmax may publish units m+1 and m+2 (short units need no PV of their
   // own before their last tile) while an epilogue warp still waits for unit m; four barriers
   // (and four m / l slots) keep every waiter within one phase of its barrier
-  uint64_t* ml_full = o_free + 2;                 // [4]        (each CTA; its 8 softmax warps)
+  uint64_t* ml_full = o_free + 2;                 // [4]        unused (named barriers 1-4)
   // slot u % 4 reused by unit u + 4 only after the epilogue read it (a warpgroup with no tile
   // in a run of 1-tile units would otherwise publish 4+ units ahead)
   uint64_t* ml_empty = ml_full + 4;               // [4]        (each CTA; its 4 epilogue warps)
@@ -231,7 +235,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_init(&o_free[i], 8);
     }
     for (int i = 0; i < 4; ++i) {
-      mbar_init(&ml_full[i], 8);
       mbar_init(&ml_empty[i], 4);
     }
     mbar_init(pv_done, 1);
@@ -691,7 +694,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       st_shared_f32(xb + ((g * 2 + 0) * 128 + rloc) * 4, m_loc);
       st_shared_f32(xb + ((g * 2 + 1) * 128 + rloc) * 4, l);
       __syncwarp();
-      if (lane == 0) mbar_arrive(&ml_full[m & 3]);
+      // hardware named barrier 1 + m % 4 (8 softmax + 4 epilogue warps): the epilogue warps
+      // wait for it in bar.sync, descheduled -- polling the former mbarrier spun ~390 times per
+      // unit through a suspend-hint try_wait that wakes on every barrier event of the CTA (ncu:
+      // 20 % of the kernel's issued instructions, on the softmax warps' sub-partitions)
+      named_bar_arrive(kMlBarBase + (m & 3), kMlBarThreads);
       gbase += nkv;
       ++m;
     }
@@ -742,7 +749,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         continue;
       }
-      pwait(&ml_full[m & 3], (m >> 2) & 1, CTX(13, m, 0), GESR_PAIR_EPI_SLEEP);
+      named_bar_sync(kMlBarBase + (m & 3), kMlBarThreads);
       if (sub == 0 && lane == 0) GESR_T3(5, m);
       const uint32_t xb = xch + ((m & 3) * 2 * 2 * 128) * 4;
       const float mA = ld_shared_f32(xb + (0 * 128 + rloc) * 4);
