@@ -219,7 +219,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const uint32_t buf = local & 1;
       const uint32_t aphase = (local >> 1) & 1;
       const int row0 = m_blk * 2 * kBM + static_cast<int>(rank) * kBM + static_cast<int>(sub) * 32;
-      mbar_wait_sleep(&tfull_bar[buf], aphase);
+      // one warp of each 4-warp column part polls the accumulator's mbarrier and releases the
+      // other three through hardware named barrier 1 + part (they wait descheduled): 16 warps
+      // polling a try_wait that wakes on every barrier event of the CTA cost issue slots and
+      // power for the whole mainloop of every tile
+      if (sub == 0) mbar_wait_sleep(&tfull_bar[buf], aphase);
+      named_bar_sync(1 + part, 128);
       tc_fence_after();
       const uint32_t tm_row = tmem_base + ((sub * 32) << 16) + buf * BN;
 #pragma unroll 1

@@ -69,12 +69,13 @@ def traffic(csv_path, config, tag):
     hdr = rows[0]
     ir = [i for i, h in enumerate(hdr) if h.startswith("dram__bytes_read.sum")][0]
     iw = [i for i, h in enumerate(hdr) if h.startswith("dram__bytes_write.sum")][0]
-    unit = 1e9 if "Gbyte" in hdr[ir] else (1e6 if "Mbyte" in hdr[ir] else 1.0)
+    def scale(h):
+        return 1e9 if "Gbyte" in h else (1e6 if "Mbyte" in h else (1e3 if "Kbyte" in h else 1.0))
     kern = {}
     projs = 0
     for r in rows[1:]:
         name = r[0]
-        b = (float(r[ir]) + float(r[iw])) * unit
+        b = float(r[ir]) * scale(hdr[ir]) + float(r[iw]) * scale(hdr[iw])
         if "proj_kernel" in name:
             projs += 1
             if projs == 2:
