@@ -121,11 +121,24 @@ constexpr int kKeys = 128;                       // keys per tile (S columns)
 constexpr int kThreads = 512;
 constexpr uint32_t kQBytes = 128 * kD * 2;       // 32 KB: Q tile, [2 col blocks][128 rows][64]
 constexpr uint32_t kHalfBytes = 16384;           // K half [2][64 keys][64] or V half [128][64]
-constexpr int kKStages = 4;                     // K-half ring
-constexpr int kVStages = 5;                     // V-half ring
+// Q tiles are double-buffered: unit m+1's Q is loaded while unit m's S MMAs still read unit m's
+// (a single buffer made every unit wait for its Q load after the previous unit's last S MMA:
+// ~2k cycles of drained pipeline per work item)
+#ifndef GESR_PAIR_QBUFS
+#define GESR_PAIR_QBUFS 2
+#endif
+#ifndef GESR_PAIR_KST
+#define GESR_PAIR_KST 4
+#endif
+#ifndef GESR_PAIR_VST
+#define GESR_PAIR_VST (GESR_PAIR_QBUFS == 2 ? 3 : 5)
+#endif
+constexpr int kQBufs = GESR_PAIR_QBUFS;
+constexpr int kKStages = GESR_PAIR_KST;         // K-half ring
+constexpr int kVStages = GESR_PAIR_VST;         // V-half ring
 constexpr int kStages = kKStages + kVStages;
 constexpr uint32_t kQOff = 0;
-constexpr uint32_t kRingOff = kQBytes;
+constexpr uint32_t kRingOff = kQBufs * kQBytes;
 constexpr uint32_t kStgOff = kRingOff + kStages * kHalfBytes;        // 4 x 2 KB boxes per epilogue warp
 constexpr uint32_t kBarOff = kStgOff + 4 * 8192;
 constexpr uint32_t kXchOff = kBarOff + 512;                          // [unit % 4][WG][m, l][row]
@@ -183,9 +196,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  uint64_t* q_full = reinterpret_cast<uint64_t*>(smem + kBarOff);   // leader's used
-  uint64_t* q_empty = q_full + 1;                 // each CTA
-  uint64_t* kv_full = q_empty + 1;                // [kStages]  K ring, then V ring (leader's used)
+  uint64_t* q_full = reinterpret_cast<uint64_t*>(smem + kBarOff);   // [2] leader's used
+  uint64_t* q_empty = q_full + 2;                 // [2] each CTA
+  uint64_t* kv_full = q_empty + 2;                // [kStages]  K ring, then V ring (leader's used)
   uint64_t* kv_empty = kv_full + kStages;         // [kStages]  (each CTA)
   uint64_t* s_full = kv_empty + kStages;          // [2]        (each CTA)
   uint64_t* s_free = s_full + 2;                  //            (leader; 4 warps x 2 CTAs per S)
@@ -202,7 +215,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t* ml_empty = ml_full + 4;               // [4]        (each CTA; its 4 epilogue warps)
   uint64_t* pv_done = ml_empty + 4;               //            (each CTA; one phase per PV)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 1);
-  static_assert((2 + 2 * kStages + 2 * 6 + 8 + 1) * 8 + 4 <= kXchOff - kBarOff, "barrier area");
+  static_assert((4 + 2 * kStages + 2 * 6 + 8 + 1) * 8 + 4 <= kXchOff - kBarOff, "barrier area");
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -218,8 +231,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     tma_prefetch_desc(&map_kh);
     tma_prefetch_desc(&map_vh);
     if (p.o_tma) tma_prefetch_desc(&map_o);
-    mbar_init(q_full, 1);
-    mbar_init(q_empty, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&q_full[i], 1);
+      mbar_init(&q_empty[i], 1);
+    }
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&kv_full[s], 1);
       mbar_init(&kv_empty[s], 1);
@@ -338,18 +353,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         uint32_t kph = 0;
         while (stream_next(st, tl)) {
           if (tl.t == 0) {
-            // the unit's Q: the previous unit's S MMAs must be done with the single Q buffer
-            if (tl.m > 0) pwait(q_empty, (tl.m - 1) & 1, CTX(1, tl.m, tl.t));
+            // unit m's Q buffer (m % kQBufs) must be done with unit m - kQBufs's S MMAs
+            const int qb = tl.m % kQBufs;
+            if (tl.m >= kQBufs) pwait(&q_empty[qb], ((tl.m / kQBufs) - 1) & 1, CTX(1, tl.m, tl.t));
             GESR_T3(3, tl.m);
             const int32_t qrow = static_cast<int32_t>(static_cast<int64_t>(tl.x.h) * p.total_C + tl.x.cbeg) +
                                  static_cast<int32_t>(rank) * 128;
-            if (rank == 0) mbar_arrive_expect_tx(q_full, 2 * kQBytes);
+            uint8_t* qdst = smem + kQOff + qb * kQBytes;
+            if (rank == 0) mbar_arrive_expect_tx(&q_full[qb], 2 * kQBytes);
 #if GESR_PAIR_L2HINT >= 1
-            tma_load_2d_pair_hint(smem + kQOff, &map_q, q_full, 0, qrow, pol_first);
-            tma_load_2d_pair_hint(smem + kQOff + kQBytes / 2, &map_q, q_full, 64, qrow, pol_first);
+            tma_load_2d_pair_hint(qdst, &map_q, &q_full[qb], 0, qrow, pol_first);
+            tma_load_2d_pair_hint(qdst + kQBytes / 2, &map_q, &q_full[qb], 64, qrow, pol_first);
 #else
-            tma_load_2d_pair(smem + kQOff, &map_q, q_full, 0, qrow);
-            tma_load_2d_pair(smem + kQOff + kQBytes / 2, &map_q, q_full, 64, qrow);
+            tma_load_2d_pair(qdst, &map_q, &q_full[qb], 0, qrow);
+            tma_load_2d_pair(qdst + kQBytes / 2, &map_q, &q_full[qb], 64, qrow);
 #endif
           }
           const int slot = kst;
@@ -394,7 +411,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       while (stream_next(st, tl)) {
         const int buf = tl.t & 1;
         if (tl.t == 0) {
-          pwait(q_full, tl.m & 1, CTX(4, tl.m, tl.t));   // the unit's Q tile (both CTAs)
+          // the unit's Q tile (both CTAs)
+          pwait(&q_full[tl.m % kQBufs], (tl.m / kQBufs) & 1, CTX(4, tl.m, tl.t));
           if (lane == 0) GESR_T3(0, tl.m);
         }
         // the single S buffer's previous S must have been loaded into registers (both CTAs)
@@ -409,12 +427,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (elect_one()) {
 #pragma unroll
           for (int ks = 0; ks < kD / 16; ++ks)
-            mma_ss_pair(tmem + kTS, kdesc(sQ, kQBytes / 2, ks), kdesc(kb, 8192, ks), idesc_s,
+            mma_ss_pair(tmem + kTS, kdesc(sQ + (tl.m % kQBufs) * kQBytes, kQBytes / 2, ks),
+                        kdesc(kb, 8192, ks), idesc_s,
                         ks > 0 ? 1u : 0u);
           mma_commit_pair_mc(&s_full[buf], 0x3);
           mma_commit_pair_mc(&kv_empty[slot], 0x3);
           // the unit's last S: its Q buffer may be reloaded
-          if (tl.t == tl.x.nkv - 1) mma_commit_pair_mc(q_empty, 0x3);
+          if (tl.t == tl.x.nkv - 1) mma_commit_pair_mc(&q_empty[tl.m % kQBufs], 0x3);
         }
         __syncwarp();
       }
