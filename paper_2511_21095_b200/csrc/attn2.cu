@@ -127,11 +127,13 @@ constexpr uint32_t kHalfBytes = 16384;           // K half [2][64 keys][64] or V
 #ifndef GESR_PAIR_QBUFS
 #define GESR_PAIR_QBUFS 2
 #endif
+// ring stages (measured with two Q buffers, base-clock ncu at 3h: K 4 / V 3 5.382 ms, K 3 / V 4
+// 5.372 ms; one Q buffer with K 4 / V 5: 5.449 ms)
 #ifndef GESR_PAIR_KST
-#define GESR_PAIR_KST 4
+#define GESR_PAIR_KST (GESR_PAIR_QBUFS == 2 ? 3 : 4)
 #endif
 #ifndef GESR_PAIR_VST
-#define GESR_PAIR_VST (GESR_PAIR_QBUFS == 2 ? 3 : 5)
+#define GESR_PAIR_VST (GESR_PAIR_QBUFS == 2 ? 4 : 5)
 #endif
 constexpr int kQBufs = GESR_PAIR_QBUFS;
 constexpr int kKStages = GESR_PAIR_KST;         // K-half ring
