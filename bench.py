@@ -59,6 +59,11 @@ def _args(argv=None):
                          "overlapped on three streams); 1 = copy in, score, copy out")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--gather", action="store_true", help="NCCL gather of scores after timing")
+    ap.add_argument("--hma-order", default="serial", choices=["fork", "kv", "serial"],
+                    help="where gesr_hma_count runs in the step: forked first on a side stream, "
+                         "forked after the K/V projection, or on the main stream after the "
+                         "attention (the persistent projection / attention kernels leave no room "
+                         "for HMA CTAs, so it serialises in every order: DESIGN.md s6)")
     return ap.parse_args(argv)
 
 
@@ -195,9 +200,9 @@ class GpuEngine:
     """One rank's device state: the batch of its requests, preallocated buffers, and the step
     (binding.score_step: kv_project -> tasa_score, hma_count forked on a side stream)."""
 
-    def __init__(self, device, out_dtype):
+    def __init__(self, device, out_dtype, hma_order="serial"):
         import torch
-        self.dev, self.out_dtype = device, out_dtype
+        self.dev, self.out_dtype, self.hma_order = device, out_dtype, hma_order
         self.reduce_device = device
         self.events = {}
         self.stream = torch.cuda.current_stream(device)
@@ -220,7 +225,8 @@ class GpuEngine:
 
     def step(self, record=False):
         self.gb.score_step(self.batch, self.bufs, act=self.cfg.act, chunk=self.cfg.chunk,
-                           stream=self.stream, events=self.events if record else None)
+                           stream=self.stream, hma_order=self.hma_order,
+                           events=self.events if record else None)
 
     def sync(self):
         import torch
@@ -386,7 +392,7 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     out_dtype = torch.bfloat16 if args.out_dtype == "bf16" else torch.float32
-    eng = GpuEngine(dev, out_dtype)
+    eng = GpuEngine(dev, out_dtype, args.hma_order)
     res = orchestrate(args.config, rank, world, args.steps, args.warmup, eng)
     cfg, batch, bufs = res["cfg"], eng.batch, eng.bufs
     kv_ms, tasa_ms, hma_ms = eng.call_ms("kv0", "kv1"), eng.call_ms("kv1", "t1"), \
@@ -427,7 +433,7 @@ def main():
                    "requests_per_rank": res["per_rank_requests"],
                    "H": cfg.H, "d": cfg.d, "D_in": cfg.D_in, "F": cfg.F, "L": list(cfg.L),
                    "C": list(cfg.C), "out_dtype": args.out_dtype, "act": "silu",
-                   "parallelism": f"dp{world}",
+                   "parallelism": f"dp{world}", "hma_order": args.hma_order,
                    "l2": "inputs larger than L2 (per GPU: U and HMA item ids exceed 126 MB); "
                          "no flush"},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_sus,
