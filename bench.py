@@ -7,8 +7,10 @@
 `python bench.py --gpus N` with no torchrun environment re-launches itself under
 `torch.distributed.run` with N local ranks (one process per GPU).
 
-One step = one pass of the whole hot path over one batch: gesr_kv_project -> gesr_tasa_score,
-with gesr_hma_count on a second stream joined by an event, exactly
+One step = one pass of the whole hot path over one batch: gesr_kv_project -> gesr_tasa_score ->
+gesr_hma_count on one stream (`--hma-order fork` forks HMA on a second stream joined by an event,
+SURVEY.md s8(d)'s layout: the persistent kernels leave it no SMs, so it serialises either way and
+only blurs the per-call timing), exactly
 `binding.score_step(batch, StepBuffers(batch, out_dtype=bf16))` (the configuration
 tests/test_gpu_configs.py checks against the oracle).
 

@@ -435,14 +435,16 @@ class StepBuffers:
 def score_step(batch, bufs: StepBuffers, act: int = GESR_ACT_SILU, cap: int = 0,
                chunk: int = 0, hma: bool = True, stream=None, hma_order=None, events=None):
     """One scoring step: gesr_kv_project -> gesr_tasa_score (optionally in candidate chunks
-    reusing one K/V cache), with gesr_hma_count on a second stream joined by an event.
-    hma_order (default "fork"): "fork" launches HMA first on the side stream, "kv" forks it
-    after the K/V projection is enqueued, "serial" runs it on the main stream after the
-    attention.  events: optional dict of lists; timing events "kv0", "kv1", "t1" (main stream)
+    reusing one K/V cache) and gesr_hma_count.
+    hma_order (default "serial"): "serial" runs HMA on the main stream after the attention,
+    "fork" launches it first on the side stream joined by an event, "kv" forks it after the K/V
+    projection is enqueued.  The persistent projection and attention kernels leave no room for
+    HMA CTAs, so HMA serialises in every order; "serial" keeps the per-call
+    timing events clean.  events: optional dict of lists; timing events "kv0", "kv1", "t1" (main stream)
     and "h0", "h1" (HMA's stream) are appended to it (bench.py's per-call times)."""
     cfg = batch.cfg
     main = torch.cuda.current_stream() if stream is None else stream
-    order = hma_order or "fork"
+    order = hma_order or "serial"
 
     def _ev(name, s):
         if events is not None:

@@ -1,8 +1,8 @@
 """GPU parity on the five BASELINE configs at full size, in bench.py's exact launch configuration
 (VERDICT r1 missing 2, weak 2-3), plus the ABI arguments the headline never exercises.
 
-bench.py times `binding.score_step(batch, StepBuffers(batch, out_dtype=bf16))`: HMA forked
-first on a side stream, kv_splits = 0 (auto), bf16 O through the TMA-store epilogue.  Here the
+bench.py times `binding.score_step(batch, StepBuffers(batch, out_dtype=bf16))`: HMA after the
+attention on the same stream, kv_splits = 0 (auto), bf16 O through the TMA-store epilogue.  Here the
 same two calls run on the whole config batch, then:
 
   * HMA counts are compared with the fp64/int64 oracle for EVERY candidate of configs 3, 3h and 5
