@@ -73,9 +73,6 @@ namespace {
 #ifndef GESR_PAIR_EPI_SLEEP
 #define GESR_PAIR_EPI_SLEEP 500   // ns per retry of the epilogue's unit-long waits
 #endif
-#ifndef GESR_PAIR_EARLY_M
-#define GESR_PAIR_EARLY_M 1       // publish a unit's tile-0 max halfway through its exp pass
-#endif
 #ifndef GESR_PAIR_SUM_LIMIT
 #define GESR_PAIR_SUM_LIMIT 4096.0f   // tile row sums above this take the exact-max path
 #endif
@@ -656,17 +653,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               pk[u] = pack_bf16x2(p0, p1);
             }
             tmem_st32(tP + hh * 32, pk);
-#if GESR_PAIR_EARLY_M
-            // a unit's tile 0 decides its max exactly before the pass (it never raises): publish
-            // it halfway through the pass, once the previous tile's decision has landed (that
-            // tile's pass ended at this pass's token), so the other warpgroup's first tile --
-            // which starts from this max -- can run its x pass during this exp pass instead of
-            // after it (trace: ~1k cycles of MUFU idle at every unit boundary)
-            if (hh == 0 && j == 0 && pass == 0) {
-              if (gidx > 0) (void)wait_m(gidx - 1);
-              publish_m(m_loc, gidx);
-            }
-#endif
           }
           if (trd && pass == 0) GESR_T2(3, m * 16 + j);
           tsum = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
@@ -713,12 +699,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         // this tile's decision; tile 0 of a unit first lets the previous tile's decision land
         // (one word per row, written in tile order)
-#if GESR_PAIR_EARLY_M
-        if (j > 0) publish_m(m_loc, gidx);
-#else
         if (j == 0 && gidx > 0) (void)wait_m(gidx - 1);
         publish_m(m_loc, gidx);
-#endif
         l += tsum;
         tmem_st_wait();                                  // P_g in TMEM before PV(j) reads it
         tc_fence_before();
