@@ -118,7 +118,7 @@ __device__ __forceinline__ int bucket_count(const HmaSmem& s, uint32_t tab,
 
 // The fast path's lookup with raw shared addresses (no generic-to-shared conversion per access)
 // and the bucket read predicated on the filter bit: lanes whose bit is clear issue no bucket
-// traffic and keep ~key in the compare registers (never equal to key).
+// traffic (their compare registers are undefined and the count is masked to 0).
 __device__ __forceinline__ int fast_count(uint32_t s_bkt, uint32_t s_bits, uint32_t tab,
                                           unsigned long long key) {
   const uint32_t h = key_hash(key);
@@ -128,14 +128,15 @@ __device__ __forceinline__ int fast_count(uint32_t s_bkt, uint32_t s_bits, uint3
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(word) : "r"(s_bits + ((fb >> 5) << 2)));
   const uint32_t maybe = (word >> (fb & 31u)) & 1u;
   const uint32_t addr = s_bkt + ((base + shr_clamp(h, sh)) << 5);
-  unsigned long long k0 = ~key, k1 = ~key, k2 = ~key, k3 = ~key;
+  unsigned long long k0, k1, k2, k3;     // undefined where the bit is clear: masked below
   asm volatile(
       "{\n .reg .pred p;\n setp.ne.u32 p, %4, 0;\n"
       " @p ld.shared.v2.u64 {%0, %1}, [%5];\n"
       " @p ld.shared.v2.u64 {%2, %3}, [%5+16];\n}\n"
-      : "+l"(k0), "+l"(k1), "+l"(k2), "+l"(k3)
+      : "=l"(k0), "=l"(k1), "=l"(k2), "=l"(k3)
       : "r"(maybe), "r"(addr));
-  return (k0 == key) + (k1 == key) + (k2 == key) + (k3 == key);
+  const int c = (k0 == key) + (k1 == key) + (k2 == key) + (k3 == key);
+  return maybe ? c : 0;
 }
 
 // Everything the bucket lookup does not cover: stash entries, global-memory fields.
