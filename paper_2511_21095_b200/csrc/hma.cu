@@ -7,32 +7,35 @@
 // multiplicity lookup: each item ID contributes the number of times it occurs in the user's
 // list of the same field.  Exact integer arithmetic; bit-identical to the definition.
 //
-// B200 design.  The kernel is bound by the item-ID stream (~8.5 int64 IDs per (candidate,
-// field) segment, read once); round 1's version spent ~114 instructions per ID (owner-map
-// writes, 64-bit window probes with continuation tests) and ran at 0.31 of HBM.  This one is
-// built around a per-ID instruction budget of ~40:
+// B200 design.  The kernel streams the item-ID CSR (~8.5 int64 IDs per (candidate, field)
+// segment at the headline, 1.1 GB, read once).  It is bound by instruction issue, not DRAM,
+// unless a 32-ID window costs well under ~60 warp instructions (round-2 v3: ~111, 0.34 of HBM).
+// v4 is built around that budget:
 //   grid (B, Y): CTA (b, y) owns request b and candidate chunks y, y+Y, ... of `chunk` rows.
-//   1. Table build: the request's F user lists go into per-field BUCKETED hash tables in shared
-//      memory -- 2^k buckets of 4 64-bit slots (32 bytes, two 16-byte reads), one slot per
-//      OCCURRENCE of a user ID (so a lookup counts matching slots; no count array), >= 2 buckets
-//      per ID (mean bucket load <= 1/2).  A bucket that overflows spills into a small per-CTA
-//      stash; a field whose list does not fit the pool is looked up in global memory.  An empty
-//      slot holds a FILLER key that hashes into the other half of the table (bucket index top
-//      bit flipped), so no key that hashes to this bucket can equal it: every int64 value,
-//      INT64_MIN included, is an ordinary ID and a lookup needs no emptiness test.  A 16-bit-
-//      per-bucket bitmap of the user IDs' hashes is read first (one 32-bit shared load); the
-//      bucket (two 16-byte loads, predicated) only for the ~28% of IDs whose bit is set.
+//   1. Tables.  The request's F user lists go into per-field hash tables in shared memory:
+//      16-byte buckets of TWO 64-bit slots (one 16-byte read per lookup), >= 4 buckets per ID,
+//      one slot per OCCURRENCE of a user ID (a lookup counts matching slots).  Each field's
+//      table is built by one warp, which retries with a new hash seed until no bucket
+//      overflows (expected < 2 tries at 64 IDs in 256 buckets); a field that never fits (a user
+//      ID repeated 3+ times, or a list too long for the pool) is scanned in global memory.
+//      An empty slot holds a FILLER key chosen per (field, seed) to hash into the other half of
+//      the table, so no key that hashes to a bucket can equal its fillers: every int64 value,
+//      INT64_MIN included, is an ordinary ID and a lookup needs no emptiness test.  The field's
+//      table word is also its hash multiplier (odd by construction): h = mix(key) * tab.
+//      An 8-bit-per-bucket bitmap of the user IDs' hashes is read first (one 32-bit shared
+//      load); the bucket only where the bit is set (~28% of IDs: matches + false positives).
 //   2. Scan: each warp takes 32 consecutive (candidate, field) segments (their IDs are one
 //      contiguous range of the CSR stream) and walks the range in 32-ID windows, one coalesced
 //      8-byte load per lane, 4 windows in flight.  The segment of each ID position comes from
 //      the segment starts that fall in the window: lane k contributes bit (off_k - base), one
 //      redux.sync.or forms the window's start mask, and position l's segment is the running
-//      start count plus popc(mask & lanemask_le) - 1 (no owner map in shared memory; groups
-//      with an empty segment take a binary-search path).  The segment's table word comes by
-//      shuffle from its lane; the lookup is hash -> bucket -> two 16-byte reads -> four 64-bit
-//      compares; hits go to a per-warp shared counter (predicated shared atomics), and lane k
-//      stores segment k's count (one coalesced 128-byte store per group).
+//      start count plus popc(mask & lanemask_le) - 1 (groups with an empty segment take a
+//      binary-search path).  The segment's table word comes by shuffle; a hit is a predicated
+//      shared reduction on the warp's counter of that segment, and lane k stores segment k's
+//      count (one coalesced 128-byte store per group).
 #include <cuda_runtime.h>
+
+#include <type_traits>
 
 #include "kernels.h"
 #include "ptx.cuh"
@@ -45,51 +48,52 @@ constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
 constexpr int kChunkMin = 256;             // candidates per CTA chunk (runtime: 256 or 1024)
 constexpr int kChunkMax = 1024;
-constexpr int kPoolBuckets = 2048;         // 4 slots each: 64 KB of keys per CTA
-constexpr int kStash = 256;                // overflowing user IDs (key, field)
+constexpr int kPoolBuckets = 4096;         // 16-byte buckets (2 slots): 64 KB of keys per CTA
+constexpr int kMinBuckets = 4;             // a field owns whole 32-bit bitmap words
+constexpr int kMaxSeeds = 32;              // hash seeds tried per field before going global
 constexpr int kMaxFields = 256;
 constexpr int kWinUnroll = 4;              // 32-ID windows in flight per warp
 constexpr int kFastMaxIds = 32 * 64;       // groups up to this many IDs take the fast path
-constexpr uint32_t kMulLo = 0x9E3779B1u;
+constexpr uint32_t kBitsOffset = kPoolBuckets * 16;   // byte offset of the bitmap
 constexpr uint32_t kMulHi = 0x85EBCA77u;
-__host__ __device__ constexpr uint32_t key_hash_c(unsigned long long key) {
-  return (static_cast<uint32_t>(key) * kMulLo) ^ (static_cast<uint32_t>(key >> 32) * kMulHi);
-}
-// empty-slot fillers: kFill[0] fills buckets whose index has top bit 0 (its own hash has top bit
-// 1), kFill[1] the others; tables have >= 2 buckets, so the top hash bit is the bucket's
-constexpr unsigned long long kFill0 = 1ull, kFill1 = 2ull;
-static_assert((key_hash_c(kFill0) >> 31) == 1u && (key_hash_c(kFill1) >> 31) == 0u, "fillers");
 
-// table word of a field: first bucket (bits 0-11), hash shift (12-17), flags
-constexpr uint32_t kFlagStash = 1u << 18;    // some of the field's IDs are in the stash
-constexpr uint32_t kFlagGlobal = 1u << 19;   // the field's list is scanned in global memory
+// Table word of a field (also its hash multiplier, odd by construction):
+//   bits 0-4   sh3 = 32 - log2(#buckets) - 3 (odd: tables have 4^k buckets), so
+//              h >> sh3 = 8 * bucket + 3 bitmap bits; a wrapping shift by the word itself
+//              uses exactly these bits (no decode)
+//   bits 5-14  8 * first bucket (tables start at multiples of 4 buckets)
+//   bits 15-31 hash seed (varies the multiplier between build attempts)
+// Lookup: h = mix(key) * tab; fb = (tab & 0x7fe0) + (h >> (tab & 31)) is the bitmap bit and
+// fb >> 3 the bucket; the top bit of h selects the table half (and so the filler).
+__device__ __forceinline__ uint32_t key_mix(unsigned long long key) {
+  return static_cast<uint32_t>(key) + static_cast<uint32_t>(key >> 32) * kMulHi;
+}
+__device__ __forceinline__ uint32_t filter_pos(uint32_t tab, uint32_t h) {
+  return (tab & 0x7fe0u) + __funnelshift_r(h, 0u, tab);
+}
 
 struct HmaSmem {
-  ulonglong2 bkt[kPoolBuckets][2];           // empty slots hold the bucket half's filler
-  // prefilter: 16 bits per bucket (a field's bits follow its buckets' order), bit h >> (shift-4)
-  // set for every user ID of the field; a lookup reads one 32-bit word (few bank conflicts) and
-  // touches its bucket only if the bit is set -- ~28% of IDs (matches + ~3% false positives)
-  uint32_t bits[kPoolBuckets / 2];
-  unsigned long long stash_key[kStash];
-  int stash_field[kStash];
+  ulonglong2 bkt[kPoolBuckets];              // at byte 0: empty slots hold the half's filler
+  uint32_t bits[kPoolBuckets * 8 / 32];      // at kBitsOffset: 8 bits per bucket
   uint32_t tab[kMaxFields];
+  int glob[kMaxFields];                      // 1: the field's list is scanned in global memory
   long long uoff[kMaxFields + 1];            // this request's user_offsets (F+1)
   int warp_cnt[kWarps][32];
-  int stash_n;
-  int slow_any;                              // some field has stash entries or goes global
+  alignas(16) uint32_t smask[kWarps][kFastMaxIds / 32];  // per warp: bit p set where a segment starts
+  int slow_any;                              // some field is scanned in global memory
 };
+static_assert(offsetof(HmaSmem, bits) == kBitsOffset, "bitmap offset");
 
-__device__ __forceinline__ uint32_t key_hash(unsigned long long key) { return key_hash_c(key); }
-// PTX shifts clamp the shift amount (>= 32 gives 0), unlike C++ shifts
-__device__ __forceinline__ uint32_t shr_clamp(uint32_t a, uint32_t n) {
-  uint32_t r;
-  asm("shr.b32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(n));
-  return r;
-}
-__device__ __forceinline__ uint32_t shl_clamp(uint32_t a, uint32_t n) {
-  uint32_t r;
-  asm("shl.b32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(n));
-  return r;
+// Streamed item IDs (L2-prefetched, read once).  Where pos >= n the result is left undefined:
+// the lookup masks those positions, so no move or zero-fill is spent on them.
+__device__ __forceinline__ unsigned long long ld_ids(const int64_t* ptr, int pos, int n) {
+  unsigned long long v;
+  asm volatile(
+      "{\n .reg .pred p;\n setp.lt.s32 p, %1, %2;\n"
+      " @p ld.global.nc.L1::no_allocate.u64 %0, [%3];\n}\n"
+      : "=l"(v)
+      : "r"(pos), "r"(n), "l"(ptr));
+  return v;
 }
 // Bulk L2 prefetch of the byte range [lo, hi) (rounded out to 16-byte boundaries): one
 // instruction brings a whole group's IDs toward L2 while the warp works on the group before it.
@@ -101,67 +105,68 @@ __device__ __forceinline__ void prefetch_l2_range(const void* lo, const void* hi
                  "r"(static_cast<uint32_t>(b - a))
                  : "memory");
 }
-__device__ __forceinline__ uint32_t bucket_of(uint32_t tab, unsigned long long key) {
-  return (tab & 4095u) + shr_clamp(key_hash(key), (tab >> 12) & 63u);
+
+// One lookup of the fast path: bitmap bit, then the 16-byte bucket -- lanes whose bit is clear
+// (or, in a group's tail windows, whose position is past the end) all read bucket 0 instead, a
+// broadcast that costs no extra shared-memory wavefront, and their match is masked (a predicated
+// bucket load would keep its registers live across loop iterations).  A pure function of its
+// inputs (non-volatile asm, no memory clobber: the tables are read-only during the scan), so
+// the chains of consecutive windows can overlap; returns the matching slots' count.
+template <bool kCheck>
+__device__ __forceinline__ uint32_t lookup_count(uint32_t bits0, uint32_t bkt0, uint32_t tab,
+                                                 unsigned long long key, int lane, int lim) {
+  const uint32_t h = key_mix(key) * tab;
+  const uint32_t fb = filter_pos(tab, h);
+  const uint32_t waddr = bits0 + ((fb >> 3) & ~3u);
+  const uint32_t bkt = bkt0 + ((fb << 1) & ~15u);
+  uint32_t c;
+  if (kCheck) {
+    asm("{\n .reg .pred p, q, r, v;\n .reg .b32 w, ad;\n .reg .b64 a, b;\n"
+        " ld.shared.u32 w, [%2];\n"
+        " setp.lt.s32 v, %6, %7;\n"
+        " shf.r.wrap.b32 w, w, w, %3;\n"
+        " and.b32 w, w, 1;\n"
+        " setp.ne.and.u32 p, w, 0, v;\n"
+        " selp.b32 ad, %4, %5, p;\n"
+        " ld.shared.v2.u64 {a, b}, [ad];\n"
+        " setp.eq.and.u64 q, a, %1, p;\n"
+        " setp.eq.and.u64 r, b, %1, p;\n"
+        " selp.u32 %0, 1, 0, q;\n"
+        " @r add.u32 %0, %0, 1;\n}\n"
+        : "=r"(c)
+        : "l"(key), "r"(waddr), "r"(fb), "r"(bkt), "r"(bkt0), "r"(lane), "r"(lim));
+  } else {
+    asm("{\n .reg .pred p, q, r;\n .reg .b32 w, ad;\n .reg .b64 a, b;\n"
+        " ld.shared.u32 w, [%2];\n"
+        " shf.r.wrap.b32 w, w, w, %3;\n"
+        " and.b32 w, w, 1;\n"
+        " setp.ne.u32 p, w, 0;\n"
+        " selp.b32 ad, %4, %5, p;\n"
+        " ld.shared.v2.u64 {a, b}, [ad];\n"
+        " setp.eq.and.u64 q, a, %1, p;\n"
+        " setp.eq.and.u64 r, b, %1, p;\n"
+        " selp.u32 %0, 1, 0, q;\n"
+        " @r add.u32 %0, %0, 1;\n}\n"
+        : "=r"(c)
+        : "l"(key), "r"(waddr), "r"(fb), "r"(bkt), "r"(bkt0));
+  }
+  return c;
 }
 
-__device__ __forceinline__ uint32_t filter_bit(uint32_t tab, uint32_t h) {
-  return (tab & 4095u) * 16u + shr_clamp(h, ((tab >> 12) & 63u) - 4u);
-}
-__device__ __forceinline__ int bucket_count(const HmaSmem& s, uint32_t tab,
-                                            unsigned long long key) {
-  const uint32_t b = bucket_of(tab, key);
-  const ulonglong2 a = s.bkt[b][0];
-  const ulonglong2 c = s.bkt[b][1];
-  return (a.x == key) + (a.y == key) + (c.x == key) + (c.y == key);
-}
-
-// The fast path's lookup with raw shared addresses (no generic-to-shared conversion per access)
-// and the bucket read predicated on the filter bit: lanes whose bit is clear issue no bucket
-// traffic (their compare registers are undefined and the count is masked to 0).
-__device__ __forceinline__ int fast_count(uint32_t s_bkt, uint32_t s_bits, uint32_t tab,
-                                          unsigned long long key) {
-  const uint32_t h = key_hash(key);
-  const uint32_t base = tab & 4095u, sh = (tab >> 12) & 63u;
-  const uint32_t fb = base * 16u + shr_clamp(h, sh - 4u);
-  uint32_t word;
-  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(word) : "r"(s_bits + ((fb >> 5) << 2)));
-  const uint32_t maybe = (word >> (fb & 31u)) & 1u;
-  const uint32_t addr = s_bkt + ((base + shr_clamp(h, sh)) << 5);
-  unsigned long long k0, k1, k2, k3;     // undefined where the bit is clear: masked below
-  asm volatile(
-      "{\n .reg .pred p;\n setp.ne.u32 p, %4, 0;\n"
-      " @p ld.shared.v2.u64 {%0, %1}, [%5];\n"
-      " @p ld.shared.v2.u64 {%2, %3}, [%5+16];\n}\n"
-      : "=l"(k0), "=l"(k1), "=l"(k2), "=l"(k3)
-      : "r"(maybe), "r"(addr));
-  const int c = (k0 == key) + (k1 == key) + (k2 == key) + (k3 == key);
-  return maybe ? c : 0;
-}
-
-// Everything the bucket lookup does not cover: stash entries, global-memory fields.
-__device__ __noinline__ int slow_count(const HmaSmem& s, const HmaParams& p, int f, uint32_t tab,
+// Any field, any key (generic path): global scan for fields that did not fit, else the table.
+__device__ __noinline__ int lookup_any(const HmaSmem& s, const HmaParams& p, int f,
                                        unsigned long long key) {
-  if (tab & kFlagGlobal) {     // (INT64_MIN included: the scan compares raw values)
+  if (s.glob[f]) {
     int c = 0;
     for (long long i = s.uoff[f]; i < s.uoff[f + 1]; ++i)
       c += (static_cast<unsigned long long>(__ldg(p.user_ids + i)) == key) ? 1 : 0;
     return c;
   }
-  const uint32_t fb = filter_bit(tab, key_hash(key));
-  int c = ((s.bits[fb >> 5] >> (fb & 31u)) & 1u) ? bucket_count(s, tab, key) : 0;
-  if (tab & kFlagStash) {
-    const int n = s.stash_n < kStash ? s.stash_n : kStash;
-    for (int i = 0; i < n; ++i) c += (s.stash_field[i] == f && s.stash_key[i] == key) ? 1 : 0;
-  }
-  return c;
-}
-
-__device__ __forceinline__ int lookup_any(const HmaSmem& s, const HmaParams& p, int f,
-                                          uint32_t tab, unsigned long long key) {
-  if (tab & (kFlagStash | kFlagGlobal)) return slow_count(s, p, f, tab, key);
-  const uint32_t fb = filter_bit(tab, key_hash(key));
-  return ((s.bits[fb >> 5] >> (fb & 31u)) & 1u) ? bucket_count(s, tab, key) : 0;
+  const uint32_t tab = s.tab[f];
+  const uint32_t fb = filter_pos(tab, key_mix(key) * tab);
+  if (((s.bits[fb >> 5] >> (fb & 31u)) & 1u) == 0u) return 0;   // (global fields: tab unused)
+  const ulonglong2 b = s.bkt[fb >> 3];
+  return (b.x == key) + (b.y == key);
 }
 
 __global__ void __launch_bounds__(kThreads, 2)
@@ -178,165 +183,228 @@ __global__ void __launch_bounds__(kThreads, 2)
   const int lane = tid & 31;
   const int warp = tid >> 5;
 
-  // ---- 1. per-field bucketed tables of the request's user lists
+  // ---- 1. per-field tables of the request's user lists
   for (int f = tid; f <= F; f += kThreads) s.uoff[f] = p.user_offsets[static_cast<int64_t>(b) * F + f];
-  __syncthreads();
-  if (tid == 0) {
-    int used = 0;
-    s.slow_any = 0;
-    s.stash_n = 0;
-    for (int f = 0; f < F; ++f) {
-      const long long n = s.uoff[f + 1] - s.uoff[f];
-      // 2^k >= 2 buckets, >= 2 per ID (mean load <= 2 of 4 slots) when the pool allows, else
-      // >= 1 per ID
-      int nb = 2, shift = 31;
-      while (nb < 2 * n && nb < kPoolBuckets) { nb <<= 1; --shift; }
-      if (used + nb > kPoolBuckets && nb > n && nb > 2) { nb >>= 1; ++shift; }
-      if (nb >= n && used + nb <= kPoolBuckets) {
-        s.tab[f] = static_cast<uint32_t>(used) | (static_cast<uint32_t>(shift & 63) << 12);
-        used += nb;
-      } else {
-        s.tab[f] = kFlagGlobal;
-        s.slow_any = 1;
-      }
-    }
-  }
-  for (int i = tid; i < kPoolBuckets / 2; i += kThreads) s.bits[i] = 0u;
   for (int i = tid; i < kWarps * 32; i += kThreads) (&s.warp_cnt[0][0])[i] = 0;
   __syncthreads();
-  // empty slots: each field's lower half of buckets gets kFill0, the upper half kFill1
-  for (int f = 0; f < F; ++f) {
-    const uint32_t t = s.tab[f];
-    if (t & kFlagGlobal) continue;
-    const int base = static_cast<int>(t & 4095u);
-    const int nb = 1 << (32 - static_cast<int>((t >> 12) & 63u));
-    for (int i = tid; i < nb; i += kThreads) {
-      const unsigned long long e = (i < nb / 2) ? kFill0 : kFill1;
-      s.bkt[base + i][0] = make_ulonglong2(e, e);
-      s.bkt[base + i][1] = make_ulonglong2(e, e);
+  if (tid == 0) {   // bucket ranges: 4^k >= max(4, 4n) buckets, >= n if the pool is short
+    int used = 0;
+    s.slow_any = 0;
+    for (int f = 0; f < F; ++f) {
+      const long long n = s.uoff[f + 1] - s.uoff[f];
+      int nb = kMinBuckets, lg = 2;
+      while (nb < 4 * n && nb < kPoolBuckets) { nb <<= 2; lg += 2; }
+      while (used + nb > kPoolBuckets && nb >= 4 * n && nb > kMinBuckets) { nb >>= 2; lg -= 2; }
+      if (used + nb <= kPoolBuckets && nb >= n) {
+        s.tab[f] = (static_cast<uint32_t>(used) << 3) | static_cast<uint32_t>(32 - lg - 3);
+        s.glob[f] = 0;
+        used += nb;
+      } else {
+        s.tab[f] = 1u;
+        s.glob[f] = 1;
+        s.slow_any = 1;
+      }
     }
   }
   __syncthreads();
-  {
-    const long long u0 = s.uoff[0];
-    const long long un = s.uoff[F] - u0;
-    for (long long i = tid; i < un; i += kThreads) {
-      const long long pos = u0 + i;
-      int lo = 0, hi = F - 1;                 // owning field: last f with uoff[f] <= pos
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (s.uoff[mid] <= pos) lo = mid; else hi = mid - 1;
+  // one warp per field: fill, insert, retry with the next seed while a bucket overflows
+  for (int f = warp; f < F; f += kWarps) {
+    if (s.glob[f]) continue;
+    const uint32_t t0 = s.tab[f];
+    const int base = static_cast<int>((t0 & 0x7fe0u) >> 3);
+    const int lg = 32 - 3 - static_cast<int>(t0 & 31u);
+    const int nb = 1 << lg;
+    const long long u0 = s.uoff[f];
+    const int n = static_cast<int>(s.uoff[f + 1] - u0);
+    bool ok = false;
+    for (int seed = 0; seed < kMaxSeeds && !ok; ++seed) {
+      const uint32_t t = (t0 & 0x7fffu) | (static_cast<uint32_t>(seed + 1) * 0x2f5a3u) << 15;
+      // fillers: the smallest values whose hash lands in the upper (fill_lo) / lower (fill_hi)
+      // half; lower-half buckets hold fill_lo, upper-half buckets fill_hi
+      const uint32_t top = (key_mix(static_cast<unsigned long long>(lane + 1)) * t) >> 31;
+      const uint32_t up = __ballot_sync(0xffffffffu, top != 0u);
+      const uint32_t lo = ~up;
+      if (up == 0u || lo == 0u) continue;
+      const unsigned long long fill_lo = static_cast<unsigned long long>(__ffs(up));
+      const unsigned long long fill_hi = static_cast<unsigned long long>(__ffs(lo));
+      for (int i = lane; i < nb; i += 32) {
+        const unsigned long long e = (i < nb / 2) ? fill_lo : fill_hi;
+        s.bkt[base + i] = make_ulonglong2(e, e);
       }
-      const int f = lo;
-      const uint32_t t = s.tab[f];
-      if (t & kFlagGlobal) continue;
-      const unsigned long long key = static_cast<unsigned long long>(__ldg(p.user_ids + pos));
-      const uint32_t fb = filter_bit(t, key_hash(key));
-      atomicOr(&s.bits[fb >> 5], 1u << (fb & 31u));
-      const uint32_t bk = bucket_of(t, key);
-      unsigned long long* slots = reinterpret_cast<unsigned long long*>(&s.bkt[bk][0]);
-      const unsigned long long fill = (bk - (t & 4095u)) < (1u << (31 - ((t >> 12) & 63u))) ? kFill0 : kFill1;
-      bool placed = false;
-      for (int q = 0; q < 4 && !placed; ++q)
-        placed = atomicCAS(slots + q, fill, key) == fill;
-      if (!placed) {
-        const int at = atomicAdd(&s.stash_n, 1);
-        if (at < kStash) {
-          s.stash_key[at] = key;
-          s.stash_field[at] = f;
-          atomicOr(&s.tab[f], kFlagStash);
-        } else {
-          atomicOr(&s.tab[f], kFlagGlobal);    // stash full: this field scans global memory
-        }
-        s.slow_any = 1;
+      for (int i = lane; i < nb / 4; i += 32) s.bits[base / 4 + i] = 0u;
+      __syncwarp();
+      bool over = false;
+      for (int i = lane; i < n; i += 32) {
+        const unsigned long long key = static_cast<unsigned long long>(__ldg(p.user_ids + u0 + i));
+        const uint32_t h = key_mix(key) * t;
+        const uint32_t fb = filter_pos(t, h);
+        const unsigned long long fill = (h >> 31) ? fill_hi : fill_lo;
+        unsigned long long* slots = reinterpret_cast<unsigned long long*>(&s.bkt[fb >> 3]);
+        if (atomicCAS(slots, fill, key) != fill && atomicCAS(slots + 1, fill, key) != fill)
+          over = true;
+        atomicOr(&s.bits[fb >> 5], 1u << (fb & 31u));
       }
+      ok = !__any_sync(0xffffffffu, over);
+      if (ok && lane == 0) s.tab[f] = t;
+      __syncwarp();
+    }
+    if (!ok && lane == 0) {
+      s.glob[f] = 1;
+      s.slow_any = 1;
     }
   }
   __syncthreads();
   const bool slow_any = s.slow_any != 0;
-  const uint32_t s_bkt = smem_u32(&s.bkt[0][0]);
-  const uint32_t s_bits = smem_u32(&s.bits[0]);
 
-  // ---- 2. the item-ID stream, 32 segments per warp step
+  // ---- 2. the item-ID stream, 32 segments per warp step.  Positions are 32-bit offsets from
+  // the chunk's first item ID (a chunk holding 2^31 IDs or more takes a 64-bit lane-per-segment
+  // loop instead).
+  const uint32_t cnt_base = smem_u32(&s.warp_cnt[warp][0]);
+  const uint32_t le_mask = 0xffffffffu >> (31 - lane);               // lanemask_le
   for (int64_t c0 = first; c0 < ce; c0 += static_cast<int64_t>(gridDim.y) * chunk) {
     const int64_t c1 = (c0 + chunk < ce) ? c0 + chunk : ce;
-    const int64_t seg_begin = c0 * F, seg_end = c1 * F;
-    int64_t g = seg_begin + static_cast<int64_t>(warp) * 32;
-    constexpr int64_t kStep = static_cast<int64_t>(kWarps) * 32;
-    int64_t off_cur = 0, end_cur = 0, off_nxt = 0, end_nxt = 0;
-    auto fetch_offsets = [&](int64_t gg, int64_t& o, int64_t& e) {
-      if (gg < seg_end) {
-        const int ns = (seg_end - gg) < 32 ? static_cast<int>(seg_end - gg) : 32;
-        o = __ldg(p.item_offsets + gg + (lane < ns ? lane : ns));
-        e = __ldg(p.item_offsets + gg + ns);
+    const int64_t seg_begin = c0 * F;
+    const int nseg_chunk = static_cast<int>((c1 - c0) * F);
+    const int64_t id0 = __ldg(p.item_offsets + seg_begin);
+    if (__ldg(p.item_offsets + seg_begin + nseg_chunk) - id0 >= (1ll << 31)) {
+      // a chunk of 2^31 or more item IDs: one lane per segment, 64-bit offsets (slow, exact)
+      for (int q = tid; q < nseg_chunk; q += kThreads) {
+        const int64_t seg = seg_begin + q;
+        int c = 0;
+        for (int64_t i = __ldg(p.item_offsets + seg); i < __ldg(p.item_offsets + seg + 1); ++i)
+          c += lookup_any(s, p, q % F, static_cast<unsigned long long>(__ldg(p.item_ids + i)));
+        if (p.cap > 0 && c > p.cap) c = p.cap;
+        p.counts[seg] = c;
+        if (p.E != nullptr) {
+          const int64_t rowE = static_cast<int64_t>(c) + static_cast<int64_t>(q % F) * (p.cap + 1);
+          for (int k = 0; k < p.dh_chunks; ++k) p.emb[seg * p.dh_chunks + k] = __ldg(p.E + rowE * p.dh_chunks + k);
+        }
+      }
+      continue;
+    }
+    const bool fast_chunk = !slow_any;
+    const int64_t* idp = p.item_ids + id0;
+    // low 32 bits of the chunk's offsets: exact relative positions when the chunk is < 2^31 IDs
+    const uint32_t* offp = reinterpret_cast<const uint32_t*>(p.item_offsets + seg_begin);
+    const uint32_t id0lo = static_cast<uint32_t>(id0);
+    int gl = warp * 32;                                               // group's first segment
+    constexpr int kStep = kWarps * 32;
+    // lane k: start of segment gg+k (lanes past the group: its end); e: the group's end.  Raw
+    // low words: the chunk base is subtracted where the values are used, a group later, so no
+    // instruction waits on these loads early
+    auto fetch = [&](int gg, uint32_t& o, uint32_t& e) {
+      if (gg < nseg_chunk) {
+        const int ns = nseg_chunk - gg < 32 ? nseg_chunk - gg : 32;
+        o = __ldg(offp + 2 * (gg + (lane < ns ? lane : ns)));
+        e = __ldg(offp + 2 * (gg + ns));
+      } else {
+        o = id0lo;
+        e = id0lo;
       }
     };
-    fetch_offsets(g, off_cur, end_cur);
-    fetch_offsets(g + kStep, off_nxt, end_nxt);
+    uint32_t off_cur, end_cur, off_nxt, end_nxt;
+    fetch(gl, off_cur, end_cur);
+    fetch(gl + kStep, off_nxt, end_nxt);
     {
-      const int64_t s0 = __shfl_sync(0xffffffffu, off_cur, 0);
-      if (lane == 0 && g < seg_end) prefetch_l2_range(p.item_ids + s0, p.item_ids + end_cur);
+      const int s0 = static_cast<int>(__shfl_sync(0xffffffffu, off_cur, 0) - id0lo);
+      if (lane == 0 && gl < nseg_chunk) prefetch_l2_range(idp + s0, idp + static_cast<int>(end_cur - id0lo));
     }
-    int my_f = static_cast<int>((g - seg_begin + lane) % F);   // seg_begin % F == 0
-    const int f_step = (kWarps * 32) % F;
-    for (; g < seg_end; g += kStep) {
-      const int nseg = (seg_end - g) < 32 ? static_cast<int>(seg_end - g) : 32;
-      // lane k holds the start offset of segment g+k; lanes nseg..31 hold the end offset
-      const int64_t my_off = off_cur;
-      const int64_t end = end_cur;
-      // the next group's IDs toward L2 (its offsets arrived during this group's predecessor),
-      // then the offsets two groups ahead into registers
-      {
-        const int64_t s1 = __shfl_sync(0xffffffffu, off_nxt, 0);
-        if (lane == 0 && g + kStep < seg_end) prefetch_l2_range(p.item_ids + s1, p.item_ids + end_nxt);
-      }
+    int my_f = (gl + lane) % F;                                       // seg_begin % F == 0
+    const int f_step = kStep % F;
+    unsigned long long kk[kWinUnroll];     // IDs of the next kWinUnroll windows, in flight
+    for (; gl < nseg_chunk; gl += kStep) {
+      const int nseg = nseg_chunk - gl < 32 ? nseg_chunk - gl : 32;
+      const int my_off = static_cast<int>(off_cur - id0lo);
+      const int end = static_cast<int>(end_cur - id0lo);
+      const int start = __shfl_sync(0xffffffffu, my_off, 0);
+      const int nstart = static_cast<int>(__shfl_sync(0xffffffffu, off_nxt, 0) - id0lo);
+      const int n_next = static_cast<int>(end_nxt - id0lo) - nstart;   // 0 past the chunk
+      if (lane == 0 && n_next > 0) prefetch_l2_range(idp + nstart, idp + nstart + n_next);
       off_cur = off_nxt;
       end_cur = end_nxt;
-      fetch_offsets(g + 2 * kStep, off_nxt, end_nxt);
-      const int64_t start = __shfl_sync(0xffffffffu, my_off, 0);
-      const int64_t nxt = __shfl_down_sync(0xffffffffu, my_off, 1);
-      const int64_t my_end = lane + 1 < nseg ? nxt : end;
-      const int n_ids = static_cast<int>(end - start);
+      fetch(gl + 2 * kStep, off_nxt, end_nxt);
+      const int nxt = __shfl_down_sync(0xffffffffu, my_off, 1);
+      const int my_end = lane + 1 < nseg ? nxt : end;
+      const int n_ids = end - start;
       const uint32_t my_tab = s.tab[my_f];
-      const int64_t* ids = p.item_ids + start;
+      const int64_t* idl = idp + start + lane;
       const bool empty_seg = lane < nseg && my_end == my_off;
-      if (!__any_sync(0xffffffffu, empty_seg) && n_ids <= kFastMaxIds) {
-        // fast path: every segment of the group non-empty, so segment starts are distinct
-        const uint32_t rel = static_cast<uint32_t>(my_off - start);   // lanes >= nseg: n_ids
-        const uint32_t le_mask = 0xffffffffu >> (31 - lane);         // lanemask_le
-        int cum = 0;
-        for (int base = 0; base < n_ids; base += kWinUnroll * 32) {
-          unsigned long long kk[kWinUnroll];
 #pragma unroll
-          for (int u = 0; u < kWinUnroll; ++u) {
-            const int pos = base + u * 32 + lane;
-            kk[u] = pos < n_ids ? static_cast<unsigned long long>(__ldg(ids + pos)) : 0ull;
-          }
+      for (int u = 0; u < kWinUnroll; ++u) kk[u] = ld_ids(idl + u * 32, u * 32 + lane, n_ids);
+      if (fast_chunk && !__any_sync(0xffffffffu, empty_seg) && n_ids <= kFastMaxIds) {
+        // fast path: every segment of the group non-empty (segment starts distinct), every
+        // field in a shared-memory table.  The group's segment starts go into a bitmask over its
+        // ID positions; a window's word of it gives each position's segment by one popc.
+        uint32_t* smask = s.smask[warp];
+        const int nwin = (n_ids + 31) >> 5;                            // <= 64
+        if (lane < nwin) smask[lane] = 0u;
+        if (lane + 32 < nwin) smask[lane + 32] = 0u;
+        __syncwarp();
+        if (lane < nseg) {
+          const uint32_t rel = static_cast<uint32_t>(my_off - start);
+          atomicOr(&smask[rel >> 5], 1u << (rel & 31u));
+        }
+        __syncwarp();
+        int cum_m1 = -1;                                             // starts so far, minus 1
+        // shared address of the start mask, passed through a volatile asm after the barrier:
+        // the (non-volatile) window loads below cannot be hoisted above it
+        uint32_t sm_addr;
+        asm volatile("mov.u32 %0, %1;" : "=r"(sm_addr) : "r"(smem_u32(smask)));
+        const uint32_t bits0 = smem_u32(&s.bits[0]), bkt0 = smem_u32(&s.bkt[0]);
+        auto window = [&](unsigned long long key, int w, auto check) {
+          uint32_t starts;
+          asm("ld.shared.u32 %0, [%1];" : "=r"(starts) : "r"(sm_addr + 4u * w));
+          const int seg = cum_m1 + __popc(starts & le_mask);
+          cum_m1 += __popc(starts);
+          const uint32_t t = __shfl_sync(0xffffffffu, my_tab, seg);
+          const uint32_t c = lookup_count<decltype(check)::value>(bits0, bkt0, t, key, lane,
+                                                                  n_ids - w * 32);
+          asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %1, 0;\n"
+                       " @q red.shared.add.u32 [%0], %1;\n}\n"
+                       ::"r"(cnt_base + 4u * static_cast<uint32_t>(seg)), "r"(c) : "memory");
+        };
+        // two full windows with every shared-memory read before either counter update, so the
+        // two lookup chains overlap
+        auto window2 = [&](unsigned long long k0, unsigned long long k1, int w) {
+          uint32_t st0, st1;
+          asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(st0), "=r"(st1) : "r"(sm_addr + 4u * w));
+          const int seg0 = cum_m1 + __popc(st0 & le_mask);
+          cum_m1 += __popc(st0);
+          const int seg1 = cum_m1 + __popc(st1 & le_mask);
+          cum_m1 += __popc(st1);
+          const uint32_t t0 = __shfl_sync(0xffffffffu, my_tab, seg0);
+          const uint32_t t1 = __shfl_sync(0xffffffffu, my_tab, seg1);
+          const uint32_t c0 = lookup_count<false>(bits0, bkt0, t0, k0, lane, 0);
+          const uint32_t c1 = lookup_count<false>(bits0, bkt0, t1, k1, lane, 0);
+          asm volatile("{\n .reg .pred q, r;\n setp.ne.u32 q, %2, 0;\n setp.ne.u32 r, %3, 0;\n"
+                       " @q red.shared.add.u32 [%0], %2;\n"
+                       " @r red.shared.add.u32 [%1], %3;\n}\n"
+                       ::"r"(cnt_base + 4u * static_cast<uint32_t>(seg0)),
+                         "r"(cnt_base + 4u * static_cast<uint32_t>(seg1)), "r"(c0), "r"(c1)
+                       : "memory");
+        };
+        // full windows, kWinUnroll at a time, each refilling its key register kWinUnroll
+        // windows ahead; then the last <= kWinUnroll windows (already loaded) with the check
+        const int nfull = n_ids >> 5;
+        int w0 = 0;
+        for (; w0 + kWinUnroll <= nfull; w0 += kWinUnroll) {
 #pragma unroll
-          for (int u = 0; u < kWinUnroll; ++u) {
-            const int wbase = base + u * 32;
-            if (wbase >= n_ids) break;                                  // warp-uniform
-            // shl by >= 32 gives 0: only starts inside the window set a bit
-            const uint32_t bit = lane < nseg ? shl_clamp(1u, rel - static_cast<uint32_t>(wbase)) : 0u;
-            const uint32_t starts = __reduce_or_sync(0xffffffffu, bit);
-            const int seg = cum + __popc(starts & le_mask) - 1;
-            cum += __popc(starts);
-            const unsigned long long key = kk[u];
-            const bool valid = wbase + lane < n_ids;
-            const uint32_t t = __shfl_sync(0xffffffffu, my_tab, seg & 31);
-            int c;
-            if (!slow_any) {
-              c = fast_count(s_bkt, s_bits, t, key);
-            } else {
-              const int f = __shfl_sync(0xffffffffu, my_f, seg & 31);
-              c = valid ? lookup_any(s, p, f, t, key) : 0;
-            }
-            if (valid && c != 0) atomicAdd(&s.warp_cnt[warp][seg], c);
+          for (int u = 0; u < kWinUnroll; u += 2) {
+            window2(kk[u], kk[u + 1], w0 + u);
+            const int nw = (w0 + kWinUnroll + u) * 32;
+            kk[u] = ld_ids(idl + nw, nw + lane, n_ids);
+            kk[u + 1] = ld_ids(idl + nw + 32, nw + 32 + lane, n_ids);
           }
         }
+#pragma unroll
+        for (int u = 0; u < kWinUnroll; ++u) {
+          if (w0 + u < nwin) window(kk[u], w0 + u, std::true_type{});
+        }
       } else {
-        // a group with empty segments (or very long lists): owning segment by binary search
-        const int rel = static_cast<int>(my_off - start);
+        // generic path (a group with empty segments, very long lists, or a CTA with a field
+        // in global memory): owning segment by binary search over the segment starts
+        const int rel = my_off - start;
+        const int64_t* ids = idp + start;
         for (int base = 0; base < n_ids; base += 32) {
           const int pos = base + lane;
           const bool ok = pos < n_ids;
@@ -348,9 +416,8 @@ __global__ void __launch_bounds__(kThreads, 2)
             if (o <= pos) k += step;
           }
           const int f = __shfl_sync(0xffffffffu, my_f, k);
-          const uint32_t t = __shfl_sync(0xffffffffu, my_tab, k);
           if (ok) {
-            const int c = lookup_any(s, p, f, t, key);
+            const int c = lookup_any(s, p, f, key);
             if (c != 0) atomicAdd(&s.warp_cnt[warp][k], c);
           }
         }
@@ -359,13 +426,14 @@ __global__ void __launch_bounds__(kThreads, 2)
       if (lane < nseg) {
         int c = s.warp_cnt[warp][lane];
         if (p.cap > 0 && c > p.cap) c = p.cap;
-        p.counts[g + lane] = c;
+        const int64_t seg = seg_begin + gl + lane;
+        p.counts[seg] = c;
         if (p.E != nullptr) {
           // offset embedding (stride cap + 1: DESIGN.md R14): segment
-          // g + lane = (candidate t, field f) owns out[t][f D_h, (f + 1) D_h) -- contiguous
+          // seg = (candidate t, field f) owns out[t][f D_h, (f + 1) D_h) -- contiguous
           const int64_t rowE = static_cast<int64_t>(c) + static_cast<int64_t>(my_f) * (p.cap + 1);
           const uint4* src = p.E + rowE * p.dh_chunks;
-          uint4* dst = p.emb + (g + lane) * p.dh_chunks;
+          uint4* dst = p.emb + seg * p.dh_chunks;
           for (int q = 0; q < p.dh_chunks; ++q) dst[q] = __ldg(src + q);
         }
       }
