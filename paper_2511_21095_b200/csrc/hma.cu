@@ -26,7 +26,7 @@
 //      load); the bucket only where the bit is set (~28% of IDs: matches + false positives).
 //   2. Scan: each warp takes 32 consecutive (candidate, field) segments (their IDs are one
 //      contiguous range of the CSR stream) and walks the range in 32-ID windows, one coalesced
-//      8-byte load per lane, 4 windows in flight.  The segment of each ID position comes from
+//      8-byte load per lane, 4 windows in flight, the next group's range prefetched to L2.  The segment of each ID position comes from
 //      the segment starts that fall in the window: lane k contributes bit (off_k - base), one
 //      redux.sync.or forms the window's start mask, and position l's segment is the running
 //      start count plus popc(mask & lanemask_le) - 1 (groups with an empty segment take a
@@ -95,17 +95,6 @@ __device__ __forceinline__ unsigned long long ld_ids(const int64_t* ptr, int pos
       : "r"(pos), "r"(n), "l"(ptr));
   return v;
 }
-// Bulk L2 prefetch of the byte range [lo, hi) (rounded out to 16-byte boundaries): one
-// instruction brings a whole group's IDs toward L2 while the warp works on the group before it.
-__device__ __forceinline__ void prefetch_l2_range(const void* lo, const void* hi) {
-  const uintptr_t a = reinterpret_cast<uintptr_t>(lo) & ~uintptr_t(15);
-  const uintptr_t b = (reinterpret_cast<uintptr_t>(hi) + 15) & ~uintptr_t(15);
-  if (b > a)
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a),
-                 "r"(static_cast<uint32_t>(b - a))
-                 : "memory");
-}
-
 // One lookup of the fast path: bitmap bit, then the 16-byte bucket -- lanes whose bit is clear
 // (or, in a group's tail windows, whose position is past the end) all read bucket 0 instead, a
 // broadcast that costs no extra shared-memory wavefront, and their match is masked (a predicated
@@ -187,6 +176,15 @@ __global__ void __launch_bounds__(kThreads, 2)
   for (int f = tid; f <= F; f += kThreads) s.uoff[f] = p.user_offsets[static_cast<int64_t>(b) * F + f];
   for (int i = tid; i < kWarps * 32; i += kThreads) (&s.warp_cnt[0][0])[i] = 0;
   __syncthreads();
+  // the first 64 IDs of this warp's first field are loaded now, while thread 0 lays out the
+  // tables (their latency would otherwise sit between the two barriers and the build)
+  unsigned long long pre0 = 0ull, pre1 = 0ull;
+  if (warp < F) {
+    const long long u0 = s.uoff[warp];
+    const long long n = s.uoff[warp + 1] - u0;
+    if (lane < n) pre0 = static_cast<unsigned long long>(__ldg(p.user_ids + u0 + lane));
+    if (lane + 32 < n) pre1 = static_cast<unsigned long long>(__ldg(p.user_ids + u0 + lane + 32));
+  }
   if (tid == 0) {   // bucket ranges: 4^k >= max(4, 4n) buckets, >= n if the pool is short
     int used = 0;
     s.slow_any = 0;
@@ -235,7 +233,9 @@ __global__ void __launch_bounds__(kThreads, 2)
       __syncwarp();
       bool over = false;
       for (int i = lane; i < n; i += 32) {
-        const unsigned long long key = static_cast<unsigned long long>(__ldg(p.user_ids + u0 + i));
+        const unsigned long long key =
+            f == warp && i < 64 ? (i < 32 ? pre0 : pre1)
+                                : static_cast<unsigned long long>(__ldg(p.user_ids + u0 + i));
         const uint32_t h = key_mix(key) * t;
         const uint32_t fb = filter_pos(t, h);
         const unsigned long long fill = (h >> 31) ? fill_hi : fill_lo;
@@ -307,7 +307,9 @@ __global__ void __launch_bounds__(kThreads, 2)
     fetch(gl + kStep, off_nxt, end_nxt);
     {
       const int s0 = static_cast<int>(__shfl_sync(0xffffffffu, off_cur, 0) - id0lo);
-      if (lane == 0 && gl < nseg_chunk) prefetch_l2_range(idp + s0, idp + static_cast<int>(end_cur - id0lo));
+      const uintptr_t a0 = (reinterpret_cast<uintptr_t>(idp + s0) & ~uintptr_t(127)) + 128u * lane;
+      if (gl < nseg_chunk && a0 < reinterpret_cast<uintptr_t>(idp + static_cast<int>(end_cur - id0lo)))
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(a0));
     }
     int my_f = (gl + lane) % F;                                       // seg_begin % F == 0
     const int f_step = kStep % F;
@@ -319,7 +321,11 @@ __global__ void __launch_bounds__(kThreads, 2)
       const int start = __shfl_sync(0xffffffffu, my_off, 0);
       const int nstart = static_cast<int>(__shfl_sync(0xffffffffu, off_nxt, 0) - id0lo);
       const int n_next = static_cast<int>(end_nxt - id0lo) - nstart;   // 0 past the chunk
-      if (lane == 0 && n_next > 0) prefetch_l2_range(idp + nstart, idp + nstart + n_next);
+      {   // the next group's IDs toward L2, one 128-byte line per lane (a group is ~17 lines)
+        const uintptr_t a0 = (reinterpret_cast<uintptr_t>(idp + nstart) & ~uintptr_t(127)) + 128u * lane;
+        if (n_next > 0 && a0 < reinterpret_cast<uintptr_t>(idp + nstart + n_next))
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(a0));
+      }
       off_cur = off_nxt;
       end_cur = end_nxt;
       fetch(gl + 2 * kStep, off_nxt, end_nxt);
@@ -384,7 +390,8 @@ __global__ void __launch_bounds__(kThreads, 2)
                        : "memory");
         };
         // full windows, kWinUnroll at a time, each refilling its key register kWinUnroll
-        // windows ahead; then the last <= kWinUnroll windows (already loaded) with the check
+        // windows ahead; then the last <= kWinUnroll windows (already loaded), the partial one
+        // with the position check
         const int nfull = n_ids >> 5;
         int w0 = 0;
         for (; w0 + kWinUnroll <= nfull; w0 += kWinUnroll) {
@@ -396,9 +403,21 @@ __global__ void __launch_bounds__(kThreads, 2)
             kk[u + 1] = ld_ids(idl + nw + 32, nw + 32 + lane, n_ids);
           }
         }
+        // the last <= kWinUnroll windows, two at a time while two remain full
+        if (w0 + 2 <= nfull) {
+          window2(kk[0], kk[1], w0);
+          if (w0 + 3 < nwin) {
+            // (w0 + 4 > nfull here: window w0 + 2 is full, w0 + 3 the partial one)
+            window(kk[2], w0 + 2, std::false_type{});
+            window(kk[3], w0 + 3, std::true_type{});
+          } else if (w0 + 2 < nwin) {
+            window(kk[2], w0 + 2, std::true_type{});
+          }
+        } else {
 #pragma unroll
-        for (int u = 0; u < kWinUnroll; ++u) {
-          if (w0 + u < nwin) window(kk[u], w0 + u, std::true_type{});
+          for (int u = 0; u < kWinUnroll; ++u) {
+            if (w0 + u < nwin) window(kk[u], w0 + u, std::true_type{});
+          }
         }
       } else {
         // generic path (a group with empty segments, very long lists, or a CTA with a field
