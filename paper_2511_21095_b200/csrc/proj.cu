@@ -36,6 +36,18 @@
 
 namespace gesr {
 
+#ifdef GESR_PROJ_PROF
+// Wait profile (scripts/proj_prof.py; -DGESR_PROJ_PROF builds only).  Per CTA: [0] producer
+// cycles waiting for a free stage, [1] MMA issuer cycles waiting for a loaded stage, [2] MMA
+// cycles waiting for a free accumulator, [3] MMA warp total, [4] epilogue warp 4 cycles
+// waiting for a full accumulator.
+__device__ unsigned long long g_projprof[296][8];
+#define PROF_ADD(i, t) atomicAdd(&g_projprof[blockIdx.x][i], static_cast<unsigned long long>(clock64() - (t)))
+#define PROF_WAIT(i, call) do { const long long _tw = clock64(); call; if (lane_id() == 0) PROF_ADD(i, _tw); } while (0)
+#else
+#define PROF_WAIT(i, call) call
+#endif
+
 namespace {
 
 constexpr int kBM = 128;             // rows per CTA; a pair tile is 256 rows
@@ -153,7 +165,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int nb = ((n0 < p.n_split) ? n0 : n0 - p.n_split) + static_cast<int>(rank) * (BN / 2);
         const int ma = m_blk * 2 * kBM + static_cast<int>(rank) * kBM;
         for (int kb = 0; kb < num_kb; ++kb) {
-          mbar_wait_sleep(&empty_bar[stage], phase ^ 1);
+          PROF_WAIT(0, mbar_wait_sleep(&empty_bar[stage], phase ^ 1));
           uint8_t* sa = smem + stage * S::kStageBytes;
           uint8_t* sb = sa + kABytes;
           if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], 2 * S::kStageBytes);
@@ -170,14 +182,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
+#ifdef GESR_PROJ_PROF
+      const long long tstart = clock64();
+#endif
       for (; local < my_tiles; ++local) {
         const uint32_t buf = local & 1;
         const uint32_t aphase = (local >> 1) & 1;
-        mbar_wait_sleep(&tempty_bar[buf], aphase ^ 1);
+        PROF_WAIT(2, mbar_wait_sleep(&tempty_bar[buf], aphase ^ 1));
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + buf * BN;
         for (int kb = 0; kb < num_kb; ++kb) {
-          mbar_wait_sleep(&full_bar[stage], phase);
+          PROF_WAIT(1, mbar_wait_sleep(&full_bar[stage], phase));
           tc_fence_after();
           if (elect_one()) {
             const uint32_t sa = smem_u32(smem + stage * S::kStageBytes);
@@ -195,6 +210,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if (++stage == S::kStages) { stage = 0; phase ^= 1; }
         }
       }
+#ifdef GESR_PROJ_PROF
+      if (lane_id() == 0) PROF_ADD(3, tstart);
+#endif
     }
   } else if (warp >= 4) {
     // ---------------- epilogue (both CTAs): TMEM -> regs -> act -> bf16 -> smem -> TMA store
@@ -223,8 +241,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       // other three through hardware named barrier 1 + part (they wait descheduled): 16 warps
       // polling a try_wait that wakes on every barrier event of the CTA cost issue slots and
       // power for the whole mainloop of every tile
+#ifdef GESR_PROJ_PROF
+      const long long tw4 = clock64();
+#endif
       if (sub == 0) mbar_wait_sleep(&tfull_bar[buf], aphase);
       named_bar_sync(1 + part, 128);
+#ifdef GESR_PROJ_PROF
+      if (warp == 4 && lane == 0) PROF_ADD(4, tw4);
+#endif
       tc_fence_after();
       const uint32_t tm_row = tmem_base + ((sub * 32) << 16) + buf * BN;
 #pragma unroll 1
@@ -325,6 +349,17 @@ cudaError_t launch_bn(const CUtensorMap& ma, const CUtensorMap& mb0, const CUten
 }
 
 }  // namespace
+
+#ifdef GESR_PROJ_PROF
+extern "C" int gesr_debug_projprof_copy(void* host, int reset) {
+  int r = static_cast<int>(cudaMemcpyFromSymbol(host, g_projprof, sizeof(g_projprof)));
+  if (reset) {
+    static unsigned long long zero[296][8];
+    cudaMemcpyToSymbol(g_projprof, zero, sizeof(zero));
+  }
+  return r;
+}
+#endif
 
 int proj_pick_bn(int N) {
   if (N % 256 == 0) return 256;
