@@ -2,7 +2,7 @@
 # configs 3h and 5, and one ncu --set full capture of the current kernel.  TAG names the outputs.
 TAG=${TAG:-hma}
 mkdir -p gpurun_out
-[ "${TESTS:-1}" = 1 ] && timeout 900 python -m pytest tests -m gpu -q -x -p no:cacheprovider -k "hma or HMA or configs" > gpurun_out/hma_tests_$TAG.log 2>&1; echo exit=$? >> gpurun_out/hma_tests_$TAG.log
+[ "${TESTS:-1}" = 1 ] && timeout 900 python -m pytest tests -m gpu -q -x -p no:cacheprovider -k "hma or HMA or configs or smoke" > gpurun_out/hma_tests_$TAG.log 2>&1; echo exit=$? >> gpurun_out/hma_tests_$TAG.log
 for cfg in 3h 5; do for rep in 1 2 3; do for f in build/ab/*.so; do
   GESR_LIB=$PWD/$f timeout 120 python scripts/hma_ab.py $cfg >> gpurun_out/hma_ab_$TAG.txt 2>&1
 done; done; done
