@@ -293,8 +293,12 @@ __global__ void __launch_bounds__(kThreads, 2)
     // low words: the chunk base is subtracted where the values are used, a group later, so no
     // instruction waits on these loads early
     auto fetch = [&](int gg, uint32_t& o, uint32_t& e) {
-      if (gg < nseg_chunk) {
-        const int ns = nseg_chunk - gg < 32 ? nseg_chunk - gg : 32;
+      if (gg + 32 <= nseg_chunk) {         // a full group (all but the chunk's last)
+        const uint32_t* q = offp + 2 * gg;
+        o = __ldg(q + 2 * lane);
+        e = __ldg(q + 64);
+      } else if (gg < nseg_chunk) {
+        const int ns = nseg_chunk - gg;
         o = __ldg(offp + 2 * (gg + (lane < ns ? lane : ns)));
         e = __ldg(offp + 2 * (gg + ns));
       } else {
@@ -302,6 +306,9 @@ __global__ void __launch_bounds__(kThreads, 2)
         e = id0lo;
       }
     };
+    int32_t* const cnt_out = p.counts + seg_begin;
+    const int cap = p.cap;
+    const bool emb = p.E != nullptr;
     uint32_t off_cur, end_cur, off_nxt, end_nxt;
     fetch(gl, off_cur, end_cur);
     fetch(gl + kStep, off_nxt, end_nxt);
@@ -444,13 +451,13 @@ __global__ void __launch_bounds__(kThreads, 2)
       __syncwarp();
       if (lane < nseg) {
         int c = s.warp_cnt[warp][lane];
-        if (p.cap > 0 && c > p.cap) c = p.cap;
-        const int64_t seg = seg_begin + gl + lane;
-        p.counts[seg] = c;
-        if (p.E != nullptr) {
+        if (cap > 0 && c > cap) c = cap;
+        cnt_out[gl + lane] = c;
+        if (emb) {
+          const int64_t seg = seg_begin + gl + lane;
           // offset embedding (stride cap + 1: DESIGN.md R14): segment
           // seg = (candidate t, field f) owns out[t][f D_h, (f + 1) D_h) -- contiguous
-          const int64_t rowE = static_cast<int64_t>(c) + static_cast<int64_t>(my_f) * (p.cap + 1);
+          const int64_t rowE = static_cast<int64_t>(c) + static_cast<int64_t>(my_f) * (cap + 1);
           const uint4* src = p.E + rowE * p.dh_chunks;
           uint4* dst = p.emb + seg * p.dh_chunks;
           for (int q = 0; q < p.dh_chunks; ++q) dst[q] = __ldg(src + q);
