@@ -5,7 +5,7 @@ NVFLAGS   := -O3 -std=c++17 -lineinfo $(ARCH) -Xcompiler -fPIC -Iinclude
 PKG       := paper_2511_21095_b200
 SRC       := $(PKG)/csrc
 BUILD     := build
-OBJS      := $(BUILD)/proj.o $(BUILD)/attn.o $(BUILD)/attn2.o $(BUILD)/hma.o $(BUILD)/stu.o $(BUILD)/nro.o $(BUILD)/debug.o $(BUILD)/capi.o
+OBJS      := $(BUILD)/proj.o $(BUILD)/attn.o $(BUILD)/attn2.o $(BUILD)/hma.o $(BUILD)/stu.o $(BUILD)/nro.o $(BUILD)/debug.o $(BUILD)/hostpath.o $(BUILD)/capi.o
 HDRS      := $(SRC)/kernels.h $(SRC)/ptx.cuh include/gesr.h
 
 all: $(PKG)/libgesr.so oracle/liboracle.so

@@ -467,8 +467,8 @@ def main():
                           pin(batch.cand_offsets), pin(batch.U), pin(batch.T), batch.W_q.cpu(),
                           batch.W_k.cpu(), batch.W_v.cpu(), pin(batch.user_ids),
                           pin(batch.user_offsets), pin(batch.item_ids), pin(batch.item_offsets))
-        scorer = gb.PipelinedHostScorer(hb, n_chunks=args.e2e_chunks, out_dtype=bufs.O.dtype,
-                                        act=cfg.act, device=dev)
+        scorer = gb.HostPlan(hb, n_chunks=args.e2e_chunks, out_dtype=bufs.O.dtype, act=cfg.act,
+                             device=dev)
         h_O = torch.empty(bufs.O.shape, dtype=bufs.O.dtype).pin_memory()
         h_counts = torch.empty(bufs.counts.shape, dtype=torch.int32).pin_memory()
         h2d = scorer.h2d_bytes
@@ -493,9 +493,10 @@ def main():
             e_ms = float(t.item())
         line["e2e"] = {"value": res["cands_per_step"] * n_e2e / (e_ms / 1e3), "unit": UNIT,
                        "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": n_e2e,
-                       "chunks": len(scorer.chunks),
+                       "chunks": min(args.e2e_chunks, batch.B),
+                       "api": "gesr_score_host (C ABI, host buffers in and out)",
                        "pipeline": "request chunks: H2D of chunk i+1 and D2H of chunk i-1 "
-                                   "overlap the kernels of chunk i (PipelinedHostScorer)"}
+                                   "overlap the kernels of chunk i (csrc/hostpath.cu)"}
 
     # ---------------------------------------------------------------- optional score gather
     if args.gather and world > 1:

@@ -329,6 +329,47 @@ gesr_status gesr_hma_count_embed(const int64_t* user_ids, const int64_t* user_of
                                  const void* E, int32_t D_h, void* emb,
                                  void* stream);
 
+/* ---------------------------------------------------------------- end to end from HOST memory
+ * One whole scoring step -- gesr_kv_project -> gesr_tasa_score -> gesr_hma_count, exactly the
+ * device-resident step -- for a batch whose inputs are in HOST memory, with the results written
+ * to HOST memory (the e2e path of a serving host).  The requests are cut into n_chunks
+ * contiguous ranges (chunk k = requests [B*k/n_chunks, B*(k+1)/n_chunks)); per chunk the inputs
+ * are copied host->device, the three calls run on `stream`, and O / counts are copied
+ * device->host, pipelined over two device buffer sets and two internal copy streams (while the
+ * kernels of chunk k run, chunk k+1 is copied in and chunk k-1 out).  Each chunk's offsets are
+ * rebased on the device (the caller's host buffers are never written).  Results are
+ * bit-identical to the device-resident step (rows depend only on their own request: reading R9;
+ * split-L auto as in gesr_tasa_score).
+ *
+ * gesr_host_chunk_maxima -- per-chunk maxima {requests, history rows, candidate rows, user IDs,
+ *   item IDs} of that cut (host offsets; the sizes gesr_host_plan_create needs).
+ * gesr_host_plan_create -- allocates the two device buffer sets (sized by `maxima`), their
+ *   workspaces, events and the copy streams on the current device; *plan is owned by the caller
+ *   and released with gesr_host_plan_destroy (after all work using it has completed).
+ * gesr_score_host -- enqueues one step:
+ *   U [total_L, D_in] / T [total_C, D_in] bf16, HOST (pinned for asynchronous DMA; pageable
+ *   memory works but the copies then serialise with the host); seq_offsets / cand_offsets
+ *   [B+1], user_offsets [B*F+1], item_offsets [total_C*F+1], user_ids, item_ids: int64 HOST;
+ *   W_q [H*d, D_in], W_k / W_v [H*d, D_in] bf16 DEVICE (model weights, resident); act as
+ *   gesr_kv_project; scale 1/sqrt(d); cap as gesr_hma_count; O [total_C, H*d] (o_dtype of the
+ *   plan) and counts int32 [total_C, F]: HOST (written).  Asynchronous: ordered after prior work
+ *   on `stream`; O / counts are complete when `stream` reaches the point after this call.
+ *   GESR_ERR_WORKSPACE if a chunk exceeds the plan's maxima. */
+typedef struct gesr_host_plan gesr_host_plan;
+gesr_status gesr_host_chunk_maxima(const int64_t* seq_offsets, const int64_t* cand_offsets,
+                                   const int64_t* user_offsets, const int64_t* item_offsets,
+                                   int64_t B, int32_t F, int32_t n_chunks, int64_t* maxima);
+gesr_status gesr_host_plan_create(const int64_t* maxima, int32_t D_in, int32_t H, int32_t d,
+                                  int32_t F, int32_t o_dtype, gesr_host_plan** plan);
+gesr_status gesr_host_plan_destroy(gesr_host_plan* plan);
+gesr_status gesr_score_host(gesr_host_plan* plan, int32_t n_chunks,
+                            const void* U, const int64_t* seq_offsets,
+                            const void* T, const int64_t* cand_offsets, int64_t B,
+                            const void* W_q, const void* W_k, const void* W_v, int32_t act,
+                            const int64_t* user_ids, const int64_t* user_offsets,
+                            const int64_t* item_ids, const int64_t* item_offsets, int32_t cap,
+                            void* O, int32_t* counts, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -96,6 +96,11 @@ def lib():
                                                    _i32, _vp, ctypes.c_size_t, _vp]),
             ("gesr_layer_norm", ctypes.c_int, [_vp, _i64, _i32, _vp, _vp, ctypes.c_float, _vp, _vp]),
             ("gesr_stu_output", ctypes.c_int, [_vp, _i64, _i32, _vp, _i32, _vp, _vp, _vp, _vp, ctypes.c_float, _vp, _vp, _vp, _i32, _i32, _i32, _vp, _vp, ctypes.c_size_t, _vp]),
+            ("gesr_host_chunk_maxima", ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _i32, _i32, _vp]),
+            ("gesr_host_plan_create", ctypes.c_int, [_vp, _i32, _i32, _i32, _i32, _i32, _vp]),
+            ("gesr_host_plan_destroy", ctypes.c_int, [_vp]),
+            ("gesr_score_host", ctypes.c_int, [_vp, _i32, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp,
+                                               _i32, _vp, _vp, _vp, _vp, _i32, _vp, _vp, _vp]),
     ):
         if not hasattr(L, name) and os.environ.get("GESR_LIB"):
             continue
@@ -498,9 +503,9 @@ def score_step(batch, bufs: StepBuffers, act: int = GESR_ACT_SILU, cap: int = 0,
 
 
 def plan_chunks(hb, n_chunks: int, pin: bool = False) -> list:
-    """Cut a host batch into n_chunks contiguous request ranges (host logic of
-    PipelinedHostScorer): per chunk the row / candidate ranges, the sliced inputs and the
-    offsets rebased to the chunk (seq, cand, user [b*F], item [t*F] offsets start at 0)."""
+    """Cut a host batch into n_chunks contiguous request ranges -- the cut gesr_score_host makes
+    (a Python mirror used by the tests): per chunk the row / candidate ranges, the sliced inputs
+    and the offsets rebased to the chunk (seq, cand, user [b*F], item [t*F] offsets at 0)."""
     F, B = hb.cfg.F, hb.B
     so, co = hb.seq_offsets.tolist(), hb.cand_offsets.tolist()
     uo, io = hb.user_offsets, hb.item_offsets
@@ -520,94 +525,64 @@ def plan_chunks(hb, n_chunks: int, pin: bool = False) -> list:
     return chunks
 
 
-class PipelinedHostScorer:
-    """End-to-end scoring of a HOST-resident batch (pinned CPU tensors) through the C ABI, with
-    the requests cut into chunks pipelined over three CUDA streams: while the kernels of chunk i
-    run, chunk i+1's inputs are copied host->device and chunk i-1's outputs device->host (the
-    copy engines of both directions and the SMs all busy).  Two device buffer sets alternate
-    between chunks.  Per chunk: gesr_kv_project -> gesr_tasa_score -> gesr_hma_count on the
-    compute stream.  Results land in the caller's pinned host O / counts.
+def host_chunk_maxima(hb, n_chunks: int) -> list:
+    """gesr_host_chunk_maxima: per-chunk maxima {requests, history rows, candidate rows, user
+    IDs, item IDs} of the contiguous request cut gesr_score_host uses (host offsets)."""
+    m = (ctypes.c_int64 * 5)()
+    _check(lib().gesr_host_chunk_maxima(_ptr(hb.seq_offsets), _ptr(hb.cand_offsets),
+                                        _ptr(hb.user_offsets), _ptr(hb.item_offsets), hb.B,
+                                        hb.cfg.F, n_chunks, m))
+    return list(m)
 
-        sc = PipelinedHostScorer(host_batch, n_chunks=8, out_dtype=torch.bfloat16)
-        sc.run(h_O, h_counts)      # enqueues everything; torch.cuda.synchronize() to wait
+
+class HostPlan:
+    """End-to-end scoring of a HOST-resident batch through the C ABI: `gesr_score_host` (the
+    native runtime in csrc/hostpath.cu) cuts the requests into n_chunks, pipelines each chunk's
+    host->device copies, gesr_kv_project -> gesr_tasa_score -> gesr_hma_count and the
+    device->host copies of O / counts over two device buffer sets and two copy streams.  This
+    class only marshals: it creates the plan (device buffers sized by gesr_host_chunk_maxima)
+    and passes host pointers.
+
+        plan = HostPlan(host_batch, n_chunks=16, out_dtype=torch.bfloat16)
+        plan.run(h_O, h_counts)      # enqueued on the current stream; synchronize to read
     """
 
-    def __init__(self, hb, n_chunks: int = 8, out_dtype=torch.bfloat16, act: int = GESR_ACT_SILU,
-                 cap: int = 0, device=None):
+    def __init__(self, hb, n_chunks: int = 16, out_dtype=torch.bfloat16,
+                 act: int = GESR_ACT_SILU, cap: int = 0, device=None):
         cfg = hb.cfg
-        self.cfg, self.act, self.cap, self.out_dtype = cfg, act, cap, out_dtype
+        self.hb, self.cfg, self.act, self.cap, self.n_chunks = hb, cfg, act, cap, n_chunks
+        self.out_dtype = out_dtype
         dev = torch.device("cuda") if device is None else torch.device(device)
-        F = cfg.F
-        self.chunks = plan_chunks(hb, n_chunks, pin=True)
-        mx = lambda k: max(c[k].shape[0] for c in self.chunks)   # noqa: E731
-        H, d = cfg.H, cfg.d
-        mB, mL, mC = max(c["B"] for c in self.chunks), mx("h_U"), mx("h_T")
-        ws = max(tasa_workspace_bytes(c["B"], c["h_T"].shape[0], H, d, 0) for c in self.chunks)
-        self.sets = []
-        for _ in range(2):
-            self.sets.append(dict(
-                so=torch.empty(mB + 1, dtype=torch.int64, device=dev),
-                co=torch.empty(mB + 1, dtype=torch.int64, device=dev),
-                uo=torch.empty(mB * F + 1, dtype=torch.int64, device=dev),
-                io=torch.empty(mC * F + 1, dtype=torch.int64, device=dev),
-                U=torch.empty(mL, cfg.D_in, dtype=torch.bfloat16, device=dev),
-                T=torch.empty(mC, cfg.D_in, dtype=torch.bfloat16, device=dev),
-                ui=torch.empty(mx("h_ui"), dtype=torch.int64, device=dev),
-                ii=torch.empty(mx("h_ii"), dtype=torch.int64, device=dev),
-                K=torch.empty(H * mL * d, dtype=torch.bfloat16, device=dev),   # [H, nL, d] views
-                V=torch.empty(H * mL * d, dtype=torch.bfloat16, device=dev),
-                O=torch.empty(mC, H * d, dtype=out_dtype, device=dev),
-                counts=torch.empty(mC, F, dtype=torch.int32, device=dev),
-                ws=torch.empty(max(ws, 256), dtype=torch.uint8, device=dev),
-                h2d=torch.cuda.Event(), done=torch.cuda.Event(), free=torch.cuda.Event()))
-        self.W = (hb.W_q.to(dev), hb.W_k.to(dev), hb.W_v.to(dev))
-        self.s_in = torch.cuda.Stream(device=dev)
-        self.s_out = torch.cuda.Stream(device=dev)
-        self.h2d_bytes = sum(c[k].numel() * c[k].element_size() for c in self.chunks
-                             for k in ("h_so", "h_co", "h_uo", "h_io", "h_U", "h_T", "h_ui", "h_ii"))
+        self.W = tuple(w.to(dev).contiguous() for w in (hb.W_q, hb.W_k, hb.W_v))
+        maxima = (ctypes.c_int64 * 5)(*host_chunk_maxima(hb, n_chunks))
+        self._plan = ctypes.c_void_p()
+        with torch.cuda.device(dev):
+            _check(lib().gesr_host_plan_create(
+                maxima, cfg.D_in, cfg.H, cfg.d, cfg.F,
+                GESR_OUT_BF16 if out_dtype == torch.bfloat16 else GESR_OUT_F32,
+                ctypes.byref(self._plan)))
+        self.h2d_bytes = sum(t.numel() * t.element_size() for t in (
+            hb.U, hb.T, hb.user_ids, hb.item_ids)) + 8 * (
+            2 * (hb.B + n_chunks) + hb.B * cfg.F + n_chunks + hb.total_C * cfg.F + n_chunks)
 
     def run(self, h_O, h_counts, stream=None):
-        """Enqueue one end-to-end pass; h_O [total_C, H*d] and h_counts [total_C, F] pinned."""
-        cfg, (W_q, W_k, W_v) = self.cfg, self.W
-        main = torch.cuda.current_stream() if stream is None else stream
-        start = torch.cuda.Event()
-        start.record(main)
-        self.s_in.wait_event(start)
-        self.s_out.wait_event(start)
-        for i, c in enumerate(self.chunks):
-            s = self.sets[i % 2]
-            nL, nC = c["h_U"].shape[0], c["h_T"].shape[0]
-            nu, ni = c["h_ui"].shape[0], c["h_ii"].shape[0]
-            with torch.cuda.stream(self.s_in):
-                if i >= 2:
-                    self.s_in.wait_event(s["free"])
-                for dst, src, n in (("so", "h_so", c["B"] + 1), ("co", "h_co", c["B"] + 1),
-                                    ("uo", "h_uo", c["B"] * cfg.F + 1),
-                                    ("io", "h_io", nC * cfg.F + 1), ("U", "h_U", nL),
-                                    ("T", "h_T", nC), ("ui", "h_ui", nu), ("ii", "h_ii", ni)):
-                    s[dst][:n].copy_(c[src], non_blocking=True)
-                s["h2d"].record(self.s_in)
-            main.wait_event(s["h2d"])
-            U, T = s["U"][:nL], s["T"][:nC]
-            K = s["K"][:cfg.H * nL * cfg.d].view(cfg.H, nL, cfg.d)
-            V = s["V"][:cfg.H * nL * cfg.d].view(cfg.H, nL, cfg.d)
-            if nL > 0:
-                kv_project(U, W_k, W_v, cfg.H, cfg.d, self.act, K_cache=K, V_cache=V,
-                           stream=main)
-            O, cnt = s["O"][:nC], s["counts"][:nC]
-            tasa_score(T, s["co"][:c["B"] + 1], W_q, K, V,
-                       s["so"][:c["B"] + 1], cfg.H, cfg.d, self.act, O=O, want_lse=False,
-                       workspace=s["ws"], stream=main)
-            hma_count(s["ui"][:max(nu, 1)], s["uo"][:c["B"] * cfg.F + 1], s["ii"][:max(ni, 1)],
-                      s["io"][:nC * cfg.F + 1], s["co"][:c["B"] + 1], cfg.F, self.cap,
-                      counts=cnt, stream=main)
-            s["done"].record(main)
-            with torch.cuda.stream(self.s_out):
-                self.s_out.wait_event(s["done"])
-                c0, c1 = c["cands"]
-                h_O[c0:c1].copy_(O, non_blocking=True)
-                h_counts[c0:c1].copy_(cnt, non_blocking=True)
-                s["free"].record(self.s_out)
-        end = torch.cuda.Event()
-        end.record(self.s_out)
-        main.wait_event(end)
+        """Enqueue one end-to-end step; h_O [total_C, H*d] and h_counts [total_C, F] on the host
+        (pinned for asynchronous copies); inputs from the host batch given at construction."""
+        hb = self.hb
+        W_q, W_k, W_v = self.W
+        _check(lib().gesr_score_host(
+            self._plan, self.n_chunks, _ptr(hb.U), _ptr(hb.seq_offsets), _ptr(hb.T),
+            _ptr(hb.cand_offsets), hb.B, _ptr(W_q), _ptr(W_k), _ptr(W_v), self.act,
+            _ptr(hb.user_ids), _ptr(hb.user_offsets), _ptr(hb.item_ids), _ptr(hb.item_offsets),
+            self.cap, _ptr(h_O), _ptr(h_counts), _stream(stream)))
+
+    def close(self):
+        if getattr(self, "_plan", None) and self._plan.value:
+            lib().gesr_host_plan_destroy(self._plan)
+            self._plan = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -74,6 +74,14 @@ gesr_status cuda_fail(cudaError_t e, const char* where) {
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
+}  // namespace
+
+// error reporting for the other host translation units (hostpath.cu): the same thread-local
+// message gesr_last_error() returns
+gesr_status gesr_internal_fail(gesr_status s, const char* msg) { return fail(s, "%s", msg); }
+
+namespace {
+
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,

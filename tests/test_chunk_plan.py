@@ -39,3 +39,32 @@ def test_chunks_partition_and_rebase(n):
                 s0, s1 = int(c["h_io"][t * F + f]), int(c["h_io"][t * F + f + 1])
                 g0, g1 = io[(c0 + t) * F + f], io[(c0 + t) * F + f + 1]
                 assert np.array_equal(c["h_ii"][s0:s1].numpy(), hb.item_ids[g0:g1].numpy())
+
+
+@pytest.mark.parametrize("n", [1, 3, 7, 64])
+def test_native_chunk_maxima_match_the_cut(n):
+    """gesr_host_chunk_maxima (host code in libgesr.so, no GPU needed) reports the maxima of
+    exactly the cut plan_chunks mirrors: {requests, history rows, candidate rows, user IDs,
+    item IDs} per chunk."""
+    cfg = configs.get("2").with_(B=23)
+    hb = inputs.make_batch(cfg)
+    ch = gb.plan_chunks(hb, n)
+    want = [max(c["B"] for c in ch), max(c["h_U"].shape[0] for c in ch),
+            max(c["h_T"].shape[0] for c in ch), max(c["h_ui"].numel() for c in ch),
+            max(c["h_ii"].numel() for c in ch)]
+    assert gb.host_chunk_maxima(hb, n) == want
+
+
+def test_score_host_argument_errors():
+    """gesr_score_host / gesr_host_plan_create reject bad arguments before touching a device."""
+    import ctypes
+    L = gb.lib()
+    m = (ctypes.c_int64 * 5)(1, 1, 1, 1, 1)
+    plan = ctypes.c_void_p()
+    assert L.gesr_host_plan_create(m, 0, 1, 32, 1, 1, ctypes.byref(plan)) == gb.GESR_ERR_INVALID_ARG
+    bad = (ctypes.c_int64 * 5)(1, -1, 1, 1, 1)
+    assert L.gesr_host_plan_create(bad, 32, 1, 32, 1, 1, ctypes.byref(plan)) == gb.GESR_ERR_INVALID_ARG
+    assert L.gesr_score_host(None, 1, None, None, None, None, 1, None, None, None, 1, None, None,
+                             None, None, 0, None, None, None) == gb.GESR_ERR_INVALID_ARG
+    assert "null plan" in L.gesr_last_error().decode()
+    assert L.gesr_host_plan_destroy(None) == gb.GESR_OK

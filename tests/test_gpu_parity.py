@@ -573,10 +573,11 @@ def test_hma_structured_ids(pattern):
     assert want.sum() > 0
 
 
-def test_pipelined_host_scorer_matches_score_step_exactly():
-    """End-to-end path (host-resident pinned inputs, request chunks pipelined over H2D / kernel /
-    D2H streams) gives the same O and counts as score_step on device-resident inputs: rows are
-    independent of batch composition (reading R9; no split-L at these sizes)."""
+def test_score_host_matches_score_step_exactly():
+    """End-to-end path through the C ABI (gesr_score_host: host-resident pinned inputs, request
+    chunks pipelined over H2D / kernels / D2H inside the library) gives the same O and counts as
+    score_step on device-resident inputs: rows are independent of batch composition (reading
+    R9; no split-L at these sizes).  Also pageable host buffers and a single chunk."""
     dev = _cuda()
     cfg = configs.get("2")
     bt = inputs.make_batch(cfg)
@@ -587,15 +588,16 @@ def test_pipelined_host_scorer_matches_score_step_exactly():
     hb = inputs.Batch(cfg, bt.requests, pin(bt.seq_offsets), pin(bt.cand_offsets), pin(bt.U),
                       pin(bt.T), bt.W_q, bt.W_k, bt.W_v, pin(bt.user_ids), pin(bt.user_offsets),
                       pin(bt.item_ids), pin(bt.item_offsets))
-    for chunks in (1, 3, 5):
-        sc = gb.PipelinedHostScorer(hb, n_chunks=chunks, out_dtype=torch.bfloat16, device=dev)
+    for batch, chunks in ((hb, 1), (hb, 3), (hb, 5), (bt, 4)):
+        plan = gb.HostPlan(batch, n_chunks=chunks, out_dtype=torch.bfloat16, device=dev)
         h_O = torch.zeros(O.shape, dtype=O.dtype).pin_memory()
         h_c = torch.zeros(counts.shape, dtype=torch.int32).pin_memory()
-        sc.run(h_O, h_c)
-        sc.run(h_O, h_c)           # twice: buffer sets reused across passes
+        plan.run(h_O, h_c)
+        plan.run(h_O, h_c)         # twice: buffer sets reused across passes
         torch.cuda.synchronize()
         assert torch.equal(h_O, O.cpu()), chunks
         assert torch.equal(h_c, counts.cpu()), chunks
+        plan.close()
 
 
 def test_hma_int64_min_in_long_and_short_lists():
