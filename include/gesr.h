@@ -354,7 +354,10 @@ gesr_status gesr_hma_count_embed(const int64_t* user_ids, const int64_t* user_of
  *   gesr_kv_project; scale 1/sqrt(d); cap as gesr_hma_count; O [total_C, H*d] (o_dtype of the
  *   plan) and counts int32 [total_C, F]: HOST (written).  Asynchronous: ordered after prior work
  *   on `stream`; O / counts are complete when `stream` reaches the point after this call.
- *   GESR_ERR_WORKSPACE if a chunk exceeds the plan's maxima. */
+ *   GESR_ERR_WORKSPACE if a chunk exceeds the plan's maxima (checked before anything is
+ *   enqueued).  A plan serves one call at a time (not thread-safe) on the device it was created
+ *   on; after an error returned mid-way (GESR_ERR_CUDA), synchronise the device before reusing or
+ *   destroying the plan. */
 typedef struct gesr_host_plan gesr_host_plan;
 gesr_status gesr_host_chunk_maxima(const int64_t* seq_offsets, const int64_t* cand_offsets,
                                    const int64_t* user_offsets, const int64_t* item_offsets,

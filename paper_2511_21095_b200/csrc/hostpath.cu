@@ -194,6 +194,10 @@ gesr_status gesr_score_host(gesr_host_plan* plan, int32_t n_chunks,
       !O || !counts)
     return hfail(GESR_ERR_INVALID_ARG, "gesr_score_host: null required pointer");
   if (B < 0) return hfail(GESR_ERR_INVALID_ARG, "gesr_score_host: B < 0");
+  int dev = -1;
+  cudaGetDevice(&dev);
+  if (dev != plan->dev)
+    return hfail(GESR_ERR_INVALID_ARG, "gesr_score_host: the plan belongs to another device");
   const int32_t F = plan->F, H = plan->H, d = plan->d, D_in = plan->D_in;
   const int32_t n = clamp_chunks(B, n_chunks);
   // every chunk must fit the plan (checked before anything is enqueued)
