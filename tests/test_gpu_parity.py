@@ -600,6 +600,37 @@ def test_score_host_matches_score_step_exactly():
         plan.close()
 
 
+@pytest.mark.parametrize("B,L,C", [(20, ("uniform", 0, 5), ("uniform", 0, 300)),
+                                   (16, ("uniform", 0, 400), ("uniform", 0, 4))])
+def test_score_host_jagged_d128_fp32_cap(B, L, C):
+    """gesr_score_host on a jagged d=128 batch (the CTA-pair kernel) with empty histories (first
+    case: 3 of 20) or empty candidate lists (second: 2 of 16), fp32 output and an HMA cap:
+    bit-identical to the device-resident calls with the same options."""
+    dev = _cuda()
+    cfg = configs.get("3").with_(B=B, L=L, C=C, F=4)
+    bt = inputs.make_batch(cfg)
+    g = bt.to(dev)
+    K, V = gb.kv_project(g.U, g.W_k, g.W_v, cfg.H, cfg.d, cfg.act)
+    O, _ = gb.tasa_score(g.T, g.cand_offsets, g.W_q, K, V, g.seq_offsets, cfg.H, cfg.d, cfg.act,
+                         want_lse=False)
+    counts = gb.hma_count(g.user_ids, g.user_offsets, g.item_ids, g.item_offsets,
+                          g.cand_offsets, cfg.F, 3)
+    torch.cuda.synchronize()
+    pin = lambda t: t.contiguous().pin_memory()   # noqa: E731
+    hb = inputs.Batch(cfg, bt.requests, pin(bt.seq_offsets), pin(bt.cand_offsets), pin(bt.U),
+                      pin(bt.T), bt.W_q, bt.W_k, bt.W_v, pin(bt.user_ids), pin(bt.user_offsets),
+                      pin(bt.item_ids), pin(bt.item_offsets))
+    for chunks in (2, 4):
+        plan = gb.HostPlan(hb, n_chunks=chunks, out_dtype=torch.float32, cap=3, device=dev)
+        h_O = torch.full(O.shape, float("nan"), dtype=torch.float32).pin_memory()
+        h_c = torch.full(counts.shape, -1, dtype=torch.int32).pin_memory()
+        plan.run(h_O, h_c)
+        torch.cuda.synchronize()
+        assert torch.equal(h_O, O.cpu()), chunks
+        assert torch.equal(h_c, counts.cpu()), chunks
+        plan.close()
+
+
 def test_hma_int64_min_in_long_and_short_lists():
     """INT64_MIN inside a user list too long for the shared-memory tables (the
     global-memory path) and inside short lists (the bucket path: an ordinary key there), plus
