@@ -17,7 +17,13 @@
  *                     c = sum_i sum_j [u_i == t_j], optionally min(c, M)  (PAPER.md:308-312,
  *                     s3.4.1).
  *
- * Conventions (all calls):
+ * One more entry point runs the same step for a batch in HOST memory (the serving host's end to
+ * end path): gesr_score_host with its plan (gesr_host_plan_create / _destroy,
+ * gesr_host_chunk_maxima) -- see the end of this header; the conventions below apply to the
+ * device calls, and that section states where the host path differs (host pointers, device
+ * allocation in the plan, host<->device copies).
+ *
+ * Conventions (all device calls):
  *   - Every array pointer is a DEVICE pointer owned by the caller; the library never frees or
  *     retains a pointer after the call returns.  bf16 arrays are IEEE bfloat16 bit patterns.
  *   - `stream` is a cudaStream_t (passed as void*; NULL = legacy default stream).  Calls are
