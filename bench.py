@@ -444,7 +444,12 @@ def main():
                                "inside the step",
                      "peak_source": f"{peak_src} bf16_tflops_sustained (MEASURED_PEAKS.json): "
                                     "the kernel runs inside back-to-back steps",
-                     "peak_burst": peak_burst, "frac_burst": achieved / peak_burst},
+                     "peak_burst": peak_burst, "frac_burst": achieved / peak_burst,
+                     "algorithmic_bytes": cnt["tasa_bytes"],
+                     "traffic_source": "profiles/ncu_traffic.json (ncu --set full, DRAM read + "
+                                       "write of the q-projection and attention launches); "
+                                       "the excess over algorithmic_bytes is the Q round trip "
+                                       "through HBM and K/V re-reads"},
         "step_roofline": {"roof_ms_sustained": step_roof(peak_sus) * 1e3,
                           "frac_sustained": step_roof(peak_sus) * 1e3 / ms_per_step,
                           "roof_ms_burst": step_roof(peak_burst) * 1e3,
