@@ -502,6 +502,25 @@ def main():
                        "api": "gesr_score_host (C ABI, host buffers in and out)",
                        "pipeline": "request chunks: H2D of chunk i+1 and D2H of chunk i-1 "
                                    "overlap the kernels of chunk i (csrc/hostpath.cu)"}
+        # the bound of this leg: one pinned host -> device copy of the same size class, timed
+        # alone on the copy engine (best of 3)
+        src = hb.U.reshape(-1)[: min(hb.U.numel(), 1 << 29)]
+        dst = torch.empty(src.shape, dtype=src.dtype, device=dev)
+        best = float("inf")
+        for _ in range(3):
+            a.record(main_stream)
+            with torch.cuda.stream(main_stream):
+                dst.copy_(src, non_blocking=True)
+            b.record(main_stream)
+            torch.cuda.synchronize()
+            best = min(best, a.elapsed_time(b))
+        copy_gbs = src.numel() * src.element_size() / (best / 1e3) / 1e9
+        h2d_gbs = h2d * n_e2e / (e_ms / 1e3) / 1e9
+        line["e2e"]["h2d_bound"] = {"achieved_gbs": h2d_gbs, "copy_gbs": copy_gbs,
+                                    "frac": h2d_gbs / copy_gbs,
+                                    "copy": f"pinned host -> device, {src.numel() * 2 >> 20} MiB, "
+                                            "best of 3, measured in this run"}
+        del dst
 
     # ---------------------------------------------------------------- optional score gather
     if args.gather and world > 1:
