@@ -551,6 +551,7 @@ class HostPlan:
                  act: int = GESR_ACT_SILU, cap: int = 0, device=None):
         cfg = hb.cfg
         self.hb, self.cfg, self.act, self.cap, self.n_chunks = hb, cfg, act, cap, n_chunks
+        n_cut = max(1, min(n_chunks, hb.B))     # the library's clamp (csrc/hostpath.cu)
         self.out_dtype = out_dtype
         dev = torch.device("cuda") if device is None else torch.device(device)
         self.W = tuple(w.to(dev).contiguous() for w in (hb.W_q, hb.W_k, hb.W_v))
@@ -563,7 +564,7 @@ class HostPlan:
                 ctypes.byref(self._plan)))
         self.h2d_bytes = sum(t.numel() * t.element_size() for t in (
             hb.U, hb.T, hb.user_ids, hb.item_ids)) + 8 * (
-            2 * (hb.B + n_chunks) + hb.B * cfg.F + n_chunks + hb.total_C * cfg.F + n_chunks)
+            2 * (hb.B + n_cut) + hb.B * cfg.F + n_cut + hb.total_C * cfg.F + n_cut)
 
     def run(self, h_O, h_counts, stream=None):
         """Enqueue one end-to-end step; h_O [total_C, H*d] and h_counts [total_C, F] on the host

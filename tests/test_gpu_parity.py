@@ -685,3 +685,31 @@ def test_chunked_score_step_workspace_large_chunked_request():
     O_or, _ = oracle.tasa_score(T, co, sub.W_q, K, V, sub.seq_offsets, cfg.H, cfg.d, act=cfg.act)
     _attn_tol(O[torch.as_tensor(rows, device=dev)].float().cpu().numpy(), O_or, "chunked C=5120")
     assert reqs == [0]
+
+
+@pytest.mark.parametrize("B,chunks", [(3, 8), (1, 4), (2, 2)])
+def test_score_host_more_chunks_than_requests(B, chunks):
+    """gesr_score_host with n_chunks >= B (the library clamps the cut to one request per chunk):
+    bit-identical to the device-resident step, and the counts match the oracle's definition."""
+    dev = _cuda()
+    cfg = configs.get("2").with_(B=B)
+    bt = inputs.make_batch(cfg)
+    g = bt.to(dev)
+    bufs = gb.StepBuffers(g, out_dtype=torch.bfloat16)
+    O, counts = gb.score_step(g, bufs)
+    torch.cuda.synchronize()
+    pin = lambda t: t.contiguous().pin_memory()   # noqa: E731
+    hb = inputs.Batch(cfg, bt.requests, pin(bt.seq_offsets), pin(bt.cand_offsets), pin(bt.U),
+                      pin(bt.T), bt.W_q, bt.W_k, bt.W_v, pin(bt.user_ids), pin(bt.user_offsets),
+                      pin(bt.item_ids), pin(bt.item_offsets))
+    plan = gb.HostPlan(hb, n_chunks=chunks, out_dtype=torch.bfloat16, device=dev)
+    h_O = torch.full(O.shape, float("nan"), dtype=O.dtype).pin_memory()
+    h_c = torch.full(counts.shape, -1, dtype=torch.int32).pin_memory()
+    plan.run(h_O, h_c)
+    torch.cuda.synchronize()
+    plan.close()
+    assert torch.equal(h_O, O.cpu())
+    assert torch.equal(h_c, counts.cpu())
+    ref = oracle.hma_count(bt.user_ids, bt.user_offsets, bt.item_ids, bt.item_offsets,
+                           bt.cand_offsets, cfg.F)
+    assert (h_c.numpy() == ref).all()
