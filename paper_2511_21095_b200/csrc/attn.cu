@@ -134,6 +134,8 @@ __global__ void __launch_bounds__(AttnCfg<D>::kThreads, 1)
   // w % U, head w / U): neighbouring CTAs work on the pairs of the same (request, head) at the
   // same time, so each K/V slab is fetched from HBM once and re-read from L2.  The next unit's
   // Q load and first S MMA overlap the current unit's epilogue.
+  pdl_launch_dependents();
+  pdl_wait();
   const int U = __ldg(p.unit_count);
   const int W = U * p.H;
   if (static_cast<int>(blockIdx.x) >= W) return;   // uniform for the whole CTA
@@ -602,6 +604,8 @@ __global__ void build_units_kernel(const int64_t* __restrict__ seq_offsets,
                                    int causal) {
   __shared__ int warp_sums[32];
   __shared__ int running;
+  pdl_launch_dependents();
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const int w = threadIdx.x >> 5;
   const int nw = blockDim.x >> 5;
@@ -662,6 +666,8 @@ __global__ void __launch_bounds__(256) attn_self_merge_kernel(const AttnParams p
                                                               const __nv_bfloat16* __restrict__ Ks,
                                                               const __nv_bfloat16* __restrict__ Vs,
                                                               int d, float scale) {
+  pdl_launch_dependents();
+  pdl_wait();
   const int64_t item = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (item >= p.total_C * p.H) return;
@@ -695,6 +701,8 @@ __global__ void __launch_bounds__(256) attn_self_merge_kernel(const AttnParams p
 
 // total_L == 0: every candidate has an empty history -> O = 0, lse = -inf (R6)
 __global__ void attn_empty_kernel(AttnParams p, int D) {
+  pdl_launch_dependents();
+  pdl_wait();
   const int64_t HD = static_cast<int64_t>(p.H) * D;
   const int64_t n = p.total_C * HD;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
@@ -721,14 +729,9 @@ cudaError_t launch_d(const CUtensorMap& mq, const CUtensorMap& mk, const CUtenso
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t work = max_units * p.H;
   const unsigned grid = static_cast<unsigned>(work < sms ? work : sms);
-  if (p.hstu)
-    attn_kernel<D, false, true><<<grid, C::kThreads, C::kSmemBytes, stream>>>(mq, mk, mv, mo, p);
-  else if (p.causal)
-    attn_kernel<D, true, false><<<grid, C::kThreads, C::kSmemBytes, stream>>>(mq, mk, mv, mo, p);
-  else
-    attn_kernel<D, false, false><<<grid, C::kThreads, C::kSmemBytes, stream>>>(mq, mk, mv, mo, p);
-  count_launch();
-  return cudaGetLastError();
+  auto* fn = p.hstu ? attn_kernel<D, false, true>
+                    : (p.causal ? attn_kernel<D, true, false> : attn_kernel<D, false, false>);
+  return launch_pdl(fn, dim3(grid), dim3(C::kThreads), C::kSmemBytes, stream, mq, mk, mv, mo, p);
 }
 
 }  // namespace
@@ -741,9 +744,8 @@ extern "C" int gesr_debug_trace_copy(void* host) {
 
 cudaError_t launch_build_units(const int64_t* seq_offsets, const int64_t* cand_offsets, int64_t B,
                                int4* units, int* count, int causal, cudaStream_t stream) {
-  build_units_kernel<<<1, 1024, 0, stream>>>(seq_offsets, cand_offsets, B, units, count, causal);
-  count_launch();
-  return cudaGetLastError();
+  return launch_pdl(build_units_kernel, dim3(1), dim3(1024), 0, stream, seq_offsets, cand_offsets,
+                    B, units, count, causal);
 }
 
 cudaError_t launch_attn(int d, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
@@ -761,17 +763,14 @@ cudaError_t launch_attn_self_merge(const AttnParams& p, const void* Q, const voi
                                    const void* V_self, int d, float scale, cudaStream_t stream) {
   const int64_t n = p.total_C * p.H;
   if (n == 0) return cudaSuccess;
-  attn_self_merge_kernel<<<static_cast<unsigned>((n + 7) / 8), 256, 0, stream>>>(
-      p, static_cast<const __nv_bfloat16*>(Q), static_cast<const __nv_bfloat16*>(K_self),
-      static_cast<const __nv_bfloat16*>(V_self), d, scale);
-  count_launch();
-  return cudaGetLastError();
+  return launch_pdl(attn_self_merge_kernel, dim3(static_cast<unsigned>((n + 7) / 8)), dim3(256), 0,
+                    stream, p, static_cast<const __nv_bfloat16*>(Q),
+                    static_cast<const __nv_bfloat16*>(K_self),
+                    static_cast<const __nv_bfloat16*>(V_self), d, scale);
 }
 
 cudaError_t launch_attn_empty(const AttnParams& p, int d, cudaStream_t stream) {
-  attn_empty_kernel<<<1184, 256, 0, stream>>>(p, d);
-  count_launch();
-  return cudaGetLastError();
+  return launch_pdl(attn_empty_kernel, dim3(1184), dim3(256), 0, stream, p, d);
 }
 
 }  // namespace gesr

@@ -187,6 +187,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                      const __grid_constant__ CUtensorMap map_kh,
                      const __grid_constant__ CUtensorMap map_vh,
                      const __grid_constant__ CUtensorMap map_o, const AttnParams p) {
+  pdl_launch_dependents();
+  pdl_wait();
   const int U = __ldg(p.unit_count);
   const int S = p.splits;
   const int W = U * p.H * S;
@@ -888,6 +890,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 // O_s / l_s and (m_s, l_s) with m in log2 units of the scaled score; O = sum_s w_s (O_s / l_s) /
 // sum_s w_s with w_s = l_s 2^(m_s - max_s m_s), summed in split order (deterministic).
 __global__ void __launch_bounds__(128) attn_combine_kernel(const AttnParams p, int d) {
+  pdl_launch_dependents();
+  pdl_wait();
   const int64_t rh = blockIdx.x;                   // row * H + h
   const int64_t row = rh / p.H;
   const int h = static_cast<int>(rh % p.H);
@@ -924,9 +928,8 @@ __global__ void __launch_bounds__(128) attn_combine_kernel(const AttnParams p, i
 cudaError_t launch_attn_combine(const AttnParams& p, int d, cudaStream_t stream) {
   const int64_t n = p.total_C * p.H;
   if (n == 0) return cudaSuccess;
-  attn_combine_kernel<<<static_cast<unsigned>(n), 128, 0, stream>>>(p, d);
-  count_launch();
-  return cudaGetLastError();
+  return launch_pdl(attn_combine_kernel, dim3(static_cast<unsigned>(n)), dim3(128), 0, stream, p,
+                    d);
 }
 
 #ifdef GESR_TRACE
@@ -976,12 +979,8 @@ cudaError_t launch_attn_pair(const CUtensorMap& mq, const CUtensorMap& mkh, cons
   }
   const int64_t work = max_units * p.H * p.splits;
   const unsigned pairs = static_cast<unsigned>(work < max_pairs ? work : max_pairs);
-  if (p.causal)
-    attn_pair_kernel<true><<<2 * pairs, kThreads, kSmemBytes, stream>>>(mq, mkh, mvh, mo, p);
-  else
-    attn_pair_kernel<false><<<2 * pairs, kThreads, kSmemBytes, stream>>>(mq, mkh, mvh, mo, p);
-  count_launch();
-  return cudaGetLastError();
+  return launch_pdl(p.causal ? attn_pair_kernel<true> : attn_pair_kernel<false>, dim3(2 * pairs),
+                    dim3(kThreads), kSmemBytes, stream, mq, mkh, mvh, mo, p);
 }
 
 }  // namespace gesr

@@ -162,6 +162,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     hma_kernel(const HmaParams p, const int chunk) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   HmaSmem& s = *reinterpret_cast<HmaSmem*>(smem_raw);
+  pdl_launch_dependents();
+  pdl_wait();
   const int b = blockIdx.x;
   const int64_t cb = p.cand_offsets[b];
   const int64_t ce = p.cand_offsets[b + 1];
@@ -486,9 +488,7 @@ cudaError_t launch_hma(const HmaParams& p, cudaStream_t stream) {
   if (y < 1) y = 1;
   if (y > 65535) y = 65535;
   dim3 grid(static_cast<unsigned>(p.B), static_cast<unsigned>(y));
-  hma_kernel<<<grid, kThreads, smem, stream>>>(p, chunk);
-  count_launch();
-  return cudaGetLastError();
+  return launch_pdl(hma_kernel, grid, dim3(kThreads), smem, stream, p, chunk);
 }
 
 }  // namespace gesr

@@ -21,6 +21,31 @@ void device_cache_store(int slot, int value);
 // Every kernel launch of the library is counted (gesr_launch_count(): the bench's
 // gpu_launches claim is read from it, not typed in).
 void count_launch();
+// Launch with programmatic stream serialisation (PDL, ptx.cuh pdl_wait): the kernel's CTAs may
+// be scheduled as soon as every CTA of the previous kernel on the stream has started, and wait
+// in pdl_wait() for its completion -- the launch latency and the prologue (barrier init, TMEM
+// allocation, tensor-map prefetch) overlap the previous kernel's tail.  Only kernels that call
+// pdl_wait() in every CTA before touching global memory are launched this way.  -DGESR_PDL=0
+// builds plain stream-ordered launches (A/B).
+#ifndef GESR_PDL
+#define GESR_PDL 1
+#endif
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t stream, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = GESR_PDL;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  count_launch();
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<Args&&>(args)...);
+}
 // GESR_DEBUG=1: device check of a jagged offsets array [n + 1] (debug.cu); traps if
 // offsets[0] != 0, offsets decrease, or offsets[n] != total.  tag names the array in the report.
 cudaError_t launch_check_offsets(const int64_t* offsets, int64_t n, int64_t total, int tag,

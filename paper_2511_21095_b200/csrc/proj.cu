@@ -150,6 +150,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_launch_dependents();
+  pdl_wait();         // the prologue above touched no global memory
 
   if (warp == 0) {
     if (elect_one()) {
@@ -343,9 +345,8 @@ cudaError_t launch_bn(const CUtensorMap& ma, const CUtensorMap& mb0, const CUten
   q.m_major = p.num_m_blocks >= num_sms / 2 ? 1 : 0;
   const int work = q.m_major ? p.num_m_blocks : p.num_m_blocks * p.num_n_blocks;
   const int pairs = work < num_sms / 2 ? work : num_sms / 2;
-  proj_kernel<BN><<<2 * pairs, kThreads, S::kBytes, stream>>>(ma, mb0, mb1, mo0, mo1, q);
-  count_launch();
-  return cudaGetLastError();
+  return launch_pdl(proj_kernel<BN>, dim3(2 * pairs), dim3(kThreads), S::kBytes, stream, ma, mb0,
+                    mb1, mo0, mo1, q);
 }
 
 }  // namespace

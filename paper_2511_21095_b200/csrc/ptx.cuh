@@ -343,6 +343,18 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
 
 
 // ------------------------------------------------------------------------------------------
+// programmatic dependent launch (PDL).  A kernel launched by launch_pdl (kernels.h) may be
+// scheduled while its predecessor on the stream is still running.  pdl_wait() blocks until that
+// predecessor grid has completed and its writes are visible (a no-op for a plain launch); every
+// PDL kernel calls it in every CTA before its first global read or write, so the ordering stays
+// transitive along the stream.  pdl_launch_dependents() lets the successor's CTAs be scheduled
+// (onto SMs this grid leaves free) and run their prologue, hiding the launch gap.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// ------------------------------------------------------------------------------------------
 // clusters and the 2-SM (cta_group::2) variants
 
 __device__ __forceinline__ uint32_t cluster_ctarank() {
