@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(AttnCfg<D>::kThreads, 1)
   // Q load and first S MMA overlap the current unit's epilogue.
   pdl_launch_dependents();
   pdl_wait();
-  const int U = __ldg(p.unit_count);
+  const int U = unit_count_of(p);
   const int W = U * p.H;
   if (static_cast<int>(blockIdx.x) >= W) return;   // uniform for the whole CTA
 
@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(AttnCfg<D>::kThreads, 1)
   };
   // the unit descriptor of work item w is one 16-byte load; it is fetched one item ahead and
   // decoded only when used, so its latency overlaps the current unit
-  auto fetch = [&](int w) { return __ldg(p.units + (w % U)); };
+  auto fetch = [&](int w) { return unit_of(p, w % U); };
   auto decode = [&](int w, int4 d) {
     Work x;
     x.h = w / U;

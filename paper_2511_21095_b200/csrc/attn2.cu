@@ -189,7 +189,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                      const __grid_constant__ CUtensorMap map_o, const AttnParams p) {
   pdl_launch_dependents();
   pdl_wait();
-  const int U = __ldg(p.unit_count);
+  const int U = unit_count_of(p);
   const int S = p.splits;
   const int W = U * p.H * S;
   const int pair = static_cast<int>(blockIdx.x >> 1);
@@ -275,7 +275,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const uint32_t sRing = smem_u32(smem + kRingOff);
 
   // the unit descriptor of work item w is one 16-byte load, fetched one item ahead
-  auto fetch = [&](int w) { return __ldg(p.units + (w % U)); };
+  auto fetch = [&](int w) { return unit_of(p, w % U); };
   // w -> (unit w % U, split (w / U) % S, head w / (U S)): neighbouring pairs share a head and
   // run the units of one request at the same time (K/V shared in L2; measured: a pair taking
   // a contiguous block of items, units of a request back to back, read 11% MORE from HBM)
@@ -886,40 +886,58 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   }
 }
 
-// Split-L merge (one CTA of d threads per (candidate, head)): the s-th partial holds
-// O_s / l_s and (m_s, l_s) with m in log2 units of the scaled score; O = sum_s w_s (O_s / l_s) /
-// sum_s w_s with w_s = l_s 2^(m_s - max_s m_s), summed in split order (deterministic).
-__global__ void __launch_bounds__(128) attn_combine_kernel(const AttnParams p, int d) {
+// Split-L merge, one warp per (candidate, head), lane k owning columns 4k..4k+3 (d = 128: the
+// pair kernel is the only one that splits): the s-th partial holds O_s / l_s and (m_s, l_s) with
+// m in log2 units of the scaled score; O = sum_s w_s (O_s / l_s) / sum_s w_s with
+// w_s = l_s 2^(m_s - max_s m_s), summed in split order (deterministic).  Every split's (m, l) is
+// a broadcast load and its 512-byte row one coalesced 16-byte load per lane, all independent.
+constexpr int kCombineWarps = 8;
+__global__ void __launch_bounds__(kCombineWarps * 32) attn_combine_kernel(const AttnParams p) {
   pdl_launch_dependents();
   pdl_wait();
-  const int64_t rh = blockIdx.x;                   // row * H + h
-  const int64_t row = rh / p.H;
-  const int h = static_cast<int>(rh % p.H);
-  const int j = threadIdx.x;
-  const int S = p.splits;
   const int64_t stride = p.total_C * p.H;
-  float mmax = -INFINITY;
+  const int64_t rh = static_cast<int64_t>(blockIdx.x) * kCombineWarps + (threadIdx.x >> 5);
+  if (rh >= stride) return;                        // row * H + h
+  const int lane = threadIdx.x & 31;
+  const int S = p.splits;                          // <= kMaxSplits = 64
+  // lane k: (m, l) of splits k and k + 32, loaded at once; the max by a butterfly (exact)
+  float2 ml0 = make_float2(0.f, 0.f), ml1 = make_float2(0.f, 0.f);
+  if (lane < S) ml0 = __ldg(p.part_ml + lane * stride + rh);
+  if (lane + 32 < S) ml1 = __ldg(p.part_ml + (lane + 32) * stride + rh);
+  float mmax = fmaxf(ml0.y > 0.f ? ml0.x : -INFINITY, ml1.y > 0.f ? ml1.x : -INFINITY);
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) mmax = fmaxf(mmax, __shfl_xor_sync(0xffffffffu, mmax, o));
+  // w_s = l_s 2^(m_s - max), negative for an empty split (skipped)
+  const float w0 = ml0.y > 0.f ? ml0.y * exp2f(ml0.x - mmax) : -1.f;
+  const float w1 = ml1.y > 0.f ? ml1.y * exp2f(ml1.x - mmax) : -1.f;
+  float wsum = 0.f;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  const float4* po = reinterpret_cast<const float4*>(p.part_o) + rh * 32 + lane;
+#pragma unroll 4
   for (int s = 0; s < S; ++s) {
-    const float2 ml = p.part_ml[s * stride + rh];
-    if (ml.y > 0.f) mmax = fmaxf(mmax, ml.x);
-  }
-  float wsum = 0.f, acc = 0.f;
-  for (int s = 0; s < S; ++s) {
-    const float2 ml = p.part_ml[s * stride + rh];
-    if (ml.y > 0.f) {
-      const float w = ml.y * exp2f(ml.x - mmax);
+    const float4 o = __ldg(po + s * stride * 32);
+    const float w = __shfl_sync(0xffffffffu, s < 32 ? w0 : w1, s & 31);
+    if (w >= 0.f) {
       wsum += w;
-      if (j < d) acc += w * p.part_o[(s * stride + rh) * d + j];
+      acc.x += w * o.x;
+      acc.y += w * o.y;
+      acc.z += w * o.z;
+      acc.w += w * o.w;
     }
   }
-  const float v = wsum > 0.f ? acc / wsum : 0.f;
-  if (j < d) {
-    if (p.o_bf16)
-      static_cast<__nv_bfloat16*>(p.O)[row * p.H * d + h * d + j] = __float2bfloat16_rn(v);
-    else
-      static_cast<float*>(p.O)[row * p.H * d + h * d + j] = v;
+  const float4 v = wsum > 0.f ? make_float4(acc.x / wsum, acc.y / wsum, acc.z / wsum, acc.w / wsum)
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+  const int64_t o0 = rh * 128 + 4 * lane;          // O [total_C, H, 128] = [row][h][col]
+  if (p.o_bf16) {
+    __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+    uint2 u;
+    u.x = *reinterpret_cast<uint32_t*>(&a);
+    u.y = *reinterpret_cast<uint32_t*>(&b);
+    *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(p.O) + o0) = u;
+  } else {
+    *reinterpret_cast<float4*>(static_cast<float*>(p.O) + o0) = v;
   }
-  if (j == 0 && p.lse != nullptr)
+  if (lane == 0 && p.lse != nullptr)
     p.lse[rh] = wsum > 0.f ? (mmax + log2f(wsum)) * 0.69314718055994530942f : -INFINITY;
 }
 
@@ -928,8 +946,10 @@ __global__ void __launch_bounds__(128) attn_combine_kernel(const AttnParams p, i
 cudaError_t launch_attn_combine(const AttnParams& p, int d, cudaStream_t stream) {
   const int64_t n = p.total_C * p.H;
   if (n == 0) return cudaSuccess;
-  return launch_pdl(attn_combine_kernel, dim3(static_cast<unsigned>(n)), dim3(128), 0, stream, p,
-                    d);
+  if (d != 128) return cudaErrorInvalidValue;
+  return launch_pdl(attn_combine_kernel,
+                    dim3(static_cast<unsigned>((n + kCombineWarps - 1) / kCombineWarps)),
+                    dim3(kCombineWarps * 32), 0, stream, p);
 }
 
 #ifdef GESR_TRACE

@@ -220,7 +220,7 @@ gesr_status run_projection(const void* X, int64_t M, int32_t K, const void* W0, 
                            const float* b0, const float* b1, int32_t H, int32_t d, int32_t act,
                            void* out0, void* out1, cudaStream_t stream) {
   const int HD = H * d;
-  const int bn = gesr::proj_pick_bn(HD);
+  const int bn = gesr::proj_pick_bn(M, HD, W1 ? 2 : 1, num_sms());
   CUtensorMap ma, mb0, mb1;
   gesr_status s = make_map_2d(&ma, X, static_cast<uint64_t>(M), static_cast<uint64_t>(K), 128, 64,
                               CU_TENSOR_MAP_SWIZZLE_128B, "X");
@@ -257,7 +257,7 @@ gesr_status run_projection(const void* X, int64_t M, int32_t K, const void* W0, 
 gesr_status run_projection_rm(const void* X, int64_t M, int32_t K, const void* W, const float* b,
                               int32_t N, int32_t act, const void* residual, void* out,
                               cudaStream_t stream) {
-  const int bn = gesr::proj_pick_bn(N);
+  const int bn = gesr::proj_pick_bn(M, N, 1, num_sms());
   CUtensorMap ma, mb, mo;
   gesr_status s = make_map_2d(&ma, X, static_cast<uint64_t>(M), static_cast<uint64_t>(K), 128, 64,
                               CU_TENSOR_MAP_SWIZZLE_128B, "X");
@@ -483,8 +483,9 @@ static gesr_status tasa_impl(const void* T, int64_t total_C, int32_t D_in, const
     return self_merge();
   }
 
-  p.units = units;
-  p.unit_count = count;
+  // B = 1: the kernels derive the single request's units (kernels.h unit_of), no work-list launch
+  p.units = B == 1 ? nullptr : units;
+  p.unit_count = B == 1 ? nullptr : count;
   p.splits = (causal || hstu) ? 1 : pick_splits(B, total_C, total_L, H, d, kv_splits);
   p.causal = causal;
   p.hstu = hstu ? 1 : 0;
@@ -494,8 +495,11 @@ static gesr_status tasa_impl(const void* T, int64_t total_C, int32_t D_in, const
     p.part_o = reinterpret_cast<float*>(part + split_ml_bytes(total_C, H, p.splits));
   }
   const bool pair = d == 128 && pair_attention_enabled() && !hstu;
-  cudaError_t e = gesr::launch_build_units(seq_offsets, cand_offsets, B, units, count, causal, st);
-  if (e != cudaSuccess) return cuda_fail(e, "build_units launch");
+  cudaError_t e = cudaSuccess;
+  if (B != 1) {
+    e = gesr::launch_build_units(seq_offsets, cand_offsets, B, units, count, causal, st);
+    if (e != cudaSuccess) return cuda_fail(e, "build_units launch");
+  }
   s = run_projection(T, total_C, D_in, W_q, nullptr, b_q, nullptr, H, d, act, Q, nullptr, st);
   if (s != GESR_OK) return s;
 

@@ -72,7 +72,11 @@ struct ProjParams {
   int64_t res_ld;
 };
 
-int proj_pick_bn(int n_split);
+// Tile width: the widest of 256 / 128 / 64 dividing N (the columns of one weight; `ways`
+// weights stacked along N) whose (256-row x bn) tiles still give every CTA pair of the device
+// one; narrower for few rows (a 512-row chunk: 64, so 16 pairs run the 8-deep K loop and the
+// epilogue instead of 4); N not a multiple of 64: 32.
+int proj_pick_bn(int64_t M, int N, int ways, int num_sms);
 cudaError_t launch_proj(const CUtensorMap& map_a, const CUtensorMap& map_b0,
                         const CUtensorMap& map_b1, const CUtensorMap& map_o0,
                         const CUtensorMap& map_o1, const ProjParams& p, int bn, int num_sms,
@@ -108,6 +112,23 @@ struct AttnParams {
 };
 
 constexpr int kUnitRows = 256;   // candidates per work unit (two 128-row Q tiles)
+
+#ifdef __CUDACC__
+// The attention kernels' work list.  p.units == nullptr: one request (B = 1), whose offsets are
+// {0, total} by the ABI contract, so unit u follows from total_L / total_C without a
+// build_units launch: {0, L, 256 u, rows} (causal: L = 256 u + rows, as build_units_kernel).
+__device__ __forceinline__ int unit_count_of(const AttnParams& p) {
+  return p.units != nullptr ? __ldg(p.unit_count)
+                            : static_cast<int>((p.total_C + kUnitRows - 1) / kUnitRows);
+}
+__device__ __forceinline__ int4 unit_of(const AttnParams& p, int u) {
+  if (p.units != nullptr) return __ldg(p.units + u);
+  const int c0 = u * kUnitRows;
+  const int left = static_cast<int>(p.total_C) - c0;
+  const int rows = left < kUnitRows ? left : kUnitRows;
+  return make_int4(0, p.causal ? c0 + rows : static_cast<int>(p.total_L), c0, rows);
+}
+#endif
 
 // causal = 1: queries are the history rows (cand_offsets == seq_offsets), unit k of request b
 // is {s0, 256 k + rows, s0 + 256 k, rows} (keys up to the unit's last query row)

@@ -362,10 +362,15 @@ extern "C" int gesr_debug_projprof_copy(void* host, int reset) {
 }
 #endif
 
-int proj_pick_bn(int N) {
-  if (N % 256 == 0) return 256;
-  if (N % 128 == 0) return 128;
-  if (N % 64 == 0) return 64;
+#ifndef GESR_PROJ_MIN_BN
+#define GESR_PROJ_MIN_BN 64
+#endif
+int proj_pick_bn(int64_t M, int N, int ways, int num_sms) {
+  const int64_t m_blocks = (M + 2 * kBM - 1) / (2 * kBM);
+  for (int bn = 256; bn > GESR_PROJ_MIN_BN; bn >>= 1)
+    if (N % bn == 0 && m_blocks * ways * (N / bn) >= num_sms / 2) return bn;
+  for (int bn = GESR_PROJ_MIN_BN; bn >= 32; bn >>= 1)
+    if (N % bn == 0) return bn;
   return 32;
 }
 
