@@ -46,8 +46,8 @@ namespace {
 
 constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
-constexpr int kChunkMin = 256;             // candidates per CTA chunk (runtime: 256 or 1024)
-constexpr int kChunkMax = 1024;
+constexpr int kChunkMax = 1024;            // candidates per CTA chunk (runtime: 1024 >> k)
+constexpr int kChunkFloor = 32;
 constexpr int kPoolBuckets = 4096;         // 16-byte buckets (2 slots): 64 KB of keys per CTA
 constexpr int kMinBuckets = 4;             // a field owns whole 32-bit bitmap words
 constexpr int kMaxSeeds = 32;              // hash seeds tried per field before going global
@@ -479,11 +479,14 @@ cudaError_t launch_hma(const HmaParams& p, cudaStream_t stream) {
   const int smem = static_cast<int>(sizeof(HmaSmem));
   cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(hma_kernel), smem);
   if (e != cudaSuccess) return e;
-  // Large chunks amortise the per-CTA table build; small ones keep the grid >= 4 CTAs per SM
-  // when there are few requests (config 4: B = 1, C = 4096).
+  // Large chunks amortise the per-CTA table build; 256-candidate chunks when that leaves fewer
+  // than 4 CTAs per SM; and with very few requests the chunk halves (down to 32 candidates)
+  // while the grid is smaller than the SM count (config 4: B = 1, C = 4096 -> 128 CTAs of 32
+  // candidates, 23 -> 12 us; config 2's 256 CTAs keep 256: more table builds cost more there).
   int64_t per = p.B > 0 ? (p.total_C + p.B - 1) / p.B : 1;
   int chunk = kChunkMax;
-  if (p.B * ((per + kChunkMax - 1) / kChunkMax) < 4 * 148) chunk = kChunkMin;
+  if (p.B * ((per + kChunkMax - 1) / kChunkMax) < 4 * 148) chunk = 256;
+  while (chunk > kChunkFloor && p.B * ((per + chunk - 1) / chunk) < 148) chunk >>= 1;
   int64_t y = (per + chunk - 1) / chunk;
   if (y < 1) y = 1;
   if (y > 65535) y = 65535;
