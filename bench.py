@@ -60,6 +60,9 @@ def _args(argv=None):
                     help="request chunks of the end-to-end pipeline (H2D / kernels / D2H "
                          "overlapped on three streams); 1 = copy in, score, copy out")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--graph", action="store_true",
+                    help="time replays of one step captured into a CUDA graph (launch-bound "
+                         "configs 1, 2, 4: no per-call host overhead)")
     ap.add_argument("--gather", action="store_true", help="NCCL gather of scores after timing")
     ap.add_argument("--hma-order", default="serial", choices=["fork", "kv", "serial"],
                     help="where gesr_hma_count runs in the step: forked first on a side stream, "
@@ -202,12 +205,16 @@ class GpuEngine:
     """One rank's device state: the batch of its requests, preallocated buffers, and the step
     (binding.score_step: kv_project -> tasa_score, hma_count forked on a side stream)."""
 
-    def __init__(self, device, out_dtype, hma_order="serial"):
+    L2_FLUSH_BYTES = 256 << 20          # > 2x the 126 MB L2
+
+    def __init__(self, device, out_dtype, hma_order="serial", graph=False):
         import torch
         self.dev, self.out_dtype, self.hma_order = device, out_dtype, hma_order
         self.reduce_device = device
         self.events = {}
-        self.stream = torch.cuda.current_stream(device)
+        # graph capture needs a non-default stream
+        self.stream = torch.cuda.Stream(device) if graph else torch.cuda.current_stream(device)
+        self.use_graph, self.graph = graph, None
 
     def setup(self, cfg, reqs):
         import torch
@@ -219,6 +226,12 @@ class GpuEngine:
         self.bufs = gb.StepBuffers(self.batch, out_dtype=self.out_dtype)
         self.candidates = self.batch.total_C
         self.gb = gb
+        b = self.batch
+        self.input_bytes = sum(t.numel() * t.element_size() for t in (
+            b.U, b.T, b.W_q, b.W_k, b.W_v, b.user_ids, b.item_ids, b.item_offsets))
+        # inputs that fit in L2 would stay resident across steps: flush it before each step
+        self.flush = (torch.empty(self.L2_FLUSH_BYTES, dtype=torch.uint8, device=self.dev)
+                      if self.input_bytes < self.L2_FLUSH_BYTES else None)
 
     def broadcast_weights(self, group=None):
         import torch.distributed as dist
@@ -234,19 +247,63 @@ class GpuEngine:
         import torch
         torch.cuda.synchronize(self.dev)
 
+    def capture(self):
+        """--graph: one whole step captured into a CUDA graph (the C-ABI calls allocate nothing
+        and never synchronise the host), replayed as the timed step."""
+        import torch
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(self.stream):
+            with torch.cuda.graph(self.graph, stream=self.stream):
+                self.step()
+        torch.cuda.synchronize(self.dev)
+
+    def _replay(self):
+        import torch
+        with torch.cuda.stream(self.stream):     # replay() launches on the current stream
+            self.graph.replay()
+
     def time_steps(self, steps):
         import torch
-        self.launch0 = self.gb.launch_count()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        with ClockSampler(self.dev.index) as clk:
-            a.record(self.stream)
-            for _ in range(steps):
-                self.step(record=True)
-            b.record(self.stream)
+        if self.use_graph and self.graph is None:
+            self.capture()
+            n0 = self.gb.launch_count()
+            self.step()                     # launches per step (a replay does not count them)
             torch.cuda.synchronize(self.dev)
-        self.launches = self.gb.launch_count() - self.launch0
+            self.graph_launches = self.gb.launch_count() - n0
+        self.launch0 = self.gb.launch_count()
+        ev = lambda: torch.cuda.Event(enable_timing=True)   # noqa: E731
+        with ClockSampler(self.dev.index) as clk:
+            if self.flush is None:
+                # inputs larger than L2: the K steps back to back between two events
+                a, b = ev(), ev()
+                a.record(self.stream)
+                for _ in range(steps):
+                    self._replay() if self.graph is not None else self.step(record=True)
+                b.record(self.stream)
+                torch.cuda.synchronize(self.dev)
+                ms = a.elapsed_time(b)
+            else:
+                # L2 flushed (a 256 MB memset) before every step, each step timed alone
+                pairs = []
+                for _ in range(steps):
+                    with torch.cuda.stream(self.stream):
+                        self.flush.zero_()
+                    a, b = ev(), ev()
+                    a.record(self.stream)
+                    self._replay() if self.graph is not None else self.step(record=True)
+                    b.record(self.stream)
+                    pairs.append((a, b))
+                torch.cuda.synchronize(self.dev)
+                ms = sum(a.elapsed_time(b) for a, b in pairs)
+        self.launches = (self.gb.launch_count() - self.launch0 if self.graph is None
+                         else self.graph_launches * steps)
         self.clocks = clk.summary()
-        return a.elapsed_time(b)
+        if self.graph is not None:
+            # per-call times (roofline numerators) from a few eager steps after the timed region
+            for _ in range(min(steps, 5)):
+                self.step(record=True)
+            torch.cuda.synchronize(self.dev)
+        return ms
 
     def call_ms(self, a, b):
         import numpy as np
@@ -394,7 +451,7 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     out_dtype = torch.bfloat16 if args.out_dtype == "bf16" else torch.float32
-    eng = GpuEngine(dev, out_dtype, args.hma_order)
+    eng = GpuEngine(dev, out_dtype, args.hma_order, graph=args.graph)
     res = orchestrate(args.config, rank, world, args.steps, args.warmup, eng)
     cfg, batch, bufs = res["cfg"], eng.batch, eng.bufs
     kv_ms, tasa_ms, hma_ms = eng.call_ms("kv0", "kv1"), eng.call_ms("kv1", "t1"), \
@@ -436,8 +493,11 @@ def main():
                    "H": cfg.H, "d": cfg.d, "D_in": cfg.D_in, "F": cfg.F, "L": list(cfg.L),
                    "C": list(cfg.C), "out_dtype": args.out_dtype, "act": "silu",
                    "parallelism": f"dp{world}", "hma_order": args.hma_order,
-                   "l2": "inputs larger than L2 (per GPU: U and HMA item ids exceed 126 MB); "
-                         "no flush"},
+                   "l2": ("inputs larger than L2 (per GPU: U and HMA item ids exceed 126 MB); "
+                          "no flush" if eng.flush is None else
+                          f"inputs {eng.input_bytes / 2**20:.1f} MiB fit in L2: a 256 MiB memset "
+                          "flushes it before every step, each step timed alone (flush excluded)"),
+                   "cuda_graph": bool(args.graph)},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_sus,
                      "unit": "TFLOP/s", "frac": achieved / peak_sus, "traffic": traffic,
                      "kernel": "gesr_tasa_score (q-projection + attention kernels), timed "
