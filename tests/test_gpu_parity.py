@@ -713,3 +713,47 @@ def test_score_host_more_chunks_than_requests(B, chunks):
     ref = oracle.hma_count(bt.user_ids, bt.user_offsets, bt.item_ids, bt.item_offsets,
                            bt.cand_offsets, cfg.F)
     assert (h_c.numpy() == ref).all()
+
+
+@pytest.mark.parametrize("B,kv_splits", [(4, 1), (1, 0)])
+def test_back_to_back_steps_keep_stream_order(B, kv_splits):
+    """Steps on alternating inputs, enqueued back to back with no host synchronisation, sharing
+    ONE K/V cache and work buffer (so a later step's projection overwrites what the previous
+    step's attention reads): the hot-path kernels are launched with programmatic dependent
+    launch (csrc/kernels.h launch_pdl), so this checks that every kernel still waits for its
+    predecessor (read-after-write and write-after-read along the stream, B = 1 with split-L and
+    the combine kernel included).  Each step's O and counts must equal its inputs' reference,
+    bit for bit."""
+    dev = _cuda()
+    cfg = configs.get("3h").with_(B=B)
+    bts = [inputs.make_batch(cfg, requests=list(range(i * B, (i + 1) * B)), device=dev)
+           for i in range(2)]
+    K = torch.empty((cfg.H, bts[0].U.shape[0], cfg.d), dtype=torch.bfloat16, device=dev)
+    V = torch.empty_like(K)
+    ws = torch.empty(gb.tasa_workspace_bytes(B, bts[0].total_C, cfg.H, cfg.d, kv_splits),
+                     dtype=torch.uint8, device=dev)
+    ref = []
+    for bt in bts:
+        k, v = gb.kv_project(bt.U, bt.W_k, bt.W_v, cfg.H, cfg.d, cfg.act)
+        O, _ = gb.tasa_score(bt.T, bt.cand_offsets, bt.W_q, k, v, bt.seq_offsets, cfg.H, cfg.d,
+                             cfg.act, kv_splits=kv_splits, out_dtype=torch.bfloat16,
+                             want_lse=False)
+        c = gb.hma_count(bt.user_ids, bt.user_offsets, bt.item_ids, bt.item_offsets,
+                         bt.cand_offsets, cfg.F)
+        torch.cuda.synchronize()
+        ref.append((O.clone(), c.clone()))
+    n = 8
+    outs = [torch.empty_like(ref[i % 2][0]) for i in range(n)]
+    cnts = [torch.empty_like(ref[i % 2][1]) for i in range(n)]
+    torch.cuda.synchronize()
+    for i in range(n):
+        bt = bts[i % 2]
+        gb.kv_project(bt.U, bt.W_k, bt.W_v, cfg.H, cfg.d, cfg.act, K_cache=K, V_cache=V)
+        gb.tasa_score(bt.T, bt.cand_offsets, bt.W_q, K, V, bt.seq_offsets, cfg.H, cfg.d, cfg.act,
+                      kv_splits=kv_splits, O=outs[i], want_lse=False, workspace=ws)
+        gb.hma_count(bt.user_ids, bt.user_offsets, bt.item_ids, bt.item_offsets,
+                     bt.cand_offsets, cfg.F, counts=cnts[i])
+    torch.cuda.synchronize()
+    for i in range(n):
+        assert torch.equal(outs[i], ref[i % 2][0]), i
+        assert torch.equal(cnts[i], ref[i % 2][1]), i
