@@ -30,6 +30,13 @@
  *     asynchronous on that stream: no host synchronisation, no device allocation, no
  *     host<->device copies; they are CUDA-graph capturable.  Safe to call concurrently from
  *     several threads on different streams.
+ *   - The hot-path kernels are launched with programmatic stream serialisation (programmatic
+ *     dependent launch): each may be scheduled while the previous kernel on `stream` still runs
+ *     and waits for its completion before touching memory, so stream order holds for the
+ *     caller's work before and after a call exactly as with plain launches.  The kernels allow
+ *     their successor to be scheduled early; a caller's own PDL-launched kernel that follows a
+ *     call must execute griddepcontrol.wait (cudaGridDependencySynchronize) before reading the
+ *     call's outputs, as PDL requires of any such kernel.
  *   - Host-checkable argument errors return GESR_ERR_INVALID_ARG BEFORE any launch and write
  *     nothing; unsupported options return GESR_ERR_UNSUPPORTED; a too-small workspace returns
  *     GESR_ERR_WORKSPACE; a failed launch returns GESR_ERR_CUDA.  gesr_last_error() gives a
