@@ -515,6 +515,12 @@ def main():
                           "roof_ms_burst": step_roof(peak_burst) * 1e3,
                           "frac_burst": step_roof(peak_burst) * 1e3 / ms_per_step,
                           "kv_ms": kv_ms, "tasa_ms": tasa_ms, "hma_ms": hma_ms,
+                          # SURVEY s8(d)'s MUFU ceiling beside the tensor roofline: the softmax's
+                          # exps at 16 ex2 / clk / SM on 148 SMs at the maximum SM clock
+                          "exps": cnt["exps"],
+                          "mufu_ceiling_ms": cnt["exps"] / (16 * 148 * float(
+                              peaks.get("sm_max_mhz", 1965.0)) * 1e6) * 1e3,
+                          "attn_tensor_ms_burst": cnt["attn_flop"] / (peak_burst * 1e12) * 1e3,
                           "kv_tflops": cnt["kv_flop"] / (kv_ms / 1e3) / 1e12,
                           "hma_gbs": cnt["hma_bytes"] / (hma_ms / 1e3) / 1e9},
         "gpu_launches": eng.launches,
