@@ -110,6 +110,26 @@ gesr_status gesr_kv_project(const void* U, int64_t total_L, int32_t D_in,
                             void* K_cache, void* V_cache,
                             void* stream);
 
+/* gesr_kv_project_gather -- gesr_kv_project with the history rows looked up in an embedding
+ * table inside the projection: U[m] = E[rows[m]], K = act(U W_k^T + b_k), V = act(U W_v^T + b_v).
+ * PAPER.md:407 (s4 serving): "MoA serving combines the item POST ID with the user history
+ * sequence IDs ... looked up in the shared embedding table that was learnt during training to
+ * obtain the input embeddings for the MoA module (U, T)"; the shared table.  The
+ * looked-up rows are never written to memory: the projection's TMA producer gathers them
+ * (tile::gather4, four table rows per load) straight into its 128B-swizzled operand tiles.
+ *   E        bf16 [n_E, D_in] row-major embedding table, 1 <= n_E < 2^31.
+ *   rows     int32 [total_L], 4-byte aligned: table row of each history row; repeats allowed.
+ *            0 <= rows[m] < n_E is required and not checked (an out-of-range row is undefined
+ *            behaviour).
+ *   Everything else as gesr_kv_project; the result is bit-identical to gesr_kv_project on the
+ *   materialised U = E[rows]. */
+gesr_status gesr_kv_project_gather(const void* E, int64_t n_E, int32_t D_in, const int32_t* rows,
+                                   int64_t total_L, const void* W_k, const void* W_v,
+                                   const float* b_k, const float* b_v,
+                                   int32_t H, int32_t d, int32_t act,
+                                   void* K_cache, void* V_cache,
+                                   void* stream);
+
 /* Workspace bytes gesr_tasa_score needs for this problem (an upper bound that depends only on
  * the arguments, never on device data).  Returns 0 for invalid arguments. */
 size_t gesr_tasa_workspace_bytes(int64_t B, int64_t total_C, int32_t H, int32_t d,

@@ -10,6 +10,9 @@ Every function wraps one entry point of ``oracle/oracle.cpp`` (plain C++17, fp64
 blocking/fusion), each citing the passage it follows:
 
 * :func:`kv_project`  -- K/V = act(U W^T + b) per head. PAPER.md:335-341 (s3.4.2).
+* :func:`kv_project_gather` -- the same with the history rows looked up in the shared
+  embedding table first, U = E[rows].  PAPER.md:407 (s4 serving: history sequence IDs looked up
+  in the shared embedding table to obtain U).
 * :func:`tasa_score`  -- candidate rows of the target-aware masked softmax attention over the
   request's history.  PAPER.md:341, 346 (s3.4.2).
 * :func:`full_masked_attention` -- brute force over the full (L+C)^2 mask.  SPEC.md:289-297.
@@ -161,6 +164,17 @@ def kv_project(U, W_k, W_v, H, d, act=1, b_k=None, b_v=None, threads=None):
                           pbk, pbv, H, d, act, _p(K, _c_f64p), _p(V, _c_f64p),
                           threads or default_threads())
     return K, V
+
+
+def kv_project_gather(E, rows, W_k, W_v, H, d, act=1, b_k=None, b_v=None, threads=None):
+    """K, V fp64 [H, len(rows), d] = act(E[rows] W^T + b): the lookup of the history IDs in the
+    shared embedding table, then :func:`kv_project`."""
+    import torch
+    E = E if isinstance(E, torch.Tensor) else torch.as_tensor(E)
+    idx = torch.as_tensor(np.asarray(rows, dtype=np.int64))
+    assert idx.numel() == 0 or (int(idx.min()) >= 0 and int(idx.max()) < E.shape[0])
+    U = E.index_select(0, idx)          # step 1: the table lookup (a library gather)
+    return kv_project(U, W_k, W_v, H, d, act=act, b_k=b_k, b_v=b_v, threads=threads)
 
 
 def tasa_score(T, cand_offsets, W_q, K, V, seq_offsets, H, d, act=1, b_q=None, scale=None,

@@ -5,6 +5,7 @@ memory and the current CUDA stream; there is NO CPU fallback: calling with CPU t
 without the built library, raises.
 
   kv_project(U, W_k, W_v, H, d, ...)      -> (K_cache, V_cache)   gesr_kv_project
+  kv_project_gather(E, rows, W_k, W_v, ...) -> (K_cache, V_cache)  gesr_kv_project_gather
   tasa_score(T, cand_offsets, W_q, K, V, seq_offsets, H, d, ...) -> (O, lse)   gesr_tasa_score
   hma_count(user_ids, user_offsets, item_ids, item_offsets, cand_offsets, F, cap) -> counts
   nro_cross_score(T, cand_offsets, W_q, q_gate, K, V, seq_offsets, j, d) -> T_cross
@@ -101,6 +102,8 @@ def lib():
             ("gesr_host_plan_destroy", ctypes.c_int, [_vp]),
             ("gesr_score_host", ctypes.c_int, [_vp, _i32, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp,
                                                _i32, _vp, _vp, _vp, _vp, _i32, _vp, _vp, _vp]),
+            ("gesr_kv_project_gather", ctypes.c_int, [_vp, _i64, _i32, _vp, _i64, _vp, _vp, _vp,
+                                                      _vp, _i32, _i32, _i32, _vp, _vp, _vp]),
     ):
         if not hasattr(L, name) and os.environ.get("GESR_LIB"):
             continue
@@ -181,6 +184,26 @@ def kv_project(U, W_k, W_v, H: int, d: int, act: int = GESR_ACT_SILU, b_k=None, 
     _check(lib().gesr_kv_project(_ptr(U), total_L, D_in, _ptr(W_k), _ptr(W_v), _ptr(b_k),
                                  _ptr(b_v), H, d, act, _ptr(K_cache), _ptr(V_cache),
                                  _stream(stream)))
+    return K_cache, V_cache
+
+
+@_on_stream
+def kv_project_gather(E, rows, W_k, W_v, H: int, d: int, act: int = GESR_ACT_SILU, b_k=None,
+                      b_v=None, K_cache=None, V_cache=None, stream=None):
+    """K_cache, V_cache bf16 [H, len(rows), d] = act(E[rows] W^T + b) with the table lookup
+    fused into the projection (gesr_kv_project_gather; E bf16 [n_E, D_in], rows int32)."""
+    _dev(E, rows, W_k, W_v, b_k, b_v, K_cache, V_cache)
+    if rows.dtype != torch.int32:
+        raise GesrError(GESR_ERR_INVALID_ARG, "rows must be int32")
+    n_E, D_in = E.shape
+    total_L = rows.numel()
+    if K_cache is None:
+        K_cache = torch.empty((H, total_L, d), dtype=torch.bfloat16, device=E.device)
+    if V_cache is None:
+        V_cache = torch.empty((H, total_L, d), dtype=torch.bfloat16, device=E.device)
+    _check(lib().gesr_kv_project_gather(_ptr(E), n_E, D_in, _ptr(rows), total_L, _ptr(W_k),
+                                        _ptr(W_v), _ptr(b_k), _ptr(b_v), H, d, act,
+                                        _ptr(K_cache), _ptr(V_cache), _stream(stream)))
     return K_cache, V_cache
 
 

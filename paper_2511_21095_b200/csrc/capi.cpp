@@ -216,14 +216,21 @@ size_t units_end(int64_t B, int64_t total_C) {
 }
 
 // Projection launch shared by K/V and Q: X [M, K] -> out0/out1 [H, M, d] head-major.
+// gather != NULL: X row m is row gather[m] of the [table_rows, K] table X (TMA gather4, box
+// {64 cols, 1 row}).
 gesr_status run_projection(const void* X, int64_t M, int32_t K, const void* W0, const void* W1,
                            const float* b0, const float* b1, int32_t H, int32_t d, int32_t act,
-                           void* out0, void* out1, cudaStream_t stream) {
+                           void* out0, void* out1, cudaStream_t stream,
+                           const int32_t* gather = nullptr, int64_t table_rows = 0) {
   const int HD = H * d;
   const int bn = gesr::proj_pick_bn(M, HD, W1 ? 2 : 1, num_sms());
   CUtensorMap ma, mb0, mb1;
-  gesr_status s = make_map_2d(&ma, X, static_cast<uint64_t>(M), static_cast<uint64_t>(K), 128, 64,
-                              CU_TENSOR_MAP_SWIZZLE_128B, "X");
+  gesr_status s = gather != nullptr
+                      ? make_map_2d(&ma, X, static_cast<uint64_t>(table_rows),
+                                    static_cast<uint64_t>(K), 1, 64, CU_TENSOR_MAP_SWIZZLE_128B,
+                                    "E (gather)")
+                      : make_map_2d(&ma, X, static_cast<uint64_t>(M), static_cast<uint64_t>(K),
+                                    128, 64, CU_TENSOR_MAP_SWIZZLE_128B, "X");
   if (s != GESR_OK) return s;
   // a CTA pair computes 256 x bn; each CTA stages its 128 rows of X and bn/2 weight rows
   s = make_map_2d(&mb0, W0, HD, K, bn / 2, 64, CU_TENSOR_MAP_SWIZZLE_128B, "W0");
@@ -247,6 +254,8 @@ gesr_status run_projection(const void* X, int64_t M, int32_t K, const void* W0, 
   p.bias1 = b1;
   p.out0 = static_cast<__nv_bfloat16*>(out0);
   p.out1 = static_cast<__nv_bfloat16*>(out1);
+  p.gather = gather;
+  p.table = gather != nullptr ? static_cast<const __nv_bfloat16*>(X) : nullptr;
   cudaError_t e = gesr::launch_proj(ma, mb0, mb1, mo0, mo1, p, bn, num_sms(), stream);
   if (e != cudaSuccess) return cuda_fail(e, "proj_kernel launch");
   return GESR_OK;
@@ -329,6 +338,29 @@ gesr_status gesr_kv_project(const void* U, int64_t total_L, int32_t D_in, const 
     return fail(GESR_ERR_INVALID_ARG, "pointers must be 16-byte aligned");
   return run_projection(U, total_L, D_in, W_k, W_v, b_k, b_v, H, d, act, K_cache, V_cache,
                         static_cast<cudaStream_t>(stream));
+}
+
+gesr_status gesr_kv_project_gather(const void* E, int64_t n_E, int32_t D_in, const int32_t* rows,
+                                   int64_t total_L, const void* W_k, const void* W_v,
+                                   const float* b_k, const float* b_v, int32_t H, int32_t d,
+                                   int32_t act, void* K_cache, void* V_cache, void* stream) {
+  gesr_status s = check_common(D_in, H, d, act);
+  if (s != GESR_OK) return s;
+  if (total_L < 0) return fail(GESR_ERR_INVALID_ARG, "total_L=%lld < 0", (long long)total_L);
+  if (total_L >= (int64_t(1) << 31) / H)
+    return fail(GESR_ERR_INVALID_ARG, "H*total_L exceeds the 2^31 TMA coordinate range");
+  if (n_E < 1 || n_E >= (int64_t(1) << 31))
+    return fail(GESR_ERR_INVALID_ARG, "n_E=%lld must be in [1, 2^31)", (long long)n_E);
+  if (total_L == 0) return GESR_OK;
+  if (!E || !rows || !W_k || !W_v || !K_cache || !V_cache)
+    return fail(GESR_ERR_INVALID_ARG, "null required pointer");
+  if (!aligned16(E) || !aligned16(W_k) || !aligned16(W_v) || !aligned16(K_cache) ||
+      !aligned16(V_cache) || !aligned16(b_k) || !aligned16(b_v))
+    return fail(GESR_ERR_INVALID_ARG, "pointers must be 16-byte aligned");
+  if ((reinterpret_cast<uintptr_t>(rows) & 3u) != 0)
+    return fail(GESR_ERR_INVALID_ARG, "rows must be 4-byte aligned");
+  return run_projection(E, total_L, D_in, W_k, W_v, b_k, b_v, H, d, act, K_cache, V_cache,
+                        static_cast<cudaStream_t>(stream), rows, n_E);
 }
 
 // Split-L (d = 128, pair kernel): a forced kv_splits = s > 1 cuts every (unit, head) into s

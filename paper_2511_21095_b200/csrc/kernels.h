@@ -70,6 +70,10 @@ struct ProjParams {
   // optional residual added after the activation: out[r][c] += residual[r * res_ld + c]
   const __nv_bfloat16* residual;
   int64_t res_ld;
+  // optional row gather (gesr_kv_project_gather): X row m is row gather[m] of the table that
+  // map_a describes (box {64, 1}); loaded by TMA tile::gather4, four rows per instruction
+  const int32_t* gather;
+  const __nv_bfloat16* table;   // the gathered table's base (row stride K), for L2 prefetch
 };
 
 // Tile width: the widest of 256 / 128 / 64 dividing N (the columns of one weight; `ways`

@@ -55,6 +55,10 @@ constexpr int kBK = 64;              // 64 bf16 = 128 bytes = one 128B-swizzle r
 constexpr int kEpiWarps = 16;        // 4 per SM sub-partition: latency hiding by TLP
 constexpr int kThreads = (4 + kEpiWarps) * 32;
 constexpr uint32_t kABytes = kBM * kBK * 2;   // 16 KB
+#ifndef GESR_GATHER_WARPS
+#define GESR_GATHER_WARPS 3
+#endif
+constexpr int kGatherWarps = GESR_GATHER_WARPS;   // warps issuing the gather4 loads (1-3)
 constexpr int kBoxes = 1;   // staging boxes per epilogue warp (2 measured slower: one fewer stage)
 
 template <int BN>
@@ -69,7 +73,8 @@ struct ProjSmem {
   static constexpr uint32_t kTmemCols = (2 * BN) < 32 ? 32 : 2 * BN;
   static constexpr uint32_t kStagingOffset = kStages * kStageBytes;
   static constexpr uint32_t kBarOffset = kStagingOffset + kStagingBytes;
-  static constexpr uint32_t kBytes = kBarOffset + 256 + 1024;  // + barriers + alignment slack
+  static constexpr uint32_t kIdsOffset = kBarOffset + 256;     // gathered row ids of a tile
+  static constexpr uint32_t kBytes = kIdsOffset + 512 + 1024;  // + ids + alignment slack
   static_assert(kBytes <= 232448, "shared memory budget");
 };
 
@@ -153,29 +158,59 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   pdl_launch_dependents();
   pdl_wait();         // the prologue above touched no global memory
 
-  if (warp == 0) {
-    if (elect_one()) {
-      // ---------------- TMA producer (both CTAs)
-      int stage = 0;
-      uint32_t phase = 0;
-      TileCursor cur(tiles);
-      for (int i = 0; i < my_tiles; ++i, cur.next()) {
-        const int m_blk = cur.m, n_blk = cur.n;
-        const int n0 = n_blk * BN;
-        // B comes from map_b0 for columns < n_split, else map_b1 (W_k / W_v stacked along N)
-        const CUtensorMap* mb = (n0 < p.n_split) ? &map_b0 : &map_b1;
-        const int nb = ((n0 < p.n_split) ? n0 : n0 - p.n_split) + static_cast<int>(rank) * (BN / 2);
-        const int ma = m_blk * 2 * kBM + static_cast<int>(rank) * kBM;
+  // gather issuers: warp 0, then warps 3 and 2 (idle otherwise; warp 2 only allocates TMEM)
+  const int issuer = warp == 0 ? 0 : (warp == 3 ? 1 : (warp == 2 ? 2 : -1));
+  if (warp == 0 || (p.gather != nullptr && issuer >= 0 && issuer < kGatherWarps)) {
+    // ---------------- TMA producer (both CTAs; one elected lane issues; warp 0 stages a tile's
+    // gathered row ids and, with a gather, kGatherWarps warps split its gather4 loads: one
+    // thread issuing ~256 gather4 per tile cannot keep up with the MMAs)
+    const bool helper = issuer != 0;
+    int4* ids = reinterpret_cast<int4*>(smem + S::kIdsOffset);
+    int stage = 0;
+    uint32_t phase = 0;
+    TileCursor cur(tiles);
+    for (int i = 0; i < my_tiles; ++i, cur.next()) {
+      const int m_blk = cur.m, n_blk = cur.n;
+      const int n0 = n_blk * BN;
+      // B comes from map_b0 for columns < n_split, else map_b1 (W_k / W_v stacked along N)
+      const CUtensorMap* mb = (n0 < p.n_split) ? &map_b0 : &map_b1;
+      const int nb = ((n0 < p.n_split) ? n0 : n0 - p.n_split) + static_cast<int>(rank) * (BN / 2);
+      const int ma = m_blk * 2 * kBM + static_cast<int>(rank) * kBM;
+      if (p.gather != nullptr && !helper) {
+        // rows ma + 4 lane .. + 3 of X are table rows gather[...]; rows past M repeat row M - 1
+        // (their outputs are clipped by the output map)
+        __syncwarp();
+        int r[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int64_t m = static_cast<int64_t>(ma) + 4 * lane + q;
+          r[q] = __ldg(p.gather + (m < p.M ? m : p.M - 1));
+        }
+        ids[lane] = make_int4(r[0], r[1], r[2], r[3]);
+        __syncwarp();
+      }
+      if (kGatherWarps > 1 && p.gather != nullptr) named_bar_sync(8, 32 * kGatherWarps);   // ids staged
+      if (elect_one()) {
+        const int ng = p.gather != nullptr ? kGatherWarps : 1;
+        const int g0 = issuer * (kBM / 4) / ng, g1 = (issuer + 1) * (kBM / 4) / ng;
         for (int kb = 0; kb < num_kb; ++kb) {
           PROF_WAIT(0, mbar_wait_sleep(&empty_bar[stage], phase ^ 1));
           uint8_t* sa = smem + stage * S::kStageBytes;
           uint8_t* sb = sa + kABytes;
-          if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], 2 * S::kStageBytes);
-          tma_load_2d_pair(sa, &map_a, &full_bar[stage], kb * kBK, ma);
-          tma_load_2d_pair(sb, mb, &full_bar[stage], kb * kBK, nb);
+          if (rank == 0 && !helper) mbar_arrive_expect_tx(&full_bar[stage], 2 * S::kStageBytes);
+          if (p.gather != nullptr) {
+#pragma unroll 4
+            for (int g = g0; g < g1; ++g)
+              tma_gather4_pair(sa + g * 4 * kBK * 2, &map_a, &full_bar[stage], kb * kBK, ids[g]);
+          } else {
+            tma_load_2d_pair(sa, &map_a, &full_bar[stage], kb * kBK, ma);
+          }
+          if (!helper) tma_load_2d_pair(sb, mb, &full_bar[stage], kb * kBK, nb);
           if (++stage == S::kStages) { stage = 0; phase ^= 1; }
         }
       }
+      __syncwarp();
+      if (kGatherWarps > 1 && p.gather != nullptr) named_bar_sync(8, 32 * kGatherWarps);   // ids consumed
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer (leader CTA only)

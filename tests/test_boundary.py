@@ -59,6 +59,27 @@ def kv(L, U=FAKE, total_L=10, D_in=64, Wk=FAKE, Wv=FAKE, bk=None, bv=None, H=2, 
     return L.gesr_kv_project(U, total_L, D_in, Wk, Wv, bk, bv, H, d, act, K, V, None)
 
 
+def kvg(L, E=FAKE, n_E=100, D_in=64, rows=FAKE, total_L=10, Wk=FAKE, Wv=FAKE, H=2, d=64, act=1,
+        K=FAKE, V=FAKE):
+    return L.gesr_kv_project_gather(E, n_E, D_in, rows, total_L, Wk, Wv, None, None, H, d, act,
+                                    K, V, None)
+
+
+def test_kv_project_gather_validation(L):
+    """gesr_kv_project_gather rejects bad arguments before any launch (no GPU needed)."""
+    assert kvg(L, n_E=0) == gb.GESR_ERR_INVALID_ARG
+    assert "n_E" in L.gesr_last_error().decode()
+    assert kvg(L, n_E=1 << 31) == gb.GESR_ERR_INVALID_ARG
+    assert kvg(L, d=48) == gb.GESR_ERR_INVALID_ARG
+    assert kvg(L, D_in=20) == gb.GESR_ERR_INVALID_ARG
+    assert kvg(L, total_L=-1) == gb.GESR_ERR_INVALID_ARG
+    assert kvg(L, rows=None) == gb.GESR_ERR_INVALID_ARG
+    assert kvg(L, E=None) == gb.GESR_ERR_INVALID_ARG
+    assert kvg(L, E=MIS) == gb.GESR_ERR_INVALID_ARG
+    assert kvg(L, rows=P(0x10002)) == gb.GESR_ERR_INVALID_ARG
+    assert kvg(L, total_L=0, rows=None) == gb.GESR_OK      # empty problem: valid no-op
+
+
 def test_kv_project_validation(L):
     assert kv(L, d=48) == gb.GESR_ERR_INVALID_ARG
     assert "d=48" in L.gesr_last_error().decode()

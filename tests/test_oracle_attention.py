@@ -64,6 +64,36 @@ def test_kv_project_equals_torch_linear(act):
     np.testing.assert_allclose(V, Vt, rtol=1e-13, atol=1e-13)
 
 
+@pytest.mark.parametrize("act", [0, 1])
+def test_kv_project_gather_pins(act):
+    """oracle.kv_project_gather (the history rows are the shared embedding
+    table's rows of the history IDs): each output row is torch fp64 linear(+SiLU) of the table
+    row its ID names, written out row by row with scalar Python loops on a small case (a wrong
+    index, e.g. position m instead of rows[m], or a transposed W fails); repeated IDs give
+    identical rows; permuting the IDs permutes the rows."""
+    g = torch.Generator().manual_seed(7)
+    H, d, D_in, n_E = 2, 4, 8, 11
+    E = _rand_bf16(g, n_E, D_in)
+    Wk = _rand_bf16(g, H * d, D_in, scale=0.3)
+    Wv = _rand_bf16(g, H * d, D_in, scale=0.3)
+    rows = np.array([3, 10, 0, 3, 7, 7, 1], dtype=np.int32)
+    K, V = oracle.kv_project_gather(E, rows, Wk, Wv, H, d, act=act)
+    Ef, Wkf, Wvf = E.double().numpy(), Wk.double().numpy(), Wv.double().numpy()
+    for m, r in enumerate(rows):
+        for h in range(H):
+            for j in range(d):
+                n = h * d + j
+                yk = sum(Ef[r, k] * Wkf[n, k] for k in range(D_in))
+                yv = sum(Ef[r, k] * Wvf[n, k] for k in range(D_in))
+                if act:
+                    yk, yv = yk / (1 + math.exp(-yk)), yv / (1 + math.exp(-yv))
+                assert abs(K[h, m, j] - yk) < 1e-12 and abs(V[h, m, j] - yv) < 1e-12
+    assert np.array_equal(K[:, 0], K[:, 3]) and np.array_equal(V[:, 4], V[:, 5])
+    perm = np.array([6, 2, 0, 5, 1, 4, 3])
+    Kp, Vp = oracle.kv_project_gather(E, rows[perm], Wk, Wv, H, d, act=act)
+    assert np.array_equal(Kp, K[:, perm]) and np.array_equal(Vp, V[:, perm])
+
+
 def _oracle_tasa(so, co, U, T, Wq, Wk, Wv, H, d, act, scale=None):
     K, V = oracle.kv_project(U, Wk, Wv, H, d, act=act)
     return oracle.tasa_score(T, co, Wq, K, V, so, H, d, act=act, scale=scale)
