@@ -23,6 +23,9 @@
 //             arrival on the leader's TMEM-empty barrier (no CTA-wide barrier: the slowest
 //             warp no longer holds the others).  (Direct per-thread 16-byte global stores
 //             touched 32 rows per instruction and capped the kernel at ~35% tensor-pipe.)
+// Gather mode (gesr_kv_project_gather): X row m is table row gather[m]; warp 0
+// stages a tile's 128 row ids in shared memory and warps 0, 3 and 2 issue the A operand as TMA
+// tile::gather4 loads (four 128-byte table-row slices each, same 128B-swizzled layout).
 // The epilogue of tile i overlaps the MMAs of tile i+1.  Tile order is m-major for large M
 // (ProjTiles): a pair takes all n-blocks of one 256-row block back to back, so X is read from
 // HBM exactly once (ncu: 2.16 GB DRAM reads for the 2.15 GB U, against 3.0 GB interleaved).
