@@ -177,6 +177,25 @@ gesr_status gesr_tasa_score(const void* T, int64_t total_C, int32_t D_in,
                             void* workspace, size_t workspace_bytes,
                             void* stream);
 
+/* gesr_tasa_score_gather -- gesr_tasa_score with the candidate rows looked up in the shared
+ * embedding table inside the Q projection: T[t] = E[rows[t]] (the candidate POST
+ * IDs looked up in the shared table to obtain T), as gesr_kv_project_gather does
+ * for the history.  The looked-up rows are never written to memory (TMA tile::gather4 loads).
+ *   E        bf16 [n_E, D_in] row-major table, 1 <= n_E < 2^31, 16-byte aligned.
+ *   rows     int32 [total_C], 4-byte aligned; 0 <= rows[t] < n_E is required and not checked.
+ * All other arguments, the workspace size and the error behaviour are those of
+ * gesr_tasa_score (flag GESR_TASA_SELF_KEY -> GESR_ERR_UNSUPPORTED); the result is bit-identical
+ * to gesr_tasa_score on the materialised T = E[rows]. */
+gesr_status gesr_tasa_score_gather(const void* E, int64_t n_E, int32_t D_in, const int32_t* rows,
+                                   int64_t total_C, const int64_t* cand_offsets,
+                                   const void* W_q, const float* b_q, int32_t act,
+                                   const void* K_cache, const void* V_cache,
+                                   const int64_t* seq_offsets, int64_t B, int64_t total_L,
+                                   int32_t H, int32_t d, float scale, int32_t kv_splits,
+                                   uint32_t flags, void* O, int32_t o_dtype, float* lse,
+                                   void* workspace, size_t workspace_bytes,
+                                   void* stream);
+
 /* gesr_tasa_score_self -- gesr_tasa_score with the candidate SELF KEY: each candidate also
  * attends to its own key (the diagonal SPEC.md's mask keeps; DESIGN.md
  * reading R2 -- SURVEY s8(f) f1, the first piece of the full STU candidate row):

@@ -104,6 +104,10 @@ def lib():
                                                _i32, _vp, _vp, _vp, _vp, _i32, _vp, _vp, _vp]),
             ("gesr_kv_project_gather", ctypes.c_int, [_vp, _i64, _i32, _vp, _i64, _vp, _vp, _vp,
                                                       _vp, _i32, _i32, _i32, _vp, _vp, _vp]),
+            ("gesr_tasa_score_gather", ctypes.c_int, [_vp, _i64, _i32, _vp, _i64, _vp, _vp, _vp,
+                                                      _i32, _vp, _vp, _vp, _i64, _i64, _i32, _i32,
+                                                      ctypes.c_float, _i32, ctypes.c_uint32, _vp,
+                                                      _i32, _vp, _vp, ctypes.c_size_t, _vp]),
     ):
         if not hasattr(L, name) and os.environ.get("GESR_LIB"):
             continue
@@ -245,6 +249,37 @@ def tasa_score(T, cand_offsets, W_q, K_cache, V_cache, seq_offsets, H: int, d: i
                                  B, total_L, H, d, float(scale), kv_splits, flags, _ptr(O),
                                  o_dtype, _ptr(lse), _ptr(workspace), workspace.numel(),
                                  _stream(stream)))
+    return O, lse
+
+
+@_on_stream
+def tasa_score_gather(E, rows, cand_offsets, W_q, K_cache, V_cache, seq_offsets, H: int, d: int,
+                      act: int = GESR_ACT_SILU, b_q=None, scale: float = 0.0, kv_splits: int = 0,
+                      flags: int = 0, out_dtype=torch.float32, want_lse: bool = True, O=None,
+                      lse=None, workspace=None, stream=None):
+    """gesr_tasa_score_gather: tasa_score with T = E[rows] looked up inside the Q projection
+    (E bf16 [n_E, D_in], rows int32 [total_C])."""
+    _dev(E, rows, cand_offsets, W_q, K_cache, V_cache, seq_offsets, b_q, O, lse, workspace)
+    if rows.dtype != torch.int32:
+        raise GesrError(GESR_ERR_INVALID_ARG, "rows must be int32")
+    n_E, D_in = E.shape
+    total_C = rows.numel()
+    B = cand_offsets.numel() - 1
+    total_L = K_cache.shape[1]
+    if O is None:
+        O = torch.empty((total_C, H * d), dtype=out_dtype, device=E.device)
+    o_dtype = GESR_OUT_BF16 if O.dtype == torch.bfloat16 else GESR_OUT_F32
+    if lse is None and want_lse:
+        lse = torch.empty((total_C, H), dtype=torch.float32, device=E.device)
+    if workspace is None:
+        nbytes = tasa_workspace_bytes(B, total_C, H, d, kv_splits)
+        workspace = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=E.device)
+    _check(lib().gesr_tasa_score_gather(_ptr(E), n_E, D_in, _ptr(rows), total_C,
+                                        _ptr(cand_offsets), _ptr(W_q), _ptr(b_q), act,
+                                        _ptr(K_cache), _ptr(V_cache), _ptr(seq_offsets), B,
+                                        total_L, H, d, float(scale), kv_splits, flags, _ptr(O),
+                                        o_dtype, _ptr(lse), _ptr(workspace), workspace.numel(),
+                                        _stream(stream)))
     return O, lse
 
 

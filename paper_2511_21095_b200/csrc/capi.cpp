@@ -418,7 +418,10 @@ static gesr_status tasa_impl(const void* T, int64_t total_C, int32_t D_in, const
                       int32_t H, int32_t d, float scale, int32_t kv_splits, uint32_t flags,
                       const void* K_self, const void* V_self, void* O, int32_t o_dtype,
                       float* lse, void* workspace, size_t workspace_bytes, void* stream,
-                      int causal = 0, bool validate_only = false) {
+                      int causal = 0, bool validate_only = false,
+                      const int32_t* t_rows = nullptr, int64_t n_E = 0) {
+  // t_rows != NULL (gesr_tasa_score_gather): T is an [n_E, D_in] table and candidate row t is
+  // its row t_rows[t], gathered by the Q projection
   const bool self = K_self != nullptr || V_self != nullptr;
   gesr_status s = check_common(D_in, H, d, act);
   if (s != GESR_OK) return s;
@@ -451,6 +454,8 @@ static gesr_status tasa_impl(const void* T, int64_t total_C, int32_t D_in, const
   if (total_C == 0 || B == 0) return GESR_OK;
   if (!T || !cand_offsets || !W_q || !seq_offsets || !O || !workspace)
     return fail(GESR_ERR_INVALID_ARG, "null required pointer");
+  if (t_rows != nullptr && (reinterpret_cast<uintptr_t>(t_rows) & 3u) != 0)
+    return fail(GESR_ERR_INVALID_ARG, "rows must be 4-byte aligned");
   if (total_L > 0 && (!K_cache || !V_cache))
     return fail(GESR_ERR_INVALID_ARG, "null K/V cache with total_L > 0");
   if (self && (!K_self || !V_self || !aligned16(K_self) || !aligned16(V_self)))
@@ -510,7 +515,8 @@ static gesr_status tasa_impl(const void* T, int64_t total_C, int32_t D_in, const
     cudaError_t e = gesr::launch_attn_empty(p, d, st);
     if (e != cudaSuccess) return cuda_fail(e, "attn_empty launch");
     if (!self) return GESR_OK;
-    s = run_projection(T, total_C, D_in, W_q, nullptr, b_q, nullptr, H, d, act, Q, nullptr, st);
+    s = run_projection(T, total_C, D_in, W_q, nullptr, b_q, nullptr, H, d, act, Q, nullptr, st,
+                       t_rows, n_E);
     if (s != GESR_OK) return s;
     return self_merge();
   }
@@ -532,7 +538,8 @@ static gesr_status tasa_impl(const void* T, int64_t total_C, int32_t D_in, const
     e = gesr::launch_build_units(seq_offsets, cand_offsets, B, units, count, causal, st);
     if (e != cudaSuccess) return cuda_fail(e, "build_units launch");
   }
-  s = run_projection(T, total_C, D_in, W_q, nullptr, b_q, nullptr, H, d, act, Q, nullptr, st);
+  s = run_projection(T, total_C, D_in, W_q, nullptr, b_q, nullptr, H, d, act, Q, nullptr, st,
+                       t_rows, n_E);
   if (s != GESR_OK) return s;
 
   CUtensorMap mq, mk, mv;
@@ -578,6 +585,24 @@ gesr_status gesr_tasa_score(const void* T, int64_t total_C, int32_t D_in,
   return tasa_impl(T, total_C, D_in, cand_offsets, W_q, b_q, act, K_cache, V_cache, seq_offsets,
                    B, total_L, H, d, scale, kv_splits, flags, nullptr, nullptr, O, o_dtype, lse,
                    workspace, workspace_bytes, stream);
+}
+
+gesr_status gesr_tasa_score_gather(const void* E, int64_t n_E, int32_t D_in, const int32_t* rows,
+                                   int64_t total_C, const int64_t* cand_offsets, const void* W_q,
+                                   const float* b_q, int32_t act, const void* K_cache,
+                                   const void* V_cache, const int64_t* seq_offsets, int64_t B,
+                                   int64_t total_L, int32_t H, int32_t d, float scale,
+                                   int32_t kv_splits, uint32_t flags, void* O, int32_t o_dtype,
+                                   float* lse, void* workspace, size_t workspace_bytes,
+                                   void* stream) {
+  if (n_E < 1 || n_E >= (int64_t(1) << 31))
+    return fail(GESR_ERR_INVALID_ARG, "n_E=%lld must be in [1, 2^31)", (long long)n_E);
+  if (total_C > 0 && B > 0 && !rows) return fail(GESR_ERR_INVALID_ARG, "null required pointer");
+  if (flags & GESR_TASA_SELF_KEY)
+    return fail(GESR_ERR_UNSUPPORTED, "GESR_TASA_SELF_KEY is not offered with the gather");
+  return tasa_impl(E, total_C, D_in, cand_offsets, W_q, b_q, act, K_cache, V_cache, seq_offsets,
+                   B, total_L, H, d, scale, kv_splits, flags, nullptr, nullptr, O, o_dtype, lse,
+                   workspace, workspace_bytes, stream, 0, false, rows, n_E);
 }
 
 gesr_status gesr_tasa_score_self(const void* T, int64_t total_C, int32_t D_in,

@@ -80,6 +80,20 @@ def test_kv_project_gather_validation(L):
     assert kvg(L, total_L=0, rows=None) == gb.GESR_OK      # empty problem: valid no-op
 
 
+def test_tasa_score_gather_validation(L):
+    """gesr_tasa_score_gather: table size, rows alignment and the unsupported self-key flag
+    are rejected before any launch."""
+    def call(n_E=100, rows=FAKE, flags=0, total_C=10, B=2):
+        return L.gesr_tasa_score_gather(FAKE, n_E, 64, rows, total_C, FAKE, FAKE, None, 1, FAKE,
+                                        FAKE, FAKE, B, 20, 2, 64, 0.0, 0, flags, FAKE, 0, None,
+                                        P(0x100000), 1 << 30, None)
+    assert call(n_E=0) == gb.GESR_ERR_INVALID_ARG
+    assert call(rows=None) == gb.GESR_ERR_INVALID_ARG
+    assert call(rows=P(0x10002)) == gb.GESR_ERR_INVALID_ARG
+    assert call(flags=1) == gb.GESR_ERR_UNSUPPORTED
+    assert call(total_C=0, rows=None) == gb.GESR_OK
+
+
 def test_kv_project_validation(L):
     assert kv(L, d=48) == gb.GESR_ERR_INVALID_ARG
     assert "d=48" in L.gesr_last_error().decode()

@@ -75,3 +75,52 @@ def test_kv_project_gather_feeds_attention_like_dense():
                           cfg.act, kv_splits=1)
     torch.cuda.synchronize()
     assert torch.equal(O, O0)
+
+
+@pytest.mark.parametrize("name,B,kv_splits", [("2", 16, 1), ("3", 6, 0), ("4", 1, 0)])
+def test_tasa_score_gather_bit_identical_to_materialised(name, B, kv_splits):
+    """gesr_tasa_score_gather (T = E[rows] inside the Q projection) equals gesr_tasa_score on the
+    materialised T, for the 1-CTA (d = 64) and CTA-pair (d = 128, split-L at B = 1) kernels."""
+    dev = _cuda()
+    cfg = configs.get(name).with_(B=B)
+    bt = inputs.make_batch(cfg, hma=False, device=dev)
+    n_E = 2000
+    g = torch.Generator().manual_seed(11)
+    E = torch.randn(n_E, cfg.D_in, generator=g).to(torch.bfloat16).to(dev)
+    rows = torch.randint(0, n_E, (bt.total_C,), generator=g, dtype=torch.int32).to(dev)
+    K, V = gb.kv_project(bt.U, bt.W_k, bt.W_v, cfg.H, cfg.d, cfg.act)
+    O, lse = gb.tasa_score_gather(E, rows, bt.cand_offsets, bt.W_q, K, V, bt.seq_offsets, cfg.H,
+                                  cfg.d, cfg.act, kv_splits=kv_splits)
+    O0, lse0 = gb.tasa_score(E.index_select(0, rows.long()), bt.cand_offsets, bt.W_q, K, V,
+                             bt.seq_offsets, cfg.H, cfg.d, cfg.act, kv_splits=kv_splits)
+    torch.cuda.synchronize()
+    assert torch.equal(O, O0) and torch.equal(lse, lse0)
+
+
+def test_fused_lookup_step_matches_oracle():
+    """The serving step with both lookups fused (history and candidate IDs looked
+    up in ONE shared table, then the MoA attention): gesr_kv_project_gather +
+    gesr_tasa_score_gather against the fp64 oracle on the looked-up rows, within the attention
+    tolerance of tests/test_gpu_parity.py."""
+    from test_gpu_parity import MAX_ABS, MEAN_ABS
+    dev = _cuda()
+    cfg = configs.get("3").with_(B=3, L=("uniform", 1, 300), C=("uniform", 1, 300))
+    bt = inputs.make_batch(cfg, hma=False)
+    n_E = 5000
+    g = torch.Generator().manual_seed(13)
+    E = torch.randn(n_E, cfg.D_in, generator=g).to(torch.bfloat16)
+    hist = torch.randint(0, n_E, (bt.U.shape[0],), generator=g, dtype=torch.int32)
+    cand = torch.randint(0, n_E, (bt.total_C,), generator=g, dtype=torch.int32)
+    Eg = E.to(dev)
+    K, V = gb.kv_project_gather(Eg, hist.to(dev), bt.W_k.to(dev), bt.W_v.to(dev), cfg.H, cfg.d,
+                                cfg.act)
+    O, _ = gb.tasa_score_gather(Eg, cand.to(dev), bt.cand_offsets.to(dev), bt.W_q.to(dev), K, V,
+                                bt.seq_offsets.to(dev), cfg.H, cfg.d, cfg.act)
+    torch.cuda.synchronize()
+    K_or, V_or = oracle.kv_project_gather(E, hist.numpy(), bt.W_k, bt.W_v, cfg.H, cfg.d,
+                                          act=cfg.act)
+    T = E.index_select(0, cand.long())
+    O_or, _ = oracle.tasa_score(T, bt.cand_offsets, bt.W_q, K_or, V_or, bt.seq_offsets, cfg.H,
+                                cfg.d, act=cfg.act)
+    err = np.abs(O.cpu().numpy().astype(np.float64) - O_or)
+    assert err.max() < MAX_ABS and err.mean() < MEAN_ABS, (err.max(), err.mean())
