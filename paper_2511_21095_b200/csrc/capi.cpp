@@ -255,7 +255,6 @@ gesr_status run_projection(const void* X, int64_t M, int32_t K, const void* W0, 
   p.out0 = static_cast<__nv_bfloat16*>(out0);
   p.out1 = static_cast<__nv_bfloat16*>(out1);
   p.gather = gather;
-  p.table = gather != nullptr ? static_cast<const __nv_bfloat16*>(X) : nullptr;
   cudaError_t e = gesr::launch_proj(ma, mb0, mb1, mo0, mo1, p, bn, num_sms(), stream);
   if (e != cudaSuccess) return cuda_fail(e, "proj_kernel launch");
   return GESR_OK;

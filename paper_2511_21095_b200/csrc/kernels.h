@@ -73,7 +73,6 @@ struct ProjParams {
   // optional row gather (gesr_kv_project_gather): X row m is row gather[m] of the table that
   // map_a describes (box {64, 1}); loaded by TMA tile::gather4, four rows per instruction
   const int32_t* gather;
-  const __nv_bfloat16* table;   // the gathered table's base (row stride K), for L2 prefetch
 };
 
 // Tile width: the widest of 256 / 128 / 64 dividing N (the columns of one weight; `ways`
