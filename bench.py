@@ -587,6 +587,44 @@ def main():
                                     "copy": f"pinned host -> device, {src.numel() * 2 >> 20} MiB, "
                                             "best of 3, measured in this run"}
         del dst
+        # the serving form of PAPER.md:407: the host sends table row ids, the shared embedding
+        # table stays on the device (here a random row permutation of [U; T], so E[rows]
+        # reproduces this batch exactly) and the projections gather the rows
+        nL, nC = batch.U.shape[0], batch.T.shape[0]
+        gperm = torch.Generator().manual_seed(2511)
+        perm = torch.randperm(nL + nC, generator=gperm)
+        E_tab = torch.cat([batch.U, batch.T]).index_select(0, perm.to(dev))
+        inv = torch.empty_like(perm)
+        inv[perm] = torch.arange(nL + nC)
+        hist_rows = inv[:nL].to(torch.int32).pin_memory()
+        cand_rows = inv[nL:].to(torch.int32).pin_memory()
+        h_O2 = torch.empty_like(h_O).pin_memory()
+        h_c2 = torch.empty_like(h_counts).pin_memory()
+        scorer.run_ids(E_tab, hist_rows, cand_rows, h_O2, h_c2, stream=main_stream)
+        torch.cuda.synchronize()
+        same = bool(torch.equal(h_O2, h_O) and torch.equal(h_c2, h_counts))
+        if world > 1:
+            dist.barrier()
+        a.record(main_stream)
+        for _ in range(n_e2e):
+            scorer.run_ids(E_tab, hist_rows, cand_rows, h_O2, h_c2, stream=main_stream)
+        b.record(main_stream)
+        torch.cuda.synchronize()
+        i_ms = a.elapsed_time(b)
+        if world > 1:
+            t = torch.tensor([i_ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            i_ms = float(t.item())
+        line["e2e_ids"] = {
+            "value": res["cands_per_step"] * n_e2e / (i_ms / 1e3), "unit": UNIT,
+            "h2d_bytes_per_step": scorer.h2d_bytes_ids(hist_rows, cand_rows),
+            "d2h_bytes_per_step": d2h, "steps": n_e2e,
+            "api": "gesr_score_host_ids (C ABI: host row ids, device-resident embedding table "
+                   "gathered inside the projections, PAPER.md:407)",
+            "table": f"{nL + nC} rows x {cfg.D_in} bf16 on the device (a row permutation of "
+                     "[U; T]): model state like the weights, not a per-step input",
+            "bit_identical_to_e2e": same}
+        del E_tab
 
     # ---------------------------------------------------------------- optional score gather
     if args.gather and world > 1:

@@ -425,6 +425,26 @@ gesr_status gesr_score_host(gesr_host_plan* plan, int32_t n_chunks,
                             const int64_t* item_ids, const int64_t* item_offsets, int32_t cap,
                             void* O, int32_t* counts, void* stream);
 
+/* gesr_score_host_ids -- gesr_score_host for the serving form PAPER.md:407 describes: the host
+ * holds IDs, not embeddings ("MoA serving combines the item POST ID with the user history
+ * sequence IDs ... looked up in the shared embedding table ... to obtain the input embeddings
+ * U, T").  The table stays resident on the device; per chunk only the int32 row ids (with the
+ * HMA lists and offsets) cross PCIe, and the projections gather the rows
+ * (gesr_kv_project_gather, gesr_tasa_score_gather).
+ *   E          DEVICE bf16 [n_E, D_in] embedding table (plan's D_in), 1 <= n_E < 2^31.
+ *   hist_rows  HOST int32 [seq_offsets[B]]: table row of each history row (replaces U).
+ *   cand_rows  HOST int32 [cand_offsets[B]]: table row of each candidate (replaces T).
+ * Everything else, the plan and the error behaviour as gesr_score_host; the results equal
+ * gesr_score_host's on U = E[hist_rows], T = E[cand_rows] bit for bit. */
+gesr_status gesr_score_host_ids(gesr_host_plan* plan, int32_t n_chunks,
+                                const void* E, int64_t n_E,
+                                const int32_t* hist_rows, const int64_t* seq_offsets,
+                                const int32_t* cand_rows, const int64_t* cand_offsets, int64_t B,
+                                const void* W_q, const void* W_k, const void* W_v, int32_t act,
+                                const int64_t* user_ids, const int64_t* user_offsets,
+                                const int64_t* item_ids, const int64_t* item_offsets, int32_t cap,
+                                void* O, int32_t* counts, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

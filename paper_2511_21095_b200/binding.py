@@ -102,6 +102,9 @@ def lib():
             ("gesr_host_plan_destroy", ctypes.c_int, [_vp]),
             ("gesr_score_host", ctypes.c_int, [_vp, _i32, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp,
                                                _i32, _vp, _vp, _vp, _vp, _i32, _vp, _vp, _vp]),
+            ("gesr_score_host_ids", ctypes.c_int, [_vp, _i32, _vp, _i64, _vp, _vp, _vp, _vp,
+                                                   _i64, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _vp,
+                                                   _i32, _vp, _vp, _vp]),
             ("gesr_kv_project_gather", ctypes.c_int, [_vp, _i64, _i32, _vp, _i64, _vp, _vp, _vp,
                                                       _vp, _i32, _i32, _i32, _vp, _vp, _vp]),
             ("gesr_tasa_score_gather", ctypes.c_int, [_vp, _i64, _i32, _vp, _i64, _vp, _vp, _vp,
@@ -634,6 +637,28 @@ class HostPlan:
             _ptr(hb.cand_offsets), hb.B, _ptr(W_q), _ptr(W_k), _ptr(W_v), self.act,
             _ptr(hb.user_ids), _ptr(hb.user_offsets), _ptr(hb.item_ids), _ptr(hb.item_offsets),
             self.cap, _ptr(h_O), _ptr(h_counts), _stream(stream)))
+
+    def run_ids(self, E, hist_rows, cand_rows, h_O, h_counts, stream=None):
+        """gesr_score_host_ids: the same step with the host holding int32 table row ids
+        (hist_rows [total_L], cand_rows [total_C]) instead of U / T; E is the device-resident
+        bf16 [n_E, D_in] shared embedding table."""
+        hb = self.hb
+        W_q, W_k, W_v = self.W
+        for t in (hist_rows, cand_rows):
+            if t.dtype != torch.int32 or t.is_cuda:
+                raise GesrError(GESR_ERR_INVALID_ARG, "row ids must be int32 host tensors")
+        _check(lib().gesr_score_host_ids(
+            self._plan, self.n_chunks, _ptr(E), E.shape[0], _ptr(hist_rows),
+            _ptr(hb.seq_offsets), _ptr(cand_rows), _ptr(hb.cand_offsets), hb.B, _ptr(W_q),
+            _ptr(W_k), _ptr(W_v), self.act, _ptr(hb.user_ids), _ptr(hb.user_offsets),
+            _ptr(hb.item_ids), _ptr(hb.item_offsets), self.cap, _ptr(h_O), _ptr(h_counts),
+            _stream(stream)))
+
+    def h2d_bytes_ids(self, hist_rows, cand_rows):
+        """Host->device bytes per run_ids: the row ids replace U and T."""
+        hb = self.hb
+        return self.h2d_bytes - sum(t.numel() * t.element_size() for t in (hb.U, hb.T)) + \
+            4 * (hist_rows.numel() + cand_rows.numel())
 
     def close(self):
         if getattr(self, "_plan", None) and self._plan.value:

@@ -182,7 +182,14 @@ gesr_status gesr_host_plan_create(const int64_t* maxima, int32_t D_in, int32_t H
   return GESR_OK;
 }
 
-gesr_status gesr_score_host(gesr_host_plan* plan, int32_t n_chunks,
+}  // extern "C"
+
+namespace {
+
+// The chunk pipeline of gesr_score_host (E == NULL: U / T are host bf16 rows) and
+// gesr_score_host_ids (E != NULL: U / T are host int32 row ids into the device table E, and
+// the projections gather the rows themselves).
+gesr_status score_host_impl(gesr_host_plan* plan, int32_t n_chunks, const void* E, int64_t n_E,
                             const void* U, const int64_t* seq_offsets,
                             const void* T, const int64_t* cand_offsets, int64_t B,
                             const void* W_q, const void* W_k, const void* W_v, int32_t act,
@@ -212,6 +219,8 @@ gesr_status gesr_score_host(gesr_host_plan* plan, int32_t n_chunks,
   const size_t HD = static_cast<size_t>(H) * d;
   const size_t osz = plan->o_dtype == GESR_OUT_BF16 ? 2 : 4;
   const float scale = 1.0f / std::sqrt(static_cast<float>(d));
+  const bool ids = E != nullptr;
+  const size_t row_bytes = ids ? 4 : static_cast<size_t>(D_in) * 2;   // per U / T row
   const char* Uh = static_cast<const char*>(U);
   const char* Th = static_cast<const char*>(T);
   char* Oh = static_cast<char*>(O);
@@ -234,8 +243,8 @@ gesr_status gesr_score_host(gesr_host_plan* plan, int32_t n_chunks,
     h2d(s.co, cand_offsets + c.b0, (nB + 1) * 8);
     h2d(s.uo, user_offsets + c.b0 * F, (nB * F + 1) * 8);
     h2d(s.io, item_offsets + c.c0 * F, (nC * F + 1) * 8);
-    h2d(s.U, Uh + c.r0 * D_in * 2, nL * D_in * 2);
-    h2d(s.T, Th + c.c0 * D_in * 2, nC * D_in * 2);
+    h2d(s.U, Uh + c.r0 * row_bytes, nL * row_bytes);
+    h2d(s.T, Th + c.c0 * row_bytes, nC * row_bytes);
     h2d(s.ui, user_ids + c.u0, nU * 8);
     h2d(s.ii, item_ids + c.i0, nI * 8);
     if (e == cudaSuccess) e = cudaEventRecord(s.h2d, plan->s_in);
@@ -250,10 +259,17 @@ gesr_status gesr_score_host(gesr_host_plan* plan, int32_t n_chunks,
     if (e != cudaSuccess) return hcuda(e, "gesr_score_host: rebase_kernel launch");
     gesr_status r = GESR_OK;
     if (nL > 0)
-      r = gesr_kv_project(s.U, nL, D_in, W_k, W_v, nullptr, nullptr, H, d, act, s.K, s.V, st);
+      r = ids ? gesr_kv_project_gather(E, n_E, D_in, static_cast<const int32_t*>(s.U), nL, W_k,
+                                       W_v, nullptr, nullptr, H, d, act, s.K, s.V, st)
+              : gesr_kv_project(s.U, nL, D_in, W_k, W_v, nullptr, nullptr, H, d, act, s.K, s.V,
+                                st);
     if (r == GESR_OK)
-      r = gesr_tasa_score(s.T, nC, D_in, s.co, W_q, nullptr, act, s.K, s.V, s.so, nB, nL, H, d,
-                          scale, 0, 0u, s.O, plan->o_dtype, nullptr, s.ws, s.ws_bytes, st);
+      r = ids ? gesr_tasa_score_gather(E, n_E, D_in, static_cast<const int32_t*>(s.T), nC, s.co,
+                                       W_q, nullptr, act, s.K, s.V, s.so, nB, nL, H, d, scale, 0,
+                                       0u, s.O, plan->o_dtype, nullptr, s.ws, s.ws_bytes, st)
+              : gesr_tasa_score(s.T, nC, D_in, s.co, W_q, nullptr, act, s.K, s.V, s.so, nB, nL,
+                                H, d, scale, 0, 0u, s.O, plan->o_dtype, nullptr, s.ws,
+                                s.ws_bytes, st);
     if (r == GESR_OK)
       r = gesr_hma_count(s.ui, s.uo, s.ii, s.io, s.co, nB, nC, F, cap, s.counts, st);
     if (r != GESR_OK) return r;
@@ -270,6 +286,38 @@ gesr_status gesr_score_host(gesr_host_plan* plan, int32_t n_chunks,
   e = cudaEventRecord(plan->end, plan->s_out);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(st, plan->end, 0);
   return e == cudaSuccess ? GESR_OK : hcuda(e, "gesr_score_host: join");
+}
+
+}  // namespace
+
+extern "C" {
+
+gesr_status gesr_score_host(gesr_host_plan* plan, int32_t n_chunks,
+                            const void* U, const int64_t* seq_offsets,
+                            const void* T, const int64_t* cand_offsets, int64_t B,
+                            const void* W_q, const void* W_k, const void* W_v, int32_t act,
+                            const int64_t* user_ids, const int64_t* user_offsets,
+                            const int64_t* item_ids, const int64_t* item_offsets, int32_t cap,
+                            void* O, int32_t* counts, void* stream) {
+  return score_host_impl(plan, n_chunks, nullptr, 0, U, seq_offsets, T, cand_offsets, B, W_q,
+                         W_k, W_v, act, user_ids, user_offsets, item_ids, item_offsets, cap, O,
+                         counts, stream);
+}
+
+gesr_status gesr_score_host_ids(gesr_host_plan* plan, int32_t n_chunks, const void* E,
+                                int64_t n_E, const int32_t* hist_rows,
+                                const int64_t* seq_offsets, const int32_t* cand_rows,
+                                const int64_t* cand_offsets, int64_t B, const void* W_q,
+                                const void* W_k, const void* W_v, int32_t act,
+                                const int64_t* user_ids, const int64_t* user_offsets,
+                                const int64_t* item_ids, const int64_t* item_offsets, int32_t cap,
+                                void* O, int32_t* counts, void* stream) {
+  if (!E) return hfail(GESR_ERR_INVALID_ARG, "gesr_score_host_ids: null table");
+  if (n_E < 1 || n_E >= (int64_t(1) << 31))
+    return hfail(GESR_ERR_INVALID_ARG, "gesr_score_host_ids: n_E must be in [1, 2^31)");
+  return score_host_impl(plan, n_chunks, E, n_E, hist_rows, seq_offsets, cand_rows, cand_offsets,
+                         B, W_q, W_k, W_v, act, user_ids, user_offsets, item_ids, item_offsets,
+                         cap, O, counts, stream);
 }
 
 }  // extern "C"

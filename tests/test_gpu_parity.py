@@ -757,3 +757,34 @@ def test_back_to_back_steps_keep_stream_order(B, kv_splits):
     for i in range(n):
         assert torch.equal(outs[i], ref[i % 2][0]), i
         assert torch.equal(cnts[i], ref[i % 2][1]), i
+
+
+@pytest.mark.parametrize("chunks", [1, 3])
+def test_score_host_ids_matches_score_host(chunks):
+    """gesr_score_host_ids (host holds table row ids; the device-resident shared table is
+    gathered inside the projections) gives exactly gesr_score_host's O and
+    counts when E[hist_rows] = U and E[cand_rows] = T (E = a row permutation of [U; T])."""
+    dev = _cuda()
+    cfg = configs.get("3").with_(B=6, L=("uniform", 0, 300), C=("uniform", 0, 400))
+    bt = inputs.make_batch(cfg)
+    pin = lambda t: t.contiguous().pin_memory()   # noqa: E731
+    hb = inputs.Batch(cfg, bt.requests, pin(bt.seq_offsets), pin(bt.cand_offsets), pin(bt.U),
+                      pin(bt.T), bt.W_q, bt.W_k, bt.W_v, pin(bt.user_ids), pin(bt.user_offsets),
+                      pin(bt.item_ids), pin(bt.item_offsets))
+    nL, nC = bt.U.shape[0], bt.T.shape[0]
+    g = torch.Generator().manual_seed(21)
+    perm = torch.randperm(nL + nC, generator=g)
+    E = torch.cat([bt.U, bt.T])[perm].to(dev)           # row perm[j] of [U; T] at j
+    inv = torch.empty_like(perm)
+    inv[perm] = torch.arange(nL + nC)
+    hist_rows = pin(inv[:nL].to(torch.int32))
+    cand_rows = pin(inv[nL:].to(torch.int32))
+    plan = gb.HostPlan(hb, n_chunks=chunks, out_dtype=torch.bfloat16, device=dev)
+    O1 = torch.full((nC, cfg.H * cfg.d), float("nan"), dtype=torch.bfloat16).pin_memory()
+    c1 = torch.full((nC, cfg.F), -1, dtype=torch.int32).pin_memory()
+    O2, c2 = O1.clone().pin_memory(), c1.clone().pin_memory()
+    plan.run(O1, c1)
+    plan.run_ids(E, hist_rows, cand_rows, O2, c2)
+    torch.cuda.synchronize()
+    plan.close()
+    assert torch.equal(O1, O2) and torch.equal(c1, c2)
