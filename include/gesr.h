@@ -23,6 +23,11 @@
  * device calls, and that section states where the host path differs (host pointers, device
  * allocation in the plan, host<->device copies).
  *
+ * Serving from IDs (history and candidate IDs looked up in the shared embedding
+ * table to obtain U and T): gesr_kv_project_gather and gesr_tasa_score_gather fuse the lookup
+ * into the projections (the rows are never written to memory), and gesr_score_host_ids runs
+ * the host path from row IDs with the table resident on the device.
+ *
  * Conventions (all device calls):
  *   - Every array pointer is a DEVICE pointer owned by the caller; the library never frees or
  *     retains a pointer after the call returns.  bf16 arrays are IEEE bfloat16 bit patterns.
