@@ -164,3 +164,34 @@ def test_tasa_identity_bf16_out_forced_splits(d):
                            kv_splits=1, out_dtype=torch.bfloat16, want_lse=False)
     torch.cuda.synchronize()
     assert torch.equal(O1b, outs[1])
+
+
+def test_config5_lpt_shard_rows_bit_identical_to_larger_batch():
+    """SURVEY s8(e) / VERDICT r1 next 4: an LPT shard of config 5's 8192 requests (the
+    partition bench.py --gpus N --config 5 uses, here into 32 shards) scored alone gives exactly
+    the rows the same requests get inside a larger batch (that shard followed by another one):
+    d = 128 CTA-pair attention at a fixed kv_splits = 1, K/V projection and HMA counts.  Rows
+    depend only on their own request, so the multi-GPU result is the single-GPU result."""
+    from paper_2511_21095_b200 import shard
+    dev = torch.device("cuda", 0)
+    cfg = configs.get("5")
+    L, C = inputs.request_lengths(cfg)
+    parts = shard.lpt_partition(shard.request_cost(cfg, L.numpy(), C.numpy()), 32)
+    a, b = [int(x) for x in parts[3]], [int(x) for x in parts[17]]
+
+    def run(reqs):
+        bt = inputs.make_batch(cfg, requests=reqs, device=dev)
+        K, V = gb.kv_project(bt.U, bt.W_k, bt.W_v, cfg.H, cfg.d, cfg.act)
+        O, lse = gb.tasa_score(bt.T, bt.cand_offsets, bt.W_q, K, V, bt.seq_offsets, cfg.H, cfg.d,
+                               cfg.act, kv_splits=1, out_dtype=torch.bfloat16)
+        c = gb.hma_count(bt.user_ids, bt.user_offsets, bt.item_ids, bt.item_offsets,
+                         bt.cand_offsets, cfg.F)
+        torch.cuda.synchronize()
+        return bt, K, O, lse, c
+
+    bt_a, K_a, O_a, lse_a, c_a = run(a)
+    _, K_u, O_u, lse_u, c_u = run(a + b)
+    nL, nC = bt_a.U.shape[0], bt_a.T.shape[0]
+    assert torch.equal(K_u[:, :nL], K_a)
+    assert torch.equal(O_u[:nC], O_a) and torch.equal(lse_u[:nC], lse_a)
+    assert torch.equal(c_u[:nC], c_a)
