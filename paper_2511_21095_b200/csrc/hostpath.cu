@@ -315,6 +315,13 @@ gesr_status gesr_score_host_ids(gesr_host_plan* plan, int32_t n_chunks, const vo
   if (!E) return hfail(GESR_ERR_INVALID_ARG, "gesr_score_host_ids: null table");
   if (n_E < 1 || n_E >= (int64_t(1) << 31))
     return hfail(GESR_ERR_INVALID_ARG, "gesr_score_host_ids: n_E must be in [1, 2^31)");
+  cudaPointerAttributes pa;
+  if (plan && (cudaPointerGetAttributes(&pa, E) != cudaSuccess || pa.type != cudaMemoryTypeDevice ||
+               pa.device != plan->dev)) {
+    (void)cudaGetLastError();
+    return hfail(GESR_ERR_INVALID_ARG,
+                 "gesr_score_host_ids: E must be device memory on the plan's device");
+  }
   return score_host_impl(plan, n_chunks, E, n_E, hist_rows, seq_offsets, cand_rows, cand_offsets,
                          B, W_q, W_k, W_v, act, user_ids, user_offsets, item_ids, item_offsets,
                          cap, O, counts, stream);

@@ -786,5 +786,7 @@ def test_score_host_ids_matches_score_host(chunks):
     plan.run(O1, c1)
     plan.run_ids(E, hist_rows, cand_rows, O2, c2)
     torch.cuda.synchronize()
+    with pytest.raises(gb.GesrError):          # the table must be device memory
+        plan.run_ids(E.cpu(), hist_rows, cand_rows, O2, c2)
     plan.close()
     assert torch.equal(O1, O2) and torch.equal(c1, c2)
