@@ -124,3 +124,24 @@ def test_fused_lookup_step_matches_oracle():
                                 cfg.d, act=cfg.act)
     err = np.abs(O.cpu().numpy().astype(np.float64) - O_or)
     assert err.max() < MAX_ABS and err.mean() < MEAN_ABS, (err.max(), err.mean())
+
+
+def test_tasa_score_gather_hstu_flag_and_bias():
+    """The gather feeds the same Q projection for the HSTU-normalisation flag and a query bias."""
+    dev = _cuda()
+    cfg = configs.get("2").with_(B=8)
+    bt = inputs.make_batch(cfg, hma=False, device=dev)
+    n_E = 700
+    g = torch.Generator().manual_seed(17)
+    E = torch.randn(n_E, cfg.D_in, generator=g).to(torch.bfloat16).to(dev)
+    rows = torch.randint(0, n_E, (bt.total_C,), generator=g, dtype=torch.int32).to(dev)
+    bq = torch.linspace(-0.2, 0.2, cfg.H * cfg.d, device=dev)
+    K, V = gb.kv_project(bt.U, bt.W_k, bt.W_v, cfg.H, cfg.d, cfg.act)
+    T = E.index_select(0, rows.long())
+    for flags in (0, gb.GESR_TASA_HSTU_SILU):
+        O, _ = gb.tasa_score_gather(E, rows, bt.cand_offsets, bt.W_q, K, V, bt.seq_offsets, cfg.H,
+                                    cfg.d, cfg.act, b_q=bq, flags=flags, want_lse=False)
+        O0, _ = gb.tasa_score(T, bt.cand_offsets, bt.W_q, K, V, bt.seq_offsets, cfg.H, cfg.d,
+                              cfg.act, b_q=bq, flags=flags, want_lse=False)
+        torch.cuda.synchronize()
+        assert torch.equal(O, O0), flags
