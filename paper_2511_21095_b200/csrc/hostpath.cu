@@ -215,6 +215,9 @@ gesr_status score_host_impl(gesr_host_plan* plan, int32_t n_chunks, const void* 
       return hfail(GESR_ERR_WORKSPACE, "gesr_score_host: a chunk exceeds the plan's maxima");
   }
   if (B == 0) return GESR_OK;
+  if ((seq_offsets[B] > 0 && !U) || (cand_offsets[B] > 0 && !T) ||
+      (user_offsets[B * F] > 0 && !user_ids) || (item_offsets[cand_offsets[B] * F] > 0 && !item_ids))
+    return hfail(GESR_ERR_INVALID_ARG, "gesr_score_host: null input rows / ids");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const size_t HD = static_cast<size_t>(H) * d;
   const size_t osz = plan->o_dtype == GESR_OUT_BF16 ? 2 : 4;
