@@ -95,3 +95,20 @@ def test_hma_multi_chunk_requests_and_empty_item_lists():
     items = _items_from(users, B, C, F, rng, lo=0, hi=9)   # some empty item lists
     want = _run(users, items, np.concatenate([[0], np.cumsum(C)]), F)
     assert (want == 0).any() and want.sum() > 0
+
+
+@pytest.mark.parametrize("F,ulen,B,C", [(1, 64, 40, 300), (33, 16, 6, 200), (256, 4, 2, 40),
+                                        (64, 64, 3, 50)])
+def test_hma_field_count_extremes(F, ulen, B, C):
+    """F from 1 to kMaxFields = 256 (a segment group then spans many candidates or one
+    candidate spans many groups; the shared-memory pool is split F ways, so at F = 64 with 64 IDs
+    per list some fields must shrink their tables or go global)."""
+    rng = np.random.default_rng(F * 1000 + ulen)
+    users = [rng.integers(-(1 << 40), 1 << 40, size=int(rng.integers(0, ulen + 1)))
+             for _ in range(B * F)]
+    Cs = [int(rng.integers(1, C + 1)) for _ in range(B)]
+    items = _items_from(users, B, Cs, F, rng, lo=0, hi=12)
+    co = np.concatenate([[0], np.cumsum(Cs)])
+    want = _run(users, items, co, F)
+    assert want.sum() > 0
+    _run(users, items, co, F, cap=1)
