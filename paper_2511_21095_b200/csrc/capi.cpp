@@ -223,7 +223,17 @@ gesr_status run_projection(const void* X, int64_t M, int32_t K, const void* W0, 
                            void* out0, void* out1, cudaStream_t stream,
                            const int32_t* gather = nullptr, int64_t table_rows = 0) {
   const int HD = H * d;
-  const int bn = gesr::proj_pick_bn(M, HD, W1 ? 2 : 1, num_sms());
+  // gather mode on a large row count: 512-wide tiles (two N = 256 MMAs per K step, one TMEM
+  // accumulator), so each gathered A tile feeds twice the MMA work -- the gathered projections
+  // are bound by issuing the gather4 loads
+#ifndef GESR_GATHER_BN512
+#define GESR_GATHER_BN512 1
+#endif
+  const int bn = (GESR_GATHER_BN512 && gather != nullptr && HD % 512 == 0 &&
+                  (M + 255) / 256 >= num_sms() / 2)
+                     ? 512
+                     : gesr::proj_pick_bn(M, HD, W1 ? 2 : 1, num_sms());
+  const uint32_t b_box = bn >= 512 ? 128 : static_cast<uint32_t>(bn / 2);
   CUtensorMap ma, mb0, mb1;
   gesr_status s = gather != nullptr
                       ? make_map_2d(&ma, X, static_cast<uint64_t>(table_rows),
@@ -233,9 +243,9 @@ gesr_status run_projection(const void* X, int64_t M, int32_t K, const void* W0, 
                                     128, 64, CU_TENSOR_MAP_SWIZZLE_128B, "X");
   if (s != GESR_OK) return s;
   // a CTA pair computes 256 x bn; each CTA stages its 128 rows of X and bn/2 weight rows
-  s = make_map_2d(&mb0, W0, HD, K, bn / 2, 64, CU_TENSOR_MAP_SWIZZLE_128B, "W0");
+  s = make_map_2d(&mb0, W0, HD, K, b_box, 64, CU_TENSOR_MAP_SWIZZLE_128B, "W0");
   if (s != GESR_OK) return s;
-  s = make_map_2d(&mb1, W1 ? W1 : W0, HD, K, bn / 2, 64, CU_TENSOR_MAP_SWIZZLE_128B, "W1");
+  s = make_map_2d(&mb1, W1 ? W1 : W0, HD, K, b_box, 64, CU_TENSOR_MAP_SWIZZLE_128B, "W1");
   if (s != GESR_OK) return s;
   CUtensorMap mo0, mo1;
   s = make_out_map(&mo0, out0, H, M, d, "out0");

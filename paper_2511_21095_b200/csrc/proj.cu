@@ -73,7 +73,10 @@ struct ProjSmem {
   static constexpr uint32_t kStagingBytes = kEpiWarps * 2048 * kBoxes;
   static constexpr int kStages = (224 * 1024 - kStagingBytes) / kStageBytes > 8
                                      ? 8 : (224 * 1024 - kStagingBytes) / kStageBytes;
-  static constexpr uint32_t kTmemCols = (2 * BN) < 32 ? 32 : 2 * BN;
+  // accumulator buffers in TMEM: two (the epilogue of tile i overlaps the MMAs of tile i+1),
+  // one for BN = 512 (the gather mode's double-width tile: 512 columns fill TMEM)
+  static constexpr int kAccBufs = BN >= 512 ? 1 : 2;
+  static constexpr uint32_t kTmemCols = (kAccBufs * BN) < 32 ? 32 : kAccBufs * BN;
   static constexpr uint32_t kStagingOffset = kStages * kStageBytes;
   static constexpr uint32_t kBarOffset = kStagingOffset + kStagingBytes;
   static constexpr uint32_t kIdsOffset = kBarOffset + 256;     // gathered row ids of a tile
@@ -208,7 +211,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           } else {
             tma_load_2d_pair(sa, &map_a, &full_bar[stage], kb * kBK, ma);
           }
-          if (!helper) tma_load_2d_pair(sb, mb, &full_bar[stage], kb * kBK, nb);
+          if (!helper) {
+            if constexpr (BN >= 512) {
+              // two 128-row weight boxes per CTA: box j of CTA r holds rows 256 j + 128 r + [0,
+              // 128), so the pair MMA j (N = 256) covers columns [256 j, 256 j + 256) in order
+              const int nl = nb - static_cast<int>(rank) * (BN / 2) + static_cast<int>(rank) * 128;
+              tma_load_2d_pair(sb, mb, &full_bar[stage], kb * kBK, nl);
+              tma_load_2d_pair(sb + 128 * kBK * 2, mb, &full_bar[stage], kb * kBK, nl + 256);
+            } else {
+              tma_load_2d_pair(sb, mb, &full_bar[stage], kb * kBK, nb);
+            }
+          }
           if (++stage == S::kStages) { stage = 0; phase ^= 1; }
         }
       }
@@ -218,7 +231,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     // ---------------- MMA issuer (leader CTA only)
     if (rank == 0) {
-      const uint32_t idesc = make_idesc_bf16(2 * kBM, BN, 0, 0);
+      const uint32_t idesc = make_idesc_bf16(2 * kBM, BN >= 512 ? 256 : BN, 0, 0);
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
@@ -226,8 +239,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const long long tstart = clock64();
 #endif
       for (; local < my_tiles; ++local) {
-        const uint32_t buf = local & 1;
-        const uint32_t aphase = (local >> 1) & 1;
+        const uint32_t buf = local % S::kAccBufs;
+        const uint32_t aphase = (local / S::kAccBufs) & 1;
         PROF_WAIT(2, mbar_wait_sleep(&tempty_bar[buf], aphase ^ 1));
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + buf * BN;
@@ -242,6 +255,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               const uint64_t ad = make_sdesc(sa + k * 32, 16, 1024, kSwizzle128B);
               const uint64_t bd = make_sdesc(sb + k * 32, 16, 1024, kSwizzle128B);
               mma_ss_pair(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+              if constexpr (BN >= 512) {
+                const uint64_t bd1 = make_sdesc(sb + 128 * kBK * 2 + k * 32, 16, 1024,
+                                                kSwizzle128B);
+                mma_ss_pair(d_tmem + 256, ad, bd1, idesc, (kb | k) != 0 ? 1u : 0u);
+              }
             }
             mma_commit_pair_mc(&empty_bar[stage], 0x3);
             if (kb == num_kb - 1) mma_commit_pair_mc(&tfull_bar[buf], 0x3);
@@ -274,8 +292,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     TileCursor cur(tiles);
     for (; local < my_tiles; ++local, cur.next()) {
       const int m_blk = cur.m, n_blk = cur.n;
-      const uint32_t buf = local & 1;
-      const uint32_t aphase = (local >> 1) & 1;
+      const uint32_t buf = local % S::kAccBufs;
+      const uint32_t aphase = (local / S::kAccBufs) & 1;
       const int row0 = m_blk * 2 * kBM + static_cast<int>(rank) * kBM + static_cast<int>(sub) * 32;
       // one warp of each 4-warp column part polls the accumulator's mbarrier and releases the
       // other three through hardware named barrier 1 + part (they wait descheduled): 16 warps
@@ -417,6 +435,7 @@ cudaError_t launch_proj(const CUtensorMap& map_a, const CUtensorMap& map_b0,
                         const CUtensorMap& map_o1, const ProjParams& p, int bn, int num_sms,
                         cudaStream_t stream) {
   switch (bn) {
+    case 512: return launch_bn<512>(map_a, map_b0, map_b1, map_o0, map_o1, p, num_sms, stream);
     case 256: return launch_bn<256>(map_a, map_b0, map_b1, map_o0, map_o1, p, num_sms, stream);
     case 128: return launch_bn<128>(map_a, map_b0, map_b1, map_o0, map_o1, p, num_sms, stream);
     case 64: return launch_bn<64>(map_a, map_b0, map_b1, map_o0, map_o1, p, num_sms, stream);
