@@ -145,3 +145,30 @@ def test_tasa_score_gather_hstu_flag_and_bias():
                               cfg.act, b_q=bq, flags=flags, want_lse=False)
         torch.cuda.synchronize()
         assert torch.equal(O, O0), flags
+
+
+@pytest.mark.parametrize("kv_splits,out_dtype", [(3, torch.float32), (1, torch.bfloat16)])
+def test_tasa_score_gather_splits_lse_and_dtypes(kv_splits, out_dtype):
+    """Forced key splits (combine kernel) with the lse output, fp32 and bf16 O, both biases on
+    the gathered K/V projection: every output equals the materialised path's."""
+    dev = _cuda()
+    cfg = configs.get("3").with_(B=5, L=("uniform", 1, 700), C=("uniform", 1, 600))
+    bt = inputs.make_batch(cfg, hma=False, device=dev)
+    n_E = 4000
+    g = torch.Generator().manual_seed(23)
+    E = torch.randn(n_E, cfg.D_in, generator=g).to(torch.bfloat16).to(dev)
+    hist = torch.randint(0, n_E, (bt.U.shape[0],), generator=g, dtype=torch.int32).to(dev)
+    cand = torch.randint(0, n_E, (bt.total_C,), generator=g, dtype=torch.int32).to(dev)
+    bk = torch.linspace(-0.1, 0.2, cfg.H * cfg.d, device=dev)
+    bv = torch.linspace(0.3, -0.3, cfg.H * cfg.d, device=dev)
+    K, V = gb.kv_project_gather(E, hist, bt.W_k, bt.W_v, cfg.H, cfg.d, cfg.act, b_k=bk, b_v=bv)
+    K0, V0 = gb.kv_project(E.index_select(0, hist.long()), bt.W_k, bt.W_v, cfg.H, cfg.d,
+                           cfg.act, b_k=bk, b_v=bv)
+    O, lse = gb.tasa_score_gather(E, cand, bt.cand_offsets, bt.W_q, K, V, bt.seq_offsets, cfg.H,
+                                  cfg.d, cfg.act, kv_splits=kv_splits, out_dtype=out_dtype)
+    O0, lse0 = gb.tasa_score(E.index_select(0, cand.long()), bt.cand_offsets, bt.W_q, K0, V0,
+                             bt.seq_offsets, cfg.H, cfg.d, cfg.act, kv_splits=kv_splits,
+                             out_dtype=out_dtype)
+    torch.cuda.synchronize()
+    assert torch.equal(K, K0) and torch.equal(V, V0)
+    assert torch.equal(O, O0) and torch.equal(lse, lse0)
