@@ -647,6 +647,8 @@ class HostPlan:
         for t in (hist_rows, cand_rows):
             if t.dtype != torch.int32 or t.is_cuda:
                 raise GesrError(GESR_ERR_INVALID_ARG, "row ids must be int32 host tensors")
+        if E.dim() != 2 or E.shape[1] != self.cfg.D_in or E.dtype != torch.bfloat16:
+            raise GesrError(GESR_ERR_INVALID_ARG, "E must be bf16 [n_E, D_in] with the plan's D_in")
         _check(lib().gesr_score_host_ids(
             self._plan, self.n_chunks, _ptr(E), E.shape[0], _ptr(hist_rows),
             _ptr(hb.seq_offsets), _ptr(cand_rows), _ptr(hb.cand_offsets), hb.B, _ptr(W_q),
