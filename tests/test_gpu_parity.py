@@ -759,8 +759,10 @@ def test_back_to_back_steps_keep_stream_order(B, kv_splits):
         assert torch.equal(cnts[i], ref[i % 2][1]), i
 
 
-@pytest.mark.parametrize("chunks", [1, 3])
-def test_score_host_ids_matches_score_host(chunks):
+@pytest.mark.parametrize("chunks,out_dtype,cap", [(1, torch.bfloat16, 0),
+                                                   (3, torch.bfloat16, 0),
+                                                   (2, torch.float32, 3)])
+def test_score_host_ids_matches_score_host(chunks, out_dtype, cap):
     """gesr_score_host_ids (host holds table row ids; the device-resident shared table is
     gathered inside the projections) gives exactly gesr_score_host's O and
     counts when E[hist_rows] = U and E[cand_rows] = T (E = a row permutation of [U; T])."""
@@ -779,8 +781,8 @@ def test_score_host_ids_matches_score_host(chunks):
     inv[perm] = torch.arange(nL + nC)
     hist_rows = pin(inv[:nL].to(torch.int32))
     cand_rows = pin(inv[nL:].to(torch.int32))
-    plan = gb.HostPlan(hb, n_chunks=chunks, out_dtype=torch.bfloat16, device=dev)
-    O1 = torch.full((nC, cfg.H * cfg.d), float("nan"), dtype=torch.bfloat16).pin_memory()
+    plan = gb.HostPlan(hb, n_chunks=chunks, out_dtype=out_dtype, cap=cap, device=dev)
+    O1 = torch.full((nC, cfg.H * cfg.d), float("nan"), dtype=out_dtype).pin_memory()
     c1 = torch.full((nC, cfg.F), -1, dtype=torch.int32).pin_memory()
     O2, c2 = O1.clone().pin_memory(), c1.clone().pin_memory()
     plan.run(O1, c1)
