@@ -178,6 +178,15 @@ def _dev(*ts):
             raise GesrError(GESR_ERR_INVALID_ARG, "all tensors must be contiguous")
 
 
+def _check_cache(K_cache, V_cache, H, total_L, d):
+    """The head-major cache's row stride is total_L: a cache of another shape would be written
+    with one layout and read (tasa_score takes total_L from K_cache.shape[1]) with another."""
+    for t in (K_cache, V_cache):
+        if tuple(t.shape) != (H, total_L, d) or t.dtype != torch.bfloat16:
+            raise GesrError(GESR_ERR_INVALID_ARG, f"K/V cache must be bf16 {(H, total_L, d)}, "
+                            f"got {t.dtype} {tuple(t.shape)}")
+
+
 @_on_stream
 def kv_project(U, W_k, W_v, H: int, d: int, act: int = GESR_ACT_SILU, b_k=None, b_v=None,
                K_cache=None, V_cache=None, stream=None):
@@ -188,6 +197,7 @@ def kv_project(U, W_k, W_v, H: int, d: int, act: int = GESR_ACT_SILU, b_k=None, 
         K_cache = torch.empty((H, total_L, d), dtype=torch.bfloat16, device=U.device)
     if V_cache is None:
         V_cache = torch.empty((H, total_L, d), dtype=torch.bfloat16, device=U.device)
+    _check_cache(K_cache, V_cache, H, total_L, d)
     _check(lib().gesr_kv_project(_ptr(U), total_L, D_in, _ptr(W_k), _ptr(W_v), _ptr(b_k),
                                  _ptr(b_v), H, d, act, _ptr(K_cache), _ptr(V_cache),
                                  _stream(stream)))
@@ -208,6 +218,7 @@ def kv_project_gather(E, rows, W_k, W_v, H: int, d: int, act: int = GESR_ACT_SIL
         K_cache = torch.empty((H, total_L, d), dtype=torch.bfloat16, device=E.device)
     if V_cache is None:
         V_cache = torch.empty((H, total_L, d), dtype=torch.bfloat16, device=E.device)
+    _check_cache(K_cache, V_cache, H, total_L, d)
     _check(lib().gesr_kv_project_gather(_ptr(E), n_E, D_in, _ptr(rows), total_L, _ptr(W_k),
                                         _ptr(W_v), _ptr(b_k), _ptr(b_v), H, d, act,
                                         _ptr(K_cache), _ptr(V_cache), _stream(stream)))

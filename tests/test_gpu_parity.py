@@ -792,3 +792,16 @@ def test_score_host_ids_matches_score_host(chunks, out_dtype, cap):
         plan.run_ids(E.cpu(), hist_rows, cand_rows, O2, c2)
     plan.close()
     assert torch.equal(O1, O2) and torch.equal(c1, c2)
+
+
+def test_kv_cache_shape_is_checked():
+    """A K/V cache whose row count differs from the history's would be written with one
+    head-major stride and read with another: the binding rejects it."""
+    dev = _cuda()
+    cfg = configs.get("2").with_(B=2)
+    bt = inputs.make_batch(cfg, hma=False, device=dev)
+    L = bt.U.shape[0]
+    K = torch.empty((cfg.H, L + 1, cfg.d), dtype=torch.bfloat16, device=dev)
+    V = torch.empty_like(K)
+    with pytest.raises(gb.GesrError):
+        gb.kv_project(bt.U, bt.W_k, bt.W_v, cfg.H, cfg.d, cfg.act, K_cache=K, V_cache=V)
