@@ -31,3 +31,35 @@ for name, B, splits in (("3h", 2, 1), ("3h", 1, 0), ("2", 16, 0)):
     print(name, B, splits, "mismatching steps:", nb, "of", n)
     bad += nb
 print("PDL stress", "OK" if bad == 0 else "FAILED")
+
+# the host path: 40 back-to-back gesr_score_host / _ids calls (copy streams, two buffer sets,
+# chunk pipeline) into distinct pinned outputs, each compared with the device-resident step
+cfg = configs.get("3").with_(B=24)
+bt = inputs.make_batch(cfg)
+pin = lambda t: t.contiguous().pin_memory()   # noqa: E731
+hb = inputs.Batch(cfg, bt.requests, pin(bt.seq_offsets), pin(bt.cand_offsets), pin(bt.U),
+                  pin(bt.T), bt.W_q, bt.W_k, bt.W_v, pin(bt.user_ids), pin(bt.user_offsets),
+                  pin(bt.item_ids), pin(bt.item_offsets))
+g = bt.to(dev)
+bufs = gb.StepBuffers(g, out_dtype=torch.bfloat16)
+O_ref, c_ref = gb.score_step(g, bufs)
+torch.cuda.synchronize()
+O_ref, c_ref = O_ref.cpu(), c_ref.cpu()
+nL, nC = bt.U.shape[0], bt.T.shape[0]
+perm = torch.randperm(nL + nC, generator=torch.Generator().manual_seed(1))
+E = torch.cat([bt.U, bt.T])[perm].to(dev)
+inv = torch.empty_like(perm)
+inv[perm] = torch.arange(nL + nC)
+hr, cr = pin(inv[:nL].to(torch.int32)), pin(inv[nL:].to(torch.int32))
+plan = gb.HostPlan(hb, n_chunks=5, out_dtype=torch.bfloat16, device=dev)
+outs = [(torch.empty_like(O_ref).pin_memory(), torch.empty_like(c_ref).pin_memory()) for _ in range(40)]
+for i, (o, c) in enumerate(outs):
+    if i % 2:
+        plan.run_ids(E, hr, cr, o, c)
+    else:
+        plan.run(o, c)
+torch.cuda.synchronize()
+hb_bad = sum(0 if (torch.equal(o, O_ref) and torch.equal(c, c_ref)) else 1 for o, c in outs)
+plan.close()
+print("host path: mismatching calls:", hb_bad, "of", len(outs))
+print("host stress", "OK" if hb_bad == 0 else "FAILED")
